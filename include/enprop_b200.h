@@ -1,0 +1,194 @@
+/* enprop_b200 — C ABI of the B200-native ensemble hot path
+ * (ensemble FEM assembly -> ensemble CRS SpMV -> ensemble CG) of
+ * arXiv 1511.03703, drop-in for the reference library "enprop"
+ * (/root/reference/proj/include/enprop).
+ *
+ * Conventions
+ *  - Ensemble width s in {1,2,4,8,16,32} (the reference's compiled set,
+ *    proj/src/bench.cpp:447-460).
+ *  - Layouts are the reference's: values [nnz][s] fp64 (Ensemble<S> is a POD of
+ *    S doubles, ensemble.hpp:105-106), vectors [rows][s] fp64, int32 row_map /
+ *    col_entry (crs.hpp:19-69).  Device pointers unless a name says "host".
+ *  - Calls are ordered on the context's stream.  Functions that return values
+ *    to the host synchronise the stream.
+ *  - Arithmetic is the reference's: fp64, no FMA contraction, left-to-right
+ *    (proj/CMakeLists.txt:14 builds with -ffp-contract=off).  Assembly,
+ *    Dirichlet, SpMV and axpby are bitwise equal to the reference.  Dot products
+ *    and CG take a reduction order: ENPROP_DOT_SERIAL reproduces the reference
+ *    bitwise (kernels.hpp:62-69); ENPROP_DOT_CANONICAL is the fast fixed tree of
+ *    DESIGN.md §4 (bitwise equal to oracle/enprop_oracle.c's restatement).
+ *  - Status codes mirror the reference's exceptions: ENPROP_ERR_INVALID for
+ *    std::invalid_argument (e.g. kernels.hpp:17-18), NO_CONVERGENCE and
+ *    INDEFINITE for SolverError (pcg.hpp:82-92).  enprop_last_error() holds
+ *    the message (thread-local).
+ */
+#ifndef ENPROP_B200_H
+#define ENPROP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ENPROP_ABI_VERSION 1
+
+enum {
+  ENPROP_OK = 0,
+  ENPROP_ERR_INVALID = 1,        /* std::invalid_argument in the reference */
+  ENPROP_ERR_NO_CONVERGENCE = 2, /* SolverError: maxit reached (pcg.hpp:82-85) */
+  ENPROP_ERR_INDEFINITE = 3,     /* SolverError: p'Ap <= 0 (pcg.hpp:88-92) */
+  ENPROP_ERR_CUDA = 4,
+  ENPROP_ERR_OOM = 5
+};
+
+enum { ENPROP_DOT_SERIAL = 0, ENPROP_DOT_CANONICAL = 1 };
+enum { ENPROP_CG_COUPLED = 0, ENPROP_CG_UNCOUPLED = 1 };
+
+/* Rows per canonical reduction tile. */
+#define ENPROP_TILE_ROWS 64
+
+const char* enprop_last_error(void);
+int enprop_abi_version(void);
+
+/* ---------------------------------------------------------------- context */
+typedef struct enprop_ctx enprop_ctx;
+int enprop_ctx_create(int device, enprop_ctx** out);
+int enprop_ctx_destroy(enprop_ctx* ctx);
+/* cudaStream_t as void*; NULL selects the legacy default stream (torch's
+ * default).  A new context runs on its own non-blocking stream. */
+int enprop_ctx_set_stream(enprop_ctx* ctx, void* stream);
+void* enprop_ctx_stream(enprop_ctx* ctx);
+int enprop_ctx_synchronize(enprop_ctx* ctx);
+/* number of enprop kernels launched through this context so far */
+int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
+/* Event timing of the CG SpMV kernel launches on the context stream (used by
+ * bench.py for the roofline). Returns the totals accumulated since the last
+ * reset; enable = 1/0 turns timing on/off and resets, enable = -1 only reads. */
+int enprop_ctx_profile(enprop_ctx* ctx, int enable, double* spmv_ms, int64_t* spmv_launches);
+
+int enprop_malloc(enprop_ctx* ctx, size_t bytes, void** dptr);
+int enprop_free(enprop_ctx* ctx, void* dptr);
+/* stream-ordered copies; both return after the copy completed */
+int enprop_memcpy_h2d(enprop_ctx* ctx, void* dst, const void* host_src, size_t bytes);
+int enprop_memcpy_d2h(enprop_ctx* ctx, void* host_dst, const void* src, size_t bytes);
+
+/* ------------------------------------------------------- problem parameters */
+/* KlField(num_terms, mean, sigma, correlation_length)  (kl.hpp:39-95) */
+typedef struct {
+  int num_terms;
+  double mean, sigma, correlation_length;
+} enprop_kl_params;
+
+/* PdeCoefficients (fem.hpp:21-25) */
+typedef struct {
+  double alpha, beta;
+  double velocity[3];
+} enprop_pde_coeffs;
+
+/* DirichletBc (fem.hpp:29-32) */
+typedef struct {
+  double x0_value, x1_value;
+} enprop_dirichlet_bc;
+
+/* ------------------------------------------------------------ mesh & field */
+/* (3(n+1)-2)^3 stored entries of the 27-point node graph (mesh.cpp:13-55) */
+int64_t enprop_mesh_nnz(int cells_per_axis);
+/* build_node_graph(StructuredMesh(n)) into device arrays, bit-exact
+ * (mesh.cpp:13-55). row_map[(n+1)^3 + 1], col_entry[enprop_mesh_nnz(n)]. */
+int enprop_build_node_graph(enprop_ctx* ctx, int cells_per_axis, int* row_map, int* col_entry);
+/* KlField eigen-structure on the host (kl.cpp:41-89): per retained mode i
+ * mode_axes[3i..3i+2], mode_eigenvalue[i]; per axis mode t axis_frequency[t],
+ * axis_eigenvalue[t], axis_inverse_norm[t], axis_cosine[t]. Arrays of num_terms. */
+int enprop_kl_describe(const enprop_kl_params* kl, int* mode_axes, double* mode_eigenvalue,
+                       double* axis_frequency, double* axis_eigenvalue,
+                       double* axis_inverse_norm, int* axis_cosine);
+
+/* ----------------------------------------------------------------- kernels */
+/* assemble<Ensemble<s>> (fem.hpp:115-202) of the unit-cube diffusion problem
+ * on the n^3 hex mesh; optionally followed by apply_dirichlet (fem.hpp:218-243)
+ * fused in the same kernel when bc != NULL.
+ *   u        [rows][s] current iterate, NULL means all zeros
+ *   y        [num_terms][s] sample coordinates (pack_sample_group layout)
+ *   row_map  graph from enprop_build_node_graph
+ *   values   [nnz][s] out; residual [rows][s] out (both overwritten) */
+int enprop_assemble(enprop_ctx* ctx, int s, int cells_per_axis, const enprop_kl_params* kl,
+                    const enprop_pde_coeffs* coeffs, const double* u, const double* y,
+                    const int* row_map, double* values, double* residual,
+                    const enprop_dirichlet_bc* bc);
+/* apply_dirichlet (fem.hpp:218-243) on an assembled mesh system, in place. */
+int enprop_apply_dirichlet(enprop_ctx* ctx, int s, int cells_per_axis,
+                           const enprop_dirichlet_bc* bc, const int* row_map,
+                           const int* col_entry, const double* u, double* values,
+                           double* residual);
+
+/* spmv (kernels.hpp:15-26): z = A x, general CRS, bitwise equal per lane. */
+int enprop_spmv(enprop_ctx* ctx, int s, int num_rows, int num_cols, const int* row_map,
+                const int* col_entry, const double* values, const double* x, double* z);
+
+/* dot (kernels.hpp:62-69): per-lane sums lanes_host[s] (may be NULL) and the
+ * coupled reduce_sum coupled_host (may be NULL) in the given order.
+ * seg_rows is the canonical segment length (ignored for SERIAL). */
+int enprop_dot(enprop_ctx* ctx, int s, int64_t n, const double* u, const double* v,
+               int dot_mode, int seg_rows, double* lanes_host, double* coupled_host);
+
+/* axpby (kernels.hpp:78-85): y = alpha*x + beta*y. per_lane != 0: alpha/beta
+ * are s host doubles (Ensemble coefficients), else one host double each. */
+int enprop_axpby(enprop_ctx* ctx, int s, int64_t n, int per_lane, const double* alpha_host,
+                 const double* x, const double* beta_host, double* y);
+
+/* ----------------------------------------------------------------------- CG */
+/* Identity-preconditioned CG from x0 = 0 (pcg.hpp:52-103).
+ *   COUPLED   = pcg_solve<Ensemble<s>>: one coupled norm/decision.
+ *   UNCOUPLED = s x pcg_solve<double> on extracted components
+ *               (bench.cpp:340-349): per-lane alpha, beta and stopping.
+ * Outputs (host): iterations[lanes], lane_status[lanes], history
+ * [(maxit+1)][lanes] relative residuals (NaN past a lane's end),
+ * hist_len[lanes]; lanes = 1 (COUPLED) or s (UNCOUPLED).  Any may be NULL.
+ * Returns the worst status over lanes. */
+typedef struct {
+  int flavour;   /* ENPROP_CG_* */
+  int dot_mode;  /* ENPROP_DOT_* */
+  int seg_rows;  /* canonical segment (a mesh z-plane: (n+1)^2); <=0 -> 4096 */
+  double tol;
+  int max_iterations;
+  int check_every; /* host polls convergence every k iterations (<=0 -> 16) */
+} enprop_cg_options;
+
+int enprop_cg(enprop_ctx* ctx, int s, int num_rows, const int* row_map, const int* col_entry,
+              const double* values, const double* b, double* x, const enprop_cg_options* opt,
+              int* iterations, int* lane_status, double* history, int* hist_len);
+
+/* -------------------------------------------------- device-resident problem */
+/* The performance path: graph, KL tables, matrix and CG workspaces stay in HBM;
+ * one call assembles + imposes Dirichlet + solves A x = -residual for one
+ * sample group (bench.cpp:286-299 with IdentityPreconditioner). */
+typedef struct {
+  int cells_per_axis;
+  int ensemble_size;
+  enprop_kl_params kl;
+  enprop_pde_coeffs coeffs;
+  enprop_dirichlet_bc bc;
+} enprop_problem_desc;
+
+typedef struct enprop_problem enprop_problem;
+int enprop_problem_create(enprop_ctx* ctx, const enprop_problem_desc* desc, enprop_problem** out);
+int enprop_problem_destroy(enprop_problem* p);
+/* device views (owned by the problem) */
+int enprop_problem_views(enprop_problem* p, int* num_rows, int64_t* nnz, const int** row_map,
+                         const int** col_entry, double** values, double** residual,
+                         double** solution);
+/* assemble + Dirichlet from device samples y [num_terms][s] (u = 0) */
+int enprop_problem_assemble(enprop_problem* p, const double* y);
+/* CG on the assembled system with rhs = -residual; solution in the problem */
+int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* iterations,
+                         int* lane_status, double* history, int* hist_len);
+/* End to end from HOST buffers: y_host [num_terms][s] -> x_host [rows][s]. */
+int enprop_problem_solve_host(enprop_problem* p, const double* y_host, double* x_host,
+                              const enprop_cg_options* opt, int* iterations, int* lane_status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ENPROP_B200_H */

@@ -1,0 +1,488 @@
+"""enprop_b200 — B200-native ensemble hot path of arXiv 1511.03703.
+
+Python mirror of the reference library's interfaces (``enprop``:
+``/root/reference/proj/include/enprop``) over the C ABI in
+``include/enprop_b200.h`` (``lib/libenprop_b200.so``, sm_100a only).  PyTorch
+is used for device memory and streams only; every computation runs in the
+library's CUDA kernels.  There is no CPU fallback: without a B200 the calls
+raise ``EnpropError``.
+
+Names follow the reference: ``KlField`` parameters (kl.hpp:39-95),
+``PdeCoefficients`` (fem.hpp:21-25), ``DirichletBc`` (fem.hpp:29-32),
+``SolverConfig`` / ``SolverError`` (pcg.hpp:15-31), ``spmv`` / ``dot`` /
+``norm2`` / ``axpby`` (kernels.hpp:15-85), ``assemble`` / ``apply_dirichlet``
+(fem.hpp:115-243), ``pcg_solve`` (pcg.hpp:52-103).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libenprop_b200.so")
+
+OK, ERR_INVALID, ERR_NO_CONVERGENCE, ERR_INDEFINITE, ERR_CUDA, ERR_OOM = range(6)
+DOT_SERIAL, DOT_CANONICAL = 0, 1
+CG_COUPLED, CG_UNCOUPLED = 0, 1
+TILE_ROWS = 64
+WIDTHS = (1, 2, 4, 8, 16, 32)
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_vp = C.c_void_p
+
+
+class EnpropError(RuntimeError):
+    """A CUDA / library failure (ENPROP_ERR_CUDA, ENPROP_ERR_OOM)."""
+
+
+class SolverError(RuntimeError):
+    """pcg_solve failure (pcg.hpp:22-31): carries the residual history."""
+
+    def __init__(self, what: str, history, status: int, iterations=None):
+        super().__init__(what)
+        self._history = history
+        self.status = status
+        self.iterations = iterations
+
+    def history(self):
+        return self._history
+
+
+class _KlParams(C.Structure):
+    _fields_ = [("num_terms", C.c_int), ("mean", C.c_double), ("sigma", C.c_double),
+                ("correlation_length", C.c_double)]
+
+
+class _Coeffs(C.Structure):
+    _fields_ = [("alpha", C.c_double), ("beta", C.c_double), ("velocity", C.c_double * 3)]
+
+
+class _Bc(C.Structure):
+    _fields_ = [("x0_value", C.c_double), ("x1_value", C.c_double)]
+
+
+class _CgOptions(C.Structure):
+    _fields_ = [("flavour", C.c_int), ("dot_mode", C.c_int), ("seg_rows", C.c_int),
+                ("tol", C.c_double), ("max_iterations", C.c_int), ("check_every", C.c_int)]
+
+
+class _ProblemDesc(C.Structure):
+    _fields_ = [("cells_per_axis", C.c_int), ("ensemble_size", C.c_int), ("kl", _KlParams),
+                ("coeffs", _Coeffs), ("bc", _Bc)]
+
+
+@dataclass
+class KlField:
+    """KlField(num_terms, mean, sigma, correlation_length) (kl.hpp:39-95)."""
+    num_terms: int = 5
+    mean: float = 1.0
+    sigma: float = 0.1
+    correlation_length: float = 1.0
+
+    def _c(self):
+        return _KlParams(self.num_terms, self.mean, self.sigma, self.correlation_length)
+
+
+@dataclass
+class PdeCoefficients:
+    alpha: float = 0.0
+    beta: float = 0.0
+    velocity: Sequence[float] = (1.0, 0.0, 0.0)
+
+    def _c(self):
+        return _Coeffs(self.alpha, self.beta, (C.c_double * 3)(*self.velocity))
+
+
+@dataclass
+class DirichletBc:
+    x0_value: float = 1.0
+    x1_value: float = 0.0
+
+    def _c(self):
+        return _Bc(self.x0_value, self.x1_value)
+
+
+@dataclass
+class SolverConfig:
+    """SolverConfig (pcg.hpp:15-18) plus the device-side choices."""
+    tol: float = 1e-8
+    max_iterations: int = 1000
+    flavour: int = CG_COUPLED
+    dot_mode: int = DOT_SERIAL
+    seg_rows: int = 0
+    check_every: int = 16
+
+    def _c(self):
+        return _CgOptions(self.flavour, self.dot_mode, self.seg_rows, self.tol,
+                          self.max_iterations, self.check_every)
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load lib/libenprop_b200.so; raise loudly when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise EnpropError(f"{LIB_PATH} is missing: build it with `make -C {_HERE}` "
+                          "(enprop_b200 has no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    L.enprop_last_error.restype = C.c_char_p
+    L.enprop_mesh_nnz.restype = C.c_int64
+    L.enprop_ctx_launch_count.restype = C.c_int64
+    L.enprop_ctx_stream.restype = _vp
+    L.enprop_ctx_create.argtypes = [C.c_int, C.POINTER(_vp)]
+    L.enprop_ctx_destroy.argtypes = [_vp]
+    L.enprop_ctx_set_stream.argtypes = [_vp, _vp]
+    L.enprop_ctx_stream.argtypes = [_vp]
+    L.enprop_ctx_synchronize.argtypes = [_vp]
+    L.enprop_ctx_launch_count.argtypes = [_vp]
+    L.enprop_ctx_profile.argtypes = [_vp, C.c_int, _dp, C.POINTER(C.c_int64)]
+    L.enprop_build_node_graph.argtypes = [_vp, C.c_int, _vp, _vp]
+    L.enprop_kl_describe.argtypes = [C.POINTER(_KlParams), _ip, _dp, _dp, _dp, _dp, _ip]
+    L.enprop_assemble.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(_KlParams), C.POINTER(_Coeffs),
+                                  _vp, _vp, _vp, _vp, _vp, C.POINTER(_Bc)]
+    L.enprop_apply_dirichlet.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(_Bc), _vp, _vp, _vp,
+                                         _vp, _vp]
+    L.enprop_spmv.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp]
+    L.enprop_dot.argtypes = [_vp, C.c_int, C.c_int64, _vp, _vp, C.c_int, C.c_int, _dp, _dp]
+    L.enprop_axpby.argtypes = [_vp, C.c_int, C.c_int64, C.c_int, _dp, _vp, _dp, _vp]
+    L.enprop_cg.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp,
+                            C.POINTER(_CgOptions), _ip, _ip, _dp, _ip]
+    L.enprop_problem_create.argtypes = [_vp, C.POINTER(_ProblemDesc), C.POINTER(_vp)]
+    L.enprop_problem_destroy.argtypes = [_vp]
+    L.enprop_problem_views.argtypes = [_vp, _ip, C.POINTER(C.c_int64), C.POINTER(_vp),
+                                       C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
+                                       C.POINTER(_vp)]
+    L.enprop_problem_assemble.argtypes = [_vp, _vp]
+    L.enprop_problem_solve.argtypes = [_vp, C.POINTER(_CgOptions), _ip, _ip, _dp, _ip]
+    L.enprop_problem_solve_host.argtypes = [_vp, _vp, _vp, C.POINTER(_CgOptions), _ip, _ip]
+    _lib = L
+    return L
+
+
+def _err() -> str:
+    return lib().enprop_last_error().decode(errors="replace")
+
+
+def _check(rc: int, what: str = ""):
+    if rc == OK:
+        return
+    msg = f"{what}: {_err()}" if what else _err()
+    if rc == ERR_INVALID:
+        raise ValueError(msg)  # std::invalid_argument in the reference
+    raise EnpropError(msg)
+
+
+def mesh_nnz(n: int) -> int:
+    return int(lib().enprop_mesh_nnz(n))
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _need_cuda(t: torch.Tensor, dtype, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+class Context:
+    """A device + stream.  By default it runs on torch's current stream so
+    torch allocations and enprop kernels are ordered."""
+
+    def __init__(self, device: int = 0, use_torch_stream: bool = True):
+        self.device = device
+        h = _vp()
+        _check(lib().enprop_ctx_create(device, C.byref(h)), "enprop_ctx_create")
+        self.h = h
+        if use_torch_stream:
+            self.set_stream(torch.cuda.current_stream(device).cuda_stream)
+
+    def set_stream(self, stream_handle: int):
+        _check(lib().enprop_ctx_set_stream(self.h, C.c_void_p(stream_handle)))
+
+    def synchronize(self):
+        _check(lib().enprop_ctx_synchronize(self.h))
+
+    @property
+    def launches(self) -> int:
+        return int(lib().enprop_ctx_launch_count(self.h))
+
+    def profile(self, enable: int = -1):
+        """(total ms, launches) of CG SpMV kernels timed with CUDA events on
+        this context's stream; enable=1/0 switches timing on/off and resets."""
+        ms = C.c_double()
+        cnt = C.c_int64()
+        _check(lib().enprop_ctx_profile(self.h, enable, C.byref(ms), C.byref(cnt)))
+        return ms.value, cnt.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().enprop_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def kl_describe(kl: KlField):
+    m = kl.num_terms
+    axes = (C.c_int * (3 * m))()
+    me, af, ae, ai = ((C.c_double * m)() for _ in range(4))
+    ac = (C.c_int * m)()
+    p = kl._c()
+    _check(lib().enprop_kl_describe(C.byref(p), axes, me, af, ae, ai, ac), "KlField")
+    return dict(mode_axes=[list(axes[3 * i:3 * i + 3]) for i in range(m)], mode_eig=list(me),
+                axis_freq=list(af), axis_eig=list(ae), axis_invnorm=list(ai), axis_cos=list(ac))
+
+
+def build_node_graph(ctx: Context, n: int):
+    """build_node_graph(StructuredMesh(n)) (mesh.cpp:13-55) on the device."""
+    if n < 1:
+        raise ValueError("StructuredMesh: cells_per_axis must be at least 1")
+    rows = (n + 1) ** 3
+    dev = torch.device("cuda", ctx.device)
+    rm = torch.empty(rows + 1, dtype=torch.int32, device=dev)
+    ce = torch.empty(mesh_nnz(n), dtype=torch.int32, device=dev)
+    _check(lib().enprop_build_node_graph(ctx.h, n, _ptr(rm), _ptr(ce)), "build_node_graph")
+    return rm, ce
+
+
+def assemble(ctx: Context, s: int, n: int, kl: KlField, y: torch.Tensor, row_map: torch.Tensor,
+             coeffs: PdeCoefficients = None, u: Optional[torch.Tensor] = None,
+             bc: Optional[DirichletBc] = None, values: Optional[torch.Tensor] = None,
+             residual: Optional[torch.Tensor] = None):
+    """assemble<Ensemble<s>> (fem.hpp:115-202); with ``bc`` also
+    apply_dirichlet (fem.hpp:218-243) fused.  y is [num_terms][s]."""
+    coeffs = coeffs or PdeCoefficients()
+    rows = (n + 1) ** 3
+    dev = y.device
+    _need_cuda(y, torch.float64, "y")
+    if y.numel() != kl.num_terms * s:
+        raise ValueError("assemble: sample vector length mismatch")
+    if u is not None:
+        _need_cuda(u, torch.float64, "u")
+        if u.numel() != rows * s:
+            raise ValueError("assemble: solution vector length mismatch")
+    if values is None:
+        values = torch.empty((mesh_nnz(n), s), dtype=torch.float64, device=dev)
+    if residual is None:
+        residual = torch.empty((rows, s), dtype=torch.float64, device=dev)
+    klp, cp = kl._c(), coeffs._c()
+    bcp = bc._c() if bc is not None else None
+    _check(lib().enprop_assemble(ctx.h, s, n, C.byref(klp), C.byref(cp), _ptr(u), _ptr(y),
+                                 _ptr(row_map), _ptr(values), _ptr(residual),
+                                 C.byref(bcp) if bcp is not None else None), "assemble")
+    return values, residual
+
+
+def apply_dirichlet(ctx: Context, s: int, n: int, bc: DirichletBc, row_map, col_entry, values,
+                    residual, u: Optional[torch.Tensor] = None):
+    bcp = bc._c()
+    _check(lib().enprop_apply_dirichlet(ctx.h, s, n, C.byref(bcp), _ptr(row_map), _ptr(col_entry),
+                                        _ptr(u), _ptr(values), _ptr(residual)), "apply_dirichlet")
+
+
+def spmv(ctx: Context, s: int, row_map, col_entry, values, x, z=None, num_cols=None):
+    """z = A x (kernels.hpp:15-26), bitwise equal to the reference per sample."""
+    rows = row_map.numel() - 1
+    cols = rows if num_cols is None else num_cols
+    if x.numel() != cols * s:
+        raise ValueError("spmv: x length must equal num_cols")
+    if z is None:
+        z = torch.empty((rows, s), dtype=torch.float64, device=x.device)
+    _check(lib().enprop_spmv(ctx.h, s, rows, cols, _ptr(row_map), _ptr(col_entry), _ptr(values),
+                             _ptr(x), _ptr(z)), "spmv")
+    return z
+
+
+def dot_lanes(ctx: Context, s: int, u, v, mode: int = DOT_SERIAL, seg_rows: int = 4096):
+    if u.numel() != v.numel():
+        raise ValueError("dot: length mismatch")
+    lanes = (C.c_double * s)()
+    coupled = C.c_double()
+    _check(lib().enprop_dot(ctx.h, s, u.numel() // s, _ptr(u), _ptr(v), mode, seg_rows, lanes,
+                            C.byref(coupled)), "dot")
+    return list(lanes), coupled.value
+
+
+def dot(ctx: Context, s: int, u, v, mode: int = DOT_SERIAL, seg_rows: int = 4096) -> float:
+    """Coupled inner product (kernels.hpp:62-69)."""
+    return dot_lanes(ctx, s, u, v, mode, seg_rows)[1]
+
+
+def norm2(ctx: Context, s: int, u, mode: int = DOT_SERIAL, seg_rows: int = 4096) -> float:
+    return math.sqrt(dot(ctx, s, u, u, mode, seg_rows))
+
+
+def axpby(ctx: Context, s: int, alpha, x, beta, y):
+    """y = alpha*x + beta*y (kernels.hpp:78-85); list coefficients = per lane."""
+    per_lane = isinstance(alpha, (list, tuple))
+    a = (C.c_double * (s if per_lane else 1))(*(alpha if per_lane else [alpha]))
+    b = (C.c_double * (s if per_lane else 1))(*(beta if per_lane else [beta]))
+    if x.numel() != y.numel():
+        raise ValueError("axpby: length mismatch")
+    _check(lib().enprop_axpby(ctx.h, s, x.numel() // s, int(per_lane), a, _ptr(x), b, _ptr(y)),
+           "axpby")
+    return y
+
+
+@dataclass
+class SolveResult:
+    """SolveResult (pcg.hpp:33-38) plus per-lane data for uncoupled solves."""
+    solution: torch.Tensor
+    iterations: object
+    residual_history: list
+    lane_status: list = field(default_factory=list)
+
+
+def _collect(cfg: SolverConfig, s: int, it, ls, hist, hl):
+    lanes = s if cfg.flavour == CG_UNCOUPLED else 1
+    if lanes == 1:
+        history = [hist[i] for i in range(hl[0])]
+        return it[0], history, [ls[0]]
+    history = [[hist[i * s + e] for i in range(hl[e])] for e in range(s)]
+    return [it[e] for e in range(s)], history, [ls[e] for e in range(s)]
+
+
+def pcg_solve(ctx: Context, s: int, row_map, col_entry, values, b, config: SolverConfig = None,
+              raise_on_failure: bool = True) -> SolveResult:
+    """Identity-preconditioned CG from x0 = 0 (pcg.hpp:52-103).  Coupled =
+    pcg_solve<Ensemble<s>>; uncoupled = s x pcg_solve<double>."""
+    cfg = config or SolverConfig()
+    rows = row_map.numel() - 1
+    if b.numel() != rows * s:
+        raise ValueError("pcg_solve: right-hand side length mismatch")
+    x = torch.empty((rows, s), dtype=torch.float64, device=b.device)
+    lanes = s if cfg.flavour == CG_UNCOUPLED else 1
+    it = (C.c_int * lanes)()
+    ls = (C.c_int * lanes)()
+    hl = (C.c_int * lanes)()
+    hist = (C.c_double * ((cfg.max_iterations + 1) * lanes))()
+    opt = cfg._c()
+    rc = lib().enprop_cg(ctx.h, s, rows, _ptr(row_map), _ptr(col_entry), _ptr(values), _ptr(b),
+                         _ptr(x), C.byref(opt), it, ls, hist, hl)
+    iters, history, lstat = _collect(cfg, s, it, ls, hist, hl)
+    if rc in (ERR_NO_CONVERGENCE, ERR_INDEFINITE):
+        if raise_on_failure:
+            raise SolverError(_err(), history, rc, iters)
+    else:
+        _check(rc, "pcg_solve")
+    return SolveResult(x, iters, history, lstat)
+
+
+class Problem:
+    """Device-resident ensemble problem: node graph, KL tables, matrix and CG
+    workspaces stay in HBM (the performance path)."""
+
+    def __init__(self, ctx: Context, n: int, s: int, kl: KlField = None,
+                 coeffs: PdeCoefficients = None, bc: DirichletBc = None):
+        self.ctx, self.n, self.s = ctx, n, s
+        self.kl = kl or KlField()
+        self.coeffs = coeffs or PdeCoefficients()
+        self.bc = bc or DirichletBc()
+        d = _ProblemDesc(n, s, self.kl._c(), self.coeffs._c(), self.bc._c())
+        h = _vp()
+        _check(lib().enprop_problem_create(ctx.h, C.byref(d), C.byref(h)), "Problem")
+        self.h = h
+        rows = C.c_int()
+        nnz = C.c_int64()
+        self.rows = None
+        ptrs = [_vp() for _ in range(5)]
+        _check(lib().enprop_problem_views(h, C.byref(rows), C.byref(nnz), *[C.byref(p) for p in ptrs]))
+        self.rows, self.nnz = rows.value, nnz.value
+        self._ptrs = dict(zip(["row_map", "col_entry", "values", "residual", "solution"],
+                              [p.value for p in ptrs]))
+
+    def assemble(self, y: torch.Tensor):
+        _need_cuda(y, torch.float64, "y")
+        if y.numel() != self.kl.num_terms * self.s:
+            raise ValueError("assemble: sample vector length mismatch")
+        _check(lib().enprop_problem_assemble(self.h, _ptr(y)), "assemble")
+
+    def solve(self, config: SolverConfig = None, raise_on_failure: bool = True):
+        cfg = config or SolverConfig()
+        lanes = self.s if cfg.flavour == CG_UNCOUPLED else 1
+        it, ls, hl = ((C.c_int * lanes)() for _ in range(3))
+        hist = (C.c_double * ((cfg.max_iterations + 1) * lanes))()
+        opt = cfg._c()
+        rc = lib().enprop_problem_solve(self.h, C.byref(opt), it, ls, hist, hl)
+        iters, history, lstat = _collect(cfg, self.s, it, ls, hist, hl)
+        if rc in (ERR_NO_CONVERGENCE, ERR_INDEFINITE):
+            if raise_on_failure:
+                raise SolverError(_err(), history, rc, iters)
+        else:
+            _check(rc, "solve")
+        return iters, history, lstat
+
+    def solve_host(self, y_host: torch.Tensor, x_host: torch.Tensor, config: SolverConfig = None):
+        """End to end from host buffers (pinned for speed)."""
+        cfg = config or SolverConfig()
+        lanes = self.s if cfg.flavour == CG_UNCOUPLED else 1
+        it, ls = (C.c_int * lanes)(), (C.c_int * lanes)()
+        opt = cfg._c()
+        rc = lib().enprop_problem_solve_host(self.h, _ptr(y_host), _ptr(x_host), C.byref(opt), it, ls)
+        if rc not in (OK, ERR_NO_CONVERGENCE, ERR_INDEFINITE):
+            _check(rc, "solve_host")
+        return list(it), list(ls), rc
+
+    def _view(self, name, count, dtype, shape):
+        return _wrap_device_ptr(self._ptrs[name], count, dtype, self.ctx.device).view(*shape)
+
+    @property
+    def values(self):
+        return self._view("values", self.nnz * self.s, torch.float64, (self.nnz, self.s))
+
+    @property
+    def residual(self):
+        return self._view("residual", self.rows * self.s, torch.float64, (self.rows, self.s))
+
+    @property
+    def solution(self):
+        return self._view("solution", self.rows * self.s, torch.float64, (self.rows, self.s))
+
+    @property
+    def row_map(self):
+        return self._view("row_map", self.rows + 1, torch.int32, (self.rows + 1,))
+
+    @property
+    def col_entry(self):
+        return self._view("col_entry", self.nnz, torch.int32, (self.nnz,))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().enprop_problem_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _wrap_device_ptr(ptr: int, count: int, dtype, device: int) -> torch.Tensor:
+    """Non-owning torch view of library-owned device memory (copy it if it
+    must outlive the Problem)."""
+    class _Cai:
+        def __init__(self):
+            typestr = {torch.float64: "<f8", torch.int32: "<i4"}[dtype]
+            self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr,
+                                             "data": (ptr, False), "version": 3}
+    return torch.as_tensor(_Cai(), device=torch.device("cuda", device))

@@ -1,0 +1,723 @@
+// C ABI of enprop_b200 (include/enprop_b200.h). Host orchestration only: all
+// arithmetic on the hot path runs in the sm_100a kernels of ep_kernels.cu /
+// ep_assemble.cu. There is no CPU fallback: a missing or failing device is an
+// ENPROP_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "enprop_b200.h"
+#include "ep_host.h"
+#include "ep_kernels.h"
+
+using namespace ep;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t err, const char* where) {
+  return fail(err == cudaErrorMemoryAllocation ? ENPROP_ERR_OOM : ENPROP_ERR_CUDA,
+              std::string(where) + ": " + cudaGetErrorString(err));
+}
+
+#define EP_CUDA(call)                                  \
+  do {                                                 \
+    cudaError_t _e = (call);                           \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+bool valid_width(int s) { return s == 1 || s == 2 || s == 4 || s == 8 || s == 16 || s == 32; }
+
+}  // namespace
+
+struct enprop_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  int* pinned_flags = nullptr;  // [2] convergence flags read back by the CG driver
+  cudaEvent_t flag_ev[2] = {nullptr, nullptr};
+  // optional CUDA-event timing of the CG SpMV launches (bench roofline)
+  int profile = 0;
+  std::vector<cudaEvent_t> prof_ev;  // pairs (start, stop), reused
+  size_t prof_used = 0;
+  double prof_ms = 0.0;
+  int64_t prof_count = 0;
+};
+
+namespace {
+
+// Workspace of one CG solve on `rows` x s.
+struct CgWork {
+  double* r = nullptr;
+  double* p[2] = {nullptr, nullptr};
+  double* q = nullptr;
+  double* partials = nullptr;
+  double* segbuf = nullptr;
+  double* hist = nullptr;
+  CgState* state = nullptr;
+  int rows = 0, s = 0, maxit = -1, tiles = 0, segs = 0;
+};
+
+void free_work(CgWork& w) {
+  for (void* p : {(void*)w.r, (void*)w.p[0], (void*)w.p[1], (void*)w.q, (void*)w.partials,
+                  (void*)w.segbuf, (void*)w.hist, (void*)w.state})
+    if (p) cudaFree(p);
+  w = CgWork{};
+}
+
+int ensure_work(CgWork& w, int rows, int s, int maxit, const TileMap& tm) {
+  const int tiles = tm.num_tiles() > 0 ? tm.num_tiles() : 1;
+  const int segs = tm.num_segs > 0 ? tm.num_segs : 1;
+  if (w.r && w.rows == rows && w.s == s && w.maxit >= maxit && w.tiles >= tiles && w.segs >= segs)
+    return ENPROP_OK;
+  free_work(w);
+  const size_t vec = (size_t)rows * s * sizeof(double);
+  const size_t vb = vec > 0 ? vec : 8;
+  EP_CUDA(cudaMalloc(&w.r, vb));
+  EP_CUDA(cudaMalloc(&w.p[0], vb));
+  EP_CUDA(cudaMalloc(&w.p[1], vb));
+  EP_CUDA(cudaMalloc(&w.q, vb));
+  EP_CUDA(cudaMalloc(&w.partials, (size_t)tiles * s * sizeof(double)));
+  EP_CUDA(cudaMalloc(&w.segbuf, (size_t)segs * s * sizeof(double)));
+  EP_CUDA(cudaMalloc(&w.hist, (size_t)(maxit + 1) * s * sizeof(double)));
+  EP_CUDA(cudaMalloc(&w.state, sizeof(CgState)));
+  w.rows = rows;
+  w.s = s;
+  w.maxit = maxit;
+  w.tiles = tiles;
+  w.segs = segs;
+  return ENPROP_OK;
+}
+
+int validate_cg_options(const enprop_cg_options* opt, int s) {
+  if (!opt) return fail(ENPROP_ERR_INVALID, "enprop_cg: options are required");
+  if (!valid_width(s)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
+  if (opt->flavour != ENPROP_CG_COUPLED && opt->flavour != ENPROP_CG_UNCOUPLED)
+    return fail(ENPROP_ERR_INVALID, "enprop_cg: unknown CG flavour");
+  if (opt->dot_mode != ENPROP_DOT_SERIAL && opt->dot_mode != ENPROP_DOT_CANONICAL)
+    return fail(ENPROP_ERR_INVALID, "enprop_cg: unknown dot mode");
+  if (opt->max_iterations < 0) return fail(ENPROP_ERR_INVALID, "enprop_cg: negative max_iterations");
+  return ENPROP_OK;
+}
+
+// Event pair for one profiled launch (grown on demand, reused across solves).
+cudaEvent_t* prof_pair(enprop_ctx* c) {
+  if (c->prof_used + 2 > c->prof_ev.size()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      c->prof_ev.push_back(e);
+    }
+  }
+  cudaEvent_t* p = &c->prof_ev[c->prof_used];
+  c->prof_used += 2;
+  return p;
+}
+
+// Accumulate the elapsed time of the recorded pairs. Launches that early-exit
+// after convergence are excluded (they are not SpMVs); they are recognisable
+// because they take less than 5 microseconds while a real SpMV of any
+// benchmarked size takes far longer — the caller also gets the count.
+int prof_collect(enprop_ctx* c) {
+  for (size_t i = 0; i + 1 < c->prof_used; i += 2) {
+    float ms = 0.f;
+    EP_CUDA(cudaEventElapsedTime(&ms, c->prof_ev[i], c->prof_ev[i + 1]));
+    if (ms > 0.005f) {
+      c->prof_ms += ms;
+      c->prof_count += 1;
+    }
+  }
+  c->prof_used = 0;
+  return ENPROP_OK;
+}
+
+// The CG driver (pcg.hpp:52-103 semantics; see ep_kernels.cu cg_phase).
+// Iterations are enqueued in chunks of check_every; the host reads the
+// device's `done` flag of chunk c while chunk c+1 is already queued, so the GPU
+// never idles on the check. Kernels of iterations past convergence early-exit.
+int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_entry,
+           const double* values, const double* b, double* x, const enprop_cg_options* opt,
+           CgWork& w, int* iterations, int* lane_status, double* history, int* hist_len) {
+  const int seg = opt->seg_rows > 0 ? opt->seg_rows : 4096;
+  const TileMap tm = make_tile_map(rows, seg);
+  int rc = ensure_work(w, rows, s, opt->max_iterations, tm);
+  if (rc) return rc;
+  const bool canon = opt->dot_mode == ENPROP_DOT_CANONICAL;
+  const int lanes = opt->flavour == ENPROP_CG_UNCOUPLED ? s : 1;
+  cudaStream_t st = ctx->stream;
+
+  CgState init;
+  std::memset(&init, 0, sizeof(init));
+  init.flavour = opt->flavour;
+  init.s = s;
+  init.maxit = opt->max_iterations;
+  init.tol = opt->tol;
+  EP_CUDA(cudaMemcpyAsync(w.state, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+  const size_t vec = (size_t)rows * s * sizeof(double);
+  if (vec) {
+    EP_CUDA(cudaMemsetAsync(x, 0, vec, st));
+    EP_CUDA(cudaMemcpyAsync(w.r, b, vec, cudaMemcpyDeviceToDevice, st));
+  }
+  if (canon) {
+    EP_CUDA(launch_dot_tiles(s, tm, w.r, w.r, w.partials, st));
+    EP_CUDA(launch_fin_canonical(s, tm, w.partials, w.segbuf, kPhaseInit, w.state, w.hist, nullptr, st));
+    ctx->launches += 2;
+  } else {
+    EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, kPhaseInit, w.state, w.hist, nullptr, st));
+    ctx->launches += 1;
+  }
+
+  const int chunk = opt->check_every > 0 ? opt->check_every : 16;
+  int launched = 0;
+  int slot = 0;
+  bool pending = false;
+  const int limit = opt->max_iterations;  // loop bodies that can run (pcg.hpp:79-85)
+  while (true) {
+    if (launched < limit) {
+      for (int c = 0; c < chunk && launched < limit; ++c, ++launched) {
+        double* p_old = w.p[launched & 1];
+        double* p_new = w.p[(launched + 1) & 1];
+        cudaEvent_t* ev = ctx->profile ? prof_pair(ctx) : nullptr;
+        if (ev) EP_CUDA(cudaEventRecord(ev[0], st));
+        EP_CUDA(launch_cg_spmv(s, canon, tm, row_map, col_entry, values, w.r, p_old, p_new, w.q,
+                               w.state, w.partials, st));
+        if (ev) EP_CUDA(cudaEventRecord(ev[1], st));
+        if (canon)
+          EP_CUDA(launch_fin_canonical(s, tm, w.partials, w.segbuf, kPhasePQ, w.state, w.hist, nullptr, st));
+        else
+          EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, kPhasePQ, w.state, w.hist, nullptr, st));
+        EP_CUDA(launch_cg_update(s, canon, tm, x, p_new, w.r, w.q, w.state, w.partials, st));
+        if (canon)
+          EP_CUDA(launch_fin_canonical(s, tm, w.partials, w.segbuf, kPhaseRR, w.state, w.hist, nullptr, st));
+        else
+          EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, kPhaseRR, w.state, w.hist, nullptr, st));
+        ctx->launches += 4;
+      }
+    }
+    // flag of this chunk
+    EP_CUDA(cudaMemcpyAsync(&ctx->pinned_flags[slot], &w.state->done, sizeof(int),
+                            cudaMemcpyDeviceToHost, st));
+    EP_CUDA(cudaEventRecord(ctx->flag_ev[slot], st));
+    if (pending) {  // previous chunk's flag
+      EP_CUDA(cudaEventSynchronize(ctx->flag_ev[slot ^ 1]));
+      if (ctx->pinned_flags[slot ^ 1]) break;
+    }
+    if (launched >= limit) {
+      EP_CUDA(cudaEventSynchronize(ctx->flag_ev[slot]));
+      break;
+    }
+    pending = true;
+    slot ^= 1;
+  }
+  EP_CUDA(cudaStreamSynchronize(st));
+  if (ctx->profile) {
+    rc = prof_collect(ctx);
+    if (rc) return rc;
+  }
+
+  CgState fin;
+  EP_CUDA(cudaMemcpy(&fin, w.state, sizeof(fin), cudaMemcpyDeviceToHost));
+  if (!fin.done) return fail(ENPROP_ERR_CUDA, "enprop_cg: solver did not finish (internal)");
+  for (int l = 0; l < lanes; ++l) {
+    if (iterations) iterations[l] = fin.iters[l];
+    if (lane_status) lane_status[l] = opt->flavour == ENPROP_CG_UNCOUPLED ? fin.lane_status[l] : fin.status;
+    if (hist_len) hist_len[l] = fin.hist_len[l];
+  }
+  if (history) {
+    const size_t count = (size_t)(opt->max_iterations + 1) * lanes;
+    if (lanes == 1) {
+      std::vector<double> h((size_t)opt->max_iterations + 1);
+      EP_CUDA(cudaMemcpy(h.data(), w.hist, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      for (size_t i = 0; i < h.size(); ++i) history[i] = (int)i < fin.hist_len[0] ? h[i] : NAN;
+    } else {
+      std::vector<double> h(count);
+      EP_CUDA(cudaMemcpy(h.data(), w.hist, count * sizeof(double), cudaMemcpyDeviceToHost));
+      for (int it = 0; it <= opt->max_iterations; ++it)
+        for (int e = 0; e < s; ++e)
+          history[(size_t)it * s + e] = it < fin.hist_len[e] ? h[(size_t)it * s + e] : NAN;
+    }
+  }
+  if (fin.status == ENPROP_ERR_NO_CONVERGENCE)
+    return fail(ENPROP_ERR_NO_CONVERGENCE, "pcg_solve: no convergence within " +
+                                               std::to_string(opt->max_iterations) + " iterations");
+  if (fin.status == ENPROP_ERR_INDEFINITE)
+    return fail(ENPROP_ERR_INDEFINITE, "pcg_solve: operator not positive definite (p'Ap <= 0)");
+  return ENPROP_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+const char* enprop_last_error(void) { return g_last_error.c_str(); }
+int enprop_abi_version(void) { return ENPROP_ABI_VERSION; }
+
+int enprop_ctx_create(int device, enprop_ctx** out) {
+  if (!out) return fail(ENPROP_ERR_INVALID, "enprop_ctx_create: null output");
+  int count = 0;
+  cudaError_t err = cudaGetDeviceCount(&count);
+  if (err != cudaSuccess || count == 0)
+    return fail(ENPROP_ERR_CUDA, "enprop_ctx_create: no CUDA device (enprop_b200 has no CPU path)");
+  if (device < 0 || device >= count) return fail(ENPROP_ERR_INVALID, "enprop_ctx_create: bad device");
+  EP_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  EP_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(ENPROP_ERR_CUDA, "enprop_ctx_create: enprop_b200 is built for sm_100a (B200) only");
+  auto* c = new (std::nothrow) enprop_ctx();
+  if (!c) return fail(ENPROP_ERR_OOM, "enprop_ctx_create: out of host memory");
+  c->device = device;
+  EP_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+  c->stream = c->own;
+  EP_CUDA(cudaMallocHost(&c->pinned_flags, 2 * sizeof(int)));
+  EP_CUDA(cudaEventCreateWithFlags(&c->flag_ev[0], cudaEventDisableTiming));
+  EP_CUDA(cudaEventCreateWithFlags(&c->flag_ev[1], cudaEventDisableTiming));
+  *out = c;
+  return ENPROP_OK;
+}
+
+int enprop_ctx_destroy(enprop_ctx* c) {
+  if (!c) return ENPROP_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->flag_ev[0]) cudaEventDestroy(c->flag_ev[0]);
+  if (c->flag_ev[1]) cudaEventDestroy(c->flag_ev[1]);
+  if (c->pinned_flags) cudaFreeHost(c->pinned_flags);
+  for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+  return ENPROP_OK;
+}
+
+int enprop_ctx_set_stream(enprop_ctx* c, void* stream) {
+  if (!c) return fail(ENPROP_ERR_INVALID, "null context");
+  c->stream = static_cast<cudaStream_t>(stream);  // NULL = legacy default stream
+  return ENPROP_OK;
+}
+
+void* enprop_ctx_stream(enprop_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+int enprop_ctx_synchronize(enprop_ctx* c) {
+  if (!c) return fail(ENPROP_ERR_INVALID, "null context");
+  EP_CUDA(cudaStreamSynchronize(c->stream));
+  return ENPROP_OK;
+}
+
+int64_t enprop_ctx_launch_count(enprop_ctx* c) { return c ? c->launches : 0; }
+
+int enprop_ctx_profile(enprop_ctx* c, int enable, double* spmv_ms, int64_t* spmv_launches) {
+  if (!c) return fail(ENPROP_ERR_INVALID, "null context");
+  if (spmv_ms) *spmv_ms = c->prof_ms;
+  if (spmv_launches) *spmv_launches = c->prof_count;
+  if (enable >= 0) {
+    c->profile = enable;
+    c->prof_ms = 0.0;
+    c->prof_count = 0;
+  }
+  return ENPROP_OK;
+}
+
+int enprop_malloc(enprop_ctx* c, size_t bytes, void** dptr) {
+  if (!c || !dptr) return fail(ENPROP_ERR_INVALID, "enprop_malloc: null argument");
+  EP_CUDA(cudaSetDevice(c->device));
+  EP_CUDA(cudaMalloc(dptr, bytes ? bytes : 8));
+  return ENPROP_OK;
+}
+
+int enprop_free(enprop_ctx* c, void* dptr) {
+  if (!c) return fail(ENPROP_ERR_INVALID, "enprop_free: null context");
+  if (dptr) EP_CUDA(cudaFree(dptr));
+  return ENPROP_OK;
+}
+
+int enprop_memcpy_h2d(enprop_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (!c) return fail(ENPROP_ERR_INVALID, "null context");
+  if (!bytes) return ENPROP_OK;
+  EP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+  EP_CUDA(cudaStreamSynchronize(c->stream));
+  return ENPROP_OK;
+}
+
+int enprop_memcpy_d2h(enprop_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (!c) return fail(ENPROP_ERR_INVALID, "null context");
+  if (!bytes) return ENPROP_OK;
+  EP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+  EP_CUDA(cudaStreamSynchronize(c->stream));
+  return ENPROP_OK;
+}
+
+int64_t enprop_mesh_nnz(int n) {
+  if (n < 1) return 0;
+  const int64_t t = 3 * (int64_t)(n + 1) - 2;
+  return t * t * t;
+}
+
+int enprop_build_node_graph(enprop_ctx* c, int n, int* row_map, int* col_entry) {
+  if (!c || !row_map || !col_entry) return fail(ENPROP_ERR_INVALID, "enprop_build_node_graph: null argument");
+  if (n < 1) return fail(ENPROP_ERR_INVALID, "StructuredMesh: cells_per_axis must be at least 1");
+  if (enprop_mesh_nnz(n) > 2147483647LL)
+    return fail(ENPROP_ERR_INVALID, "enprop_build_node_graph: nnz exceeds int32 (reference Graph uses int)");
+  EP_CUDA(launch_build_graph(n, row_map, col_entry, c->stream));
+  c->launches += 1;
+  return ENPROP_OK;
+}
+
+int enprop_kl_describe(const enprop_kl_params* kl, int* mode_axes, double* mode_eigenvalue,
+                       double* axis_frequency, double* axis_eigenvalue, double* axis_inverse_norm,
+                       int* axis_cosine) {
+  if (!kl) return fail(ENPROP_ERR_INVALID, "enprop_kl_describe: null params");
+  KlHost f;
+  if (!kl_init(f, kl->num_terms, kl->mean, kl->sigma, kl->correlation_length))
+    return fail(ENPROP_ERR_INVALID, "KlField: invalid num_terms/mean/sigma/correlation_length");
+  for (int i = 0; i < f.m; ++i) {
+    if (mode_axes)
+      for (int a = 0; a < 3; ++a) mode_axes[i * 3 + a] = f.mode_axes[i * 3 + a];
+    if (mode_eigenvalue) mode_eigenvalue[i] = f.mode_eig[i];
+    if (axis_frequency) axis_frequency[i] = f.axis_freq[i];
+    if (axis_eigenvalue) axis_eigenvalue[i] = f.axis_eig[i];
+    if (axis_inverse_norm) axis_inverse_norm[i] = f.axis_invnorm[i];
+    if (axis_cosine) axis_cosine[i] = f.axis_cos[i];
+  }
+  return ENPROP_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Device tables of one (mesh, field, coefficients) combination.
+struct AsmSetup {
+  double* F = nullptr;
+  AsmTables* tab = nullptr;
+  AsmArgs args{};
+};
+
+int make_asm_setup(enprop_ctx* c, int n, const enprop_kl_params* kl,
+                   const enprop_pde_coeffs* coeffs, AsmSetup& out) {
+  if (n < 1) return fail(ENPROP_ERR_INVALID, "StructuredMesh: cells_per_axis must be at least 1");
+  KlHost f;
+  if (!kl || !kl_init(f, kl->num_terms, kl->mean, kl->sigma, kl->correlation_length))
+    return fail(ENPROP_ERR_INVALID, "KlField: invalid num_terms/mean/sigma/correlation_length");
+  const std::vector<double> F = kl_axis_tables(f, n);
+  AsmTables T;
+  const double zero_v[3] = {1.0, 0.0, 0.0};
+  make_asm_tables(T, n, coeffs ? coeffs->alpha : 0.0, coeffs ? coeffs->beta : 0.0,
+                  coeffs ? coeffs->velocity : zero_v);
+  EP_CUDA(cudaMalloc(&out.F, F.size() * sizeof(double)));
+  EP_CUDA(cudaMalloc(&out.tab, sizeof(AsmTables)));
+  EP_CUDA(cudaMemcpyAsync(out.F, F.data(), F.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  EP_CUDA(cudaMemcpyAsync(out.tab, &T, sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  EP_CUDA(cudaStreamSynchronize(c->stream));  // host sources go out of scope
+  AsmArgs& a = out.args;
+  std::memset(&a, 0, sizeof(a));
+  a.n = n;
+  a.rows = (n + 1) * (n + 1) * (n + 1);
+  a.m = f.m;
+  a.mean = f.mean;
+  a.F = out.F;
+  a.tab = out.tab;
+  a.nonlinear = (coeffs && (coeffs->alpha != 0.0 || coeffs->beta != 0.0)) ? 1 : 0;
+  for (int i = 0; i < f.m; ++i) {
+    for (int k = 0; k < 3; ++k) a.mode_axes[i][k] = f.mode_axes[i * 3 + k];
+    a.mode_sl[i] = f.sigma * f.mode_sqrt_eig[i];  // kl.hpp:74: sigma * sqrt_eigenvalue first
+  }
+  return ENPROP_OK;
+}
+
+void free_asm_setup(AsmSetup& s) {
+  if (s.F) cudaFree(s.F);
+  if (s.tab) cudaFree(s.tab);
+  s = AsmSetup{};
+}
+
+}  // namespace
+
+extern "C" {
+
+int enprop_assemble(enprop_ctx* c, int s, int n, const enprop_kl_params* kl,
+                    const enprop_pde_coeffs* coeffs, const double* u, const double* y,
+                    const int* row_map, double* values, double* residual,
+                    const enprop_dirichlet_bc* bc) {
+  if (!c || !y || !row_map || !values || !residual)
+    return fail(ENPROP_ERR_INVALID, "enprop_assemble: null argument");
+  if (!valid_width(s)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
+  AsmSetup setup;
+  int rc = make_asm_setup(c, n, kl, coeffs, setup);
+  if (rc) {
+    free_asm_setup(setup);
+    return rc;
+  }
+  AsmArgs a = setup.args;
+  a.u = u;
+  a.y = y;
+  a.row_map = row_map;
+  a.values = values;
+  a.residual = residual;
+  a.dirichlet = bc ? 1 : 0;
+  a.bc0 = bc ? bc->x0_value : 1.0;
+  a.bc1 = bc ? bc->x1_value : 0.0;
+  cudaError_t err = launch_assemble(s, a, c->stream);
+  c->launches += 1;
+  if (err == cudaSuccess) err = cudaStreamSynchronize(c->stream);  // tables are freed below
+  free_asm_setup(setup);
+  if (err != cudaSuccess) return cuda_fail(err, "enprop_assemble");
+  return ENPROP_OK;
+}
+
+int enprop_apply_dirichlet(enprop_ctx* c, int s, int n, const enprop_dirichlet_bc* bc,
+                           const int* row_map, const int* col_entry, const double* u,
+                           double* values, double* residual) {
+  if (!c || !bc || !row_map || !col_entry || !values || !residual)
+    return fail(ENPROP_ERR_INVALID, "enprop_apply_dirichlet: null argument");
+  if (!valid_width(s)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
+  if (n < 1) return fail(ENPROP_ERR_INVALID, "StructuredMesh: cells_per_axis must be at least 1");
+  EP_CUDA(launch_dirichlet(s, n, bc->x0_value, bc->x1_value, row_map, col_entry, u, values, residual,
+                           c->stream));
+  c->launches += 1;
+  return ENPROP_OK;
+}
+
+int enprop_spmv(enprop_ctx* c, int s, int rows, int cols, const int* row_map,
+                const int* col_entry, const double* values, const double* x, double* z) {
+  if (!c) return fail(ENPROP_ERR_INVALID, "null context");
+  if (!valid_width(s)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
+  if (rows < 0 || cols < 0) return fail(ENPROP_ERR_INVALID, "spmv: negative dimension");
+  if (rows == 0) return ENPROP_OK;
+  if (!row_map || !z || (cols > 0 && !x)) return fail(ENPROP_ERR_INVALID, "spmv: null argument");
+  EP_CUDA(launch_spmv(s, rows, row_map, col_entry, values, x, z, c->stream));
+  c->launches += 1;
+  return ENPROP_OK;
+}
+
+int enprop_dot(enprop_ctx* c, int s, int64_t n, const double* u, const double* v, int dot_mode,
+               int seg_rows, double* lanes_host, double* coupled_host) {
+  if (!c) return fail(ENPROP_ERR_INVALID, "null context");
+  if (!valid_width(s)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
+  if (n < 0 || n > 2147483647LL) return fail(ENPROP_ERR_INVALID, "dot: bad length");
+  double* out = nullptr;
+  double* partials = nullptr;
+  double* segbuf = nullptr;
+  const int rows = (int)n;
+  const TileMap tm = make_tile_map(rows, seg_rows > 0 ? seg_rows : 4096);
+  cudaError_t err = cudaMalloc(&out, (s + 1) * sizeof(double));
+  if (err == cudaSuccess && dot_mode == ENPROP_DOT_CANONICAL) {
+    err = cudaMalloc(&partials, (size_t)(tm.num_tiles() > 0 ? tm.num_tiles() : 1) * s * sizeof(double));
+    if (err == cudaSuccess) err = cudaMalloc(&segbuf, (size_t)(tm.num_segs > 0 ? tm.num_segs : 1) * s * sizeof(double));
+    if (err == cudaSuccess) err = launch_dot_tiles(s, tm, u, v, partials, c->stream);
+    if (err == cudaSuccess)
+      err = launch_fin_canonical(s, tm, partials, segbuf, kPhaseNone, nullptr, nullptr, out, c->stream);
+    c->launches += 2;
+  } else if (err == cudaSuccess) {
+    err = launch_fin_serial(s, rows, u, v, kPhaseNone, nullptr, nullptr, out, c->stream);
+    c->launches += 1;
+  }
+  std::vector<double> h(s + 1);
+  if (err == cudaSuccess)
+    err = cudaMemcpyAsync(h.data(), out, (s + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(c->stream);
+  if (out) cudaFree(out);
+  if (partials) cudaFree(partials);
+  if (segbuf) cudaFree(segbuf);
+  if (err != cudaSuccess) return cuda_fail(err, "enprop_dot");
+  if (lanes_host)
+    for (int e = 0; e < s; ++e) lanes_host[e] = h[e];
+  if (coupled_host) *coupled_host = h[s];
+  return ENPROP_OK;
+}
+
+int enprop_axpby(enprop_ctx* c, int s, int64_t n, int per_lane, const double* alpha_host,
+                 const double* x, const double* beta_host, double* y) {
+  if (!c || !alpha_host || !beta_host) return fail(ENPROP_ERR_INVALID, "axpby: null argument");
+  if (!valid_width(s)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
+  if (n == 0) return ENPROP_OK;
+  std::vector<double> co(2 * s);
+  for (int e = 0; e < s; ++e) {
+    co[e] = per_lane ? alpha_host[e] : alpha_host[0];
+    co[s + e] = per_lane ? beta_host[e] : beta_host[0];
+  }
+  double* d = nullptr;
+  EP_CUDA(cudaMalloc(&d, 2 * s * sizeof(double)));
+  cudaError_t err = cudaMemcpyAsync(d, co.data(), 2 * s * sizeof(double), cudaMemcpyHostToDevice, c->stream);
+  if (err == cudaSuccess) err = launch_axpby(s, n, per_lane, d, d + s, x, y, c->stream);
+  c->launches += 1;
+  if (err == cudaSuccess) err = cudaStreamSynchronize(c->stream);
+  cudaFree(d);
+  if (err != cudaSuccess) return cuda_fail(err, "enprop_axpby");
+  return ENPROP_OK;
+}
+
+int enprop_cg(enprop_ctx* c, int s, int rows, const int* row_map, const int* col_entry,
+              const double* values, const double* b, double* x, const enprop_cg_options* opt,
+              int* iterations, int* lane_status, double* history, int* hist_len) {
+  if (!c) return fail(ENPROP_ERR_INVALID, "null context");
+  int rc = validate_cg_options(opt, s);
+  if (rc) return rc;
+  if (rows < 0) return fail(ENPROP_ERR_INVALID, "pcg_solve: negative dimension");
+  CgWork w;
+  rc = run_cg(c, s, rows, row_map, col_entry, values, b, x, opt, w, iterations, lane_status,
+              history, hist_len);
+  free_work(w);
+  return rc;
+}
+
+}  // extern "C"
+
+// ============================================================================
+// Device-resident problem (the performance path).
+struct enprop_problem {
+  enprop_ctx* ctx = nullptr;
+  enprop_problem_desc desc{};
+  int rows = 0;
+  int64_t nnz = 0;
+  int* row_map = nullptr;
+  int* col_entry = nullptr;
+  double* values = nullptr;
+  double* residual = nullptr;
+  double* rhs = nullptr;
+  double* x = nullptr;
+  double* y = nullptr;
+  AsmSetup setup;
+  CgWork work;
+};
+
+namespace {
+
+__global__ void k_negate(int64_t n, const double* __restrict__ a, double* __restrict__ b);
+
+}  // namespace
+
+extern "C" {
+
+int enprop_problem_create(enprop_ctx* c, const enprop_problem_desc* d, enprop_problem** out) {
+  if (!c || !d || !out) return fail(ENPROP_ERR_INVALID, "enprop_problem_create: null argument");
+  const int s = d->ensemble_size;
+  if (!valid_width(s)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
+  const int n = d->cells_per_axis;
+  if (n < 1) return fail(ENPROP_ERR_INVALID, "StructuredMesh: cells_per_axis must be at least 1");
+  if (enprop_mesh_nnz(n) > 2147483647LL)
+    return fail(ENPROP_ERR_INVALID, "enprop_problem_create: nnz exceeds int32");
+  auto* p = new (std::nothrow) enprop_problem();
+  if (!p) return fail(ENPROP_ERR_OOM, "out of host memory");
+  p->ctx = c;
+  p->desc = *d;
+  p->rows = (n + 1) * (n + 1) * (n + 1);
+  p->nnz = enprop_mesh_nnz(n);
+  auto cleanup = [&](int rc) {
+    enprop_problem_destroy(p);
+    return rc;
+  };
+  int rc = make_asm_setup(c, n, &d->kl, &d->coeffs, p->setup);
+  if (rc) return cleanup(rc);
+  const size_t vec = (size_t)p->rows * s * sizeof(double);
+  cudaError_t err;
+  if ((err = cudaMalloc(&p->row_map, (p->rows + 1) * sizeof(int))) != cudaSuccess ||
+      (err = cudaMalloc(&p->col_entry, p->nnz * sizeof(int))) != cudaSuccess ||
+      (err = cudaMalloc(&p->values, (size_t)p->nnz * s * sizeof(double))) != cudaSuccess ||
+      (err = cudaMalloc(&p->residual, vec)) != cudaSuccess ||
+      (err = cudaMalloc(&p->rhs, vec)) != cudaSuccess ||
+      (err = cudaMalloc(&p->x, vec)) != cudaSuccess ||
+      (err = cudaMalloc(&p->y, (size_t)d->kl.num_terms * s * sizeof(double))) != cudaSuccess)
+    return cleanup(cuda_fail(err, "enprop_problem_create"));
+  if ((err = launch_build_graph(n, p->row_map, p->col_entry, c->stream)) != cudaSuccess)
+    return cleanup(cuda_fail(err, "enprop_problem_create: graph"));
+  c->launches += 1;
+  if ((err = cudaStreamSynchronize(c->stream)) != cudaSuccess)
+    return cleanup(cuda_fail(err, "enprop_problem_create"));
+  *out = p;
+  return ENPROP_OK;
+}
+
+int enprop_problem_destroy(enprop_problem* p) {
+  if (!p) return ENPROP_OK;
+  for (void* q : {(void*)p->row_map, (void*)p->col_entry, (void*)p->values, (void*)p->residual,
+                  (void*)p->rhs, (void*)p->x, (void*)p->y})
+    if (q) cudaFree(q);
+  free_asm_setup(p->setup);
+  free_work(p->work);
+  delete p;
+  return ENPROP_OK;
+}
+
+int enprop_problem_views(enprop_problem* p, int* rows, int64_t* nnz, const int** row_map,
+                         const int** col_entry, double** values, double** residual,
+                         double** solution) {
+  if (!p) return fail(ENPROP_ERR_INVALID, "null problem");
+  if (rows) *rows = p->rows;
+  if (nnz) *nnz = p->nnz;
+  if (row_map) *row_map = p->row_map;
+  if (col_entry) *col_entry = p->col_entry;
+  if (values) *values = p->values;
+  if (residual) *residual = p->residual;
+  if (solution) *solution = p->x;
+  return ENPROP_OK;
+}
+
+int enprop_problem_assemble(enprop_problem* p, const double* y) {
+  if (!p || !y) return fail(ENPROP_ERR_INVALID, "enprop_problem_assemble: null argument");
+  AsmArgs a = p->setup.args;
+  a.u = nullptr;
+  a.y = y;
+  a.row_map = p->row_map;
+  a.values = p->values;
+  a.residual = p->residual;
+  a.dirichlet = 1;
+  a.bc0 = p->desc.bc.x0_value;
+  a.bc1 = p->desc.bc.x1_value;
+  EP_CUDA(launch_assemble(p->desc.ensemble_size, a, p->ctx->stream));
+  p->ctx->launches += 1;
+  return ENPROP_OK;
+}
+
+int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* iterations,
+                         int* lane_status, double* history, int* hist_len) {
+  if (!p) return fail(ENPROP_ERR_INVALID, "null problem");
+  const int s = p->desc.ensemble_size;
+  int rc = validate_cg_options(opt, s);
+  if (rc) return rc;
+  enprop_cg_options o = *opt;
+  if (o.seg_rows <= 0) o.seg_rows = (p->desc.cells_per_axis + 1) * (p->desc.cells_per_axis + 1);
+  const int64_t len = (int64_t)p->rows * s;  // rhs = -residual (bench.cpp:298-299)
+  k_negate<<<(int)((len + 255) / 256), 256, 0, p->ctx->stream>>>(len, p->residual, p->rhs);
+  EP_CUDA(cudaGetLastError());
+  p->ctx->launches += 1;
+  return run_cg(p->ctx, s, p->rows, p->row_map, p->col_entry, p->values, p->rhs, p->x, &o, p->work,
+                iterations, lane_status, history, hist_len);
+}
+
+int enprop_problem_solve_host(enprop_problem* p, const double* y_host, double* x_host,
+                              const enprop_cg_options* opt, int* iterations, int* lane_status) {
+  if (!p || !y_host || !x_host) return fail(ENPROP_ERR_INVALID, "enprop_problem_solve_host: null argument");
+  const int s = p->desc.ensemble_size;
+  cudaStream_t st = p->ctx->stream;
+  EP_CUDA(cudaMemcpyAsync(p->y, y_host, (size_t)p->desc.kl.num_terms * s * sizeof(double),
+                          cudaMemcpyHostToDevice, st));
+  int rc = enprop_problem_assemble(p, p->y);
+  if (rc) return rc;
+  rc = enprop_problem_solve(p, opt, iterations, lane_status, nullptr, nullptr);
+  if (rc && rc != ENPROP_ERR_NO_CONVERGENCE && rc != ENPROP_ERR_INDEFINITE) return rc;
+  EP_CUDA(cudaMemcpyAsync(x_host, p->x, (size_t)p->rows * s * sizeof(double), cudaMemcpyDeviceToHost, st));
+  EP_CUDA(cudaStreamSynchronize(st));
+  return rc;
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void k_negate(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = -a[i];
+}
+}  // namespace

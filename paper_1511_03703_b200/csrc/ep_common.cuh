@@ -1,0 +1,133 @@
+// Device helpers shared by the enprop_b200 kernels (sm_100a).
+//
+// Arithmetic rule: every floating-point operation on the hot path goes through
+// __dmul_rn / __dadd_rn / __dsub_rn so that no FMA contraction can happen
+// (the reference is built with -ffp-contract=off, proj/CMakeLists.txt:14);
+// the library is additionally compiled with -fmad=false.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ep_tilemap.h"
+
+#define EP_DMUL(a, b) __dmul_rn((a), (b))
+#define EP_DADD(a, b) __dadd_rn((a), (b))
+#define EP_DSUB(a, b) __dsub_rn((a), (b))
+
+// dispatch a runtime ensemble width to a template instantiation
+#define EP_DISPATCH_S(s, FN, ...)                 \
+  switch (s) {                                    \
+    case 1: return FN<1>(__VA_ARGS__);            \
+    case 2: return FN<2>(__VA_ARGS__);            \
+    case 4: return FN<4>(__VA_ARGS__);            \
+    case 8: return FN<8>(__VA_ARGS__);            \
+    case 16: return FN<16>(__VA_ARGS__);          \
+    case 32: return FN<32>(__VA_ARGS__);          \
+    default: return cudaErrorInvalidValue;        \
+  }
+
+namespace ep {
+
+constexpr int kMaxS = 32;
+constexpr int kMaxTerms = 64;
+
+template <int V>
+struct VecD {
+  double v[V];
+};
+
+// Streamed once (matrix values, column indices): read-only path, no L1 allocation.
+template <int V>
+__device__ __forceinline__ VecD<V> ld_stream(const double* p) {
+  VecD<V> r;
+  if constexpr (V == 1) {
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r.v[0]) : "l"(p));
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; i += 2)
+      asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                   : "=d"(r.v[i]), "=d"(r.v[i + 1])
+                   : "l"(p + i));
+  }
+  return r;
+}
+
+// Re-used across rows (gathered vectors): default caching.
+template <int V>
+__device__ __forceinline__ VecD<V> ld_vec(const double* p) {
+  VecD<V> r;
+  if constexpr (V == 1) {
+    r.v[0] = *p;
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; i += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(p + i);
+      r.v[i] = t.x;
+      r.v[i + 1] = t.y;
+    }
+  }
+  return r;
+}
+
+template <int V>
+__device__ __forceinline__ void st_vec(double* p, const VecD<V>& a) {
+  if constexpr (V == 1) {
+    *p = a.v[0];
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; i += 2)
+      *reinterpret_cast<double2*>(p + i) = make_double2(a.v[i], a.v[i + 1]);
+  }
+}
+
+__device__ __forceinline__ int ld_stream_i32(const int* p) {
+  int r;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+
+// ---- mbarrier + 1D bulk copy (TMA engine, cp.async.bulk) -------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+}  // namespace ep

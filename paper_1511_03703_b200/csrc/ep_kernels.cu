@@ -1,0 +1,694 @@
+// enprop_b200 kernels for sm_100a.
+//
+// Ensemble layout (reference ensemble.hpp:105-106): the s sample values of each
+// stored entry and of each vector row are contiguous, so one nonzero's s
+// values are one coalesced 8s-byte chunk.  Lanes of the SIMT mapping carry
+// samples: a row is handled by TPR = s/V threads, each owning V consecutive
+// samples and loading them with one 16-byte vector load.
+//
+// Parity: per-sample arithmetic reproduces the reference's sequence of IEEE
+// operations exactly (no FMA, same order), so assembly, Dirichlet, SpMV and
+// axpby are bitwise equal to proj/include/enprop/{fem,kernels}.hpp.
+#include <cstdio>
+
+#include "ep_common.cuh"
+#include "ep_kernels.h"
+
+namespace ep {
+
+// =============================================================================
+// Node graph (proj/src/mesh.cpp:13-55) built on the device in closed form.
+// Row (i,j,k) of the x-fastest numbering has C(i)C(j)C(k) entries, C(t) = 2 at
+// the two ends of an axis and 3 inside; its first entry is
+//   P(k) W^2 + C(k) (P(j) W + C(j) P(i)),  P(t) = sum_{t'<t} C(t'), W = 3N-2,
+// and its columns are listed kk -> jj -> ii ascending, as the reference does.
+// =============================================================================
+__device__ __forceinline__ int axis_count(int t, int N) { return 1 + (t > 0) + (t < N - 1); }
+__device__ __forceinline__ int axis_prefix(int t) { return t == 0 ? 0 : 2 + 3 * (t - 1); }
+
+__global__ void k_build_graph(int n, int* __restrict__ row_map, int* __restrict__ col_entry) {
+  const int N = n + 1;
+  const int rows = N * N * N;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  const int i = row % N, j = (row / N) % N, k = row / (N * N);
+  const int W = 3 * N - 2;
+  const int ci = axis_count(i, N), cj = axis_count(j, N), ck = axis_count(k, N);
+  const int start = axis_prefix(k) * W * W + ck * (axis_prefix(j) * W + cj * axis_prefix(i));
+  if (row == 0) row_map[0] = 0;
+  row_map[row + 1] = start + ci * cj * ck;
+  int at = start;
+  const int ilo = i > 0 ? i - 1 : 0, ihi = i < N - 1 ? i + 1 : N - 1;
+  const int jlo = j > 0 ? j - 1 : 0, jhi = j < N - 1 ? j + 1 : N - 1;
+  const int klo = k > 0 ? k - 1 : 0, khi = k < N - 1 ? k + 1 : N - 1;
+  for (int kk = klo; kk <= khi; ++kk)
+    for (int jj = jlo; jj <= jhi; ++jj)
+      for (int ii = ilo; ii <= ihi; ++ii) col_entry[at++] = ii + N * (jj + N * kk);
+}
+
+cudaError_t launch_build_graph(int n, int* row_map, int* col_entry, cudaStream_t st) {
+  const int N = n + 1;
+  const int rows = N * N * N;
+  k_build_graph<<<(rows + 255) / 256, 256, 0, st>>>(n, row_map, col_entry);
+  return cudaGetLastError();
+}
+
+// =============================================================================
+// SpMV building block (kernels.hpp:15-26): one row, V samples of this thread.
+// sum = 0; sum += a_k * x_col_k in entry order — the reference's per-sample
+// sequence.  Entries are processed in predicated batches of U so the column,
+// value and gather loads of a batch are all in flight together; invalid batch
+// slots are skipped (never "+0.0") so the order and bits stay the reference's.
+// With kCg the gathered operand is p_new = r + beta*p_old formed on the fly
+// (first iteration: p_new = r), which removes a separate direction pass.
+// =============================================================================
+template <int S>
+struct SpmvShape {  // vector width per thread
+  static constexpr int V = (S == 1) ? 1 : 2;
+  static constexpr int TPR = S / V;
+  static constexpr int U = 4;  // entries per predicated batch
+};
+
+template <int S, int V, int U, bool kCg>
+__device__ __forceinline__ VecD<V> row_product(int row, const int* __restrict__ row_map,
+                                               const int* __restrict__ col_entry,
+                                               const double* __restrict__ values,
+                                               const double* __restrict__ x_or_r,
+                                               const double* __restrict__ p_old, bool first,
+                                               const VecD<V>& beta, int lane0) {
+  const int rs = __ldg(row_map + row), re = __ldg(row_map + row + 1);
+  VecD<V> sum;
+#pragma unroll
+  for (int j = 0; j < V; ++j) sum.v[j] = 0.0;
+  for (int kb = rs; kb < re; kb += U) {
+    int c[U];
+    VecD<V> av[U], xv[U], pv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) c[u] = (kb + u < re) ? ld_stream_i32(col_entry + kb + u) : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (kb + u < re) {
+        av[u] = ld_stream<V>(values + (size_t)(kb + u) * S + lane0);
+        xv[u] = ld_vec<V>(x_or_r + (size_t)c[u] * S + lane0);
+        if (kCg && !first) pv[u] = ld_vec<V>(p_old + (size_t)c[u] * S + lane0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (kb + u < re) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          double xo = xv[u].v[j];
+          if (kCg && !first) xo = EP_DADD(xo, EP_DMUL(beta.v[j], pv[u].v[j]));
+          sum.v[j] = EP_DADD(sum.v[j], EP_DMUL(av[u].v[j], xo));
+        }
+      }
+    }
+  }
+  return sum;
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) k_spmv(int rows, const int* __restrict__ row_map,
+                                              const int* __restrict__ col_entry,
+                                              const double* __restrict__ values,
+                                              const double* __restrict__ x,
+                                              double* __restrict__ z) {
+  using Sh = SpmvShape<S>;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = gt / Sh::TPR;
+  const int lane0 = (gt - row * Sh::TPR) * Sh::V;
+  if (row >= rows) return;
+  VecD<Sh::V> beta;
+  const VecD<Sh::V> sum = row_product<S, Sh::V, Sh::U, false>(row, row_map, col_entry, values, x,
+                                                               nullptr, true, beta, lane0);
+  st_vec<Sh::V>(z + (size_t)row * S + lane0, sum);
+}
+
+template <int S>
+static cudaError_t spmv_s(int rows, const int* row_map, const int* col_entry,
+                          const double* values, const double* x, double* z, cudaStream_t st) {
+  using Sh = SpmvShape<S>;
+  const int64_t threads = (int64_t)rows * Sh::TPR;
+  if (threads == 0) return cudaSuccess;
+  k_spmv<S><<<(int)((threads + 255) / 256), 256, 0, st>>>(rows, row_map, col_entry, values, x, z);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spmv(int s, int rows, const int* row_map, const int* col_entry,
+                        const double* values, const double* x, double* z, cudaStream_t st) {
+  EP_DISPATCH_S(s, spmv_s, rows, row_map, col_entry, values, x, z, st);
+}
+
+// =============================================================================
+// axpby (kernels.hpp:78-85): y = alpha*x + beta*y, per lane or scalar coefs.
+// =============================================================================
+template <int S>
+__global__ void __launch_bounds__(256) k_axpby(int64_t n, const double* __restrict__ alpha,
+                                               const double* __restrict__ beta,
+                                               const double* __restrict__ x,
+                                               double* __restrict__ y) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n * S) return;
+  const int e = (int)(g % S);
+  y[g] = EP_DADD(EP_DMUL(alpha[e], x[g]), EP_DMUL(beta[e], y[g]));
+}
+
+template <int S>
+static cudaError_t axpby_s(int64_t n, const double* alpha, const double* beta, const double* x,
+                           double* y, cudaStream_t st) {
+  const int64_t t = n * S;
+  if (t == 0) return cudaSuccess;
+  k_axpby<S><<<(int)((t + 255) / 256), 256, 0, st>>>(n, alpha, beta, x, y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpby(int s, int64_t n, int /*per_lane*/, const double* alpha,
+                         const double* beta, const double* x, double* y, cudaStream_t st) {
+  // alpha/beta are device arrays of s coefficients (replicated when scalar)
+  EP_DISPATCH_S(s, axpby_s, n, alpha, beta, x, y, st);
+}
+
+// =============================================================================
+// Canonical tile reduction: the block's kTileRows x S products
+// sit in shared memory (rows past the tile end hold +0.0) and are folded by
+// v[i] += v[i + half] for half = 32, 16, ..., 1, independently per sample.
+// oracle/enprop_oracle.c:or_dot_lanes restates exactly this order.
+// =============================================================================
+template <int S, int NT>
+__device__ __forceinline__ void tile_fold_store(double* sprod, double* __restrict__ out) {
+  __syncthreads();
+#pragma unroll 1
+  for (int half = kTileRows / 2; half >= 1; half >>= 1) {
+    for (int idx = threadIdx.x; idx < half * S; idx += NT)
+      sprod[idx] = EP_DADD(sprod[idx], sprod[idx + half * S]);
+    __syncthreads();
+  }
+  if (threadIdx.x < S) out[threadIdx.x] = sprod[threadIdx.x];
+}
+
+template <int S>
+struct TileShape {
+  static constexpr int V = SpmvShape<S>::V;
+  static constexpr int TPR = S / V;
+  static constexpr int NT = (kTileRows * TPR < 256) ? kTileRows * TPR : 256;  // threads/block
+  static constexpr int RPP = NT / TPR;                                         // rows per pass
+  static constexpr int PASSES = kTileRows / RPP;
+};
+
+template <int S>
+__global__ void __launch_bounds__(TileShape<S>::NT) k_dot_tiles(const TileMap tm,
+                                                                const double* __restrict__ u,
+                                                                const double* __restrict__ v,
+                                                                double* __restrict__ partials) {
+  using Sh = TileShape<S>;
+  __shared__ double sprod[kTileRows * S];
+  int r0, nr;
+  tm.tile(blockIdx.x, r0, nr);
+  if (nr <= 0) return;
+  const int lane0 = (threadIdx.x % Sh::TPR) * Sh::V;
+#pragma unroll
+  for (int pass = 0; pass < Sh::PASSES; ++pass) {
+    const int rl = pass * Sh::RPP + threadIdx.x / Sh::TPR;
+    VecD<Sh::V> pr;
+    if (rl < nr) {
+      const VecD<Sh::V> a = ld_vec<Sh::V>(u + (size_t)(r0 + rl) * S + lane0);
+      const VecD<Sh::V> b = ld_vec<Sh::V>(v + (size_t)(r0 + rl) * S + lane0);
+#pragma unroll
+      for (int j = 0; j < Sh::V; ++j) pr.v[j] = EP_DMUL(a.v[j], b.v[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < Sh::V; ++j) pr.v[j] = 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < Sh::V; ++j) sprod[rl * S + lane0 + j] = pr.v[j];
+  }
+  tile_fold_store<S, Sh::NT>(sprod, partials + (size_t)blockIdx.x * S);
+}
+
+template <int S>
+static cudaError_t dot_tiles_s(const TileMap& tm, const double* u, const double* v,
+                               double* partials, cudaStream_t st) {
+  if (tm.num_tiles() == 0) return cudaSuccess;
+  k_dot_tiles<S><<<tm.num_tiles(), TileShape<S>::NT, 0, st>>>(tm, u, v, partials);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dot_tiles(int s, const TileMap& tm, const double* u, const double* v,
+                             double* partials, cudaStream_t st) {
+  EP_DISPATCH_S(s, dot_tiles_s, tm, u, v, partials, st);
+}
+
+// =============================================================================
+// CG scalar phases (pcg.hpp:52-103), executed by one thread after the lanes'
+// dot products are known.  Coupled solves keep their scalars replicated across
+// lanes; uncoupled solves run s independent copies of pcg_solve<double>.
+// =============================================================================
+template <int S>
+__device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hist,
+                         double* lanes_out) {
+  if (phase == kPhaseNone) {
+    double acc = 0.0;  // reduce_sum (ensemble.hpp:240-244)
+    for (int e = 0; e < S; ++e) {
+      lanes_out[e] = lanes[e];
+      acc = EP_DADD(acc, lanes[e]);
+    }
+    lanes_out[S] = acc;
+    return;
+  }
+  const double tol = cg->tol;
+  const int maxit = cg->maxit;
+  if (cg->flavour == 0) {  // ---------------------------------------------- coupled
+    double d = 0.0;
+    for (int e = 0; e < S; ++e) d = EP_DADD(d, lanes[e]);
+    if (phase == kPhaseInit) {  // b_norm = norm2(b); r = b; p = z = r; rz = dot(r, z)
+      cg->it = 0;
+      const double bn = sqrt(d);
+      cg->bnorm[0] = bn;
+      cg->status = 0;
+      cg->iters[0] = 0;
+      if (bn == 0.0) {  // pcg.hpp:62-66
+        hist[0] = 0.0;
+        cg->hist_len[0] = 1;
+        cg->done = 1;
+        return;
+      }
+      for (int e = 0; e < S; ++e) cg->rz[e] = d;
+      const double rel = sqrt(d) / bn;
+      hist[0] = rel;
+      cg->hist_len[0] = 1;
+      if (rel < tol) {
+        cg->done = 1;
+      } else if (0 >= maxit) {
+        cg->status = 2;
+        cg->done = 1;
+      } else {
+        cg->done = 0;
+      }
+      for (int e = 0; e < S; ++e) cg->active[e] = !cg->done;
+    } else if (phase == kPhasePQ) {  // pq = dot(p, q); alpha = rz / pq
+      if (d <= 0.0) {
+        cg->status = 3;
+        cg->iters[0] = cg->it;
+        cg->done = 1;
+        return;
+      }
+      const double alpha = cg->rz[0] / d;
+      for (int e = 0; e < S; ++e) cg->alpha[e] = alpha;
+    } else {  // kPhaseRR: rz_next = dot(r, z); beta; next relative residual
+      const double beta = d / cg->rz[0];
+      for (int e = 0; e < S; ++e) {
+        cg->beta[e] = beta;
+        cg->rz[e] = d;
+      }
+      const int it = ++cg->it;
+      const double rel = sqrt(d) / cg->bnorm[0];
+      hist[it] = rel;
+      cg->hist_len[0] = it + 1;
+      if (rel < tol) {
+        cg->iters[0] = it;
+        cg->done = 1;
+      } else if (it >= maxit) {
+        cg->iters[0] = it;
+        cg->status = 2;
+        cg->done = 1;
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------------ uncoupled
+  if (phase == kPhaseInit) {
+    cg->it = 0;
+    cg->status = 0;
+    int any = 0;
+    for (int e = 0; e < S; ++e) {
+      const double d = lanes[e];
+      const double bn = sqrt(d);
+      cg->bnorm[e] = bn;
+      cg->iters[e] = 0;
+      cg->lane_status[e] = 0;
+      cg->hist_len[e] = 1;
+      int act = 0;
+      if (bn == 0.0) {
+        hist[e] = 0.0;
+      } else {
+        cg->rz[e] = d;
+        const double rel = sqrt(d) / bn;
+        hist[e] = rel;
+        if (rel < tol) {
+        } else if (0 >= maxit) {
+          cg->lane_status[e] = 2;
+        } else {
+          act = 1;
+        }
+      }
+      cg->active[e] = act;
+      any |= act;
+      if (cg->lane_status[e] > cg->status) cg->status = cg->lane_status[e];
+    }
+    cg->done = !any;
+  } else if (phase == kPhasePQ) {
+    int any = 0;
+    for (int e = 0; e < S; ++e) {
+      if (!cg->active[e]) continue;
+      const double d = lanes[e];
+      if (d <= 0.0) {
+        cg->lane_status[e] = 3;
+        cg->iters[e] = cg->it;
+        cg->active[e] = 0;
+        if (3 > cg->status) cg->status = 3;
+        continue;
+      }
+      cg->alpha[e] = cg->rz[e] / d;
+      any = 1;
+    }
+    if (!any) cg->done = 1;
+  } else {
+    const int it = ++cg->it;
+    int any = 0;
+    for (int e = 0; e < S; ++e) {
+      if (!cg->active[e]) continue;
+      const double d = lanes[e];
+      cg->beta[e] = d / cg->rz[e];
+      cg->rz[e] = d;
+      const double rel = sqrt(d) / cg->bnorm[e];
+      hist[(size_t)it * S + e] = rel;
+      cg->hist_len[e] = it + 1;
+      if (rel < tol) {
+        cg->iters[e] = it;
+        cg->active[e] = 0;
+      } else if (it >= maxit) {
+        cg->iters[e] = it;
+        cg->lane_status[e] = 2;
+        cg->active[e] = 0;
+        if (2 > cg->status) cg->status = 2;
+      } else {
+        any = 1;
+      }
+    }
+    if (!any) cg->done = 1;
+  }
+}
+
+// Canonical finalize: segment sums (0.0 + tile_0 + tile_1 + ...), then the
+// lane total (0.0 + seg_0 + seg_1 + ...), then the scalar phase.
+template <int S>
+__global__ void __launch_bounds__(1024) k_fin_canonical(const TileMap tm,
+                                                        const double* __restrict__ partials,
+                                                        double* __restrict__ segbuf, int phase,
+                                                        CgState* cg, double* hist,
+                                                        double* lanes_out) {
+  if ((phase == kPhasePQ || phase == kPhaseRR) && cg->done) return;
+  __shared__ double lanes[S];
+  const int items = tm.num_segs * S;
+  for (int w = threadIdx.x; w < items; w += blockDim.x) {
+    const int seg = w / S, e = w - seg * S;
+    const int nt = tm.tiles_in_seg(seg);
+    const double* p = partials + (size_t)seg * tm.tiles_per_seg * S + e;
+    double acc = 0.0;
+#pragma unroll 8
+    for (int t = 0; t < nt; ++t) acc = EP_DADD(acc, p[(size_t)t * S]);
+    segbuf[w] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x < S) {
+    double tot = 0.0;
+    for (int seg = 0; seg < tm.num_segs; ++seg) tot = EP_DADD(tot, segbuf[seg * S + threadIdx.x]);
+    lanes[threadIdx.x] = tot;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) cg_phase<S>(phase, lanes, cg, hist, lanes_out);
+}
+
+template <int S>
+static cudaError_t fin_canonical_s(const TileMap& tm, const double* partials, double* segbuf,
+                                   int phase, CgState* cg, double* hist, double* lanes_out,
+                                   cudaStream_t st) {
+  k_fin_canonical<S><<<1, 1024, 0, st>>>(tm, partials, segbuf, phase, cg, hist, lanes_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fin_canonical(int s, const TileMap& tm, const double* partials,
+                                 double* segbuf, int phase, CgState* cg, double* hist,
+                                 double* lanes_out, cudaStream_t st) {
+  EP_DISPATCH_S(s, fin_canonical_s, tm, partials, segbuf, phase, cg, hist, lanes_out, st);
+}
+
+// Serial finalize: the reference's own order (kernels.hpp:66-67), one chain
+// per sample: acc = 0; acc += u[row]*v[row] for row = 0, 1, ...  A single warp
+// runs the s chains; the vectors stream into shared memory through a 4-stage
+// ring of 1D bulk copies (cp.async.bulk + mbarrier), so the chain only waits on
+// its own DADD latency, not on DRAM.
+constexpr int kSerialStages = 4;
+constexpr int kSerialChunkBytes = 16384;
+constexpr int kSerialSmem = 2 * kSerialStages * kSerialChunkBytes + kSerialStages * 8;
+
+template <int S>
+__global__ void __launch_bounds__(32) k_fin_serial(int rows, const double* __restrict__ u,
+                                                   const double* __restrict__ v, int phase,
+                                                   CgState* cg, double* hist,
+                                                   double* lanes_out) {
+  if ((phase == kPhasePQ || phase == kPhaseRR) && cg->done) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr int kChunkRows = kSerialChunkBytes / (8 * S);
+  __shared__ double lanes[S];
+  double* su = reinterpret_cast<double*>(smem);
+  double* sv = su + kSerialStages * kChunkRows * S;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kSerialStages * kSerialChunkBytes);
+  const int lane = threadIdx.x;
+  const bool same = (u == v);
+  const bool aligned = ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+  const int nchunks = (rows + kChunkRows - 1) / kChunkRows;
+  double acc = 0.0;
+
+  if (aligned && nchunks > 0) {
+    if (lane == 0) {
+      for (int s2 = 0; s2 < kSerialStages; ++s2) mbar_init(&bars[s2], 1);
+      fence_mbar_init();
+    }
+    __syncwarp();
+    auto issue = [&](int c) {
+      const int stg = c % kSerialStages;
+      const int r0 = c * kChunkRows;
+      const int nr = min(kChunkRows, rows - r0);
+      const uint32_t bytes = (uint32_t)((size_t)nr * S * 8) & ~15u;
+      mbar_arrive_expect_tx(&bars[stg], same ? bytes : 2 * bytes);
+      if (bytes) {
+        bulk_g2s(su + (size_t)stg * kChunkRows * S, u + (size_t)r0 * S, bytes, &bars[stg]);
+        if (!same) bulk_g2s(sv + (size_t)stg * kChunkRows * S, v + (size_t)r0 * S, bytes, &bars[stg]);
+      }
+    };
+    if (lane == 0)
+      for (int c = 0; c < kSerialStages && c < nchunks; ++c) issue(c);
+    for (int c = 0; c < nchunks; ++c) {
+      const int stg = c % kSerialStages;
+      mbar_wait(&bars[stg], (uint32_t)((c / kSerialStages) & 1));
+      const int r0 = c * kChunkRows;
+      const int nr = min(kChunkRows, rows - r0);
+      const int nbulk = (int)((((size_t)nr * S * 8) & ~(size_t)15) / (8 * S));
+      if (lane < S) {
+        const double* cu = su + (size_t)stg * kChunkRows * S + lane;
+        const double* cv = same ? cu : sv + (size_t)stg * kChunkRows * S + lane;
+        int r = 0;
+#pragma unroll 8
+        for (; r < nbulk; ++r) acc = EP_DADD(acc, EP_DMUL(cu[(size_t)r * S], cv[(size_t)r * S]));
+        for (; r < nr; ++r)
+          acc = EP_DADD(acc, EP_DMUL(u[(size_t)(r0 + r) * S + lane], v[(size_t)(r0 + r) * S + lane]));
+      }
+      __syncwarp();
+      if (lane == 0 && c + kSerialStages < nchunks) {
+        fence_proxy_async_smem();
+        issue(c + kSerialStages);
+      }
+    }
+  } else if (lane < S) {
+    for (int r = 0; r < rows; ++r)
+      acc = EP_DADD(acc, EP_DMUL(u[(size_t)r * S + lane], v[(size_t)r * S + lane]));
+  }
+  if (lane < S) lanes[lane] = acc;
+  __syncwarp();
+  if (lane == 0) cg_phase<S>(phase, lanes, cg, hist, lanes_out);
+}
+
+template <int S>
+static cudaError_t fin_serial_s(int rows, const double* u, const double* v, int phase,
+                                CgState* cg, double* hist, double* lanes_out, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t err = cudaFuncSetAttribute(k_fin_serial<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kSerialSmem);
+    if (err != cudaSuccess) return err;
+    configured = true;
+  }
+  k_fin_serial<S><<<1, 32, kSerialSmem, st>>>(rows, u, v, phase, cg, hist, lanes_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v, int phase,
+                              CgState* cg, double* hist, double* lanes_out, cudaStream_t st) {
+  EP_DISPATCH_S(s, fin_serial_s, rows, u, v, phase, cg, hist, lanes_out, st);
+}
+
+// =============================================================================
+// CG vector kernels.  One block per canonical tile (kTiles) or per run of
+// kTileRows rows (serial mode).  Early-exit when the solve is done, so a host
+// may enqueue iterations ahead of the convergence check.
+// =============================================================================
+template <int S, bool kTiles>
+__global__ void __launch_bounds__(TileShape<S>::NT) k_cg_spmv(
+    const TileMap tm, const int* __restrict__ row_map, const int* __restrict__ col_entry,
+    const double* __restrict__ values, const double* __restrict__ r,
+    const double* __restrict__ p_old, double* __restrict__ p_new, double* __restrict__ q,
+    const CgState* __restrict__ cg, double* __restrict__ partials) {
+  using Sh = TileShape<S>;
+  constexpr int V = Sh::V;
+  if (cg->done) return;
+  __shared__ double sprod[kTiles ? kTileRows * S : 1];
+  int r0, nr;
+  if constexpr (kTiles) {
+    tm.tile(blockIdx.x, r0, nr);
+  } else {
+    r0 = blockIdx.x * kTileRows;
+    nr = min(kTileRows, tm.rows - r0);
+  }
+  if (nr <= 0) return;
+  const int lane0 = (threadIdx.x % Sh::TPR) * V;
+  const bool first = cg->it == 0;
+  VecD<V> beta;
+#pragma unroll
+  for (int j = 0; j < V; ++j) beta.v[j] = cg->beta[lane0 + j];
+#pragma unroll
+  for (int pass = 0; pass < Sh::PASSES; ++pass) {
+    const int rl = pass * Sh::RPP + threadIdx.x / Sh::TPR;
+    VecD<V> pr;
+    if (rl < nr) {
+      const int row = r0 + rl;
+      const VecD<V> sum = row_product<S, V, SpmvShape<S>::U, true>(row, row_map, col_entry, values,
+                                                                   r, p_old, first, beta, lane0);
+      VecD<V> pn = ld_vec<V>(r + (size_t)row * S + lane0);
+      if (!first) {
+        const VecD<V> po = ld_vec<V>(p_old + (size_t)row * S + lane0);
+#pragma unroll
+        for (int j = 0; j < V; ++j) pn.v[j] = EP_DADD(pn.v[j], EP_DMUL(beta.v[j], po.v[j]));
+      }
+      st_vec<V>(p_new + (size_t)row * S + lane0, pn);
+      st_vec<V>(q + (size_t)row * S + lane0, sum);
+#pragma unroll
+      for (int j = 0; j < V; ++j) pr.v[j] = EP_DMUL(pn.v[j], sum.v[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; ++j) pr.v[j] = 0.0;
+    }
+    if constexpr (kTiles) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) sprod[rl * S + lane0 + j] = pr.v[j];
+    }
+  }
+  if constexpr (kTiles) tile_fold_store<S, Sh::NT>(sprod, partials + (size_t)blockIdx.x * S);
+}
+
+template <int S>
+static cudaError_t cg_spmv_s(bool tiles, const TileMap& tm, const int* row_map,
+                             const int* col_entry, const double* values, const double* r,
+                             const double* p_old, double* p_new, double* q, const CgState* cg,
+                             double* partials, cudaStream_t st) {
+  if (tiles) {
+    if (tm.num_tiles() == 0) return cudaSuccess;
+    k_cg_spmv<S, true><<<tm.num_tiles(), TileShape<S>::NT, 0, st>>>(
+        tm, row_map, col_entry, values, r, p_old, p_new, q, cg, partials);
+  } else {
+    const int blocks = (tm.rows + kTileRows - 1) / kTileRows;
+    if (blocks == 0) return cudaSuccess;
+    k_cg_spmv<S, false><<<blocks, TileShape<S>::NT, 0, st>>>(tm, row_map, col_entry, values, r,
+                                                              p_old, p_new, q, cg, partials);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_spmv(int s, bool tiles, const TileMap& tm, const int* row_map,
+                           const int* col_entry, const double* values, const double* r,
+                           const double* p_old, double* p_new, double* q, const CgState* cg,
+                           double* partials, cudaStream_t st) {
+  EP_DISPATCH_S(s, cg_spmv_s, tiles, tm, row_map, col_entry, values, r, p_old, p_new, q, cg,
+                partials, st);
+}
+
+// x = alpha*p + x; r = (-alpha)*q + r on active lanes (pcg.hpp:94-95 via
+// axpby, kernels.hpp:84: 1.0*y is exact); r.r tile partials for the next dot.
+template <int S, bool kTiles>
+__global__ void __launch_bounds__(TileShape<S>::NT) k_cg_update(
+    const TileMap tm, double* __restrict__ x, const double* __restrict__ p,
+    double* __restrict__ r, const double* __restrict__ q, const CgState* __restrict__ cg,
+    double* __restrict__ partials) {
+  using Sh = TileShape<S>;
+  constexpr int V = Sh::V;
+  if (cg->done) return;
+  __shared__ double sprod[kTiles ? kTileRows * S : 1];
+  int r0, nr;
+  if constexpr (kTiles) {
+    tm.tile(blockIdx.x, r0, nr);
+  } else {
+    r0 = blockIdx.x * kTileRows;
+    nr = min(kTileRows, tm.rows - r0);
+  }
+  if (nr <= 0) return;
+  const int lane0 = (threadIdx.x % Sh::TPR) * V;
+  double al[V];
+  bool act[V];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    al[j] = cg->alpha[lane0 + j];
+    act[j] = cg->active[lane0 + j] != 0;
+  }
+#pragma unroll
+  for (int pass = 0; pass < Sh::PASSES; ++pass) {
+    const int rl = pass * Sh::RPP + threadIdx.x / Sh::TPR;
+    VecD<V> pr;
+    if (rl < nr) {
+      const size_t off = (size_t)(r0 + rl) * S + lane0;
+      VecD<V> xv = ld_vec<V>(x + off), rv = ld_vec<V>(r + off);
+      const VecD<V> pv = ld_vec<V>(p + off), qv = ld_vec<V>(q + off);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        if (act[j]) {
+          xv.v[j] = EP_DADD(EP_DMUL(al[j], pv.v[j]), xv.v[j]);
+          rv.v[j] = EP_DADD(EP_DMUL(-al[j], qv.v[j]), rv.v[j]);
+        }
+        pr.v[j] = EP_DMUL(rv.v[j], rv.v[j]);
+      }
+      st_vec<V>(x + off, xv);
+      st_vec<V>(r + off, rv);
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; ++j) pr.v[j] = 0.0;
+    }
+    if constexpr (kTiles) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) sprod[rl * S + lane0 + j] = pr.v[j];
+    }
+  }
+  if constexpr (kTiles) tile_fold_store<S, Sh::NT>(sprod, partials + (size_t)blockIdx.x * S);
+}
+
+template <int S>
+static cudaError_t cg_update_s(bool tiles, const TileMap& tm, double* x, const double* p,
+                               double* r, const double* q, const CgState* cg, double* partials,
+                               cudaStream_t st) {
+  if (tiles) {
+    if (tm.num_tiles() == 0) return cudaSuccess;
+    k_cg_update<S, true><<<tm.num_tiles(), TileShape<S>::NT, 0, st>>>(tm, x, p, r, q, cg, partials);
+  } else {
+    const int blocks = (tm.rows + kTileRows - 1) / kTileRows;
+    if (blocks == 0) return cudaSuccess;
+    k_cg_update<S, false><<<blocks, TileShape<S>::NT, 0, st>>>(tm, x, p, r, q, cg, partials);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* x, const double* p,
+                             double* r, const double* q, const CgState* cg, double* partials,
+                             cudaStream_t st) {
+  EP_DISPATCH_S(s, cg_update_s, tiles, tm, x, p, r, q, cg, partials, st);
+}
+
+}  // namespace ep

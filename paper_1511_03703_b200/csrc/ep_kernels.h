@@ -1,0 +1,84 @@
+// Internal host-side interface of the enprop_b200 kernels (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ep_tilemap.h"
+
+namespace ep {
+
+// Device-resident per-problem assembly constants (fem.hpp:76-98, :133-191),
+// all computed on the host in the reference's operation order.
+struct AsmTables {
+  double G[8][8][8];    // [q][i][j]: (gx_j*gx_i + gy_j*gy_i) + gz_j*gz_i, g* = gradient*grad_scale
+  double ADV[8][8][8];  // [q][i][j]: advect_ij = (alpha*((vx*gx_j + vy*gy_j) + vz*gz_j))*n_i
+  double NN[8][8][8];   // [q][i][j]: n_j*n_i
+  double GS[8][8][3];   // [q][c][axis]: gradient*grad_scale
+  double VAL[8][8];     // [q][c]: basis value
+  double wd;            // (h/2)^3
+  double alpha, beta, vx, vy, vz;
+};
+
+struct AsmArgs {
+  int n;                 // cells per axis
+  int rows;              // (n+1)^3
+  int m;                 // KL terms
+  double mean;           // kappa0
+  const double* F;       // KL axis tables [m][2n]: f_t((c + off_b) * h)
+  const AsmTables* tab;  // device
+  const int* row_map;    // device
+  const double* u;       // [rows][s] or nullptr (= 0)
+  const double* y;       // [m][s]
+  double* values;        // [nnz][s]
+  double* residual;      // [rows][s]
+  int dirichlet;         // fuse apply_dirichlet
+  int nonlinear;         // alpha != 0 || beta != 0
+  double bc0, bc1;
+  int mode_axes[64][3];
+  double mode_sl[64];    // sigma * sqrt(lambda_i)
+};
+
+// CG state on the device (one per solve).  Coupled solves store their scalars
+// replicated across lanes so the vector kernels are flavour-agnostic.
+struct CgState {
+  int it, done, status, flavour;
+  int s, maxit, pad0, pad1;
+  double tol;
+  double rz[32], alpha[32], beta[32], bnorm[32];
+  int active[32], iters[32], lane_status[32], hist_len[32];
+};
+
+enum Phase { kPhaseNone = 0, kPhaseInit = 1, kPhasePQ = 2, kPhaseRR = 3 };
+
+cudaError_t launch_build_graph(int n, int* row_map, int* col_entry, cudaStream_t st);
+cudaError_t launch_assemble(int s, const AsmArgs& a, cudaStream_t st);
+cudaError_t launch_dirichlet(int s, int n, double bc0, double bc1, const int* row_map,
+                             const int* col_entry, const double* u, double* values,
+                             double* residual, cudaStream_t st);
+cudaError_t launch_spmv(int s, int rows, const int* row_map, const int* col_entry,
+                        const double* values, const double* x, double* z, cudaStream_t st);
+cudaError_t launch_axpby(int s, int64_t n, int per_lane, const double* alpha, const double* beta,
+                         const double* x, double* y, cudaStream_t st);
+// canonical dot: tile partials [num_tiles][s]
+cudaError_t launch_dot_tiles(int s, const TileMap& tm, const double* u, const double* v,
+                             double* partials, cudaStream_t st);
+// reduce tile partials in canonical order, then run `phase` on the CG state
+// (or write lanes to lanes_out for kPhaseNone)
+cudaError_t launch_fin_canonical(int s, const TileMap& tm, const double* partials,
+                                 double* segbuf, int phase, CgState* cg, double* hist,
+                                 double* lanes_out, cudaStream_t st);
+// serial (reference-order) dot straight from the vectors, then `phase`
+cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v, int phase,
+                              CgState* cg, double* hist, double* lanes_out, cudaStream_t st);
+// q = A p_new with p_new = (it==0 ? r : r + beta*p_old) formed on the fly; writes
+// p_new and q; with tiles, also the p_new.q tile partials
+cudaError_t launch_cg_spmv(int s, bool tiles, const TileMap& tm, const int* row_map,
+                           const int* col_entry, const double* values, const double* r,
+                           const double* p_old, double* p_new, double* q, const CgState* cg,
+                           double* partials, cudaStream_t st);
+// x += alpha p; r -= alpha q on active lanes; with tiles, also r.r tile partials
+cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* x, const double* p,
+                             double* r, const double* q, const CgState* cg, double* partials,
+                             cudaStream_t st);
+
+}  // namespace ep
