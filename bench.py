@@ -165,6 +165,9 @@ def run_ours(args):
     samples = args.steps * S * world
     value = samples / (ms / 1e3)
 
+    if args.profile_only:
+        print(json.dumps({"profile_only": True, "ms": ms, "iters": iters}), flush=True)
+        return
     # ---- e2e: the reference-facing call with host buffers (pinned), copies timed
     y_host = [torch.as_tensor(pack_group(pool, S, rank * groups_per_rank + g)).contiguous().pin_memory()
               for g in range(groups_per_rank)]
@@ -371,6 +374,8 @@ def main():
     ap.add_argument("--dot", choices=["canonical", "serial"], default="canonical")
     ap.add_argument("--skip-spmv", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="warm-up + timed steps only (for ncu launch lists)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -47,7 +47,7 @@ enum { ENPROP_DOT_SERIAL = 0, ENPROP_DOT_CANONICAL = 1 };
 enum { ENPROP_CG_COUPLED = 0, ENPROP_CG_UNCOUPLED = 1 };
 
 /* Rows per canonical reduction tile. */
-#define ENPROP_TILE_ROWS 64
+#define ENPROP_TILE_ROWS 16
 
 const char* enprop_last_error(void);
 int enprop_abi_version(void);

@@ -29,7 +29,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libenprop_b200.so")
 OK, ERR_INVALID, ERR_NO_CONVERGENCE, ERR_INDEFINITE, ERR_CUDA, ERR_OOM = range(6)
 DOT_SERIAL, DOT_CANONICAL = 0, 1
 CG_COUPLED, CG_UNCOUPLED = 0, 1
-TILE_ROWS = 64
+TILE_ROWS = 16
 WIDTHS = (1, 2, 4, 8, 16, 32)
 
 _dp = C.POINTER(C.c_double)
@@ -353,8 +353,7 @@ class SolveResult:
 
 
 def _collect(cfg: SolverConfig, s: int, it, ls, hist, hl):
-    lanes = s if cfg.flavour == CG_UNCOUPLED else 1
-    if lanes == 1:
+    if cfg.flavour != CG_UNCOUPLED:
         history = [hist[i] for i in range(hl[0])]
         return it[0], history, [ls[0]]
     history = [[hist[i * s + e] for i in range(hl[e])] for e in range(s)]

@@ -63,8 +63,9 @@ struct CgWork {
   double* r = nullptr;
   double* p[2] = {nullptr, nullptr};
   double* q = nullptr;
-  double* partials = nullptr;
-  double* segbuf = nullptr;
+  double* partials = nullptr;  // canonical tile partials [tiles][s]
+  double* seg_sums = nullptr;  // [segs][s]
+  int* counters = nullptr;     // [segs] arrival counters + [1] segment counter, self-resetting
   double* hist = nullptr;
   CgState* state = nullptr;
   int rows = 0, s = 0, maxit = -1, tiles = 0, segs = 0;
@@ -72,7 +73,7 @@ struct CgWork {
 
 void free_work(CgWork& w) {
   for (void* p : {(void*)w.r, (void*)w.p[0], (void*)w.p[1], (void*)w.q, (void*)w.partials,
-                  (void*)w.segbuf, (void*)w.hist, (void*)w.state})
+                  (void*)w.seg_sums, (void*)w.counters, (void*)w.hist, (void*)w.state})
     if (p) cudaFree(p);
   w = CgWork{};
 }
@@ -90,7 +91,9 @@ int ensure_work(CgWork& w, int rows, int s, int maxit, const TileMap& tm) {
   EP_CUDA(cudaMalloc(&w.p[1], vb));
   EP_CUDA(cudaMalloc(&w.q, vb));
   EP_CUDA(cudaMalloc(&w.partials, (size_t)tiles * s * sizeof(double)));
-  EP_CUDA(cudaMalloc(&w.segbuf, (size_t)segs * s * sizeof(double)));
+  EP_CUDA(cudaMalloc(&w.seg_sums, (size_t)segs * s * sizeof(double)));
+  EP_CUDA(cudaMalloc(&w.counters, (size_t)(segs + 1) * sizeof(int)));
+  EP_CUDA(cudaMemset(w.counters, 0, (size_t)(segs + 1) * sizeof(int)));
   EP_CUDA(cudaMalloc(&w.hist, (size_t)(maxit + 1) * s * sizeof(double)));
   EP_CUDA(cudaMalloc(&w.state, sizeof(CgState)));
   w.rows = rows;
@@ -99,6 +102,19 @@ int ensure_work(CgWork& w, int rows, int s, int maxit, const TileMap& tm) {
   w.tiles = tiles;
   w.segs = segs;
   return ENPROP_OK;
+}
+
+FinArgs fin_args(const CgWork& w, const TileMap& tm, int phase) {
+  FinArgs f;
+  f.partials = w.partials;
+  f.seg_sums = w.seg_sums;
+  f.seg_count = w.counters;
+  f.seg_done = w.counters + (tm.num_segs > 0 ? tm.num_segs : 1);
+  f.phase = phase;
+  f.cg = w.state;
+  f.hist = w.hist;
+  f.lanes_out = nullptr;
+  return f;
 }
 
 int validate_cg_options(const enprop_cg_options* opt, int s) {
@@ -170,10 +186,12 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
     EP_CUDA(cudaMemsetAsync(x, 0, vec, st));
     EP_CUDA(cudaMemcpyAsync(w.r, b, vec, cudaMemcpyDeviceToDevice, st));
   }
+  const FinArgs f_init = fin_args(w, tm, kPhaseInit);
+  const FinArgs f_pq = fin_args(w, tm, kPhasePQ);
+  const FinArgs f_rr = fin_args(w, tm, kPhaseRR);
   if (canon) {
-    EP_CUDA(launch_dot_tiles(s, tm, w.r, w.r, w.partials, st));
-    EP_CUDA(launch_fin_canonical(s, tm, w.partials, w.segbuf, kPhaseInit, w.state, w.hist, nullptr, st));
-    ctx->launches += 2;
+    EP_CUDA(launch_dot_tiles(s, tm, w.r, w.r, f_init, st));
+    ctx->launches += 1;
   } else {
     EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, kPhaseInit, w.state, w.hist, nullptr, st));
     ctx->launches += 1;
@@ -192,18 +210,12 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
         cudaEvent_t* ev = ctx->profile ? prof_pair(ctx) : nullptr;
         if (ev) EP_CUDA(cudaEventRecord(ev[0], st));
         EP_CUDA(launch_cg_spmv(s, canon, tm, row_map, col_entry, values, w.r, p_old, p_new, w.q,
-                               w.state, w.partials, st));
+                               f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[1], st));
-        if (canon)
-          EP_CUDA(launch_fin_canonical(s, tm, w.partials, w.segbuf, kPhasePQ, w.state, w.hist, nullptr, st));
-        else
-          EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, kPhasePQ, w.state, w.hist, nullptr, st));
-        EP_CUDA(launch_cg_update(s, canon, tm, x, p_new, w.r, w.q, w.state, w.partials, st));
-        if (canon)
-          EP_CUDA(launch_fin_canonical(s, tm, w.partials, w.segbuf, kPhaseRR, w.state, w.hist, nullptr, st));
-        else
-          EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, kPhaseRR, w.state, w.hist, nullptr, st));
-        ctx->launches += 4;
+        if (!canon) EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, kPhasePQ, w.state, w.hist, nullptr, st));
+        EP_CUDA(launch_cg_update(s, canon, tm, x, p_new, w.r, w.q, f_rr, st));
+        if (!canon) EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, kPhaseRR, w.state, w.hist, nullptr, st));
+        ctx->launches += canon ? 2 : 4;
       }
     }
     // flag of this chunk
@@ -508,18 +520,20 @@ int enprop_dot(enprop_ctx* c, int s, int64_t n, const double* u, const double* v
   if (!valid_width(s)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
   if (n < 0 || n > 2147483647LL) return fail(ENPROP_ERR_INVALID, "dot: bad length");
   double* out = nullptr;
-  double* partials = nullptr;
-  double* segbuf = nullptr;
   const int rows = (int)n;
   const TileMap tm = make_tile_map(rows, seg_rows > 0 ? seg_rows : 4096);
+  CgWork w;  // partials + counters only
   cudaError_t err = cudaMalloc(&out, (s + 1) * sizeof(double));
-  if (err == cudaSuccess && dot_mode == ENPROP_DOT_CANONICAL) {
-    err = cudaMalloc(&partials, (size_t)(tm.num_tiles() > 0 ? tm.num_tiles() : 1) * s * sizeof(double));
-    if (err == cudaSuccess) err = cudaMalloc(&segbuf, (size_t)(tm.num_segs > 0 ? tm.num_segs : 1) * s * sizeof(double));
-    if (err == cudaSuccess) err = launch_dot_tiles(s, tm, u, v, partials, c->stream);
-    if (err == cudaSuccess)
-      err = launch_fin_canonical(s, tm, partials, segbuf, kPhaseNone, nullptr, nullptr, out, c->stream);
-    c->launches += 2;
+  if (err == cudaSuccess && dot_mode == ENPROP_DOT_CANONICAL && rows > 0) {
+    const int tiles = tm.num_tiles(), segs = tm.num_segs;
+    if (err == cudaSuccess) err = cudaMalloc(&w.partials, (size_t)tiles * s * sizeof(double));
+    if (err == cudaSuccess) err = cudaMalloc(&w.seg_sums, (size_t)segs * s * sizeof(double));
+    if (err == cudaSuccess) err = cudaMalloc(&w.counters, (size_t)(segs + 1) * sizeof(int));
+    if (err == cudaSuccess) err = cudaMemsetAsync(w.counters, 0, (size_t)(segs + 1) * sizeof(int), c->stream);
+    FinArgs f = fin_args(w, tm, kPhaseNone);
+    f.lanes_out = out;
+    if (err == cudaSuccess) err = launch_dot_tiles(s, tm, u, v, f, c->stream);
+    c->launches += 1;
   } else if (err == cudaSuccess) {
     err = launch_fin_serial(s, rows, u, v, kPhaseNone, nullptr, nullptr, out, c->stream);
     c->launches += 1;
@@ -529,8 +543,7 @@ int enprop_dot(enprop_ctx* c, int s, int64_t n, const double* u, const double* v
     err = cudaMemcpyAsync(h.data(), out, (s + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
   if (err == cudaSuccess) err = cudaStreamSynchronize(c->stream);
   if (out) cudaFree(out);
-  if (partials) cudaFree(partials);
-  if (segbuf) cudaFree(segbuf);
+  free_work(w);
   if (err != cudaSuccess) return cuda_fail(err, "enprop_dot");
   if (lanes_host)
     for (int e = 0; e < s; ++e) lanes_host[e] = h[e];

@@ -170,73 +170,163 @@ cudaError_t launch_axpby(int s, int64_t n, int /*per_lane*/, const double* alpha
 }
 
 // =============================================================================
-// Canonical tile reduction: the block's kTileRows x S products
-// sit in shared memory (rows past the tile end hold +0.0) and are folded by
-// v[i] += v[i + half] for half = 32, 16, ..., 1, independently per sample.
-// oracle/enprop_oracle.c:or_dot_lanes restates exactly this order.
+// Canonical reduction (restated by oracle/enprop_oracle.c
+// or_dot_lanes).  Rows are cut into segments of seg_rows (a mesh z-plane) and
+// each segment into tiles of kTileRows = 16 rows aligned at the segment start.
+// Per sample:  tile sum  = stride-halving tree v[i] += v[i+h], h = 8,4,2,1
+//                          over the tile's products (+0.0 past the tile end);
+//              segment   = 0.0 + tile_0 + tile_1 + ...      (sequential)
+//              total     = 0.0 + seg_0 + seg_1 + ...        (sequential)
+// A block owns TPC whole tiles.  The finalize is fused into the producing
+// kernel: after writing its tile partials, a block bumps its segments' arrival
+// counters; the block that completes a segment forms the segment sum, and the
+// block that completes the last segment forms the total and runs the CG scalar
+// phase.  Counters reset themselves, so no launch or memset sits between.
 // =============================================================================
-template <int S, int NT>
-__device__ __forceinline__ void tile_fold_store(double* sprod, double* __restrict__ out) {
-  __syncthreads();
-#pragma unroll 1
-  for (int half = kTileRows / 2; half >= 1; half >>= 1) {
-    for (int idx = threadIdx.x; idx < half * S; idx += NT)
-      sprod[idx] = EP_DADD(sprod[idx], sprod[idx + half * S]);
-    __syncthreads();
-  }
-  if (threadIdx.x < S) out[threadIdx.x] = sprod[threadIdx.x];
-}
-
 template <int S>
 struct TileShape {
   static constexpr int V = SpmvShape<S>::V;
-  static constexpr int TPR = S / V;
-  static constexpr int NT = (kTileRows * TPR < 256) ? kTileRows * TPR : 256;  // threads/block
-  static constexpr int RPP = NT / TPR;                                         // rows per pass
-  static constexpr int PASSES = kTileRows / RPP;
+  static constexpr int TPR = S / V;            // threads per row
+  static constexpr int NT = 256;               // threads per block
+  static constexpr int RPC = NT / TPR;         // row slots per block
+  static constexpr int TPC = RPC / kTileRows;  // tiles per block
+  static_assert(RPC % kTileRows == 0, "a block must own whole tiles");
 };
 
 template <int S>
-__global__ void __launch_bounds__(TileShape<S>::NT) k_dot_tiles(const TileMap tm,
-                                                                const double* __restrict__ u,
-                                                                const double* __restrict__ v,
-                                                                double* __restrict__ partials) {
+__device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hist,
+                         double* lanes_out);
+
+// Row of slot `slot` of this block in canonical tiling (-1: none).
+template <int S>
+__device__ __forceinline__ int tile_row(const TileMap& tm, int slot) {
   using Sh = TileShape<S>;
-  __shared__ double sprod[kTileRows * S];
+  const int tile = blockIdx.x * Sh::TPC + slot / kTileRows;
+  if (tile >= tm.num_tiles()) return -1;
   int r0, nr;
-  tm.tile(blockIdx.x, r0, nr);
-  if (nr <= 0) return;
-  const int lane0 = (threadIdx.x % Sh::TPR) * Sh::V;
+  tm.tile(tile, r0, nr);
+  const int ri = slot % kTileRows;
+  return ri < nr ? r0 + ri : -1;
+}
+
+constexpr int kSegChunk = 64;  // tile partials staged per step of a segment sum
+
+template <int S>
+__device__ void tiles_finish(const TileMap& tm, double* sprod, const FinArgs& f) {
+  using Sh = TileShape<S>;
+  __shared__ double schunk[kSegChunk * S];
+  __shared__ double lanes[S];
+  __shared__ int s_last[Sh::TPC];
+  __shared__ int s_nlast, s_final;
+  __syncthreads();
 #pragma unroll
-  for (int pass = 0; pass < Sh::PASSES; ++pass) {
-    const int rl = pass * Sh::RPP + threadIdx.x / Sh::TPR;
-    VecD<Sh::V> pr;
-    if (rl < nr) {
-      const VecD<Sh::V> a = ld_vec<Sh::V>(u + (size_t)(r0 + rl) * S + lane0);
-      const VecD<Sh::V> b = ld_vec<Sh::V>(v + (size_t)(r0 + rl) * S + lane0);
-#pragma unroll
-      for (int j = 0; j < Sh::V; ++j) pr.v[j] = EP_DMUL(a.v[j], b.v[j]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < Sh::V; ++j) pr.v[j] = 0.0;
+  for (int half = kTileRows / 2; half >= 1; half >>= 1) {
+    for (int idx = threadIdx.x; idx < Sh::TPC * half * S; idx += Sh::NT) {
+      const int lt = idx / (half * S);
+      const int rem = idx - lt * half * S;
+      double* base = sprod + lt * kTileRows * S;
+      base[rem] = EP_DADD(base[rem], base[rem + half * S]);
     }
-#pragma unroll
-    for (int j = 0; j < Sh::V; ++j) sprod[rl * S + lane0 + j] = pr.v[j];
+    __syncthreads();
   }
-  tile_fold_store<S, Sh::NT>(sprod, partials + (size_t)blockIdx.x * S);
+  for (int idx = threadIdx.x; idx < Sh::TPC * S; idx += Sh::NT) {
+    const int lt = idx / S, e = idx - lt * S;
+    const int tile = blockIdx.x * Sh::TPC + lt;
+    int r0, nr;
+    if (tile < tm.num_tiles()) {
+      tm.tile(tile, r0, nr);
+      if (nr > 0) f.partials[(size_t)tile * S + e] = sprod[lt * kTileRows * S + e];
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int nl = 0;
+    for (int lt = 0; lt < Sh::TPC; ++lt) {
+      const int tile = blockIdx.x * Sh::TPC + lt;
+      if (tile >= tm.num_tiles()) break;
+      int r0, nr;
+      tm.tile(tile, r0, nr);
+      if (nr <= 0) continue;
+      const int seg = tile / tm.tiles_per_seg;
+      const int old = atomicAdd(&f.seg_count[seg], 1);
+      if (old == tm.tiles_in_seg(seg) - 1) s_last[nl++] = seg;
+    }
+    s_nlast = nl;
+  }
+  __syncthreads();
+  for (int k = 0; k < s_nlast; ++k) {
+    const int seg = s_last[k];
+    __threadfence();
+    const int nt = tm.tiles_in_seg(seg);
+    const double* p = f.partials + (size_t)seg * tm.tiles_per_seg * S;
+    double acc = 0.0;
+    for (int t0 = 0; t0 < nt; t0 += kSegChunk) {
+      const int cnt = min(kSegChunk, nt - t0);
+      for (int idx = threadIdx.x; idx < cnt * S; idx += Sh::NT) schunk[idx] = __ldcg(p + (size_t)t0 * S + idx);
+      __syncthreads();
+      if (threadIdx.x < S)
+        for (int t = 0; t < cnt; ++t) acc = EP_DADD(acc, schunk[t * S + threadIdx.x]);
+      __syncthreads();
+    }
+    if (threadIdx.x < S) f.seg_sums[(size_t)seg * S + threadIdx.x] = acc;
+    if (threadIdx.x == 0) f.seg_count[seg] = 0;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_final = (atomicAdd(f.seg_done, 1) == tm.num_segs - 1);
+    __syncthreads();
+    if (s_final) {
+      __threadfence();
+      if (threadIdx.x < S) {
+        double tot = 0.0;
+        for (int sg = 0; sg < tm.num_segs; ++sg) tot = EP_DADD(tot, __ldcg(f.seg_sums + (size_t)sg * S + threadIdx.x));
+        lanes[threadIdx.x] = tot;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        *f.seg_done = 0;
+        cg_phase<S>(f.phase, lanes, f.cg, f.hist, f.lanes_out);
+      }
+    }
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) k_dot_tiles(const TileMap tm, const double* __restrict__ u,
+                                                   const double* __restrict__ v, const FinArgs f) {
+  using Sh = TileShape<S>;
+  constexpr int V = Sh::V;
+  __shared__ double sprod[Sh::RPC * S];
+  const int slot = threadIdx.x / Sh::TPR;
+  const int lane0 = (threadIdx.x % Sh::TPR) * V;
+  const int row = tile_row<S>(tm, slot);
+  VecD<V> pr;
+  if (row >= 0) {
+    const VecD<V> a = ld_vec<V>(u + (size_t)row * S + lane0);
+    const VecD<V> b = ld_vec<V>(v + (size_t)row * S + lane0);
+#pragma unroll
+    for (int j = 0; j < V; ++j) pr.v[j] = EP_DMUL(a.v[j], b.v[j]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < V; ++j) pr.v[j] = 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < V; ++j) sprod[slot * S + lane0 + j] = pr.v[j];
+  tiles_finish<S>(tm, sprod, f);
 }
 
 template <int S>
 static cudaError_t dot_tiles_s(const TileMap& tm, const double* u, const double* v,
-                               double* partials, cudaStream_t st) {
-  if (tm.num_tiles() == 0) return cudaSuccess;
-  k_dot_tiles<S><<<tm.num_tiles(), TileShape<S>::NT, 0, st>>>(tm, u, v, partials);
+                               const FinArgs& f, cudaStream_t st) {
+  const int blocks = (tm.num_tiles() + TileShape<S>::TPC - 1) / TileShape<S>::TPC;
+  if (blocks == 0) return cudaSuccess;
+  k_dot_tiles<S><<<blocks, TileShape<S>::NT, 0, st>>>(tm, u, v, f);
   return cudaGetLastError();
 }
 
 cudaError_t launch_dot_tiles(int s, const TileMap& tm, const double* u, const double* v,
-                             double* partials, cudaStream_t st) {
-  EP_DISPATCH_S(s, dot_tiles_s, tm, u, v, partials, st);
+                             const FinArgs& f, cudaStream_t st) {
+  EP_DISPATCH_S(s, dot_tiles_s, tm, u, v, f, st);
 }
 
 // =============================================================================
@@ -390,50 +480,6 @@ __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hi
   }
 }
 
-// Canonical finalize: segment sums (0.0 + tile_0 + tile_1 + ...), then the
-// lane total (0.0 + seg_0 + seg_1 + ...), then the scalar phase.
-template <int S>
-__global__ void __launch_bounds__(1024) k_fin_canonical(const TileMap tm,
-                                                        const double* __restrict__ partials,
-                                                        double* __restrict__ segbuf, int phase,
-                                                        CgState* cg, double* hist,
-                                                        double* lanes_out) {
-  if ((phase == kPhasePQ || phase == kPhaseRR) && cg->done) return;
-  __shared__ double lanes[S];
-  const int items = tm.num_segs * S;
-  for (int w = threadIdx.x; w < items; w += blockDim.x) {
-    const int seg = w / S, e = w - seg * S;
-    const int nt = tm.tiles_in_seg(seg);
-    const double* p = partials + (size_t)seg * tm.tiles_per_seg * S + e;
-    double acc = 0.0;
-#pragma unroll 8
-    for (int t = 0; t < nt; ++t) acc = EP_DADD(acc, p[(size_t)t * S]);
-    segbuf[w] = acc;
-  }
-  __syncthreads();
-  if (threadIdx.x < S) {
-    double tot = 0.0;
-    for (int seg = 0; seg < tm.num_segs; ++seg) tot = EP_DADD(tot, segbuf[seg * S + threadIdx.x]);
-    lanes[threadIdx.x] = tot;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) cg_phase<S>(phase, lanes, cg, hist, lanes_out);
-}
-
-template <int S>
-static cudaError_t fin_canonical_s(const TileMap& tm, const double* partials, double* segbuf,
-                                   int phase, CgState* cg, double* hist, double* lanes_out,
-                                   cudaStream_t st) {
-  k_fin_canonical<S><<<1, 1024, 0, st>>>(tm, partials, segbuf, phase, cg, hist, lanes_out);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_fin_canonical(int s, const TileMap& tm, const double* partials,
-                                 double* segbuf, int phase, CgState* cg, double* hist,
-                                 double* lanes_out, cudaStream_t st) {
-  EP_DISPATCH_S(s, fin_canonical_s, tm, partials, segbuf, phase, cg, hist, lanes_out, st);
-}
-
 // Serial finalize: the reference's own order (kernels.hpp:66-67), one chain
 // per sample: acc = 0; acc += u[row]*v[row] for row = 0, 1, ...  A single warp
 // runs the s chains; the vectors stream into shared memory through a 4-stage
@@ -530,108 +576,106 @@ cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v,
 }
 
 // =============================================================================
-// CG vector kernels.  One block per canonical tile (kTiles) or per run of
-// kTileRows rows (serial mode).  Early-exit when the solve is done, so a host
-// may enqueue iterations ahead of the convergence check.
+// CG vector kernels.  Flat row mapping: a block of 256 threads holds RPC row
+// slots (TPR threads per row, one row per slot), so every row of the grid is in
+// flight at once.  With kTiles the slots are the block's canonical tiles and
+// the fused finalize closes the dot; without (serial order) rows are
+// contiguous and a separate k_fin_serial forms the dot.  All kernels
+// early-exit once the solve is done, so the host may enqueue ahead.
 // =============================================================================
 template <int S, bool kTiles>
-__global__ void __launch_bounds__(TileShape<S>::NT) k_cg_spmv(
+__device__ __forceinline__ int cg_row(const TileMap& tm, int slot) {
+  if constexpr (kTiles) {
+    return tile_row<S>(tm, slot);
+  } else {
+    const int row = blockIdx.x * TileShape<S>::RPC + slot;
+    return row < tm.rows ? row : -1;
+  }
+}
+
+template <int S, bool kTiles>
+__global__ void __launch_bounds__(256, 4) k_cg_spmv(
     const TileMap tm, const int* __restrict__ row_map, const int* __restrict__ col_entry,
     const double* __restrict__ values, const double* __restrict__ r,
     const double* __restrict__ p_old, double* __restrict__ p_new, double* __restrict__ q,
-    const CgState* __restrict__ cg, double* __restrict__ partials) {
+    const FinArgs f) {
   using Sh = TileShape<S>;
   constexpr int V = Sh::V;
+  const CgState* cg = f.cg;
   if (cg->done) return;
-  __shared__ double sprod[kTiles ? kTileRows * S : 1];
-  int r0, nr;
-  if constexpr (kTiles) {
-    tm.tile(blockIdx.x, r0, nr);
-  } else {
-    r0 = blockIdx.x * kTileRows;
-    nr = min(kTileRows, tm.rows - r0);
-  }
-  if (nr <= 0) return;
+  __shared__ double sprod[kTiles ? Sh::RPC * S : 1];
+  const int slot = threadIdx.x / Sh::TPR;
   const int lane0 = (threadIdx.x % Sh::TPR) * V;
   const bool first = cg->it == 0;
   VecD<V> beta;
 #pragma unroll
   for (int j = 0; j < V; ++j) beta.v[j] = cg->beta[lane0 + j];
+  const int row = cg_row<S, kTiles>(tm, slot);
+  VecD<V> pr;
+  if (row >= 0) {
+    const VecD<V> sum = row_product<S, V, SpmvShape<S>::U, true>(row, row_map, col_entry, values,
+                                                                 r, p_old, first, beta, lane0);
+    VecD<V> pn = ld_vec<V>(r + (size_t)row * S + lane0);
+    if (!first) {
+      const VecD<V> po = ld_vec<V>(p_old + (size_t)row * S + lane0);
 #pragma unroll
-  for (int pass = 0; pass < Sh::PASSES; ++pass) {
-    const int rl = pass * Sh::RPP + threadIdx.x / Sh::TPR;
-    VecD<V> pr;
-    if (rl < nr) {
-      const int row = r0 + rl;
-      const VecD<V> sum = row_product<S, V, SpmvShape<S>::U, true>(row, row_map, col_entry, values,
-                                                                   r, p_old, first, beta, lane0);
-      VecD<V> pn = ld_vec<V>(r + (size_t)row * S + lane0);
-      if (!first) {
-        const VecD<V> po = ld_vec<V>(p_old + (size_t)row * S + lane0);
-#pragma unroll
-        for (int j = 0; j < V; ++j) pn.v[j] = EP_DADD(pn.v[j], EP_DMUL(beta.v[j], po.v[j]));
-      }
-      st_vec<V>(p_new + (size_t)row * S + lane0, pn);
-      st_vec<V>(q + (size_t)row * S + lane0, sum);
-#pragma unroll
-      for (int j = 0; j < V; ++j) pr.v[j] = EP_DMUL(pn.v[j], sum.v[j]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < V; ++j) pr.v[j] = 0.0;
+      for (int j = 0; j < V; ++j) pn.v[j] = EP_DADD(pn.v[j], EP_DMUL(beta.v[j], po.v[j]));
     }
-    if constexpr (kTiles) {
+    st_vec<V>(p_new + (size_t)row * S + lane0, pn);
+    st_vec<V>(q + (size_t)row * S + lane0, sum);
 #pragma unroll
-      for (int j = 0; j < V; ++j) sprod[rl * S + lane0 + j] = pr.v[j];
-    }
+    for (int j = 0; j < V; ++j) pr.v[j] = EP_DMUL(pn.v[j], sum.v[j]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < V; ++j) pr.v[j] = 0.0;
   }
-  if constexpr (kTiles) tile_fold_store<S, Sh::NT>(sprod, partials + (size_t)blockIdx.x * S);
+  if constexpr (kTiles) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) sprod[slot * S + lane0 + j] = pr.v[j];
+    tiles_finish<S>(tm, sprod, f);
+  }
+}
+
+template <int S>
+static int cg_blocks(bool tiles, const TileMap& tm) {
+  using Sh = TileShape<S>;
+  return tiles ? (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC : (tm.rows + Sh::RPC - 1) / Sh::RPC;
 }
 
 template <int S>
 static cudaError_t cg_spmv_s(bool tiles, const TileMap& tm, const int* row_map,
                              const int* col_entry, const double* values, const double* r,
-                             const double* p_old, double* p_new, double* q, const CgState* cg,
-                             double* partials, cudaStream_t st) {
-  if (tiles) {
-    if (tm.num_tiles() == 0) return cudaSuccess;
-    k_cg_spmv<S, true><<<tm.num_tiles(), TileShape<S>::NT, 0, st>>>(
-        tm, row_map, col_entry, values, r, p_old, p_new, q, cg, partials);
-  } else {
-    const int blocks = (tm.rows + kTileRows - 1) / kTileRows;
-    if (blocks == 0) return cudaSuccess;
-    k_cg_spmv<S, false><<<blocks, TileShape<S>::NT, 0, st>>>(tm, row_map, col_entry, values, r,
-                                                              p_old, p_new, q, cg, partials);
-  }
+                             const double* p_old, double* p_new, double* q, const FinArgs& f,
+                             cudaStream_t st) {
+  const int blocks = cg_blocks<S>(tiles, tm);
+  if (blocks == 0) return cudaSuccess;
+  if (tiles)
+    k_cg_spmv<S, true><<<blocks, 256, 0, st>>>(tm, row_map, col_entry, values, r, p_old, p_new, q, f);
+  else
+    k_cg_spmv<S, false><<<blocks, 256, 0, st>>>(tm, row_map, col_entry, values, r, p_old, p_new, q, f);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_spmv(int s, bool tiles, const TileMap& tm, const int* row_map,
                            const int* col_entry, const double* values, const double* r,
-                           const double* p_old, double* p_new, double* q, const CgState* cg,
-                           double* partials, cudaStream_t st) {
-  EP_DISPATCH_S(s, cg_spmv_s, tiles, tm, row_map, col_entry, values, r, p_old, p_new, q, cg,
-                partials, st);
+                           const double* p_old, double* p_new, double* q, const FinArgs& f,
+                           cudaStream_t st) {
+  EP_DISPATCH_S(s, cg_spmv_s, tiles, tm, row_map, col_entry, values, r, p_old, p_new, q, f, st);
 }
 
 // x = alpha*p + x; r = (-alpha)*q + r on active lanes (pcg.hpp:94-95 via
-// axpby, kernels.hpp:84: 1.0*y is exact); r.r tile partials for the next dot.
+// axpby, kernels.hpp:84: 1.0*y is exact); r.r for the next dot.
 template <int S, bool kTiles>
-__global__ void __launch_bounds__(TileShape<S>::NT) k_cg_update(
-    const TileMap tm, double* __restrict__ x, const double* __restrict__ p,
-    double* __restrict__ r, const double* __restrict__ q, const CgState* __restrict__ cg,
-    double* __restrict__ partials) {
+__global__ void __launch_bounds__(256) k_cg_update(const TileMap tm, double* __restrict__ x,
+                                                   const double* __restrict__ p,
+                                                   double* __restrict__ r,
+                                                   const double* __restrict__ q, const FinArgs f) {
   using Sh = TileShape<S>;
   constexpr int V = Sh::V;
+  const CgState* cg = f.cg;
   if (cg->done) return;
-  __shared__ double sprod[kTiles ? kTileRows * S : 1];
-  int r0, nr;
-  if constexpr (kTiles) {
-    tm.tile(blockIdx.x, r0, nr);
-  } else {
-    r0 = blockIdx.x * kTileRows;
-    nr = min(kTileRows, tm.rows - r0);
-  }
-  if (nr <= 0) return;
+  __shared__ double sprod[kTiles ? Sh::RPC * S : 1];
+  const int slot = threadIdx.x / Sh::TPR;
   const int lane0 = (threadIdx.x % Sh::TPR) * V;
   double al[V];
   bool act[V];
@@ -640,55 +684,46 @@ __global__ void __launch_bounds__(TileShape<S>::NT) k_cg_update(
     al[j] = cg->alpha[lane0 + j];
     act[j] = cg->active[lane0 + j] != 0;
   }
+  const int row = cg_row<S, kTiles>(tm, slot);
+  VecD<V> pr;
+  if (row >= 0) {
+    const size_t off = (size_t)row * S + lane0;
+    VecD<V> xv = ld_vec<V>(x + off), rv = ld_vec<V>(r + off);
+    const VecD<V> pv = ld_vec<V>(p + off), qv = ld_vec<V>(q + off);
 #pragma unroll
-  for (int pass = 0; pass < Sh::PASSES; ++pass) {
-    const int rl = pass * Sh::RPP + threadIdx.x / Sh::TPR;
-    VecD<V> pr;
-    if (rl < nr) {
-      const size_t off = (size_t)(r0 + rl) * S + lane0;
-      VecD<V> xv = ld_vec<V>(x + off), rv = ld_vec<V>(r + off);
-      const VecD<V> pv = ld_vec<V>(p + off), qv = ld_vec<V>(q + off);
-#pragma unroll
-      for (int j = 0; j < V; ++j) {
-        if (act[j]) {
-          xv.v[j] = EP_DADD(EP_DMUL(al[j], pv.v[j]), xv.v[j]);
-          rv.v[j] = EP_DADD(EP_DMUL(-al[j], qv.v[j]), rv.v[j]);
-        }
-        pr.v[j] = EP_DMUL(rv.v[j], rv.v[j]);
+    for (int j = 0; j < V; ++j) {
+      if (act[j]) {
+        xv.v[j] = EP_DADD(EP_DMUL(al[j], pv.v[j]), xv.v[j]);
+        rv.v[j] = EP_DADD(EP_DMUL(-al[j], qv.v[j]), rv.v[j]);
       }
-      st_vec<V>(x + off, xv);
-      st_vec<V>(r + off, rv);
-    } else {
-#pragma unroll
-      for (int j = 0; j < V; ++j) pr.v[j] = 0.0;
+      pr.v[j] = EP_DMUL(rv.v[j], rv.v[j]);
     }
-    if constexpr (kTiles) {
+    st_vec<V>(x + off, xv);
+    st_vec<V>(r + off, rv);
+  } else {
 #pragma unroll
-      for (int j = 0; j < V; ++j) sprod[rl * S + lane0 + j] = pr.v[j];
-    }
+    for (int j = 0; j < V; ++j) pr.v[j] = 0.0;
   }
-  if constexpr (kTiles) tile_fold_store<S, Sh::NT>(sprod, partials + (size_t)blockIdx.x * S);
+  if constexpr (kTiles) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) sprod[slot * S + lane0 + j] = pr.v[j];
+    tiles_finish<S>(tm, sprod, f);
+  }
 }
 
 template <int S>
 static cudaError_t cg_update_s(bool tiles, const TileMap& tm, double* x, const double* p,
-                               double* r, const double* q, const CgState* cg, double* partials,
-                               cudaStream_t st) {
-  if (tiles) {
-    if (tm.num_tiles() == 0) return cudaSuccess;
-    k_cg_update<S, true><<<tm.num_tiles(), TileShape<S>::NT, 0, st>>>(tm, x, p, r, q, cg, partials);
-  } else {
-    const int blocks = (tm.rows + kTileRows - 1) / kTileRows;
-    if (blocks == 0) return cudaSuccess;
-    k_cg_update<S, false><<<blocks, TileShape<S>::NT, 0, st>>>(tm, x, p, r, q, cg, partials);
-  }
+                               double* r, const double* q, const FinArgs& f, cudaStream_t st) {
+  const int blocks = cg_blocks<S>(tiles, tm);
+  if (blocks == 0) return cudaSuccess;
+  if (tiles) k_cg_update<S, true><<<blocks, 256, 0, st>>>(tm, x, p, r, q, f);
+  else k_cg_update<S, false><<<blocks, 256, 0, st>>>(tm, x, p, r, q, f);
   return cudaGetLastError();
 }
 
 cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* x, const double* p,
-                             double* r, const double* q, const CgState* cg, double* partials,
-                             cudaStream_t st) {
-  EP_DISPATCH_S(s, cg_update_s, tiles, tm, x, p, r, q, cg, partials, st);
+                             double* r, const double* q, const FinArgs& f, cudaStream_t st) {
+  EP_DISPATCH_S(s, cg_update_s, tiles, tm, x, p, r, q, f, st);
 }
 
 }  // namespace ep

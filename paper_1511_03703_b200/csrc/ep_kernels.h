@@ -50,6 +50,20 @@ struct CgState {
 
 enum Phase { kPhaseNone = 0, kPhaseInit = 1, kPhasePQ = 2, kPhaseRR = 3 };
 
+// Fused canonical finalize (ep_kernels.cu tiles_finish): where the tile
+// partials go, the self-resetting arrival counters, and what to do with the
+// lane totals (a CG scalar phase, or write them to lanes_out for kPhaseNone).
+struct FinArgs {
+  double* partials;  // [num_tiles][s]
+  double* seg_sums;  // [num_segs][s]
+  int* seg_count;    // [num_segs], zero between launches
+  int* seg_done;     // [1], zero between launches
+  int phase;
+  CgState* cg;
+  double* hist;
+  double* lanes_out;  // [s + 1] for kPhaseNone
+};
+
 cudaError_t launch_build_graph(int n, int* row_map, int* col_entry, cudaStream_t st);
 cudaError_t launch_assemble(int s, const AsmArgs& a, cudaStream_t st);
 cudaError_t launch_dirichlet(int s, int n, double bc0, double bc1, const int* row_map,
@@ -59,26 +73,20 @@ cudaError_t launch_spmv(int s, int rows, const int* row_map, const int* col_entr
                         const double* values, const double* x, double* z, cudaStream_t st);
 cudaError_t launch_axpby(int s, int64_t n, int per_lane, const double* alpha, const double* beta,
                          const double* x, double* y, cudaStream_t st);
-// canonical dot: tile partials [num_tiles][s]
+// canonical dot of u.v with the fused finalize running f.phase
 cudaError_t launch_dot_tiles(int s, const TileMap& tm, const double* u, const double* v,
-                             double* partials, cudaStream_t st);
-// reduce tile partials in canonical order, then run `phase` on the CG state
-// (or write lanes to lanes_out for kPhaseNone)
-cudaError_t launch_fin_canonical(int s, const TileMap& tm, const double* partials,
-                                 double* segbuf, int phase, CgState* cg, double* hist,
-                                 double* lanes_out, cudaStream_t st);
+                             const FinArgs& f, cudaStream_t st);
 // serial (reference-order) dot straight from the vectors, then `phase`
 cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v, int phase,
                               CgState* cg, double* hist, double* lanes_out, cudaStream_t st);
 // q = A p_new with p_new = (it==0 ? r : r + beta*p_old) formed on the fly; writes
-// p_new and q; with tiles, also the p_new.q tile partials
+// p_new and q; with tiles, also the canonical p_new.q and its CG phase (f)
 cudaError_t launch_cg_spmv(int s, bool tiles, const TileMap& tm, const int* row_map,
                            const int* col_entry, const double* values, const double* r,
-                           const double* p_old, double* p_new, double* q, const CgState* cg,
-                           double* partials, cudaStream_t st);
-// x += alpha p; r -= alpha q on active lanes; with tiles, also r.r tile partials
+                           const double* p_old, double* p_new, double* q, const FinArgs& f,
+                           cudaStream_t st);
+// x += alpha p; r -= alpha q on active lanes; with tiles, also r.r and its phase
 cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* x, const double* p,
-                             double* r, const double* q, const CgState* cg, double* partials,
-                             cudaStream_t st);
+                             double* r, const double* q, const FinArgs& f, cudaStream_t st);
 
 }  // namespace ep

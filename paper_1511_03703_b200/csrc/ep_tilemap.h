@@ -4,7 +4,7 @@
 
 namespace ep {
 
-constexpr int kTileRows = 64;
+constexpr int kTileRows = 16;
 
 // Canonical tile map: rows are cut into segments of seg_rows, each segment into
 // tiles of kTileRows aligned at the segment start.

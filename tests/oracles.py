@@ -24,7 +24,7 @@ _ip = C.POINTER(C.c_int)
 
 DOT_SERIAL, DOT_CANONICAL = 0, 1
 CG_COUPLED, CG_UNCOUPLED = 0, 1
-TILE_ROWS = 64
+TILE_ROWS = 16
 
 
 def dptr(a):

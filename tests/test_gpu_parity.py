@@ -14,8 +14,8 @@ import pytest
 import torch
 
 import paper_1511_03703_b200 as ep
-from oracles import (CG_COUPLED, CG_UNCOUPLED, DOT_CANONICAL, DOT_SERIAL, Oracle, RefLib, bits,
-                     pack_group)
+from oracles import (CG_COUPLED, CG_UNCOUPLED, DOT_CANONICAL, DOT_SERIAL, TILE_ROWS, Oracle, RefLib,
+                     bits, pack_group)
 
 pytestmark = pytest.mark.gpu
 WIDTHS = (1, 2, 4, 8, 16, 32)
@@ -211,8 +211,8 @@ def test_dot_canonical_equals_restatement(ctx, s):
     for n, seg in ((1, 4096), (300, 64), (4225, 4225), (70001, 4225)):
         u, v = rng.uniform(-1, 1, (n, s)), rng.uniform(-1, 1, (n, s))
         lanes, coupled = ep.dot_lanes(ctx, s, dev(u), dev(v), ep.DOT_CANONICAL, seg)
-        assert lanes == list(O.dot_lanes(s, u, v, DOT_CANONICAL, 64, seg))
-        assert coupled == O.dot(s, u, v, DOT_CANONICAL, 64, seg)
+        assert lanes == list(O.dot_lanes(s, u, v, DOT_CANONICAL, TILE_ROWS, seg))
+        assert coupled == O.dot(s, u, v, DOT_CANONICAL, TILE_ROWS, seg)
     z = np.zeros((10, s))
     assert ep.norm2(ctx, s, dev(z)) == 0.0
 

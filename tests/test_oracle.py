@@ -10,8 +10,8 @@ import os
 import numpy as np
 import pytest
 
-from oracles import (CG_COUPLED, CG_UNCOUPLED, DOT_CANONICAL, DOT_SERIAL, REF_SO, Oracle, RefLib,
-                     bits, pack_group)
+from oracles import (CG_COUPLED, CG_UNCOUPLED, DOT_CANONICAL, DOT_SERIAL, REF_SO, TILE_ROWS, Oracle,
+                     RefLib, bits, pack_group)
 
 GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz"))
 O = Oracle()
@@ -104,17 +104,17 @@ def test_canonical_dot_definition():
     for n, seg in ((1, 7), (200, 64), (1000, 137), (4225, 4225)):
         u = rng.uniform(-1, 1, (n, 4))
         v = rng.uniform(-1, 1, (n, 4))
-        lanes = O.dot_lanes(4, u, v, DOT_CANONICAL, 64, seg)
+        lanes = O.dot_lanes(4, u, v, DOT_CANONICAL, TILE_ROWS, seg)
         for e in range(4):
             total = 0.0
             for r0 in range(0, n, seg):
                 r1 = min(r0 + seg, n)
                 sg = 0.0
-                for t0 in range(r0, r1, 64):
-                    t = np.zeros(64)
-                    k = min(64, r1 - t0)
+                for t0 in range(r0, r1, TILE_ROWS):
+                    t = np.zeros(TILE_ROWS)
+                    k = min(TILE_ROWS, r1 - t0)
                     t[:k] = u[t0:t0 + k, e] * v[t0:t0 + k, e]
-                    h = 32
+                    h = TILE_ROWS // 2
                     while h >= 1:
                         t[:h] = t[:h] + t[h:2 * h]
                         h //= 2
