@@ -63,6 +63,12 @@ void* enprop_ctx_stream(enprop_ctx* ctx);
 int enprop_ctx_synchronize(enprop_ctx* ctx);
 /* number of enprop kernels launched through this context so far */
 int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
+/* Tuning options (results are bitwise identical either way):
+ *   ENPROP_OPT_FUSED_DIRECTION (default 1): form p = r + beta p inside the CG
+ *   SpMV from gathers of r and p_old; 0 = separate direction pass, then an
+ *   SpMV with a single gather. */
+enum { ENPROP_OPT_FUSED_DIRECTION = 1 };
+int enprop_ctx_set_option(enprop_ctx* ctx, int option, int value);
 /* Event timing of the CG SpMV kernel launches on the context stream (used by
  * bench.py for the roofline). Returns the totals accumulated since the last
  * reset; enable = 1/0 turns timing on/off and resets, enable = -1 only reads. */

@@ -30,6 +30,7 @@ OK, ERR_INVALID, ERR_NO_CONVERGENCE, ERR_INDEFINITE, ERR_CUDA, ERR_OOM = range(6
 DOT_SERIAL, DOT_CANONICAL = 0, 1
 CG_COUPLED, CG_UNCOUPLED = 0, 1
 TILE_ROWS = 16
+OPT_FUSED_DIRECTION = 1
 WIDTHS = (1, 2, 4, 8, 16, 32)
 
 _dp = C.POINTER(C.c_double)
@@ -146,6 +147,7 @@ def lib() -> C.CDLL:
     L.enprop_ctx_synchronize.argtypes = [_vp]
     L.enprop_ctx_launch_count.argtypes = [_vp]
     L.enprop_ctx_profile.argtypes = [_vp, C.c_int, _dp, C.POINTER(C.c_int64)]
+    L.enprop_ctx_set_option.argtypes = [_vp, C.c_int, C.c_int]
     L.enprop_build_node_graph.argtypes = [_vp, C.c_int, _vp, _vp]
     L.enprop_kl_describe.argtypes = [C.POINTER(_KlParams), _ip, _dp, _dp, _dp, _dp, _ip]
     L.enprop_assemble.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(_KlParams), C.POINTER(_Coeffs),
@@ -220,6 +222,10 @@ class Context:
     @property
     def launches(self) -> int:
         return int(lib().enprop_ctx_launch_count(self.h))
+
+    def set_option(self, option: int, value: int):
+        """enprop_ctx_set_option (e.g. OPT_FUSED_DIRECTION); bitwise-neutral."""
+        _check(lib().enprop_ctx_set_option(self.h, option, value), "set_option")
 
     def profile(self, enable: int = -1):
         """(total ms, launches) of CG SpMV kernels timed with CUDA events on

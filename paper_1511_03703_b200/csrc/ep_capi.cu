@@ -48,6 +48,7 @@ struct enprop_ctx {
   int64_t launches = 0;
   int* pinned_flags = nullptr;  // [2] convergence flags read back by the CG driver
   cudaEvent_t flag_ev[2] = {nullptr, nullptr};
+  int fused_direction = 1;  // ENPROP_OPT_FUSED_DIRECTION
   // optional CUDA-event timing of the CG SpMV launches (bench roofline)
   int profile = 0;
   std::vector<cudaEvent_t> prof_ev;  // pairs (start, stop), reused
@@ -209,13 +210,13 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
         double* p_new = w.p[(launched + 1) & 1];
         cudaEvent_t* ev = ctx->profile ? prof_pair(ctx) : nullptr;
         if (ev) EP_CUDA(cudaEventRecord(ev[0], st));
-        EP_CUDA(launch_cg_spmv(s, canon, tm, row_map, col_entry, values, w.r, p_old, p_new, w.q,
-                               f_pq, st));
+        EP_CUDA(launch_cg_spmv(s, canon, ctx->fused_direction != 0, tm, row_map, col_entry, values,
+                               w.r, p_old, p_new, w.q, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[1], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, kPhasePQ, w.state, w.hist, nullptr, st));
         EP_CUDA(launch_cg_update(s, canon, tm, x, p_new, w.r, w.q, f_rr, st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, kPhaseRR, w.state, w.hist, nullptr, st));
-        ctx->launches += canon ? 2 : 4;
+        ctx->launches += (canon ? 2 : 4) + (ctx->fused_direction ? 0 : 1);
       }
     }
     // flag of this chunk
@@ -329,6 +330,17 @@ int enprop_ctx_synchronize(enprop_ctx* c) {
 }
 
 int64_t enprop_ctx_launch_count(enprop_ctx* c) { return c ? c->launches : 0; }
+
+int enprop_ctx_set_option(enprop_ctx* c, int option, int value) {
+  if (!c) return fail(ENPROP_ERR_INVALID, "null context");
+  switch (option) {
+    case ENPROP_OPT_FUSED_DIRECTION:
+      c->fused_direction = value ? 1 : 0;
+      return ENPROP_OK;
+    default:
+      return fail(ENPROP_ERR_INVALID, "enprop_ctx_set_option: unknown option");
+  }
+}
 
 int enprop_ctx_profile(enprop_ctx* c, int enable, double* spmv_ms, int64_t* spmv_launches) {
   if (!c) return fail(ENPROP_ERR_INVALID, "null context");

@@ -41,11 +41,11 @@ template <int V>
 __device__ __forceinline__ VecD<V> ld_stream(const double* p) {
   VecD<V> r;
   if constexpr (V == 1) {
-    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r.v[0]) : "l"(p));
+    asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r.v[0]) : "l"(p));
   } else {
 #pragma unroll
     for (int i = 0; i < V; i += 2)
-      asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+      asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
                    : "=d"(r.v[i]), "=d"(r.v[i + 1])
                    : "l"(p + i));
   }
@@ -82,7 +82,7 @@ __device__ __forceinline__ void st_vec(double* p, const VecD<V>& a) {
 
 __device__ __forceinline__ int ld_stream_i32(const int* p) {
   int r;
-  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
 }
 

@@ -80,11 +80,16 @@ __device__ __forceinline__ VecD<V> row_product(int row, const int* __restrict__ 
   VecD<V> sum;
 #pragma unroll
   for (int j = 0; j < V; ++j) sum.v[j] = 0.0;
+  // Column indices run one batch ahead, so a batch's gathers never wait on
+  // its own column loads (software pipelining of the col -> x dependency).
+  int cn[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) cn[u] = (rs + u < re) ? ld_stream_i32(col_entry + rs + u) : 0;
   for (int kb = rs; kb < re; kb += U) {
     int c[U];
     VecD<V> av[U], xv[U], pv[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) c[u] = (kb + u < re) ? ld_stream_i32(col_entry + kb + u) : 0;
+    for (int u = 0; u < U; ++u) c[u] = cn[u];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (kb + u < re) {
@@ -93,6 +98,9 @@ __device__ __forceinline__ VecD<V> row_product(int row, const int* __restrict__ 
         if (kCg && !first) pv[u] = ld_vec<V>(p_old + (size_t)c[u] * S + lane0);
       }
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      cn[u] = (kb + U + u < re) ? ld_stream_i32(col_entry + kb + U + u) : 0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (kb + u < re) {
@@ -183,24 +191,27 @@ cudaError_t launch_axpby(int s, int64_t n, int /*per_lane*/, const double* alpha
 // block that completes the last segment forms the total and runs the CG scalar
 // phase.  Counters reset themselves, so no launch or memset sits between.
 // =============================================================================
-template <int S>
+// Block shape: NT threads, TPR threads per row, RPC row slots per pass, P
+// passes per block (a thread owns P rows; their loads are issued together).
+template <int S, int P = 1>
 struct TileShape {
   static constexpr int V = SpmvShape<S>::V;
-  static constexpr int TPR = S / V;            // threads per row
-  static constexpr int NT = 256;               // threads per block
-  static constexpr int RPC = NT / TPR;         // row slots per block
-  static constexpr int TPC = RPC / kTileRows;  // tiles per block
-  static_assert(RPC % kTileRows == 0, "a block must own whole tiles");
+  static constexpr int TPR = S / V;                // threads per row
+  static constexpr int NT = 256;                   // threads per block
+  static constexpr int RPC = NT / TPR;             // row slots per pass
+  static constexpr int ROWS = RPC * P;             // row slots per block
+  static constexpr int TPC = ROWS / kTileRows;     // tiles per block
+  static_assert(RPC % kTileRows == 0, "a pass must cover whole tiles");
 };
 
 template <int S>
 __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hist,
                          double* lanes_out);
 
-// Row of slot `slot` of this block in canonical tiling (-1: none).
-template <int S>
+// Row of block slot `slot` in canonical tiling (-1: none).
+template <int S, int P>
 __device__ __forceinline__ int tile_row(const TileMap& tm, int slot) {
-  using Sh = TileShape<S>;
+  using Sh = TileShape<S, P>;
   const int tile = blockIdx.x * Sh::TPC + slot / kTileRows;
   if (tile >= tm.num_tiles()) return -1;
   int r0, nr;
@@ -209,11 +220,21 @@ __device__ __forceinline__ int tile_row(const TileMap& tm, int slot) {
   return ri < nr ? r0 + ri : -1;
 }
 
+__device__ __forceinline__ int atomic_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 constexpr int kSegChunk = 64;  // tile partials staged per step of a segment sum
 
-template <int S>
+// Tile trees + fused finalize. Ordering: threads write partials, bar.sync, then
+// one thread's acq_rel atomic publishes them (release is cumulative over the
+// CTA barrier) and, for the block completing a segment, acquires everyone
+// else's partials; partials are then read with ld.global.cg (L2).
+template <int S, int P>
 __device__ void tiles_finish(const TileMap& tm, double* sprod, const FinArgs& f) {
-  using Sh = TileShape<S>;
+  using Sh = TileShape<S, P>;
   __shared__ double schunk[kSegChunk * S];
   __shared__ double lanes[S];
   __shared__ int s_last[Sh::TPC];
@@ -238,10 +259,15 @@ __device__ void tiles_finish(const TileMap& tm, double* sprod, const FinArgs& f)
       if (nr > 0) f.partials[(size_t)tile * S + e] = sprod[lt * kTileRows * S + e];
     }
   }
-  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
     int nl = 0;
+    int cur = -1, cnt = 0;
+    auto flush = [&]() {
+      if (cnt == 0) return;
+      const int old = atomic_add_acq_rel_gpu(&f.seg_count[cur], cnt);
+      if (old + cnt == tm.tiles_in_seg(cur)) s_last[nl++] = cur;
+    };
     for (int lt = 0; lt < Sh::TPC; ++lt) {
       const int tile = blockIdx.x * Sh::TPC + lt;
       if (tile >= tm.num_tiles()) break;
@@ -249,15 +275,19 @@ __device__ void tiles_finish(const TileMap& tm, double* sprod, const FinArgs& f)
       tm.tile(tile, r0, nr);
       if (nr <= 0) continue;
       const int seg = tile / tm.tiles_per_seg;
-      const int old = atomicAdd(&f.seg_count[seg], 1);
-      if (old == tm.tiles_in_seg(seg) - 1) s_last[nl++] = seg;
+      if (seg != cur) {
+        flush();
+        cur = seg;
+        cnt = 0;
+      }
+      ++cnt;
     }
+    flush();
     s_nlast = nl;
   }
   __syncthreads();
   for (int k = 0; k < s_nlast; ++k) {
     const int seg = s_last[k];
-    __threadfence();
     const int nt = tm.tiles_in_seg(seg);
     const double* p = f.partials + (size_t)seg * tm.tiles_per_seg * S;
     double acc = 0.0;
@@ -265,18 +295,20 @@ __device__ void tiles_finish(const TileMap& tm, double* sprod, const FinArgs& f)
       const int cnt = min(kSegChunk, nt - t0);
       for (int idx = threadIdx.x; idx < cnt * S; idx += Sh::NT) schunk[idx] = __ldcg(p + (size_t)t0 * S + idx);
       __syncthreads();
-      if (threadIdx.x < S)
+      if (threadIdx.x < S) {
+#pragma unroll 8
         for (int t = 0; t < cnt; ++t) acc = EP_DADD(acc, schunk[t * S + threadIdx.x]);
+      }
       __syncthreads();
     }
     if (threadIdx.x < S) f.seg_sums[(size_t)seg * S + threadIdx.x] = acc;
-    if (threadIdx.x == 0) f.seg_count[seg] = 0;
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_final = (atomicAdd(f.seg_done, 1) == tm.num_segs - 1);
+    if (threadIdx.x == 0) {
+      f.seg_count[seg] = 0;
+      s_final = (atomic_add_acq_rel_gpu(f.seg_done, 1) == tm.num_segs - 1);
+    }
     __syncthreads();
     if (s_final) {
-      __threadfence();
       if (threadIdx.x < S) {
         double tot = 0.0;
         for (int sg = 0; sg < tm.num_segs; ++sg) tot = EP_DADD(tot, __ldcg(f.seg_sums + (size_t)sg * S + threadIdx.x));
@@ -291,36 +323,43 @@ __device__ void tiles_finish(const TileMap& tm, double* sprod, const FinArgs& f)
   }
 }
 
+constexpr int kStreamPasses = 4;  // rows per thread in the streaming (dot/update) kernels
+
 template <int S>
 __global__ void __launch_bounds__(256) k_dot_tiles(const TileMap tm, const double* __restrict__ u,
                                                    const double* __restrict__ v, const FinArgs f) {
-  using Sh = TileShape<S>;
+  constexpr int P = kStreamPasses;
+  using Sh = TileShape<S, P>;
   constexpr int V = Sh::V;
-  __shared__ double sprod[Sh::RPC * S];
-  const int slot = threadIdx.x / Sh::TPR;
+  __shared__ double sprod[Sh::ROWS * S];
   const int lane0 = (threadIdx.x % Sh::TPR) * V;
-  const int row = tile_row<S>(tm, slot);
-  VecD<V> pr;
-  if (row >= 0) {
-    const VecD<V> a = ld_vec<V>(u + (size_t)row * S + lane0);
-    const VecD<V> b = ld_vec<V>(v + (size_t)row * S + lane0);
+  VecD<V> a[P], b[P];
+  int row[P];
 #pragma unroll
-    for (int j = 0; j < V; ++j) pr.v[j] = EP_DMUL(a.v[j], b.v[j]);
-  } else {
-#pragma unroll
-    for (int j = 0; j < V; ++j) pr.v[j] = 0.0;
+  for (int ps = 0; ps < P; ++ps) {
+    row[ps] = tile_row<S, P>(tm, ps * Sh::RPC + threadIdx.x / Sh::TPR);
+    if (row[ps] >= 0) {
+      a[ps] = ld_vec<V>(u + (size_t)row[ps] * S + lane0);
+      b[ps] = ld_vec<V>(v + (size_t)row[ps] * S + lane0);
+    }
   }
 #pragma unroll
-  for (int j = 0; j < V; ++j) sprod[slot * S + lane0 + j] = pr.v[j];
-  tiles_finish<S>(tm, sprod, f);
+  for (int ps = 0; ps < P; ++ps) {
+    const int slot = ps * Sh::RPC + threadIdx.x / Sh::TPR;
+#pragma unroll
+    for (int j = 0; j < V; ++j)
+      sprod[slot * S + lane0 + j] = row[ps] >= 0 ? EP_DMUL(a[ps].v[j], b[ps].v[j]) : 0.0;
+  }
+  tiles_finish<S, P>(tm, sprod, f);
 }
 
 template <int S>
 static cudaError_t dot_tiles_s(const TileMap& tm, const double* u, const double* v,
                                const FinArgs& f, cudaStream_t st) {
-  const int blocks = (tm.num_tiles() + TileShape<S>::TPC - 1) / TileShape<S>::TPC;
+  using Sh = TileShape<S, kStreamPasses>;
+  const int blocks = (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC;
   if (blocks == 0) return cudaSuccess;
-  k_dot_tiles<S><<<blocks, TileShape<S>::NT, 0, st>>>(tm, u, v, f);
+  k_dot_tiles<S><<<blocks, Sh::NT, 0, st>>>(tm, u, v, f);
   return cudaGetLastError();
 }
 
@@ -576,52 +615,64 @@ cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v,
 }
 
 // =============================================================================
-// CG vector kernels.  Flat row mapping: a block of 256 threads holds RPC row
-// slots (TPR threads per row, one row per slot), so every row of the grid is in
-// flight at once.  With kTiles the slots are the block's canonical tiles and
-// the fused finalize closes the dot; without (serial order) rows are
-// contiguous and a separate k_fin_serial forms the dot.  All kernels
-// early-exit once the solve is done, so the host may enqueue ahead.
+// CG vector kernels.  Flat row mapping: TPR threads per row, one row per slot,
+// P slots per thread, so every row of the grid is in flight at once.  With
+// kTiles the slots are the block's canonical tiles and the fused finalize
+// closes the dot; without (serial order) rows are contiguous and a separate
+// k_fin_serial forms the dot.  All kernels early-exit once the solve is done,
+// so the host may enqueue ahead of its convergence check.
 // =============================================================================
-template <int S, bool kTiles>
+template <int S, int P, bool kTiles>
 __device__ __forceinline__ int cg_row(const TileMap& tm, int slot) {
   if constexpr (kTiles) {
-    return tile_row<S>(tm, slot);
+    return tile_row<S, P>(tm, slot);
   } else {
-    const int row = blockIdx.x * TileShape<S>::RPC + slot;
+    const int row = blockIdx.x * TileShape<S, P>::ROWS + slot;
     return row < tm.rows ? row : -1;
   }
 }
 
-template <int S, bool kTiles>
+// q = A p_new.  kFusedDir: p_new = (it == 0 ? r : r + beta*p_old) is formed on
+// the fly from gathers of r and p_old and written for the block's own rows
+// (saves the direction pass). Otherwise p_new was written by k_cg_direction
+// and is gathered directly (one gather per entry).  Both give the reference's
+// p = 1.0*z + beta*p (pcg.hpp:101) bit for bit.
+template <int S, bool kTiles, bool kFusedDir>
 __global__ void __launch_bounds__(256, 4) k_cg_spmv(
     const TileMap tm, const int* __restrict__ row_map, const int* __restrict__ col_entry,
     const double* __restrict__ values, const double* __restrict__ r,
     const double* __restrict__ p_old, double* __restrict__ p_new, double* __restrict__ q,
     const FinArgs f) {
-  using Sh = TileShape<S>;
+  using Sh = TileShape<S, 1>;
   constexpr int V = Sh::V;
   const CgState* cg = f.cg;
   if (cg->done) return;
-  __shared__ double sprod[kTiles ? Sh::RPC * S : 1];
+  __shared__ double sprod[kTiles ? Sh::ROWS * S : 1];
   const int slot = threadIdx.x / Sh::TPR;
   const int lane0 = (threadIdx.x % Sh::TPR) * V;
   const bool first = cg->it == 0;
   VecD<V> beta;
 #pragma unroll
   for (int j = 0; j < V; ++j) beta.v[j] = cg->beta[lane0 + j];
-  const int row = cg_row<S, kTiles>(tm, slot);
+  const int row = cg_row<S, 1, kTiles>(tm, slot);
   VecD<V> pr;
   if (row >= 0) {
-    const VecD<V> sum = row_product<S, V, SpmvShape<S>::U, true>(row, row_map, col_entry, values,
-                                                                 r, p_old, first, beta, lane0);
-    VecD<V> pn = ld_vec<V>(r + (size_t)row * S + lane0);
-    if (!first) {
-      const VecD<V> po = ld_vec<V>(p_old + (size_t)row * S + lane0);
+    VecD<V> sum, pn;
+    if constexpr (kFusedDir) {
+      sum = row_product<S, V, SpmvShape<S>::U, true>(row, row_map, col_entry, values, r, p_old,
+                                                     first, beta, lane0);
+      pn = ld_vec<V>(r + (size_t)row * S + lane0);
+      if (!first) {
+        const VecD<V> po = ld_vec<V>(p_old + (size_t)row * S + lane0);
 #pragma unroll
-      for (int j = 0; j < V; ++j) pn.v[j] = EP_DADD(pn.v[j], EP_DMUL(beta.v[j], po.v[j]));
+        for (int j = 0; j < V; ++j) pn.v[j] = EP_DADD(pn.v[j], EP_DMUL(beta.v[j], po.v[j]));
+      }
+      st_vec<V>(p_new + (size_t)row * S + lane0, pn);
+    } else {
+      sum = row_product<S, V, SpmvShape<S>::U, false>(row, row_map, col_entry, values, p_new,
+                                                      nullptr, true, beta, lane0);
+      pn = ld_vec<V>(p_new + (size_t)row * S + lane0);
     }
-    st_vec<V>(p_new + (size_t)row * S + lane0, pn);
     st_vec<V>(q + (size_t)row * S + lane0, sum);
 #pragma unroll
     for (int j = 0; j < V; ++j) pr.v[j] = EP_DMUL(pn.v[j], sum.v[j]);
@@ -632,50 +683,95 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
   if constexpr (kTiles) {
 #pragma unroll
     for (int j = 0; j < V; ++j) sprod[slot * S + lane0 + j] = pr.v[j];
-    tiles_finish<S>(tm, sprod, f);
+    tiles_finish<S, 1>(tm, sprod, f);
+  }
+}
+
+// p_new = (it == 0 ? r : 1.0*r + beta*p_old) on every row (split variant).
+template <int S>
+__global__ void __launch_bounds__(256) k_cg_direction(int rows, const double* __restrict__ r,
+                                                      const double* __restrict__ p_old,
+                                                      double* __restrict__ p_new,
+                                                      const CgState* __restrict__ cg) {
+  constexpr int P = kStreamPasses;
+  using Sh = TileShape<S, P>;
+  constexpr int V = Sh::V;
+  if (cg->done) return;
+  const bool first = cg->it == 0;
+  const int lane0 = (threadIdx.x % Sh::TPR) * V;
+  VecD<V> beta;
+#pragma unroll
+  for (int j = 0; j < V; ++j) beta.v[j] = cg->beta[lane0 + j];
+  VecD<V> rv[P], pv[P];
+#pragma unroll
+  for (int ps = 0; ps < P; ++ps) {
+    const int row = blockIdx.x * Sh::ROWS + ps * Sh::RPC + threadIdx.x / Sh::TPR;
+    if (row < rows) {
+      rv[ps] = ld_vec<V>(r + (size_t)row * S + lane0);
+      if (!first) pv[ps] = ld_vec<V>(p_old + (size_t)row * S + lane0);
+    }
+  }
+#pragma unroll
+  for (int ps = 0; ps < P; ++ps) {
+    const int row = blockIdx.x * Sh::ROWS + ps * Sh::RPC + threadIdx.x / Sh::TPR;
+    if (row < rows) {
+      VecD<V> pn = rv[ps];
+      if (!first) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) pn.v[j] = EP_DADD(pn.v[j], EP_DMUL(beta.v[j], pv[ps].v[j]));
+      }
+      st_vec<V>(p_new + (size_t)row * S + lane0, pn);
+    }
   }
 }
 
 template <int S>
-static int cg_blocks(bool tiles, const TileMap& tm) {
-  using Sh = TileShape<S>;
-  return tiles ? (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC : (tm.rows + Sh::RPC - 1) / Sh::RPC;
-}
-
-template <int S>
-static cudaError_t cg_spmv_s(bool tiles, const TileMap& tm, const int* row_map,
+static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, const TileMap& tm, const int* row_map,
                              const int* col_entry, const double* values, const double* r,
                              const double* p_old, double* p_new, double* q, const FinArgs& f,
                              cudaStream_t st) {
-  const int blocks = cg_blocks<S>(tiles, tm);
+  using Sh = TileShape<S, 1>;
+  const int blocks = tiles ? (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC : (tm.rows + Sh::ROWS - 1) / Sh::ROWS;
   if (blocks == 0) return cudaSuccess;
-  if (tiles)
-    k_cg_spmv<S, true><<<blocks, 256, 0, st>>>(tm, row_map, col_entry, values, r, p_old, p_new, q, f);
-  else
-    k_cg_spmv<S, false><<<blocks, 256, 0, st>>>(tm, row_map, col_entry, values, r, p_old, p_new, q, f);
+  if (!fused_dir) {
+    using Sd = TileShape<S, kStreamPasses>;
+    k_cg_direction<S><<<(tm.rows + Sd::ROWS - 1) / Sd::ROWS, 256, 0, st>>>(tm.rows, r, p_old, p_new, f.cg);
+  }
+#define EP_CG_SPMV(T, D) \
+  k_cg_spmv<S, T, D><<<blocks, 256, 0, st>>>(tm, row_map, col_entry, values, r, p_old, p_new, q, f)
+  if (tiles) {
+    if (fused_dir) EP_CG_SPMV(true, true);
+    else EP_CG_SPMV(true, false);
+  } else {
+    if (fused_dir) EP_CG_SPMV(false, true);
+    else EP_CG_SPMV(false, false);
+  }
+#undef EP_CG_SPMV
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_spmv(int s, bool tiles, const TileMap& tm, const int* row_map,
-                           const int* col_entry, const double* values, const double* r,
-                           const double* p_old, double* p_new, double* q, const FinArgs& f,
-                           cudaStream_t st) {
-  EP_DISPATCH_S(s, cg_spmv_s, tiles, tm, row_map, col_entry, values, r, p_old, p_new, q, f, st);
+cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, const TileMap& tm,
+                           const int* row_map, const int* col_entry, const double* values,
+                           const double* r, const double* p_old, double* p_new, double* q,
+                           const FinArgs& f, cudaStream_t st) {
+  EP_DISPATCH_S(s, cg_spmv_s, tiles, fused_dir, tm, row_map, col_entry, values, r, p_old, p_new, q,
+                f, st);
 }
 
 // x = alpha*p + x; r = (-alpha)*q + r on active lanes (pcg.hpp:94-95 via
-// axpby, kernels.hpp:84: 1.0*y is exact); r.r for the next dot.
+// axpby, kernels.hpp:84: 1.0*y is exact); r.r for the next dot.  P rows per
+// thread, all loads issued before any arithmetic.
 template <int S, bool kTiles>
 __global__ void __launch_bounds__(256) k_cg_update(const TileMap tm, double* __restrict__ x,
                                                    const double* __restrict__ p,
                                                    double* __restrict__ r,
                                                    const double* __restrict__ q, const FinArgs f) {
-  using Sh = TileShape<S>;
+  constexpr int P = kStreamPasses;
+  using Sh = TileShape<S, P>;
   constexpr int V = Sh::V;
   const CgState* cg = f.cg;
   if (cg->done) return;
-  __shared__ double sprod[kTiles ? Sh::RPC * S : 1];
-  const int slot = threadIdx.x / Sh::TPR;
+  __shared__ double sprod[kTiles ? Sh::ROWS * S : 1];
   const int lane0 = (threadIdx.x % Sh::TPR) * V;
   double al[V];
   bool act[V];
@@ -684,37 +780,52 @@ __global__ void __launch_bounds__(256) k_cg_update(const TileMap tm, double* __r
     al[j] = cg->alpha[lane0 + j];
     act[j] = cg->active[lane0 + j] != 0;
   }
-  const int row = cg_row<S, kTiles>(tm, slot);
-  VecD<V> pr;
-  if (row >= 0) {
-    const size_t off = (size_t)row * S + lane0;
-    VecD<V> xv = ld_vec<V>(x + off), rv = ld_vec<V>(r + off);
-    const VecD<V> pv = ld_vec<V>(p + off), qv = ld_vec<V>(q + off);
+  int row[P];
+  VecD<V> xv[P], rv[P], pv[P], qv[P];
 #pragma unroll
-    for (int j = 0; j < V; ++j) {
-      if (act[j]) {
-        xv.v[j] = EP_DADD(EP_DMUL(al[j], pv.v[j]), xv.v[j]);
-        rv.v[j] = EP_DADD(EP_DMUL(-al[j], qv.v[j]), rv.v[j]);
-      }
-      pr.v[j] = EP_DMUL(rv.v[j], rv.v[j]);
+  for (int ps = 0; ps < P; ++ps) {
+    row[ps] = cg_row<S, P, kTiles>(tm, ps * Sh::RPC + threadIdx.x / Sh::TPR);
+    if (row[ps] >= 0) {
+      const size_t off = (size_t)row[ps] * S + lane0;
+      xv[ps] = ld_vec<V>(x + off);
+      rv[ps] = ld_vec<V>(r + off);
+      pv[ps] = ld_vec<V>(p + off);
+      qv[ps] = ld_vec<V>(q + off);
     }
-    st_vec<V>(x + off, xv);
-    st_vec<V>(r + off, rv);
-  } else {
-#pragma unroll
-    for (int j = 0; j < V; ++j) pr.v[j] = 0.0;
   }
-  if constexpr (kTiles) {
 #pragma unroll
-    for (int j = 0; j < V; ++j) sprod[slot * S + lane0 + j] = pr.v[j];
-    tiles_finish<S>(tm, sprod, f);
+  for (int ps = 0; ps < P; ++ps) {
+    const int slot = ps * Sh::RPC + threadIdx.x / Sh::TPR;
+    VecD<V> pr;
+    if (row[ps] >= 0) {
+      const size_t off = (size_t)row[ps] * S + lane0;
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        if (act[j]) {
+          xv[ps].v[j] = EP_DADD(EP_DMUL(al[j], pv[ps].v[j]), xv[ps].v[j]);
+          rv[ps].v[j] = EP_DADD(EP_DMUL(-al[j], qv[ps].v[j]), rv[ps].v[j]);
+        }
+        pr.v[j] = EP_DMUL(rv[ps].v[j], rv[ps].v[j]);
+      }
+      st_vec<V>(x + off, xv[ps]);
+      st_vec<V>(r + off, rv[ps]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < V; ++j) pr.v[j] = 0.0;
+    }
+    if constexpr (kTiles) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) sprod[slot * S + lane0 + j] = pr.v[j];
+    }
   }
+  if constexpr (kTiles) tiles_finish<S, P>(tm, sprod, f);
 }
 
 template <int S>
 static cudaError_t cg_update_s(bool tiles, const TileMap& tm, double* x, const double* p,
                                double* r, const double* q, const FinArgs& f, cudaStream_t st) {
-  const int blocks = cg_blocks<S>(tiles, tm);
+  using Sh = TileShape<S, kStreamPasses>;
+  const int blocks = tiles ? (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC : (tm.rows + Sh::ROWS - 1) / Sh::ROWS;
   if (blocks == 0) return cudaSuccess;
   if (tiles) k_cg_update<S, true><<<blocks, 256, 0, st>>>(tm, x, p, r, q, f);
   else k_cg_update<S, false><<<blocks, 256, 0, st>>>(tm, x, p, r, q, f);

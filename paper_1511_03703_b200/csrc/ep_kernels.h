@@ -81,10 +81,12 @@ cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v,
                               CgState* cg, double* hist, double* lanes_out, cudaStream_t st);
 // q = A p_new with p_new = (it==0 ? r : r + beta*p_old) formed on the fly; writes
 // p_new and q; with tiles, also the canonical p_new.q and its CG phase (f)
-cudaError_t launch_cg_spmv(int s, bool tiles, const TileMap& tm, const int* row_map,
-                           const int* col_entry, const double* values, const double* r,
-                           const double* p_old, double* p_new, double* q, const FinArgs& f,
-                           cudaStream_t st);
+// fused_dir = false: a separate k_cg_direction pass writes p_new first and the
+// SpMV gathers it directly (one gather per entry instead of two)
+cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, const TileMap& tm,
+                           const int* row_map, const int* col_entry, const double* values,
+                           const double* r, const double* p_old, double* p_new, double* q,
+                           const FinArgs& f, cudaStream_t st);
 // x += alpha p; r -= alpha q on active lanes; with tiles, also r.r and its phase
 cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* x, const double* p,
                              double* r, const double* q, const FinArgs& f, cudaStream_t st);

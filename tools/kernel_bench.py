@@ -1,0 +1,85 @@
+"""Kernel-level timing of the CG step pieces at a given mesh / ensemble width
+(CUDA events on the library's stream).  Used to choose kernel variants; the
+official numbers come from bench.py.
+
+    python tools/kernel_bench.py [--n 64] [--s 32] [--steps 2]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import torch  # noqa: E402
+
+import paper_1511_03703_b200 as ep  # noqa: E402
+from oracles import Oracle, pack_group  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=64)
+    ap.add_argument("--s", type=int, default=32)
+    ap.add_argument("--steps", type=int, default=2)
+    args = ap.parse_args()
+    n, s = args.n, args.s
+    ctx = ep.Context(0)
+    O = Oracle()
+    y = torch.as_tensor(pack_group(O.draw_samples(0, s, 3), s)).cuda()
+    p = ep.Problem(ctx, n, s, ep.KlField(3, 1.0, 0.1, 1.0))
+    st = torch.cuda.current_stream()
+    out = {"n": n, "s": s}
+    # assembly
+    p.assemble(y)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(True), torch.cuda.Event(True)
+    a.record(st)
+    for _ in range(3):
+        p.assemble(y)
+    b.record(st)
+    torch.cuda.synchronize()
+    out["assemble_ms"] = a.elapsed_time(b) / 3
+    # plain spmv on the assembled matrix
+    x = torch.rand((p.rows, s), dtype=torch.float64, device="cuda")
+    z = torch.empty_like(x)
+    for _ in range(3):
+        ep.spmv(ctx, s, p.row_map, p.col_entry, p.values, x, z)
+    torch.cuda.synchronize()
+    a.record(st)
+    for _ in range(10):
+        ep.spmv(ctx, s, p.row_map, p.col_entry, p.values, x, z)
+    b.record(st)
+    torch.cuda.synchronize()
+    out["spmv_ms"] = a.elapsed_time(b) / 10
+    nnz, rows = p.nnz, p.rows
+    out["spmv_gbs"] = (nnz * (8 * s + 4) + 4 * (rows + 1) + 16 * s * rows) / (out["spmv_ms"] / 1e3) / 1e9
+    for mode_name, mode in (("canonical", ep.DOT_CANONICAL), ("serial", ep.DOT_SERIAL)):
+        for fused in (1, 0):
+            ctx.set_option(ep.OPT_FUSED_DIRECTION, fused)
+            cfg = ep.SolverConfig(tol=1e-6, max_iterations=10000, flavour=ep.CG_UNCOUPLED, dot_mode=mode)
+            p.solve(cfg)
+            torch.cuda.synchronize()
+            ctx.profile(1)
+            a.record(st)
+            its = []
+            for _ in range(args.steps):
+                it, _, _ = p.solve(cfg)
+                its.append(max(it))
+            b.record(st)
+            torch.cuda.synchronize()
+            sp_ms, sp_n = ctx.profile(0)
+            ms = a.elapsed_time(b) / args.steps
+            key = f"{mode_name}_fused{fused}"
+            out[key] = {"solve_ms": round(ms, 3), "iters": its, "ms_per_iter": round(ms / its[-1], 4),
+                        "spmv_phase_ms": round(sp_ms / max(sp_n, 1), 4)}
+            if mode_name == "serial" and args.steps > 1:
+                pass
+    ctx.set_option(ep.OPT_FUSED_DIRECTION, 1)
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
