@@ -96,9 +96,10 @@ def spmv_bytes(nnz, rows, s):
 
 
 def cg_spmv_bytes(nnz, rows, s):
-    """Algorithmic bytes of one CG SpMV launch: values, cols,
-    row_map, gathers of r and p_old (once each), writes of p_new and q."""
-    return nnz * (8 * s + 4) + 4 * (rows + 1) + 32 * s * rows
+    """Algorithmic bytes of the CG SpMV phase, split-direction
+    schedule: direction pass (read r, p_old; write p_new) + SpMV (values, cols,
+    row_map, p_new gathered once, q written once)."""
+    return 3 * 8 * s * rows + nnz * (8 * s + 4) + 4 * (rows + 1) + 16 * s * rows
 
 
 # --------------------------------------------------------------------------- ours
@@ -194,7 +195,7 @@ def run_ours(args):
     nnz, rows = prob.nnz, prob.rows
     avg_spmv_ms = spmv_ms / max(spmv_n, 1)
     achieved = cg_spmv_bytes(nnz, rows, S) / (avg_spmv_ms / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "k_cg_spmv<32,true>", "achieved": round(achieved, 1),
+    roofline = {"bound": "hbm", "kernel": "k_cg_direction<32> + k_cg_spmv<32,true,false>", "achieved": round(achieved, 1),
                 "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                 "traffic": None, "bytes_per_launch": cg_spmv_bytes(nnz, rows, S),
                 "avg_launch_ms": round(avg_spmv_ms, 4), "launches_timed": spmv_n,

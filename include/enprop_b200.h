@@ -64,7 +64,7 @@ int enprop_ctx_synchronize(enprop_ctx* ctx);
 /* number of enprop kernels launched through this context so far */
 int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
 /* Tuning options (results are bitwise identical either way):
- *   ENPROP_OPT_FUSED_DIRECTION (default 1): form p = r + beta p inside the CG
+ *   ENPROP_OPT_FUSED_DIRECTION (default 0): 1 = form p = r + beta p inside the CG
  *   SpMV from gathers of r and p_old; 0 = separate direction pass, then an
  *   SpMV with a single gather. */
 enum { ENPROP_OPT_FUSED_DIRECTION = 1 };

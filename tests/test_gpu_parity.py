@@ -423,3 +423,19 @@ def test_bench_config_64_cubed_properties(ctx):
         assert same(host(p1.values), host(p.values)[:, e:e + 1])
     p1.close()
     p.close()
+
+
+@pytest.mark.parametrize("mode", [DOT_SERIAL, DOT_CANONICAL])
+@pytest.mark.parametrize("s", [1, 8, 32])
+def test_cg_split_direction_option_is_bitwise_neutral(ctx, R, mode, s):
+    n = 9
+    rm, ce, v, b = mesh_system(R, s, n, seed=5)
+    cfg = ep.SolverConfig(tol=1e-8, flavour=ep.CG_UNCOUPLED, dot_mode=mode, seg_rows=(n + 1) ** 2)
+    args = (ctx, s, dev(rm, torch.int32), dev(ce, torch.int32), dev(v), dev(b), cfg)
+    a = ep.pcg_solve(*args)
+    ctx.set_option(ep.OPT_FUSED_DIRECTION, 1)
+    try:
+        c = ep.pcg_solve(*args)
+    finally:
+        ctx.set_option(ep.OPT_FUSED_DIRECTION, 0)
+    assert a.iterations == c.iterations and same(host(a.solution), host(c.solution))

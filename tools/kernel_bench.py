@@ -77,7 +77,7 @@ def main():
                         "spmv_phase_ms": round(sp_ms / max(sp_n, 1), 4)}
             if mode_name == "serial" and args.steps > 1:
                 pass
-    ctx.set_option(ep.OPT_FUSED_DIRECTION, 1)
+    ctx.set_option(ep.OPT_FUSED_DIRECTION, 0)
     print(json.dumps(out, indent=1))
 
 
