@@ -66,8 +66,10 @@ int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
 /* Tuning options (results are bitwise identical either way):
  *   ENPROP_OPT_FUSED_DIRECTION (default 0): 1 = form p = r + beta p inside the CG
  *   SpMV from gathers of r and p_old; 0 = separate direction pass, then an
- *   SpMV with a single gather. */
-enum { ENPROP_OPT_FUSED_DIRECTION = 1 };
+ *   SpMV with a single gather.
+ *   ENPROP_OPT_SPMV_PIPELINE (default 1): enprop_spmv loads the next batch's
+ *   column indices one batch ahead (software pipelining). */
+enum { ENPROP_OPT_FUSED_DIRECTION = 1, ENPROP_OPT_SPMV_PIPELINE = 2 };
 int enprop_ctx_set_option(enprop_ctx* ctx, int option, int value);
 /* Event timing of the CG SpMV kernel launches on the context stream (used by
  * bench.py for the roofline). Returns the totals accumulated since the last

@@ -31,6 +31,7 @@ DOT_SERIAL, DOT_CANONICAL = 0, 1
 CG_COUPLED, CG_UNCOUPLED = 0, 1
 TILE_ROWS = 16
 OPT_FUSED_DIRECTION = 1
+OPT_SPMV_PIPELINE = 2
 WIDTHS = (1, 2, 4, 8, 16, 32)
 
 _dp = C.POINTER(C.c_double)

@@ -48,6 +48,7 @@ struct enprop_ctx {
   int64_t launches = 0;
   int* pinned_flags = nullptr;  // [2] convergence flags read back by the CG driver
   cudaEvent_t flag_ev[2] = {nullptr, nullptr};
+  int spmv_pipeline = 1;    // ENPROP_OPT_SPMV_PIPELINE
   int fused_direction = 0;  // ENPROP_OPT_FUSED_DIRECTION (split measured faster on B200)
   // optional CUDA-event timing of the CG SpMV launches (bench roofline)
   int profile = 0;
@@ -337,6 +338,9 @@ int enprop_ctx_set_option(enprop_ctx* c, int option, int value) {
     case ENPROP_OPT_FUSED_DIRECTION:
       c->fused_direction = value ? 1 : 0;
       return ENPROP_OK;
+    case ENPROP_OPT_SPMV_PIPELINE:
+      c->spmv_pipeline = value ? 1 : 0;
+      return ENPROP_OK;
     default:
       return fail(ENPROP_ERR_INVALID, "enprop_ctx_set_option: unknown option");
   }
@@ -521,7 +525,7 @@ int enprop_spmv(enprop_ctx* c, int s, int rows, int cols, const int* row_map,
   if (rows < 0 || cols < 0) return fail(ENPROP_ERR_INVALID, "spmv: negative dimension");
   if (rows == 0) return ENPROP_OK;
   if (!row_map || !z || (cols > 0 && !x)) return fail(ENPROP_ERR_INVALID, "spmv: null argument");
-  EP_CUDA(launch_spmv(s, rows, row_map, col_entry, values, x, z, c->stream));
+  EP_CUDA(launch_spmv(s, rows, row_map, col_entry, values, x, z, c->spmv_pipeline != 0, c->stream));
   c->launches += 1;
   return ENPROP_OK;
 }

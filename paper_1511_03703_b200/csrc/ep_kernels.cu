@@ -69,7 +69,7 @@ struct SpmvShape {  // vector width per thread
   static constexpr int U = 4;  // entries per predicated batch
 };
 
-template <int S, int V, int U, bool kCg>
+template <int S, int V, int U, bool kCg, bool kPipe = true>
 __device__ __forceinline__ VecD<V> row_product(int row, const int* __restrict__ row_map,
                                                const int* __restrict__ col_entry,
                                                const double* __restrict__ values,
@@ -83,13 +83,15 @@ __device__ __forceinline__ VecD<V> row_product(int row, const int* __restrict__ 
   // Column indices run one batch ahead, so a batch's gathers never wait on
   // its own column loads (software pipelining of the col -> x dependency).
   int cn[U];
+  if constexpr (kPipe) {
 #pragma unroll
-  for (int u = 0; u < U; ++u) cn[u] = (rs + u < re) ? ld_stream_i32(col_entry + rs + u) : 0;
+    for (int u = 0; u < U; ++u) cn[u] = (rs + u < re) ? ld_stream_i32(col_entry + rs + u) : 0;
+  }
   for (int kb = rs; kb < re; kb += U) {
     int c[U];
     VecD<V> av[U], xv[U], pv[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) c[u] = cn[u];
+    for (int u = 0; u < U; ++u) c[u] = kPipe ? cn[u] : ((kb + u < re) ? ld_stream_i32(col_entry + kb + u) : 0);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (kb + u < re) {
@@ -98,9 +100,11 @@ __device__ __forceinline__ VecD<V> row_product(int row, const int* __restrict__ 
         if (kCg && !first) pv[u] = ld_vec<V>(p_old + (size_t)c[u] * S + lane0);
       }
     }
+    if constexpr (kPipe) {
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      cn[u] = (kb + U + u < re) ? ld_stream_i32(col_entry + kb + U + u) : 0;
+      for (int u = 0; u < U; ++u)
+        cn[u] = (kb + U + u < re) ? ld_stream_i32(col_entry + kb + U + u) : 0;
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (kb + u < re) {
@@ -116,7 +120,7 @@ __device__ __forceinline__ VecD<V> row_product(int row, const int* __restrict__ 
   return sum;
 }
 
-template <int S>
+template <int S, bool kPipe>
 __global__ void __launch_bounds__(256) k_spmv(int rows, const int* __restrict__ row_map,
                                               const int* __restrict__ col_entry,
                                               const double* __restrict__ values,
@@ -128,24 +132,29 @@ __global__ void __launch_bounds__(256) k_spmv(int rows, const int* __restrict__ 
   const int lane0 = (gt - row * Sh::TPR) * Sh::V;
   if (row >= rows) return;
   VecD<Sh::V> beta;
-  const VecD<Sh::V> sum = row_product<S, Sh::V, Sh::U, false>(row, row_map, col_entry, values, x,
-                                                               nullptr, true, beta, lane0);
+  const VecD<Sh::V> sum = row_product<S, Sh::V, Sh::U, false, kPipe>(row, row_map, col_entry,
+                                                                      values, x, nullptr, true,
+                                                                      beta, lane0);
   st_vec<Sh::V>(z + (size_t)row * S + lane0, sum);
 }
 
 template <int S>
 static cudaError_t spmv_s(int rows, const int* row_map, const int* col_entry,
-                          const double* values, const double* x, double* z, cudaStream_t st) {
+                          const double* values, const double* x, double* z, bool pipe,
+                          cudaStream_t st) {
   using Sh = SpmvShape<S>;
   const int64_t threads = (int64_t)rows * Sh::TPR;
   if (threads == 0) return cudaSuccess;
-  k_spmv<S><<<(int)((threads + 255) / 256), 256, 0, st>>>(rows, row_map, col_entry, values, x, z);
+  const int grid = (int)((threads + 255) / 256);
+  if (pipe) k_spmv<S, true><<<grid, 256, 0, st>>>(rows, row_map, col_entry, values, x, z);
+  else k_spmv<S, false><<<grid, 256, 0, st>>>(rows, row_map, col_entry, values, x, z);
   return cudaGetLastError();
 }
 
 cudaError_t launch_spmv(int s, int rows, const int* row_map, const int* col_entry,
-                        const double* values, const double* x, double* z, cudaStream_t st) {
-  EP_DISPATCH_S(s, spmv_s, rows, row_map, col_entry, values, x, z, st);
+                        const double* values, const double* x, double* z, bool pipe,
+                        cudaStream_t st) {
+  EP_DISPATCH_S(s, spmv_s, rows, row_map, col_entry, values, x, z, pipe, st);
 }
 
 // =============================================================================
@@ -309,11 +318,19 @@ __device__ void tiles_finish(const TileMap& tm, double* sprod, const FinArgs& f)
     }
     __syncthreads();
     if (s_final) {
-      if (threadIdx.x < S) {
-        double tot = 0.0;
-        for (int sg = 0; sg < tm.num_segs; ++sg) tot = EP_DADD(tot, __ldcg(f.seg_sums + (size_t)sg * S + threadIdx.x));
-        lanes[threadIdx.x] = tot;
+      double tot = 0.0;
+      for (int g0 = 0; g0 < tm.num_segs; g0 += kSegChunk) {
+        const int cnt = min(kSegChunk, tm.num_segs - g0);
+        for (int idx = threadIdx.x; idx < cnt * S; idx += Sh::NT)
+          schunk[idx] = __ldcg(f.seg_sums + (size_t)g0 * S + idx);
+        __syncthreads();
+        if (threadIdx.x < S) {
+#pragma unroll 8
+          for (int g = 0; g < cnt; ++g) tot = EP_DADD(tot, schunk[g * S + threadIdx.x]);
+        }
+        __syncthreads();
       }
+      if (threadIdx.x < S) lanes[threadIdx.x] = tot;
       __syncthreads();
       if (threadIdx.x == 0) {
         *f.seg_done = 0;

@@ -70,7 +70,8 @@ cudaError_t launch_dirichlet(int s, int n, double bc0, double bc1, const int* ro
                              const int* col_entry, const double* u, double* values,
                              double* residual, cudaStream_t st);
 cudaError_t launch_spmv(int s, int rows, const int* row_map, const int* col_entry,
-                        const double* values, const double* x, double* z, cudaStream_t st);
+                        const double* values, const double* x, double* z, bool pipe,
+                        cudaStream_t st);
 cudaError_t launch_axpby(int s, int64_t n, int per_lane, const double* alpha, const double* beta,
                          const double* x, double* y, cudaStream_t st);
 // canonical dot of u.v with the fused finalize running f.phase

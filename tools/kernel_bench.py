@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--n", type=int, default=64)
     ap.add_argument("--s", type=int, default=32)
     ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--spmv-only", action="store_true")
     args = ap.parse_args()
     n, s = args.n, args.s
     ctx = ep.Context(0)
@@ -45,17 +46,24 @@ def main():
     # plain spmv on the assembled matrix
     x = torch.rand((p.rows, s), dtype=torch.float64, device="cuda")
     z = torch.empty_like(x)
-    for _ in range(3):
-        ep.spmv(ctx, s, p.row_map, p.col_entry, p.values, x, z)
-    torch.cuda.synchronize()
-    a.record(st)
-    for _ in range(10):
-        ep.spmv(ctx, s, p.row_map, p.col_entry, p.values, x, z)
-    b.record(st)
-    torch.cuda.synchronize()
-    out["spmv_ms"] = a.elapsed_time(b) / 10
     nnz, rows = p.nnz, p.rows
-    out["spmv_gbs"] = (nnz * (8 * s + 4) + 4 * (rows + 1) + 16 * s * rows) / (out["spmv_ms"] / 1e3) / 1e9
+    for pipe in (1, 0):
+        ctx.set_option(ep.OPT_SPMV_PIPELINE, pipe)
+        for _ in range(3):
+            ep.spmv(ctx, s, p.row_map, p.col_entry, p.values, x, z)
+        torch.cuda.synchronize()
+        a.record(st)
+        for _ in range(10):
+            ep.spmv(ctx, s, p.row_map, p.col_entry, p.values, x, z)
+        b.record(st)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / 10
+        out[f"spmv_pipe{pipe}_ms"] = round(ms, 4)
+        out[f"spmv_pipe{pipe}_gbs"] = round((nnz * (8 * s + 4) + 4 * (rows + 1) + 16 * s * rows) / (ms / 1e3) / 1e9, 1)
+    ctx.set_option(ep.OPT_SPMV_PIPELINE, 1)
+    if args.spmv_only:
+        print(json.dumps(out, indent=1))
+        return
     for mode_name, mode in (("canonical", ep.DOT_CANONICAL), ("serial", ep.DOT_SERIAL)):
         for fused in (1, 0):
             ctx.set_option(ep.OPT_FUSED_DIRECTION, fused)
