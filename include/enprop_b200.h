@@ -67,7 +67,7 @@ int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
  *   ENPROP_OPT_FUSED_DIRECTION (default 0): 1 = form p = r + beta p inside the CG
  *   SpMV from gathers of r and p_old; 0 = separate direction pass, then an
  *   SpMV with a single gather.
- *   ENPROP_OPT_SPMV_PIPELINE (default 1): enprop_spmv loads the next batch's
+ *   ENPROP_OPT_SPMV_PIPELINE (default 0): 1 = enprop_spmv loads the next batch's
  *   column indices one batch ahead (software pipelining). */
 enum { ENPROP_OPT_FUSED_DIRECTION = 1, ENPROP_OPT_SPMV_PIPELINE = 2 };
 int enprop_ctx_set_option(enprop_ctx* ctx, int option, int value);

@@ -48,7 +48,7 @@ struct enprop_ctx {
   int64_t launches = 0;
   int* pinned_flags = nullptr;  // [2] convergence flags read back by the CG driver
   cudaEvent_t flag_ev[2] = {nullptr, nullptr};
-  int spmv_pipeline = 1;    // ENPROP_OPT_SPMV_PIPELINE
+  int spmv_pipeline = 0;    // ENPROP_OPT_SPMV_PIPELINE
   int fused_direction = 0;  // ENPROP_OPT_FUSED_DIRECTION (split measured faster on B200)
   // optional CUDA-event timing of the CG SpMV launches (bench roofline)
   int profile = 0;

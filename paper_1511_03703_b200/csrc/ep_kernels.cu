@@ -69,7 +69,7 @@ struct SpmvShape {  // vector width per thread
   static constexpr int U = 4;  // entries per predicated batch
 };
 
-template <int S, int V, int U, bool kCg, bool kPipe = true>
+template <int S, int V, int U, bool kCg, bool kPipe = false>
 __device__ __forceinline__ VecD<V> row_product(int row, const int* __restrict__ row_map,
                                                const int* __restrict__ col_entry,
                                                const double* __restrict__ values,
@@ -80,8 +80,9 @@ __device__ __forceinline__ VecD<V> row_product(int row, const int* __restrict__ 
   VecD<V> sum;
 #pragma unroll
   for (int j = 0; j < V; ++j) sum.v[j] = 0.0;
-  // Column indices run one batch ahead, so a batch's gathers never wait on
-  // its own column loads (software pipelining of the col -> x dependency).
+  // kPipe: column indices run one batch ahead of the gathers (software
+  // pipelining). Measured slower on B200 (6235 -> 4968 GB/s at 128^3), so off
+  // by default; kept for tuning (ENPROP_OPT_SPMV_PIPELINE).
   int cn[U];
   if constexpr (kPipe) {
 #pragma unroll

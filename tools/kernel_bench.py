@@ -60,7 +60,7 @@ def main():
         ms = a.elapsed_time(b) / 10
         out[f"spmv_pipe{pipe}_ms"] = round(ms, 4)
         out[f"spmv_pipe{pipe}_gbs"] = round((nnz * (8 * s + 4) + 4 * (rows + 1) + 16 * s * rows) / (ms / 1e3) / 1e9, 1)
-    ctx.set_option(ep.OPT_SPMV_PIPELINE, 1)
+    ctx.set_option(ep.OPT_SPMV_PIPELINE, 0)
     if args.spmv_only:
         print(json.dumps(out, indent=1))
         return
