@@ -212,10 +212,10 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
         cudaEvent_t* ev = ctx->profile ? prof_pair(ctx) : nullptr;
         if (ev) EP_CUDA(cudaEventRecord(ev[0], st));
         EP_CUDA(launch_cg_spmv(s, canon, ctx->fused_direction != 0, tm, row_map, col_entry, values,
-                               w.r, p_old, p_new, w.q, f_pq, st));
+                               w.r, p_old, p_new, w.q, x, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[1], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, kPhasePQ, w.state, w.hist, nullptr, st));
-        EP_CUDA(launch_cg_update(s, canon, tm, x, p_new, w.r, w.q, f_rr, st));
+        EP_CUDA(launch_cg_update(s, canon, tm, w.r, w.q, f_rr, st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, kPhaseRR, w.state, w.hist, nullptr, st));
         ctx->launches += (canon ? 2 : 4) + (ctx->fused_direction ? 0 : 1);
       }
@@ -235,6 +235,9 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
     pending = true;
     slot ^= 1;
   }
+  // the last finished iteration's x += alpha*p is still deferred
+  EP_CUDA(launch_cg_flush(s, rows, x, w.p, w.state, st));
+  ctx->launches += 1;
   EP_CUDA(cudaStreamSynchronize(st));
   if (ctx->profile) {
     rc = prof_collect(ctx);

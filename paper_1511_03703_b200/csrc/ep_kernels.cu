@@ -236,8 +236,6 @@ __device__ __forceinline__ int atomic_add_acq_rel_gpu(int* p, int v) {
   return old;
 }
 
-constexpr int kSegChunk = 64;  // tile partials staged per step of a segment sum
-
 // Tile trees + fused finalize. Ordering: threads write partials, bar.sync, then
 // one thread's acq_rel atomic publishes them (release is cumulative over the
 // CTA barrier) and, for the block completing a segment, acquires everyone
@@ -245,7 +243,8 @@ constexpr int kSegChunk = 64;  // tile partials staged per step of a segment sum
 template <int S, int P>
 __device__ void tiles_finish(const TileMap& tm, double* sprod, const FinArgs& f) {
   using Sh = TileShape<S, P>;
-  __shared__ double schunk[kSegChunk * S];
+  constexpr int kChunk = Sh::ROWS;  // tile partials staged per step (reuses sprod)
+  double* schunk = sprod;
   __shared__ double lanes[S];
   __shared__ int s_last[Sh::TPC];
   __shared__ int s_nlast, s_final;
@@ -301,8 +300,8 @@ __device__ void tiles_finish(const TileMap& tm, double* sprod, const FinArgs& f)
     const int nt = tm.tiles_in_seg(seg);
     const double* p = f.partials + (size_t)seg * tm.tiles_per_seg * S;
     double acc = 0.0;
-    for (int t0 = 0; t0 < nt; t0 += kSegChunk) {
-      const int cnt = min(kSegChunk, nt - t0);
+    for (int t0 = 0; t0 < nt; t0 += kChunk) {
+      const int cnt = min(kChunk, nt - t0);
       for (int idx = threadIdx.x; idx < cnt * S; idx += Sh::NT) schunk[idx] = __ldcg(p + (size_t)t0 * S + idx);
       __syncthreads();
       if (threadIdx.x < S) {
@@ -320,8 +319,8 @@ __device__ void tiles_finish(const TileMap& tm, double* sprod, const FinArgs& f)
     __syncthreads();
     if (s_final) {
       double tot = 0.0;
-      for (int g0 = 0; g0 < tm.num_segs; g0 += kSegChunk) {
-        const int cnt = min(kSegChunk, tm.num_segs - g0);
+      for (int g0 = 0; g0 < tm.num_segs; g0 += kChunk) {
+        const int cnt = min(kChunk, tm.num_segs - g0);
         for (int idx = threadIdx.x; idx < cnt * S; idx += Sh::NT)
           schunk[idx] = __ldcg(f.seg_sums + (size_t)g0 * S + idx);
         __syncthreads();
@@ -405,6 +404,13 @@ __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hi
   }
   const double tol = cg->tol;
   const int maxit = cg->maxit;
+  // Deferred x updates: RR records which lanes updated r (and so owe
+  // x += alpha*p); the next direction pass pays them, so PQ clears the record.
+  if (phase == kPhaseRR) {
+    for (int e = 0; e < S; ++e) cg->pending[e] = cg->active[e];
+  } else {
+    for (int e = 0; e < S; ++e) cg->pending[e] = 0;
+  }
   if (cg->flavour == 0) {  // ---------------------------------------------- coupled
     double d = 0.0;
     for (int e = 0; e < S; ++e) d = EP_DADD(d, lanes[e]);
@@ -660,7 +666,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
     const TileMap tm, const int* __restrict__ row_map, const int* __restrict__ col_entry,
     const double* __restrict__ values, const double* __restrict__ r,
     const double* __restrict__ p_old, double* __restrict__ p_new, double* __restrict__ q,
-    const FinArgs f) {
+    double* __restrict__ x, const FinArgs f) {
   using Sh = TileShape<S, 1>;
   constexpr int V = Sh::V;
   const CgState* cg = f.cg;
@@ -682,8 +688,13 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
       pn = ld_vec<V>(r + (size_t)row * S + lane0);
       if (!first) {
         const VecD<V> po = ld_vec<V>(p_old + (size_t)row * S + lane0);
+        VecD<V> xv = ld_vec<V>(x + (size_t)row * S + lane0);
 #pragma unroll
-        for (int j = 0; j < V; ++j) pn.v[j] = EP_DADD(pn.v[j], EP_DMUL(beta.v[j], po.v[j]));
+        for (int j = 0; j < V; ++j) {
+          pn.v[j] = EP_DADD(pn.v[j], EP_DMUL(beta.v[j], po.v[j]));
+          if (cg->pending[lane0 + j]) xv.v[j] = EP_DADD(EP_DMUL(cg->alpha[lane0 + j], po.v[j]), xv.v[j]);
+        }
+        st_vec<V>(x + (size_t)row * S + lane0, xv);
       }
       st_vec<V>(p_new + (size_t)row * S + lane0, pn);
     } else {
@@ -705,28 +716,45 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
   }
 }
 
-// p_new = (it == 0 ? r : 1.0*r + beta*p_old) on every row (split variant).
+// Direction pass (split variant), every row:
+//   x     = alpha_prev*p_old + x   on lanes that owe it (pcg.hpp:94, deferred
+//                                  from the previous iteration's update)
+//   p_new = 1.0*r + beta*p_old     (pcg.hpp:101; p_new = r when it == 0)
+// Both are the reference's operations on the same operands, only scheduled
+// where p_old is read anyway, which saves one vector pass per iteration.
+constexpr int kDirPasses = 2;
+
 template <int S>
 __global__ void __launch_bounds__(256) k_cg_direction(int rows, const double* __restrict__ r,
                                                       const double* __restrict__ p_old,
                                                       double* __restrict__ p_new,
+                                                      double* __restrict__ x,
                                                       const CgState* __restrict__ cg) {
-  constexpr int P = kStreamPasses;
+  constexpr int P = kDirPasses;
   using Sh = TileShape<S, P>;
   constexpr int V = Sh::V;
   if (cg->done) return;
   const bool first = cg->it == 0;
   const int lane0 = (threadIdx.x % Sh::TPR) * V;
   VecD<V> beta;
+  double al[V];
+  bool pend[V];
+  bool any = false;
 #pragma unroll
-  for (int j = 0; j < V; ++j) beta.v[j] = cg->beta[lane0 + j];
-  VecD<V> rv[P], pv[P];
+  for (int j = 0; j < V; ++j) {
+    beta.v[j] = cg->beta[lane0 + j];
+    al[j] = cg->alpha[lane0 + j];
+    pend[j] = !first && cg->pending[lane0 + j] != 0;
+    any |= pend[j];
+  }
+  VecD<V> rv[P], pv[P], xv[P];
 #pragma unroll
   for (int ps = 0; ps < P; ++ps) {
     const int row = blockIdx.x * Sh::ROWS + ps * Sh::RPC + threadIdx.x / Sh::TPR;
     if (row < rows) {
       rv[ps] = ld_vec<V>(r + (size_t)row * S + lane0);
       if (!first) pv[ps] = ld_vec<V>(p_old + (size_t)row * S + lane0);
+      if (any) xv[ps] = ld_vec<V>(x + (size_t)row * S + lane0);
     }
   }
 #pragma unroll
@@ -736,27 +764,60 @@ __global__ void __launch_bounds__(256) k_cg_direction(int rows, const double* __
       VecD<V> pn = rv[ps];
       if (!first) {
 #pragma unroll
-        for (int j = 0; j < V; ++j) pn.v[j] = EP_DADD(pn.v[j], EP_DMUL(beta.v[j], pv[ps].v[j]));
+        for (int j = 0; j < V; ++j) {
+          pn.v[j] = EP_DADD(pn.v[j], EP_DMUL(beta.v[j], pv[ps].v[j]));
+          if (pend[j]) xv[ps].v[j] = EP_DADD(EP_DMUL(al[j], pv[ps].v[j]), xv[ps].v[j]);
+        }
       }
       st_vec<V>(p_new + (size_t)row * S + lane0, pn);
+      if (any) st_vec<V>(x + (size_t)row * S + lane0, xv[ps]);
     }
   }
+}
+
+// After the loop: x = alpha*p_last + x on lanes still owing it (p_last is the
+// p of iteration it-1, i.e. buffer p[it & 1]).
+template <int S>
+__global__ void __launch_bounds__(256) k_cg_flush(int rows, double* __restrict__ x,
+                                                  const double* __restrict__ p0,
+                                                  const double* __restrict__ p1,
+                                                  const CgState* __restrict__ cg) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (int64_t)rows * S) return;
+  const int e = (int)(g % S);
+  if (!cg->pending[e]) return;
+  const double* p = (cg->it & 1) ? p1 : p0;
+  x[g] = EP_DADD(EP_DMUL(cg->alpha[e], p[g]), x[g]);
+}
+
+template <int S>
+static cudaError_t cg_flush_s(int rows, double* x, double* const* p, const CgState* cg,
+                              cudaStream_t st) {
+  const int64_t t = (int64_t)rows * S;
+  if (t == 0) return cudaSuccess;
+  k_cg_flush<S><<<(int)((t + 255) / 256), 256, 0, st>>>(rows, x, p[0], p[1], cg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_flush(int s, int rows, double* x, double* const* p, const CgState* cg,
+                            cudaStream_t st) {
+  EP_DISPATCH_S(s, cg_flush_s, rows, x, p, cg, st);
 }
 
 template <int S>
 static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, const TileMap& tm, const int* row_map,
                              const int* col_entry, const double* values, const double* r,
-                             const double* p_old, double* p_new, double* q, const FinArgs& f,
-                             cudaStream_t st) {
+                             const double* p_old, double* p_new, double* q, double* x,
+                             const FinArgs& f, cudaStream_t st) {
   using Sh = TileShape<S, 1>;
   const int blocks = tiles ? (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC : (tm.rows + Sh::ROWS - 1) / Sh::ROWS;
   if (blocks == 0) return cudaSuccess;
   if (!fused_dir) {
-    using Sd = TileShape<S, kStreamPasses>;
-    k_cg_direction<S><<<(tm.rows + Sd::ROWS - 1) / Sd::ROWS, 256, 0, st>>>(tm.rows, r, p_old, p_new, f.cg);
+    using Sd = TileShape<S, kDirPasses>;
+    k_cg_direction<S><<<(tm.rows + Sd::ROWS - 1) / Sd::ROWS, 256, 0, st>>>(tm.rows, r, p_old, p_new, x, f.cg);
   }
 #define EP_CG_SPMV(T, D) \
-  k_cg_spmv<S, T, D><<<blocks, 256, 0, st>>>(tm, row_map, col_entry, values, r, p_old, p_new, q, f)
+  k_cg_spmv<S, T, D><<<blocks, 256, 0, st>>>(tm, row_map, col_entry, values, r, p_old, p_new, q, x, f)
   if (tiles) {
     if (fused_dir) EP_CG_SPMV(true, true);
     else EP_CG_SPMV(true, false);
@@ -771,18 +832,17 @@ static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, const TileMap& tm, cons
 cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, const TileMap& tm,
                            const int* row_map, const int* col_entry, const double* values,
                            const double* r, const double* p_old, double* p_new, double* q,
-                           const FinArgs& f, cudaStream_t st) {
+                           double* x, const FinArgs& f, cudaStream_t st) {
   EP_DISPATCH_S(s, cg_spmv_s, tiles, fused_dir, tm, row_map, col_entry, values, r, p_old, p_new, q,
-                f, st);
+                x, f, st);
 }
 
-// x = alpha*p + x; r = (-alpha)*q + r on active lanes (pcg.hpp:94-95 via
-// axpby, kernels.hpp:84: 1.0*y is exact); r.r for the next dot.  P rows per
-// thread, all loads issued before any arithmetic.
+// r = (-alpha)*q + 1.0*r on active lanes (pcg.hpp:95 via axpby,
+// kernels.hpp:84: 1.0*y is exact); r.r for the next dot.  P rows per thread,
+// all loads issued before any arithmetic.  (x is updated one pass later, in
+// k_cg_direction / k_cg_flush.)
 template <int S, bool kTiles>
-__global__ void __launch_bounds__(256) k_cg_update(const TileMap tm, double* __restrict__ x,
-                                                   const double* __restrict__ p,
-                                                   double* __restrict__ r,
+__global__ void __launch_bounds__(256) k_cg_update(const TileMap tm, double* __restrict__ r,
                                                    const double* __restrict__ q, const FinArgs f) {
   constexpr int P = kStreamPasses;
   using Sh = TileShape<S, P>;
@@ -799,15 +859,13 @@ __global__ void __launch_bounds__(256) k_cg_update(const TileMap tm, double* __r
     act[j] = cg->active[lane0 + j] != 0;
   }
   int row[P];
-  VecD<V> xv[P], rv[P], pv[P], qv[P];
+  VecD<V> rv[P], qv[P];
 #pragma unroll
   for (int ps = 0; ps < P; ++ps) {
     row[ps] = cg_row<S, P, kTiles>(tm, ps * Sh::RPC + threadIdx.x / Sh::TPR);
     if (row[ps] >= 0) {
       const size_t off = (size_t)row[ps] * S + lane0;
-      xv[ps] = ld_vec<V>(x + off);
       rv[ps] = ld_vec<V>(r + off);
-      pv[ps] = ld_vec<V>(p + off);
       qv[ps] = ld_vec<V>(q + off);
     }
   }
@@ -816,17 +874,12 @@ __global__ void __launch_bounds__(256) k_cg_update(const TileMap tm, double* __r
     const int slot = ps * Sh::RPC + threadIdx.x / Sh::TPR;
     VecD<V> pr;
     if (row[ps] >= 0) {
-      const size_t off = (size_t)row[ps] * S + lane0;
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        if (act[j]) {
-          xv[ps].v[j] = EP_DADD(EP_DMUL(al[j], pv[ps].v[j]), xv[ps].v[j]);
-          rv[ps].v[j] = EP_DADD(EP_DMUL(-al[j], qv[ps].v[j]), rv[ps].v[j]);
-        }
+        if (act[j]) rv[ps].v[j] = EP_DADD(EP_DMUL(-al[j], qv[ps].v[j]), rv[ps].v[j]);
         pr.v[j] = EP_DMUL(rv[ps].v[j], rv[ps].v[j]);
       }
-      st_vec<V>(x + off, xv[ps]);
-      st_vec<V>(r + off, rv[ps]);
+      st_vec<V>(r + (size_t)row[ps] * S + lane0, rv[ps]);
     } else {
 #pragma unroll
       for (int j = 0; j < V; ++j) pr.v[j] = 0.0;
@@ -840,19 +893,19 @@ __global__ void __launch_bounds__(256) k_cg_update(const TileMap tm, double* __r
 }
 
 template <int S>
-static cudaError_t cg_update_s(bool tiles, const TileMap& tm, double* x, const double* p,
-                               double* r, const double* q, const FinArgs& f, cudaStream_t st) {
+static cudaError_t cg_update_s(bool tiles, const TileMap& tm, double* r, const double* q,
+                               const FinArgs& f, cudaStream_t st) {
   using Sh = TileShape<S, kStreamPasses>;
   const int blocks = tiles ? (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC : (tm.rows + Sh::ROWS - 1) / Sh::ROWS;
   if (blocks == 0) return cudaSuccess;
-  if (tiles) k_cg_update<S, true><<<blocks, 256, 0, st>>>(tm, x, p, r, q, f);
-  else k_cg_update<S, false><<<blocks, 256, 0, st>>>(tm, x, p, r, q, f);
+  if (tiles) k_cg_update<S, true><<<blocks, 256, 0, st>>>(tm, r, q, f);
+  else k_cg_update<S, false><<<blocks, 256, 0, st>>>(tm, r, q, f);
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* x, const double* p,
-                             double* r, const double* q, const FinArgs& f, cudaStream_t st) {
-  EP_DISPATCH_S(s, cg_update_s, tiles, tm, x, p, r, q, f, st);
+cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* r, const double* q,
+                             const FinArgs& f, cudaStream_t st) {
+  EP_DISPATCH_S(s, cg_update_s, tiles, tm, r, q, f, st);
 }
 
 }  // namespace ep

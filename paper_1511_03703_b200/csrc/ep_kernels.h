@@ -46,6 +46,9 @@ struct CgState {
   double tol;
   double rz[32], alpha[32], beta[32], bnorm[32];
   int active[32], iters[32], lane_status[32], hist_len[32];
+  // lanes whose x += alpha*p of the last finished iteration is still owed:
+  // x updates are deferred into the next direction pass (ep_kernels.cu)
+  int pending[32];
 };
 
 enum Phase { kPhaseNone = 0, kPhaseInit = 1, kPhasePQ = 2, kPhaseRR = 3 };
@@ -87,9 +90,12 @@ cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v,
 cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, const TileMap& tm,
                            const int* row_map, const int* col_entry, const double* values,
                            const double* r, const double* p_old, double* p_new, double* q,
-                           const FinArgs& f, cudaStream_t st);
-// x += alpha p; r -= alpha q on active lanes; with tiles, also r.r and its phase
-cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* x, const double* p,
-                             double* r, const double* q, const FinArgs& f, cudaStream_t st);
+                           double* x, const FinArgs& f, cudaStream_t st);
+// r -= alpha q on active lanes; with tiles, also r.r and its phase
+cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* r, const double* q,
+                             const FinArgs& f, cudaStream_t st);
+// after the loop: apply the still-deferred x += alpha*p of the last iteration
+cudaError_t launch_cg_flush(int s, int rows, double* x, double* const* p, const CgState* cg,
+                            cudaStream_t st);
 
 }  // namespace ep
