@@ -75,6 +75,10 @@ int enprop_ctx_set_option(enprop_ctx* ctx, int option, int value);
  * bench.py for the roofline). Returns the totals accumulated since the last
  * reset; enable = 1/0 turns timing on/off and resets, enable = -1 only reads. */
 int enprop_ctx_profile(enprop_ctx* ctx, int enable, double* spmv_ms, int64_t* spmv_launches);
+/* Per-phase totals of the profiled CG iterations: ms[0] SpMV phase, ms[1] PQ
+ * finalize (serial order only), ms[2] update, ms[3] RR finalize (serial order
+ * only), ms[4] whole iterations. */
+int enprop_ctx_profile_detail(enprop_ctx* ctx, double* ms, int64_t* iterations);
 
 int enprop_malloc(enprop_ctx* ctx, size_t bytes, void** dptr);
 int enprop_free(enprop_ctx* ctx, void* dptr);

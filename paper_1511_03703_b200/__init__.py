@@ -149,6 +149,7 @@ def lib() -> C.CDLL:
     L.enprop_ctx_launch_count.argtypes = [_vp]
     L.enprop_ctx_profile.argtypes = [_vp, C.c_int, _dp, C.POINTER(C.c_int64)]
     L.enprop_ctx_set_option.argtypes = [_vp, C.c_int, C.c_int]
+    L.enprop_ctx_profile_detail.argtypes = [_vp, _dp, C.POINTER(C.c_int64)]
     L.enprop_build_node_graph.argtypes = [_vp, C.c_int, _vp, _vp]
     L.enprop_kl_describe.argtypes = [C.POINTER(_KlParams), _ip, _dp, _dp, _dp, _dp, _ip]
     L.enprop_assemble.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(_KlParams), C.POINTER(_Coeffs),
@@ -235,6 +236,14 @@ class Context:
         cnt = C.c_int64()
         _check(lib().enprop_ctx_profile(self.h, enable, C.byref(ms), C.byref(cnt)))
         return ms.value, cnt.value
+
+    def profile_detail(self):
+        """Per-phase CG totals since the last profile(1): dict of ms and count."""
+        ms = (C.c_double * 5)()
+        n = C.c_int64()
+        _check(lib().enprop_ctx_profile_detail(self.h, ms, C.byref(n)))
+        return dict(spmv=ms[0], fin_pq=ms[1], update=ms[2], fin_rr=ms[3], iteration=ms[4],
+                    iterations=n.value)
 
     def close(self):
         if getattr(self, "h", None):

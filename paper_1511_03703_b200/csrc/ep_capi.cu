@@ -52,10 +52,11 @@ struct enprop_ctx {
   int fused_direction = 0;  // ENPROP_OPT_FUSED_DIRECTION (split measured faster on B200)
   // optional CUDA-event timing of the CG SpMV launches (bench roofline)
   int profile = 0;
-  std::vector<cudaEvent_t> prof_ev;  // pairs (start, stop), reused
+  std::vector<cudaEvent_t> prof_ev;  // 5 events per profiled iteration, reused
   size_t prof_used = 0;
-  double prof_ms = 0.0;
-  int64_t prof_count = 0;
+  double prof_ms = 0.0;       // CG SpMV phase (direction + SpMV)
+  int64_t prof_count = 0;     // profiled iterations that did work
+  double prof_detail[5] = {0, 0, 0, 0, 0};  // spmv, fin pq, update, fin rr, iteration
 };
 
 namespace {
@@ -130,31 +131,34 @@ int validate_cg_options(const enprop_cg_options* opt, int s) {
   return ENPROP_OK;
 }
 
-// Event pair for one profiled launch (grown on demand, reused across solves).
-cudaEvent_t* prof_pair(enprop_ctx* c) {
-  if (c->prof_used + 2 > c->prof_ev.size()) {
-    for (int k = 0; k < 64; ++k) {
+// Five events per profiled iteration (grown on demand, reused across solves):
+// before the SpMV phase, after it, after the PQ finalize, after the update,
+// after the RR finalize (the finalizes are separate launches in serial order).
+cudaEvent_t* prof_slot(enprop_ctx* c) {
+  if (c->prof_used + 5 > c->prof_ev.size()) {
+    for (int k = 0; k < 160; ++k) {
       cudaEvent_t e;
       if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
       c->prof_ev.push_back(e);
     }
   }
   cudaEvent_t* p = &c->prof_ev[c->prof_used];
-  c->prof_used += 2;
+  c->prof_used += 5;
   return p;
 }
 
-// Accumulate the elapsed time of the recorded pairs. Launches that early-exit
-// after convergence are excluded (they are not SpMVs); they are recognisable
-// because they take less than 5 microseconds while a real SpMV of any
-// benchmarked size takes far longer — the caller also gets the count.
+// Accumulate the recorded iterations. Iterations enqueued past convergence
+// early-exit in every kernel (a few microseconds); they are excluded by a
+// 5-microsecond threshold on the SpMV phase, far below any real SpMV here.
 int prof_collect(enprop_ctx* c) {
-  for (size_t i = 0; i + 1 < c->prof_used; i += 2) {
-    float ms = 0.f;
-    EP_CUDA(cudaEventElapsedTime(&ms, c->prof_ev[i], c->prof_ev[i + 1]));
-    if (ms > 0.005f) {
-      c->prof_ms += ms;
+  for (size_t i = 0; i + 4 < c->prof_used + 0 && i + 5 <= c->prof_used; i += 5) {
+    float t[4];
+    for (int k = 0; k < 4; ++k) EP_CUDA(cudaEventElapsedTime(&t[k], c->prof_ev[i + k], c->prof_ev[i + k + 1]));
+    if (t[0] > 0.005f) {
+      c->prof_ms += t[0];
       c->prof_count += 1;
+      for (int k = 0; k < 4; ++k) c->prof_detail[k] += t[k];
+      c->prof_detail[4] += t[0] + t[1] + t[2] + t[3];
     }
   }
   c->prof_used = 0;
@@ -209,14 +213,17 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
       for (int c = 0; c < chunk && launched < limit; ++c, ++launched) {
         double* p_old = w.p[launched & 1];
         double* p_new = w.p[(launched + 1) & 1];
-        cudaEvent_t* ev = ctx->profile ? prof_pair(ctx) : nullptr;
+        cudaEvent_t* ev = ctx->profile ? prof_slot(ctx) : nullptr;
         if (ev) EP_CUDA(cudaEventRecord(ev[0], st));
         EP_CUDA(launch_cg_spmv(s, canon, ctx->fused_direction != 0, tm, row_map, col_entry, values,
                                w.r, p_old, p_new, w.q, x, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[1], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, kPhasePQ, w.state, w.hist, nullptr, st));
+        if (ev) EP_CUDA(cudaEventRecord(ev[2], st));
         EP_CUDA(launch_cg_update(s, canon, tm, w.r, w.q, f_rr, st));
+        if (ev) EP_CUDA(cudaEventRecord(ev[3], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, kPhaseRR, w.state, w.hist, nullptr, st));
+        if (ev) EP_CUDA(cudaEventRecord(ev[4], st));
         ctx->launches += (canon ? 2 : 4) + (ctx->fused_direction ? 0 : 1);
       }
     }
@@ -357,7 +364,15 @@ int enprop_ctx_profile(enprop_ctx* c, int enable, double* spmv_ms, int64_t* spmv
     c->profile = enable;
     c->prof_ms = 0.0;
     c->prof_count = 0;
+    for (double& d : c->prof_detail) d = 0.0;
   }
+  return ENPROP_OK;
+}
+
+int enprop_ctx_profile_detail(enprop_ctx* c, double* ms, int64_t* iterations) {
+  if (!c || !ms) return fail(ENPROP_ERR_INVALID, "enprop_ctx_profile_detail: null argument");
+  for (int k = 0; k < 5; ++k) ms[k] = c->prof_detail[k];
+  if (iterations) *iterations = c->prof_count;
   return ENPROP_OK;
 }
 

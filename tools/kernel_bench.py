@@ -78,11 +78,14 @@ def main():
                 its.append(max(it))
             b.record(st)
             torch.cuda.synchronize()
+            det = ctx.profile_detail()
             sp_ms, sp_n = ctx.profile(0)
             ms = a.elapsed_time(b) / args.steps
             key = f"{mode_name}_fused{fused}"
             out[key] = {"solve_ms": round(ms, 3), "iters": its, "ms_per_iter": round(ms / its[-1], 4),
-                        "spmv_phase_ms": round(sp_ms / max(sp_n, 1), 4)}
+                        "spmv_phase_ms": round(sp_ms / max(sp_n, 1), 4),
+                        "per_iter_ms": {k: round(v / max(det["iterations"], 1), 4)
+                                        for k, v in det.items() if k != "iterations"}}
             if mode_name == "serial" and args.steps > 1:
                 pass
     ctx.set_option(ep.OPT_FUSED_DIRECTION, 0)
