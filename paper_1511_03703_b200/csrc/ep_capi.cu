@@ -199,7 +199,7 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
     EP_CUDA(launch_dot_tiles(s, tm, w.r, w.r, f_init, st));
     ctx->launches += 1;
   } else {
-    EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, kPhaseInit, w.state, w.hist, nullptr, st));
+    EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, f_init, st));
     ctx->launches += 1;
   }
 
@@ -218,11 +218,11 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
         EP_CUDA(launch_cg_spmv(s, canon, ctx->fused_direction != 0, tm, row_map, col_entry, values,
                                w.r, p_old, p_new, w.q, x, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[1], st));
-        if (!canon) EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, kPhasePQ, w.state, w.hist, nullptr, st));
+        if (!canon) EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[2], st));
         EP_CUDA(launch_cg_update(s, canon, tm, w.r, w.q, f_rr, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[3], st));
-        if (!canon) EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, kPhaseRR, w.state, w.hist, nullptr, st));
+        if (!canon) EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, f_rr, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[4], st));
         ctx->launches += (canon ? 2 : 4) + (ctx->fused_direction ? 0 : 1);
       }
@@ -558,18 +558,17 @@ int enprop_dot(enprop_ctx* c, int s, int64_t n, const double* u, const double* v
   const TileMap tm = make_tile_map(rows, seg_rows > 0 ? seg_rows : 4096);
   CgWork w;  // partials + counters only
   cudaError_t err = cudaMalloc(&out, (s + 1) * sizeof(double));
-  if (err == cudaSuccess && dot_mode == ENPROP_DOT_CANONICAL && rows > 0) {
-    const int tiles = tm.num_tiles(), segs = tm.num_segs;
-    if (err == cudaSuccess) err = cudaMalloc(&w.partials, (size_t)tiles * s * sizeof(double));
-    if (err == cudaSuccess) err = cudaMalloc(&w.seg_sums, (size_t)segs * s * sizeof(double));
-    if (err == cudaSuccess) err = cudaMalloc(&w.counters, (size_t)(segs + 1) * sizeof(int));
-    if (err == cudaSuccess) err = cudaMemsetAsync(w.counters, 0, (size_t)(segs + 1) * sizeof(int), c->stream);
-    FinArgs f = fin_args(w, tm, kPhaseNone);
-    f.lanes_out = out;
-    if (err == cudaSuccess) err = launch_dot_tiles(s, tm, u, v, f, c->stream);
-    c->launches += 1;
-  } else if (err == cudaSuccess) {
-    err = launch_fin_serial(s, rows, u, v, kPhaseNone, nullptr, nullptr, out, c->stream);
+  const int tiles = tm.num_tiles() > 0 ? tm.num_tiles() : 1;
+  const int segs = tm.num_segs > 0 ? tm.num_segs : 1;
+  if (err == cudaSuccess) err = cudaMalloc(&w.partials, (size_t)tiles * s * sizeof(double));
+  if (err == cudaSuccess) err = cudaMalloc(&w.seg_sums, (size_t)segs * s * sizeof(double));
+  if (err == cudaSuccess) err = cudaMalloc(&w.counters, (size_t)(segs + 1) * sizeof(int));
+  if (err == cudaSuccess) err = cudaMemsetAsync(w.counters, 0, (size_t)(segs + 1) * sizeof(int), c->stream);
+  FinArgs f = fin_args(w, tm, kPhaseNone);
+  f.lanes_out = out;
+  if (err == cudaSuccess) {
+    if (dot_mode == ENPROP_DOT_CANONICAL && rows > 0) err = launch_dot_tiles(s, tm, u, v, f, c->stream);
+    else err = launch_fin_serial(s, rows, u, v, f, c->stream);
     c->launches += 1;
   }
   std::vector<double> h(s + 1);

@@ -544,98 +544,126 @@ __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hi
 }
 
 // Serial finalize: the reference's own order (kernels.hpp:66-67), one chain
-// per sample: acc = 0; acc += u[row]*v[row] for row = 0, 1, ...  A single warp
-// runs the s chains; the vectors stream into shared memory through a 4-stage
-// ring of 1D bulk copies (cp.async.bulk + mbarrier), so the chain only waits on
-// its own DADD latency, not on DRAM.
-constexpr int kSerialStages = 4;
-constexpr int kSerialChunkBytes = 16384;
-constexpr int kSerialSmem = 2 * kSerialStages * kSerialChunkBytes + kSerialStages * 8;
+// per sample: acc = 0; acc += u[row]*v[row] for row = 0, 1, ...  The chains
+// are split across blocks by groups of LG = min(s, 4) samples, so a block
+// streams only one 32-byte sector per row (1/8 of the data at s = 32) instead
+// of one SM ingesting whole rows; within a block all threads stage chunks of
+// rows into shared memory (double-buffered) while LG threads run the chains,
+// so the time is the DADD dependency chain, rows x latency.  The last block
+// to finish (acq_rel counter) runs the scalar phase on all s lanes.
+constexpr int kSerialChunk = 512;  // rows staged per step
+constexpr int kSerialThreads = 256;
 
 template <int S>
-__global__ void __launch_bounds__(32) k_fin_serial(int rows, const double* __restrict__ u,
-                                                   const double* __restrict__ v, int phase,
-                                                   CgState* cg, double* hist,
-                                                   double* lanes_out) {
-  if ((phase == kPhasePQ || phase == kPhaseRR) && cg->done) return;
-  extern __shared__ __align__(128) unsigned char smem[];
-  constexpr int kChunkRows = kSerialChunkBytes / (8 * S);
-  __shared__ double lanes[S];
-  double* su = reinterpret_cast<double*>(smem);
-  double* sv = su + kSerialStages * kChunkRows * S;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * kSerialStages * kSerialChunkBytes);
-  const int lane = threadIdx.x;
-  const bool same = (u == v);
-  const bool aligned = ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
-  const int nchunks = (rows + kChunkRows - 1) / kChunkRows;
-  double acc = 0.0;
+struct SerialShape {
+  static constexpr int LG = S < 4 ? S : 4;  // lanes per block
+  static constexpr int GROUPS = S / LG;
+  static constexpr int RPT = kSerialChunk / kSerialThreads;  // rows per thread per chunk
+};
 
-  if (aligned && nchunks > 0) {
-    if (lane == 0) {
-      for (int s2 = 0; s2 < kSerialStages; ++s2) mbar_init(&bars[s2], 1);
-      fence_mbar_init();
+template <int LG>
+__device__ __forceinline__ void ld_lanes(const double* p, double* out) {
+  if constexpr (LG == 1) {
+    out[0] = __ldcg(p);
+  } else {
+#pragma unroll
+    for (int j = 0; j < LG; j += 2) {
+      const double2 t = __ldcg(reinterpret_cast<const double2*>(p + j));
+      out[j] = t.x;
+      out[j + 1] = t.y;
     }
-    __syncwarp();
-    auto issue = [&](int c) {
-      const int stg = c % kSerialStages;
-      const int r0 = c * kChunkRows;
-      const int nr = min(kChunkRows, rows - r0);
-      const uint32_t bytes = (uint32_t)((size_t)nr * S * 8) & ~15u;
-      mbar_arrive_expect_tx(&bars[stg], same ? bytes : 2 * bytes);
-      if (bytes) {
-        bulk_g2s(su + (size_t)stg * kChunkRows * S, u + (size_t)r0 * S, bytes, &bars[stg]);
-        if (!same) bulk_g2s(sv + (size_t)stg * kChunkRows * S, v + (size_t)r0 * S, bytes, &bars[stg]);
-      }
-    };
-    if (lane == 0)
-      for (int c = 0; c < kSerialStages && c < nchunks; ++c) issue(c);
-    for (int c = 0; c < nchunks; ++c) {
-      const int stg = c % kSerialStages;
-      mbar_wait(&bars[stg], (uint32_t)((c / kSerialStages) & 1));
-      const int r0 = c * kChunkRows;
-      const int nr = min(kChunkRows, rows - r0);
-      const int nbulk = (int)((((size_t)nr * S * 8) & ~(size_t)15) / (8 * S));
-      if (lane < S) {
-        const double* cu = su + (size_t)stg * kChunkRows * S + lane;
-        const double* cv = same ? cu : sv + (size_t)stg * kChunkRows * S + lane;
-        int r = 0;
-#pragma unroll 8
-        for (; r < nbulk; ++r) acc = EP_DADD(acc, EP_DMUL(cu[(size_t)r * S], cv[(size_t)r * S]));
-        for (; r < nr; ++r)
-          acc = EP_DADD(acc, EP_DMUL(u[(size_t)(r0 + r) * S + lane], v[(size_t)(r0 + r) * S + lane]));
-      }
-      __syncwarp();
-      if (lane == 0 && c + kSerialStages < nchunks) {
-        fence_proxy_async_smem();
-        issue(c + kSerialStages);
-      }
-    }
-  } else if (lane < S) {
-    for (int r = 0; r < rows; ++r)
-      acc = EP_DADD(acc, EP_DMUL(u[(size_t)r * S + lane], v[(size_t)r * S + lane]));
   }
-  if (lane < S) lanes[lane] = acc;
-  __syncwarp();
-  if (lane == 0) cg_phase<S>(phase, lanes, cg, hist, lanes_out);
 }
 
 template <int S>
-static cudaError_t fin_serial_s(int rows, const double* u, const double* v, int phase,
-                                CgState* cg, double* hist, double* lanes_out, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t err = cudaFuncSetAttribute(k_fin_serial<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           kSerialSmem);
-    if (err != cudaSuccess) return err;
-    configured = true;
+__global__ void __launch_bounds__(kSerialThreads) k_fin_serial(int rows,
+                                                                const double* __restrict__ u,
+                                                                const double* __restrict__ v,
+                                                                const FinArgs f) {
+  using Sh = SerialShape<S>;
+  constexpr int LG = Sh::LG;
+  if ((f.phase == kPhasePQ || f.phase == kPhaseRR) && f.cg->done) return;
+  extern __shared__ __align__(16) double sbuf[];  // [2][2][kSerialChunk][LG]
+  __shared__ double lanes[S];
+  __shared__ int s_final;
+  const bool same = (u == v);
+  const int lane_base = blockIdx.x * LG;
+  const int nchunks = (rows + kSerialChunk - 1) / kSerialChunk;
+  double ra[Sh::RPT][LG], rb[Sh::RPT][LG];
+  auto load = [&](int c) {
+#pragma unroll
+    for (int k = 0; k < Sh::RPT; ++k) {
+      const int row = c * kSerialChunk + k * kSerialThreads + threadIdx.x;
+      if (row < rows) {
+        ld_lanes<LG>(u + (size_t)row * S + lane_base, ra[k]);
+        if (!same) ld_lanes<LG>(v + (size_t)row * S + lane_base, rb[k]);
+      }
+    }
+  };
+  auto store = [&](int buf) {
+    double* su = sbuf + (size_t)buf * 2 * kSerialChunk * LG;
+    double* sv = su + kSerialChunk * LG;
+#pragma unroll
+    for (int k = 0; k < Sh::RPT; ++k) {
+      const int rl = k * kSerialThreads + threadIdx.x;
+#pragma unroll
+      for (int j = 0; j < LG; ++j) {
+        su[rl * LG + j] = ra[k][j];
+        if (!same) sv[rl * LG + j] = rb[k][j];
+      }
+    }
+  };
+  double acc = 0.0;
+  if (nchunks > 0) {
+    load(0);
+    store(0);
+    __syncthreads();
   }
-  k_fin_serial<S><<<1, 32, kSerialSmem, st>>>(rows, u, v, phase, cg, hist, lanes_out);
+  for (int c = 0; c < nchunks; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nchunks) load(c + 1);  // in flight while the chains run
+    if (threadIdx.x < LG) {
+      const double* su = sbuf + (size_t)buf * 2 * kSerialChunk * LG + threadIdx.x;
+      const double* sv = same ? su : su + kSerialChunk * LG;
+      const int nr = min(kSerialChunk, rows - c * kSerialChunk);
+#pragma unroll 16
+      for (int r = 0; r < nr; ++r) acc = EP_DADD(acc, EP_DMUL(su[r * LG], sv[r * LG]));
+    }
+    if (c + 1 < nchunks) store(buf ^ 1);
+    __syncthreads();
+  }
+  if (threadIdx.x < LG) f.seg_sums[lane_base + threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) s_final = (atomic_add_acq_rel_gpu(f.seg_done, 1) == Sh::GROUPS - 1);
+  __syncthreads();
+  if (s_final) {
+    if (threadIdx.x < S) lanes[threadIdx.x] = __ldcg(f.seg_sums + threadIdx.x);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      *f.seg_done = 0;
+      cg_phase<S>(f.phase, lanes, f.cg, f.hist, f.lanes_out);
+    }
+  }
+}
+
+template <int S>
+static cudaError_t fin_serial_s(int rows, const double* u, const double* v, const FinArgs& f,
+                                cudaStream_t st) {
+  using Sh = SerialShape<S>;
+  constexpr int smem = 2 * 2 * kSerialChunk * Sh::LG * (int)sizeof(double);
+  static bool configured = false;
+  if (!configured && smem > 48 * 1024) {
+    cudaError_t err = cudaFuncSetAttribute(k_fin_serial<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (err != cudaSuccess) return err;
+  }
+  configured = true;
+  k_fin_serial<S><<<Sh::GROUPS, kSerialThreads, smem, st>>>(rows, u, v, f);
   return cudaGetLastError();
 }
 
-cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v, int phase,
-                              CgState* cg, double* hist, double* lanes_out, cudaStream_t st) {
-  EP_DISPATCH_S(s, fin_serial_s, rows, u, v, phase, cg, hist, lanes_out, st);
+cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v, const FinArgs& f,
+                              cudaStream_t st) {
+  EP_DISPATCH_S(s, fin_serial_s, rows, u, v, f, st);
 }
 
 // =============================================================================

@@ -80,9 +80,10 @@ cudaError_t launch_axpby(int s, int64_t n, int per_lane, const double* alpha, co
 // canonical dot of u.v with the fused finalize running f.phase
 cudaError_t launch_dot_tiles(int s, const TileMap& tm, const double* u, const double* v,
                              const FinArgs& f, cudaStream_t st);
-// serial (reference-order) dot straight from the vectors, then `phase`
-cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v, int phase,
-                              CgState* cg, double* hist, double* lanes_out, cudaStream_t st);
+// serial (reference-order) dot straight from the vectors, then f.phase; uses
+// f.seg_sums[0..s) as the lane buffer and f.seg_done as its arrival counter
+cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v, const FinArgs& f,
+                              cudaStream_t st);
 // q = A p_new with p_new = (it==0 ? r : r + beta*p_old) formed on the fly; writes
 // p_new and q; with tiles, also the canonical p_new.q and its CG phase (f)
 // fused_dir = false: a separate k_cg_direction pass writes p_new first and the
