@@ -626,8 +626,17 @@ __global__ void __launch_bounds__(kSerialThreads) k_fin_serial(int rows,
       const double* su = sbuf + (size_t)buf * 2 * kSerialChunk * LG + threadIdx.x;
       const double* sv = same ? su : su + kSerialChunk * LG;
       const int nr = min(kSerialChunk, rows - c * kSerialChunk);
-#pragma unroll 16
-      for (int r = 0; r < nr; ++r) acc = EP_DADD(acc, EP_DMUL(su[r * LG], sv[r * LG]));
+      // batches of 16: all loads and products first, then the dependent adds,
+      // so the chain waits on DADD latency only (not on LDS + DMUL per row)
+      int r = 0;
+      for (; r + 16 <= nr; r += 16) {
+        double pr[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) pr[k] = EP_DMUL(su[(r + k) * LG], sv[(r + k) * LG]);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc = EP_DADD(acc, pr[k]);
+      }
+      for (; r < nr; ++r) acc = EP_DADD(acc, EP_DMUL(su[r * LG], sv[r * LG]));
     }
     if (c + 1 < nchunks) store(buf ^ 1);
     __syncthreads();
