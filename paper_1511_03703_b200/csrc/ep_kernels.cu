@@ -544,104 +544,68 @@ __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hi
 }
 
 // Serial finalize: the reference's own order (kernels.hpp:66-67), one chain
-// per sample: acc = 0; acc += u[row]*v[row] for row = 0, 1, ...  The chains
-// are split across blocks by groups of LG = min(s, 4) samples, so a block
-// streams only one 32-byte sector per row (1/8 of the data at s = 32) instead
-// of one SM ingesting whole rows; within a block all threads stage chunks of
-// rows into shared memory (double-buffered) while LG threads run the chains,
-// so the time is the DADD dependency chain, rows x latency.  The last block
-// to finish (acq_rel counter) runs the scalar phase on all s lanes.
-constexpr int kSerialChunk = 512;  // rows staged per step
-constexpr int kSerialThreads = 256;
+// per sample: acc = 0; acc += u[row]*v[row] for row = 0, 1, ...  The chain is
+// latency-bound (one dependent DADD per row, ~8 cycles on B200), so the design
+// keeps the chain's operands in registers: one warp per sample; in a chunk of
+// 32*K rows lane j holds the products of rows [jK, jK+K) and the running sum
+// walks lane 0 -> lane 31 by shuffles, while the next chunk's loads are in
+// flight.  A block holds the warps of LG = min(s, 4) samples (one 32-byte
+// sector per row, shared through L1).  The last block to finish (acq_rel
+// counter) runs the scalar phase on all s lanes.
+constexpr int kSerialK = 16;  // rows per lane per chunk
 
 template <int S>
 struct SerialShape {
-  static constexpr int LG = S < 4 ? S : 4;  // lanes per block
+  static constexpr int LG = S < 4 ? S : 4;  // samples (warps) per block
   static constexpr int GROUPS = S / LG;
-  static constexpr int RPT = kSerialChunk / kSerialThreads;  // rows per thread per chunk
+  static constexpr int CHUNK = 32 * kSerialK;
 };
 
-template <int LG>
-__device__ __forceinline__ void ld_lanes(const double* p, double* out) {
-  if constexpr (LG == 1) {
-    out[0] = __ldcg(p);
-  } else {
-#pragma unroll
-    for (int j = 0; j < LG; j += 2) {
-      const double2 t = __ldcg(reinterpret_cast<const double2*>(p + j));
-      out[j] = t.x;
-      out[j + 1] = t.y;
-    }
-  }
-}
-
 template <int S>
-__global__ void __launch_bounds__(kSerialThreads) k_fin_serial(int rows,
-                                                                const double* __restrict__ u,
-                                                                const double* __restrict__ v,
-                                                                const FinArgs f) {
+__global__ void __launch_bounds__(32 * SerialShape<S>::LG) k_fin_serial(
+    int rows, const double* __restrict__ u, const double* __restrict__ v, const FinArgs f) {
   using Sh = SerialShape<S>;
-  constexpr int LG = Sh::LG;
+  constexpr int K = kSerialK;
   if ((f.phase == kPhasePQ || f.phase == kPhaseRR) && f.cg->done) return;
-  extern __shared__ __align__(16) double sbuf[];  // [2][2][kSerialChunk][LG]
   __shared__ double lanes[S];
   __shared__ int s_final;
-  const bool same = (u == v);
-  const int lane_base = blockIdx.x * LG;
-  const int nchunks = (rows + kSerialChunk - 1) / kSerialChunk;
-  double ra[Sh::RPT][LG], rb[Sh::RPT][LG];
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * Sh::LG + (threadIdx.x >> 5);  // this warp's sample
+  const int nchunks = (rows + Sh::CHUNK - 1) / Sh::CHUNK;
+  double ua[K], va[K], cur[K];
   auto load = [&](int c) {
 #pragma unroll
-    for (int k = 0; k < Sh::RPT; ++k) {
-      const int row = c * kSerialChunk + k * kSerialThreads + threadIdx.x;
+    for (int k = 0; k < K; ++k) {
+      const int row = c * Sh::CHUNK + lane * K + k;
       if (row < rows) {
-        ld_lanes<LG>(u + (size_t)row * S + lane_base, ra[k]);
-        if (!same) ld_lanes<LG>(v + (size_t)row * S + lane_base, rb[k]);
-      }
-    }
-  };
-  auto store = [&](int buf) {
-    double* su = sbuf + (size_t)buf * 2 * kSerialChunk * LG;
-    double* sv = su + kSerialChunk * LG;
-#pragma unroll
-    for (int k = 0; k < Sh::RPT; ++k) {
-      const int rl = k * kSerialThreads + threadIdx.x;
-#pragma unroll
-      for (int j = 0; j < LG; ++j) {
-        su[rl * LG + j] = ra[k][j];
-        if (!same) sv[rl * LG + j] = rb[k][j];
+        ua[k] = __ldg(u + (size_t)row * S + e);
+        va[k] = __ldg(v + (size_t)row * S + e);
       }
     }
   };
   double acc = 0.0;
   if (nchunks > 0) {
     load(0);
-    store(0);
-    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) cur[k] = EP_DMUL(ua[k], va[k]);
   }
   for (int c = 0; c < nchunks; ++c) {
-    const int buf = c & 1;
-    if (c + 1 < nchunks) load(c + 1);  // in flight while the chains run
-    if (threadIdx.x < LG) {
-      const double* su = sbuf + (size_t)buf * 2 * kSerialChunk * LG + threadIdx.x;
-      const double* sv = same ? su : su + kSerialChunk * LG;
-      const int nr = min(kSerialChunk, rows - c * kSerialChunk);
-      // batches of 16: all loads and products first, then the dependent adds,
-      // so the chain waits on DADD latency only (not on LDS + DMUL per row)
-      int r = 0;
-      for (; r + 16 <= nr; r += 16) {
-        double pr[16];
+    if (c + 1 < nchunks) load(c + 1);  // in flight during the chain
+    const int base = c * Sh::CHUNK;
+    for (int j = 0; j < 32; ++j) {
+      if (lane == j) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) pr[k] = EP_DMUL(su[(r + k) * LG], sv[(r + k) * LG]);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) acc = EP_DADD(acc, pr[k]);
+        for (int k = 0; k < K; ++k)
+          if (base + j * K + k < rows) acc = EP_DADD(acc, cur[k]);
       }
-      for (; r < nr; ++r) acc = EP_DADD(acc, EP_DMUL(su[r * LG], sv[r * LG]));
+      acc = __shfl_sync(0xffffffffu, acc, j);
     }
-    if (c + 1 < nchunks) store(buf ^ 1);
-    __syncthreads();
+    if (c + 1 < nchunks) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) cur[k] = EP_DMUL(ua[k], va[k]);
+    }
   }
-  if (threadIdx.x < LG) f.seg_sums[lane_base + threadIdx.x] = acc;
+  if (lane == 0) f.seg_sums[e] = acc;
   __syncthreads();
   if (threadIdx.x == 0) s_final = (atomic_add_acq_rel_gpu(f.seg_done, 1) == Sh::GROUPS - 1);
   __syncthreads();
@@ -659,14 +623,7 @@ template <int S>
 static cudaError_t fin_serial_s(int rows, const double* u, const double* v, const FinArgs& f,
                                 cudaStream_t st) {
   using Sh = SerialShape<S>;
-  constexpr int smem = 2 * 2 * kSerialChunk * Sh::LG * (int)sizeof(double);
-  static bool configured = false;
-  if (!configured && smem > 48 * 1024) {
-    cudaError_t err = cudaFuncSetAttribute(k_fin_serial<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (err != cudaSuccess) return err;
-  }
-  configured = true;
-  k_fin_serial<S><<<Sh::GROUPS, kSerialThreads, smem, st>>>(rows, u, v, f);
+  k_fin_serial<S><<<Sh::GROUPS, 32 * Sh::LG, 0, st>>>(rows, u, v, f);
   return cudaGetLastError();
 }
 
