@@ -95,16 +95,80 @@ def spmv_bytes(nnz, rows, s):
     return nnz * (8 * s + 4) + 4 * (rows + 1) + 16 * s * rows
 
 
+def cg_iter_bytes(nnz, rows, s):
+    """Algorithmic bytes of one CG iteration in this schedule:
+    direction 5 vector passes, SpMV values/cols/row_map + 2 passes, update 3."""
+    return nnz * (8 * s + 4) + 4 * (rows + 1) + 10 * 8 * s * rows
+
+
 def cg_spmv_bytes(nnz, rows, s):
     """Algorithmic bytes of the CG SpMV phase, split-direction
-    schedule: direction pass (read r, p_old; write p_new) + SpMV (values, cols,
-    row_map, p_new gathered once, q written once)."""
-    return 3 * 8 * s * rows + nnz * (8 * s + 4) + 4 * (rows + 1) + 16 * s * rows
+    schedule: direction pass (read r, p_old, x; write p_new, x) + SpMV (values,
+    cols, row_map, p_new gathered once, q written once)."""
+    return 5 * 8 * s * rows + nnz * (8 * s + 4) + 4 * (rows + 1) + 16 * s * rows
 
 
 # --------------------------------------------------------------------------- ours
+class GroupWorker:
+    """One sample-group lane of the step: its own context, torch stream and
+    device-resident problem (graph, KL tables, matrix, CG workspace)."""
+
+    def __init__(self, ep, torch, device, kl):
+        self.stream = torch.cuda.Stream(device=device)
+        self.ctx = ep.Context(device, use_torch_stream=False)
+        self.ctx.set_stream(self.stream.cuda_stream)
+        self.prob = ep.Problem(self.ctx, N_MESH, S, kl)
+
+
+def run_groups(torch, workers, jobs, cfg, host=False):
+    """Solve jobs[i] (lists of device or host sample tensors) on workers[i]
+    concurrently (one host thread each; ctypes releases the GIL).  Returns the
+    per-worker max iteration counts and lane statuses."""
+    import threading
+    out = [None] * len(workers)
+
+    def run(i):
+        w = workers[i]
+        its, sts = [], []
+        for item in jobs[i]:
+            if host:
+                y_host, x_host = item
+                it, st, rc = w.prob.solve_host(y_host, x_host, cfg)
+            else:
+                w.prob.assemble(item)
+                it, _, st = w.prob.solve(cfg)
+            its.append(max(it))
+            sts.extend(st)
+        out[i] = (its, sts)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(len(workers))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    return out
+
+
+def timed_round(torch, workers, jobs, cfg):
+    """Device time of one concurrent round: a start event on the main stream,
+    every worker stream waits on it, and the end event waits on every worker."""
+    main = torch.cuda.current_stream()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record(main)
+    for w in workers:
+        w.stream.wait_event(start)
+    res = run_groups(torch, workers, jobs, cfg)
+    for w in workers:
+        ev = torch.cuda.Event()
+        ev.record(w.stream)
+        main.wait_event(ev)
+    end.record(main)
+    torch.cuda.synchronize()
+    return start.elapsed_time(end), res
+
+
 def run_ours(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -118,95 +182,94 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    ctx = ep.Context(local)
+    G = args.groups
     O = Oracle()  # only to draw the reference's samples (samples.cpp:7-18)
-    groups_per_rank = args.steps + args.warmup
-    pool = O.draw_samples(0, S * groups_per_rank * world, M_TERMS)
+    rounds = args.warmup + args.steps
+    # rank r, round k, worker i solves sample group ((r * rounds + k) * G + i)
+    pool = O.draw_samples(0, S * G * rounds * world, M_TERMS)
+    group_of = lambda k, i: (rank * rounds + k) * G + i  # noqa: E731
+    kl = ep.KlField(M_TERMS, 1.0, SIGMA, 1.0)
+    workers = [GroupWorker(ep, torch, local, kl) for _ in range(G)]
+    ys = {(k, i): torch.as_tensor(pack_group(pool, S, group_of(k, i))).cuda()
+          for k in range(rounds) for i in range(G)}
     cfg = ep.SolverConfig(tol=TOL, max_iterations=10000, flavour=ep.CG_UNCOUPLED,
-                          dot_mode=ep.DOT_CANONICAL if args.dot == "canonical" else ep.DOT_SERIAL,
-                          check_every=16)
-    prob = ep.Problem(ctx, N_MESH, S, ep.KlField(M_TERMS, 1.0, SIGMA, 1.0))
-    ys = [torch.as_tensor(pack_group(pool, S, rank * groups_per_rank + g)).cuda()
-          for g in range(groups_per_rank)]
-    stream = torch.cuda.current_stream()
+                          dot_mode=ep.DOT_CANONICAL if args.dot == "canonical" else ep.DOT_SERIAL)
 
-    def step(g):
-        prob.assemble(ys[g])
-        it, _, st = prob.solve(cfg)
-        return it, st
-
-    for g in range(args.warmup):
-        step(g)
-    torch.cuda.synchronize()
+    for k in range(args.warmup):
+        timed_round(torch, workers, [[ys[(k, i)]] for i in range(G)], cfg)
     if world > 1:
         dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    launches0 = ctx.launches
-    ctx.profile(1)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    iters = []
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for k in range(args.steps):
-        it, st = step(args.warmup + k)
-        iters.append(max(it))
-        assert all(v == 0 for v in st), st
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    spmv_ms, spmv_n = ctx.profile(0)
-    launches = ctx.launches - launches0
+    launches0 = sum(w.ctx.launches for w in workers)
+    jobs = [[ys[(args.warmup + k, i)] for k in range(args.steps)] for i in range(G)]
+    ms, res = timed_round(torch, workers, jobs, cfg)
+    launches = sum(w.ctx.launches for w in workers) - launches0
     clk = clocks.stop()
+    iters = [r[0] for r in res]
+    assert all(v == 0 for r in res for v in r[1]), "a lane did not converge"
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    samples = args.steps * S * world
+    samples = args.steps * G * S * world
     value = samples / (ms / 1e3)
-
     if args.profile_only:
         print(json.dumps({"profile_only": True, "ms": ms, "iters": iters}), flush=True)
         return
-    # ---- e2e: the reference-facing call with host buffers (pinned), copies timed
-    y_host = [torch.as_tensor(pack_group(pool, S, rank * groups_per_rank + g)).contiguous().pin_memory()
-              for g in range(groups_per_rank)]
-    x_host = torch.empty((prob.rows, S), dtype=torch.float64).pin_memory()
-    for g in range(min(args.warmup, 1)):
-        prob.solve_host(y_host[g], x_host, cfg)
+
+    # ---- e2e: the reference-facing C-ABI call with HOST buffers (pinned); the
+    # H2D of y and the D2H of the solution are inside the timed region
+    x_host = [torch.empty((workers[0].prob.rows, S), dtype=torch.float64).pin_memory() for _ in range(G)]
+    hjobs = [[(torch.as_tensor(pack_group(pool, S, group_of(args.warmup + k, i))).contiguous().pin_memory(),
+               x_host[i]) for k in range(args.steps)] for i in range(G)]
+    run_groups(torch, workers, [[j[0]] for j in hjobs], cfg, host=True)  # warm
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for k in range(args.steps):
-        prob.solve_host(y_host[args.warmup + k], x_host, cfg)
-    t1 = time.perf_counter()
-    e2e_s = t1 - t0
+    run_groups(torch, workers, hjobs, cfg, host=True)
+    e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
-    e2e = {"value": samples / e2e_s, "unit": "samples/s",
-           "h2d_bytes_per_step": M_TERMS * S * 8, "d2h_bytes_per_step": prob.rows * S * 8,
-           "api": "enprop_problem_solve_host (C ABI, pinned host y in / x out)"}
+    e2e = {"value": round(samples / e2e_s, 3), "unit": "samples/s",
+           "h2d_bytes_per_step": G * M_TERMS * S * 8, "d2h_bytes_per_step": G * workers[0].prob.rows * S * 8,
+           "api": "enprop_problem_solve_host (C ABI; pinned host y in, x out; G groups concurrently)"}
 
+    # ---- roofline of the dominant kernel, from a single-stream solve of the same
+    # workload (kernels of concurrent streams overlap, so they are timed alone)
     hbm, peak_kind = peaks()
-    nnz, rows = prob.nnz, prob.rows
+    w0 = workers[0]
+    w0.ctx.profile(1)
+    w0.prob.assemble(ys[(args.warmup, 0)])
+    w0.prob.solve(cfg)
+    det = w0.ctx.profile_detail()
+    spmv_ms, spmv_n = w0.ctx.profile(0)
+    nnz, rows = w0.prob.nnz, w0.prob.rows
     avg_spmv_ms = spmv_ms / max(spmv_n, 1)
     achieved = cg_spmv_bytes(nnz, rows, S) / (avg_spmv_ms / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": "k_cg_direction<32> + k_cg_spmv<32,true,false>", "achieved": round(achieved, 1),
-                "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                "traffic": None, "bytes_per_launch": cg_spmv_bytes(nnz, rows, S),
-                "avg_launch_ms": round(avg_spmv_ms, 4), "launches_timed": spmv_n,
-                "share_of_step": round(spmv_ms / ms, 3) if ms else None}
-    prob.close()
+    it_ms = det["iteration"] / max(det["iterations"], 1)
+    roofline = {"bound": "hbm", "kernel": "k_cg_direction<32> + k_cg_spmv<32,true,false>",
+                "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": None,
+                "bytes_per_launch": cg_spmv_bytes(nnz, rows, S), "avg_launch_ms": round(avg_spmv_ms, 4),
+                "launches_timed": spmv_n,
+                "share_of_iteration": round(avg_spmv_ms / it_ms, 3) if it_ms else None,
+                "iteration_bytes": cg_iter_bytes(nnz, rows, S),
+                "iteration_gbs": round(cg_iter_bytes(nnz, rows, S) / (it_ms / 1e3) / 1e9, 1) if it_ms else None,
+                "timing": "CUDA events on the solve's stream, single-stream solve"}
 
-    # ---- cfg 3: ensemble SpMV on the 128^3 matrix, s=32 (rank 0 only)
+    extra = {}
+    if rank == 0 and not args.skip_serial and args.dot == "canonical":
+        extra["serial_order"] = bench_serial(torch, ep, workers, ys, args, cfg)
     spmv_obj = None
     if rank == 0 and not args.skip_spmv:
-        spmv_obj = bench_spmv(ctx, ep, torch, pack_group, O, hbm, peak_kind)
-
+        for w in workers:
+            w.prob.close()
+        spmv_obj = bench_spmv(workers[0].ctx, ep, torch, pack_group, O, hbm, peak_kind)
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         cpu = cpu_baseline_sample()
@@ -221,20 +284,42 @@ def run_ours(args):
         "value": round(value, 3), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg2: 64^3 Q1 hex mesh, KL m=3 sigma=0.1 L=1, s=32, assembly + "
-                               "fused Dirichlet + uncoupled identity-PCG tol 1e-6 (per-sample "
-                               "stopping), samples draw_samples(seed=0), one sample group per step",
-                   "mesh": N_MESH, "ensemble_size": S, "cg": "uncoupled",
+        "config": {"workload": "cfg2: 64^3 Q1 hex mesh, KL m=3 sigma=0.1 L=1, s=32; per sample group: "
+                               "assembly + fused Dirichlet + uncoupled identity-PCG to tol 1e-6 "
+                               "(per-sample stopping); samples draw_samples(seed=0)",
+                   "step": f"{G} sample groups of s=32 solved concurrently (one stream each)",
+                   "mesh": N_MESH, "ensemble_size": S, "groups_per_step": G, "cg": "uncoupled",
                    "dot_order": args.dot, "cg_iterations_max": iters,
-                   "l2": "inputs larger than L2 (matrix 1.84 GB per step)",
+                   "l2": "inputs larger than L2 (matrix 1.84 GB per group)",
                    "parallelism": f"sample groups x {world} GPU(s)"},
         "e2e": e2e, "roofline": roofline, "gpu_launches": int(launches), "clocks": clk,
     }
+    line.update(extra)
     if spmv_obj:
         line["spmv_cfg3"] = spmv_obj
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
+
+
+def bench_serial(torch, ep, workers, ys, args, cfg):
+    """Throughput in the reference's own (serial) dot order, which reproduces
+    pcg_solve bit for bit; its chains are latency-bound, so more sample groups
+    run concurrently (workers reused round-robin) to fill the GPU."""
+    import dataclasses
+    scfg = dataclasses.replace(cfg, dot_mode=ep.DOT_SERIAL)
+    G2 = args.serial_groups
+    kl = workers[0].prob.kl
+    extra = [GroupWorker(ep, torch, torch.cuda.current_device(), kl) for _ in range(max(0, G2 - len(workers)))]
+    pool = (workers + extra)[:G2]
+    jobs = [[ys[(args.warmup + (i % args.steps), i % len(workers))]] for i in range(G2)]
+    ms, res = timed_round(torch, pool, jobs, scfg)
+    for w in extra:
+        w.prob.close()
+    samples = G2 * S
+    return {"value": round(samples / (ms / 1e3), 3), "unit": "samples/s", "groups": G2,
+            "cg_iterations_max": [r[0] for r in res],
+            "note": "DOT_SERIAL: the reference's reduction order, bitwise equal to its pcg_solve per sample"}
 
 
 def bench_spmv(ctx, ep, torch, pack_group, O, hbm, peak_kind, reps=20):
@@ -375,6 +460,10 @@ def main():
     ap.add_argument("--dot", choices=["canonical", "serial"], default="canonical")
     ap.add_argument("--skip-spmv", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-serial", action="store_true")
+    ap.add_argument("--serial-groups", type=int, default=8)
+    ap.add_argument("--groups", type=int, default=3,
+                    help="sample groups solved concurrently per step (one stream each)")
     ap.add_argument("--profile-only", action="store_true",
                     help="warm-up + timed steps only (for ncu launch lists)")
     args = ap.parse_args()
