@@ -200,6 +200,32 @@ int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* i
 int enprop_problem_solve_host(enprop_problem* p, const double* y_host, double* x_host,
                               const enprop_cg_options* opt, int* iterations, int* lane_status);
 
+/* ------------------------------------ multi-GPU: slab domain decomposition */
+/* The node planes z = k of the mesh are split over nranks like the
+ * reference's partition (partition.cpp:31-72; lower ranks take the extra
+ * plane). Each rank assembles its own rows (no communication), and each CG
+ * iteration exchanges one ghost plane with each neighbour (halo of p) and
+ * all-gathers the per-plane dot sums; totals are formed in global plane order
+ * (the canonical order), so results are bitwise independent of nranks.
+ *   nccl_id != NULL: this process is `rank` of an NCCL job, one GPU per rank
+ *                    (id from enprop_nccl_unique_id on rank 0, broadcast by the host);
+ *   nccl_id == NULL: all nranks are emulated in this process on ctx's GPU with
+ *                    stream-ordered device copies as transport (testing). */
+int enprop_nccl_unique_id(void* out, size_t bytes);
+typedef struct enprop_dist enprop_dist;
+int enprop_dist_create(enprop_ctx* ctx, const enprop_problem_desc* desc, int nranks, int rank,
+                       const void* nccl_id, enprop_dist** out);
+int enprop_dist_destroy(enprop_dist* d);
+/* assemble + Dirichlet of every local rank's rows; y [num_terms][s] on the device */
+int enprop_dist_assemble(enprop_dist* d, const double* y);
+/* CG on A x = -residual, canonical dot order (DOT_SERIAL is INVALID here) */
+int enprop_dist_solve(enprop_dist* d, const enprop_cg_options* opt, int* iterations,
+                      int* lane_status);
+/* local ranks (1 with NCCL, nranks when emulated) and their owned rows / solution */
+int enprop_dist_local_count(enprop_dist* d);
+int enprop_dist_local(enprop_dist* d, int index, int* rank, int* row_begin, int* rows,
+                      double** x);
+
 #ifdef __cplusplus
 }
 #endif

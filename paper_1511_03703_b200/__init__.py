@@ -169,6 +169,13 @@ def lib() -> C.CDLL:
     L.enprop_problem_assemble.argtypes = [_vp, _vp]
     L.enprop_problem_solve.argtypes = [_vp, C.POINTER(_CgOptions), _ip, _ip, _dp, _ip]
     L.enprop_problem_solve_host.argtypes = [_vp, _vp, _vp, C.POINTER(_CgOptions), _ip, _ip]
+    L.enprop_nccl_unique_id.argtypes = [_vp, C.c_size_t]
+    L.enprop_dist_create.argtypes = [_vp, C.POINTER(_ProblemDesc), C.c_int, C.c_int, _vp, C.POINTER(_vp)]
+    L.enprop_dist_destroy.argtypes = [_vp]
+    L.enprop_dist_assemble.argtypes = [_vp, _vp]
+    L.enprop_dist_solve.argtypes = [_vp, C.POINTER(_CgOptions), _ip, _ip]
+    L.enprop_dist_local_count.argtypes = [_vp]
+    L.enprop_dist_local.argtypes = [_vp, C.c_int, _ip, _ip, _ip, C.POINTER(_vp)]
     _lib = L
     return L
 
@@ -501,3 +508,74 @@ def _wrap_device_ptr(ptr: int, count: int, dtype, device: int) -> torch.Tensor:
             self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr,
                                              "data": (ptr, False), "version": 3}
     return torch.as_tensor(_Cai(), device=torch.device("cuda", device))
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for Dist(..., nccl_id=...) (rank 0 makes it)."""
+    buf = (C.c_char * 128)()
+    _check(lib().enprop_nccl_unique_id(buf, 128), "nccl_unique_id")
+    return bytes(buf)
+
+
+class Dist:
+    """Ensemble problem domain-decomposed into z-slabs of node planes over
+    `nranks` (partition.cpp:31-72 rule).  nccl_id=None emulates all ranks in
+    this process on one GPU (stream-ordered copies as transport); with an id,
+    this process is `rank` of an NCCL job.  Canonical dot order only; results
+    are bitwise independent of nranks."""
+
+    def __init__(self, ctx: Context, n: int, s: int, nranks: int, rank: int = 0,
+                 nccl_id: Optional[bytes] = None, kl: KlField = None,
+                 coeffs: PdeCoefficients = None, bc: DirichletBc = None):
+        self.ctx, self.n, self.s, self.nranks = ctx, n, s, nranks
+        self.kl = kl or KlField()
+        d = _ProblemDesc(n, s, self.kl._c(), (coeffs or PdeCoefficients())._c(),
+                         (bc or DirichletBc())._c())
+        h = _vp()
+        idbuf = None if nccl_id is None else (C.c_char * 128).from_buffer_copy(nccl_id)
+        _check(lib().enprop_dist_create(ctx.h, C.byref(d), nranks, rank, idbuf, C.byref(h)), "Dist")
+        self.h = h
+
+    def assemble(self, y: torch.Tensor):
+        _need_cuda(y, torch.float64, "y")
+        if y.numel() != self.kl.num_terms * self.s:
+            raise ValueError("assemble: sample vector length mismatch")
+        _check(lib().enprop_dist_assemble(self.h, _ptr(y)), "assemble")
+
+    def solve(self, config: SolverConfig = None, raise_on_failure: bool = True):
+        cfg = config or SolverConfig(dot_mode=DOT_CANONICAL)
+        lanes = self.s if cfg.flavour == CG_UNCOUPLED else 1
+        it, ls = (C.c_int * lanes)(), (C.c_int * lanes)()
+        opt = cfg._c()
+        rc = lib().enprop_dist_solve(self.h, C.byref(opt), it, ls)
+        if rc in (ERR_NO_CONVERGENCE, ERR_INDEFINITE):
+            if raise_on_failure:
+                raise SolverError(_err(), [], rc, list(it))
+        else:
+            _check(rc, "solve")
+        return (list(it) if cfg.flavour == CG_UNCOUPLED else it[0]), list(ls)
+
+    def local(self):
+        """[(rank, row_begin, rows, x view [rows][s])] of the ranks in this process."""
+        out = []
+        for i in range(lib().enprop_dist_local_count(self.h)):
+            rk, rb, rows, xp = C.c_int(), C.c_int(), C.c_int(), _vp()
+            _check(lib().enprop_dist_local(self.h, i, C.byref(rk), C.byref(rb), C.byref(rows), C.byref(xp)))
+            x = _wrap_device_ptr(xp.value, rows.value * self.s, torch.float64, self.ctx.device)
+            out.append((rk.value, rb.value, rows.value, x.view(rows.value, self.s)))
+        return out
+
+    def solution(self) -> torch.Tensor:
+        """The owned parts of the local ranks, concatenated in row order."""
+        return torch.cat([x for (_, _, _, x) in sorted(self.local(), key=lambda t: t[1])], dim=0)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().enprop_dist_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

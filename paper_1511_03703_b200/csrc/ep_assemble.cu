@@ -27,9 +27,10 @@ namespace ep {
 template <int S, bool kNonlinear, bool kHasU>
 __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-  const int row = gt / S;
+  const int lrow = gt / S;  // local row
+  const int row = a.row_begin + lrow;  // global node id
   const int e = gt - row * S;
-  if (row >= a.rows) return;
+  if (lrow >= a.rows) return;
   const int n = a.n, N = n + 1, n2 = 2 * n;
   const int i = row % N, j = (row / N) % N, k = row / (N * N);
   const AsmTables& T = *a.tab;
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
           for (int c = 0; c < 8; ++c) {
             const int node =
                 (ci + (c & 1)) + N * ((cj + ((c >> 1) & 1)) + N * (ck + ((c >> 2) & 1)));
-            ue[c] = a.u[(size_t)node * S + e];
+            ue[c] = a.u[(size_t)(node - a.u_shift) * S + e];
           }
         }
 
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
     if (i == 0 || i == n) {
 #pragma unroll
       for (int t = 0; t < 27; ++t) acc[t] = (t == 13) ? 1.0 : 0.0;
-      const double ur = kHasU ? a.u[(size_t)row * S + e] : 0.0;
+      const double ur = kHasU ? a.u[(size_t)(row - a.u_shift) * S + e] : 0.0;
       res = EP_DSUB(ur, i == 0 ? a.bc0 : a.bc1);
     } else {
 #pragma unroll
@@ -148,7 +149,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
         if (jj < 0 || jj >= N || kk < 0 || kk >= N) continue;
         if (ii == 0 || ii == n) {
           const double g = ii == 0 ? a.bc0 : a.bc1;
-          const double uc = kHasU ? a.u[(size_t)(ii + N * (jj + N * kk)) * S + e] : 0.0;
+          const double uc = kHasU ? a.u[(size_t)(ii + N * (jj + N * kk) - a.u_shift) * S + e] : 0.0;
           res = EP_DADD(res, EP_DMUL(acc[t], EP_DSUB(g, uc)));
           acc[t] = 0.0;
         }
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
     }
   }
 
-  const int rs = a.row_map[row];
+  const int rs = a.row_map[lrow];
   int pos = 0;
 #pragma unroll
   for (int t = 0; t < 27; ++t) {
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
     a.values[(size_t)(rs + pos) * S + e] = acc[t];
     ++pos;
   }
-  a.residual[(size_t)row * S + e] = res;
+  a.residual[(size_t)lrow * S + e] = res;
 }
 
 template <int S>

@@ -13,12 +13,13 @@
 
 #include "enprop_b200.h"
 #include "ep_host.h"
+#include "ep_internal.h"
 #include "ep_kernels.h"
 
 using namespace ep;
+using namespace ep_internal;
 
-namespace {
-
+namespace ep_internal {
 thread_local std::string g_last_error;
 
 int fail(int code, const std::string& msg) {
@@ -31,33 +32,8 @@ int cuda_fail(cudaError_t err, const char* where) {
               std::string(where) + ": " + cudaGetErrorString(err));
 }
 
-#define EP_CUDA(call)                                  \
-  do {                                                 \
-    cudaError_t _e = (call);                           \
-    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
-  } while (0)
-
 bool valid_width(int s) { return s == 1 || s == 2 || s == 4 || s == 8 || s == 16 || s == 32; }
-
-}  // namespace
-
-struct enprop_ctx {
-  int device = 0;
-  cudaStream_t own = nullptr;
-  cudaStream_t stream = nullptr;
-  int64_t launches = 0;
-  int* pinned_flags = nullptr;  // [2] convergence flags read back by the CG driver
-  cudaEvent_t flag_ev[2] = {nullptr, nullptr};
-  int spmv_pipeline = 0;    // ENPROP_OPT_SPMV_PIPELINE
-  int fused_direction = 0;  // ENPROP_OPT_FUSED_DIRECTION (split measured faster on B200)
-  // optional CUDA-event timing of the CG SpMV launches (bench roofline)
-  int profile = 0;
-  std::vector<cudaEvent_t> prof_ev;  // 5 events per profiled iteration, reused
-  size_t prof_used = 0;
-  double prof_ms = 0.0;       // CG SpMV phase (direction + SpMV)
-  int64_t prof_count = 0;     // profiled iterations that did work
-  double prof_detail[5] = {0, 0, 0, 0, 0};  // spmv, fin pq, update, fin rr, iteration
-};
+}  // namespace ep_internal
 
 namespace {
 
@@ -117,6 +93,7 @@ FinArgs fin_args(const CgWork& w, const TileMap& tm, int phase) {
   f.cg = w.state;
   f.hist = w.hist;
   f.lanes_out = nullptr;
+  f.seg_only = 0;
   return f;
 }
 
@@ -215,8 +192,9 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
         double* p_new = w.p[(launched + 1) & 1];
         cudaEvent_t* ev = ctx->profile ? prof_slot(ctx) : nullptr;
         if (ev) EP_CUDA(cudaEventRecord(ev[0], st));
-        EP_CUDA(launch_cg_spmv(s, canon, ctx->fused_direction != 0, tm, row_map, col_entry, values,
-                               w.r, p_old, p_new, w.q, x, f_pq, st));
+        EP_CUDA(launch_cg_spmv(s, canon, ctx->fused_direction != 0, ctx->fused_direction == 0, tm,
+                               row_map, col_entry, values, w.r, p_old, p_new, w.q, x, p_new, f_pq,
+                               st));
         if (ev) EP_CUDA(cudaEventRecord(ev[1], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[2], st));
@@ -442,14 +420,8 @@ int enprop_kl_describe(const enprop_kl_params* kl, int* mode_axes, double* mode_
 
 }  // extern "C"
 
-namespace {
+namespace ep_internal {
 
-// Device tables of one (mesh, field, coefficients) combination.
-struct AsmSetup {
-  double* F = nullptr;
-  AsmTables* tab = nullptr;
-  AsmArgs args{};
-};
 
 int make_asm_setup(enprop_ctx* c, int n, const enprop_kl_params* kl,
                    const enprop_pde_coeffs* coeffs, AsmSetup& out) {
@@ -489,7 +461,7 @@ void free_asm_setup(AsmSetup& s) {
   s = AsmSetup{};
 }
 
-}  // namespace
+}  // namespace ep_internal
 
 extern "C" {
 
@@ -639,11 +611,6 @@ struct enprop_problem {
   CgWork work;
 };
 
-namespace {
-
-__global__ void k_negate(int64_t n, const double* __restrict__ a, double* __restrict__ b);
-
-}  // namespace
 
 extern "C" {
 
@@ -736,8 +703,7 @@ int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* i
   enprop_cg_options o = *opt;
   if (o.seg_rows <= 0) o.seg_rows = (p->desc.cells_per_axis + 1) * (p->desc.cells_per_axis + 1);
   const int64_t len = (int64_t)p->rows * s;  // rhs = -residual (bench.cpp:298-299)
-  k_negate<<<(int)((len + 255) / 256), 256, 0, p->ctx->stream>>>(len, p->residual, p->rhs);
-  EP_CUDA(cudaGetLastError());
+  EP_CUDA(launch_negate(len, p->residual, p->rhs, p->ctx->stream));
   p->ctx->launches += 1;
   return run_cg(p->ctx, s, p->rows, p->row_map, p->col_entry, p->values, p->rhs, p->x, &o, p->work,
                 iterations, lane_status, history, hist_len);
@@ -761,9 +727,14 @@ int enprop_problem_solve_host(enprop_problem* p, const double* y_host, double* x
 
 }  // extern "C"
 
-namespace {
+namespace ep_internal {
 __global__ void k_negate(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) b[i] = -a[i];
 }
-}  // namespace
+cudaError_t launch_negate(int64_t n, const double* a, double* b, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_negate<<<(int)((n + 255) / 256), 256, 0, st>>>(n, a, b);
+  return cudaGetLastError();
+}
+}  // namespace ep_internal

@@ -1,0 +1,457 @@
+// Multi-GPU ensemble solve by 1-D slab decomposition of the node planes.
+//
+// Decomposition (the reference's partition.cpp:31-72 rule applied to z-planes
+// of nodes: lower ranks take the extra plane). With x-fastest numbering
+// (mesh.hpp:24-26) a z-slab is a contiguous row range, so a rank's matrix is a
+// slice of the global CRS and a ghost plane is one contiguous N^2 * s block:
+//   owned rows   [k0 N^2, k1 N^2)
+//   ext layout   [lo ghost plane | owned planes | hi ghost plane]  (gathered p)
+// Assembly needs no communication (node-centric gather over the cells around
+// each owned node). Per CG iteration: direction pass -> halo of p_new (one
+// plane to each neighbour) -> SpMV with p.q per-plane sums -> all-gather of
+// the per-plane sums -> canonical total in global plane order -> update ->
+// all-gather -> total. The canonical order makes every rank's
+// totals, hence alpha/beta/iterations/solutions, identical to the one-GPU
+// solve bit for bit, independent of the rank count.
+//
+// Transports: NCCL (one process per GPU; libnccl.so.2 loaded at run time, so
+// an already loaded copy — e.g. torch's — is shared), or an in-process
+// emulation of all ranks on one GPU where the halo and the all-gather are
+// stream-ordered device copies (no kernel waits on another rank).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "enprop_b200.h"
+#include "ep_internal.h"
+#include "ep_kernels.h"
+
+using namespace ep;
+using namespace ep_internal;
+
+namespace {
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+
+  bool load() {
+    if (h) return true;
+    h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return false;
+#define EP_SYM(f, name)                                             \
+  f = reinterpret_cast<decltype(f)>(dlsym(h, name));                \
+  if (!f) return false;
+    EP_SYM(GetUniqueId, "ncclGetUniqueId");
+    EP_SYM(CommInitRank, "ncclCommInitRank");
+    EP_SYM(CommDestroy, "ncclCommDestroy");
+    EP_SYM(Send, "ncclSend");
+    EP_SYM(Recv, "ncclRecv");
+    EP_SYM(GroupStart, "ncclGroupStart");
+    EP_SYM(GroupEnd, "ncclGroupEnd");
+    EP_SYM(AllGather, "ncclAllGather");
+    EP_SYM(GetErrorString, "ncclGetErrorString");
+#undef EP_SYM
+    return true;
+  }
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  return api;
+}
+
+#define EP_NCCL(call)                                                                   \
+  do {                                                                                  \
+    ncclResult_t _r = (call);                                                           \
+    if (_r != ncclSuccess)                                                              \
+      return fail(ENPROP_ERR_CUDA, std::string(#call) + ": " + nccl().GetErrorString(_r)); \
+  } while (0)
+
+// start of global row g in the 27-point graph (closed form, as k_build_graph)
+int64_t graph_start(int n, int64_t g) {
+  const int64_t N = n + 1, W = 3 * N - 2;
+  auto cnt = [N](int64_t t) { return 1 + (t > 0) + (t < N - 1); };
+  auto pre = [](int64_t t) { return t == 0 ? 0 : 2 + 3 * (t - 1); };
+  const int64_t i = g % N, j = (g / N) % N, k = g / (N * N);
+  if (g >= N * N * N) return (3 * N - 2) * (3 * N - 2) * (3 * N - 2);
+  return pre(k) * W * W + cnt(k) * (pre(j) * W + cnt(j) * pre(i));
+}
+
+// One rank's slab: graph slice, matrix, CG vectors (p in ext layout).
+struct DistRank {
+  int rank = 0, k0 = 0, k1 = 0;
+  int row_begin = 0, rows = 0, lo_rows = 0, hi_rows = 0, ext_begin = 0;
+  int64_t nnz = 0;
+  int* row_map = nullptr;
+  int* col_entry = nullptr;
+  double *values = nullptr, *residual = nullptr, *x = nullptr, *r = nullptr, *q = nullptr;
+  double* p[2] = {nullptr, nullptr};  // ext layout
+  TileMap tm{};
+  double *partials = nullptr, *seg_local = nullptr, *gathered = nullptr, *hist = nullptr;
+  int* counters = nullptr;
+  int* plane_pos = nullptr;
+  CgState* state = nullptr;
+};
+
+}  // namespace
+
+struct enprop_dist {
+  enprop_ctx* ctx = nullptr;
+  enprop_problem_desc desc{};
+  int nranks = 1, n = 0, N = 0, plane = 0, maxplanes = 0, maxit = -1;
+  bool emulated = true;
+  ncclComm_t comm = nullptr;
+  AsmSetup setup;
+  std::vector<DistRank> ranks;  // emulated: all ranks; NCCL: this process's rank
+};
+
+namespace {
+
+void plane_range(int N, int P, int r, int& k0, int& k1) {
+  const int base = N / P, extra = N % P;  // partition.cpp:50-58
+  k0 = r * base + std::min(r, extra);
+  k1 = k0 + base + (r < extra ? 1 : 0);
+}
+
+void free_rank(DistRank& d) {
+  for (void* q : {(void*)d.row_map, (void*)d.col_entry, (void*)d.values, (void*)d.residual,
+                  (void*)d.x, (void*)d.r, (void*)d.q, (void*)d.p[0], (void*)d.p[1],
+                  (void*)d.partials, (void*)d.seg_local, (void*)d.gathered, (void*)d.hist,
+                  (void*)d.counters, (void*)d.plane_pos, (void*)d.state})
+    if (q) cudaFree(q);
+  d = DistRank{};
+}
+
+int setup_rank(enprop_dist* D, DistRank& d, int r) {
+  const int s = D->desc.ensemble_size;
+  const int n = D->n, N = D->N, plane = D->plane, P = D->nranks;
+  d.rank = r;
+  plane_range(N, P, r, d.k0, d.k1);
+  d.row_begin = d.k0 * plane;
+  d.rows = (d.k1 - d.k0) * plane;
+  d.lo_rows = d.k0 > 0 ? plane : 0;
+  d.hi_rows = d.k1 < N ? plane : 0;
+  d.ext_begin = d.row_begin - d.lo_rows;
+  d.nnz = graph_start(n, d.row_begin + d.rows) - graph_start(n, d.row_begin);
+  const size_t vec = (size_t)d.rows * s * sizeof(double);
+  const size_t ext = (size_t)(d.lo_rows + d.rows + d.hi_rows) * s * sizeof(double);
+  d.tm = make_tile_map(d.rows, plane);
+  EP_CUDA(cudaMalloc(&d.row_map, (d.rows + 1) * sizeof(int)));
+  EP_CUDA(cudaMalloc(&d.col_entry, d.nnz * sizeof(int)));
+  EP_CUDA(cudaMalloc(&d.values, (size_t)d.nnz * s * sizeof(double)));
+  EP_CUDA(cudaMalloc(&d.residual, vec));
+  EP_CUDA(cudaMalloc(&d.x, vec));
+  EP_CUDA(cudaMalloc(&d.r, vec));
+  EP_CUDA(cudaMalloc(&d.q, vec));
+  EP_CUDA(cudaMalloc(&d.p[0], ext));
+  EP_CUDA(cudaMalloc(&d.p[1], ext));
+  EP_CUDA(cudaMemset(d.p[0], 0, ext));
+  EP_CUDA(cudaMemset(d.p[1], 0, ext));
+  EP_CUDA(cudaMalloc(&d.partials, (size_t)std::max(d.tm.num_tiles(), 1) * s * sizeof(double)));
+  EP_CUDA(cudaMalloc(&d.seg_local, (size_t)D->maxplanes * s * sizeof(double)));
+  EP_CUDA(cudaMemset(d.seg_local, 0, (size_t)D->maxplanes * s * sizeof(double)));
+  EP_CUDA(cudaMalloc(&d.gathered, (size_t)P * D->maxplanes * s * sizeof(double)));
+  EP_CUDA(cudaMalloc(&d.counters, (size_t)(D->maxplanes + 1) * sizeof(int)));
+  EP_CUDA(cudaMemset(d.counters, 0, (size_t)(D->maxplanes + 1) * sizeof(int)));
+  EP_CUDA(cudaMalloc(&d.state, sizeof(CgState)));
+  // global plane k lives at gathered[rank_of(k) * maxplanes + (k - k0(rank))]
+  std::vector<int> pos(N);
+  for (int q = 0; q < P; ++q) {
+    int a, b;
+    plane_range(N, P, q, a, b);
+    for (int k = a; k < b; ++k) pos[k] = q * D->maxplanes + (k - a);
+  }
+  EP_CUDA(cudaMalloc(&d.plane_pos, N * sizeof(int)));
+  EP_CUDA(cudaMemcpy(d.plane_pos, pos.data(), N * sizeof(int), cudaMemcpyHostToDevice));
+  EP_CUDA(launch_build_graph_range(n, d.row_begin, d.rows, d.ext_begin, d.row_map, d.col_entry,
+                                   D->ctx->stream));
+  D->ctx->launches += 1;
+  return ENPROP_OK;
+}
+
+FinArgs rank_fin(const DistRank& d, int phase) {
+  FinArgs f;
+  f.partials = d.partials;
+  f.seg_sums = d.seg_local;
+  f.seg_count = d.counters;
+  f.seg_done = d.counters + (d.tm.num_segs > 0 ? d.tm.num_segs : 1);
+  f.phase = phase;
+  f.cg = d.state;
+  f.hist = d.hist;
+  f.lanes_out = nullptr;
+  f.seg_only = 1;
+  return f;
+}
+
+// halo of the p buffer `which` (first owned plane -> rank-1's hi ghost, last
+// owned plane -> rank+1's lo ghost)
+int halo(enprop_dist* D, int which) {
+  const int s = D->desc.ensemble_size;
+  const size_t pe = (size_t)D->plane * s;
+  cudaStream_t st = D->ctx->stream;
+  if (D->emulated) {
+    for (size_t i = 0; i < D->ranks.size(); ++i) {
+      DistRank& d = D->ranks[i];
+      if (i > 0) {
+        DistRank& lo = D->ranks[i - 1];
+        EP_CUDA(cudaMemcpyAsync(lo.p[which] + (size_t)(lo.lo_rows + lo.rows) * s, d.p[which] + (size_t)d.lo_rows * s,
+                                pe * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      }
+      if (i + 1 < D->ranks.size()) {
+        DistRank& hi = D->ranks[i + 1];
+        EP_CUDA(cudaMemcpyAsync(hi.p[which], d.p[which] + (size_t)(d.lo_rows + d.rows - D->plane) * s,
+                                pe * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    return ENPROP_OK;
+  }
+  DistRank& d = D->ranks[0];
+  auto& api = nccl();
+  EP_NCCL(api.GroupStart());
+  if (d.rank > 0) {
+    EP_NCCL(api.Send(d.p[which] + (size_t)d.lo_rows * s, pe, ncclDouble, d.rank - 1, D->comm, st));
+    EP_NCCL(api.Recv(d.p[which], pe, ncclDouble, d.rank - 1, D->comm, st));
+  }
+  if (d.rank + 1 < D->nranks) {
+    EP_NCCL(api.Send(d.p[which] + (size_t)(d.lo_rows + d.rows - D->plane) * s, pe, ncclDouble, d.rank + 1, D->comm, st));
+    EP_NCCL(api.Recv(d.p[which] + (size_t)(d.lo_rows + d.rows) * s, pe, ncclDouble, d.rank + 1, D->comm, st));
+  }
+  EP_NCCL(api.GroupEnd());
+  return ENPROP_OK;
+}
+
+int allgather(enprop_dist* D) {
+  const size_t cnt = (size_t)D->maxplanes * D->desc.ensemble_size;
+  cudaStream_t st = D->ctx->stream;
+  if (D->emulated) {
+    for (auto& dst : D->ranks)
+      for (size_t q = 0; q < D->ranks.size(); ++q)
+        EP_CUDA(cudaMemcpyAsync(dst.gathered + q * cnt, D->ranks[q].seg_local, cnt * sizeof(double),
+                                cudaMemcpyDeviceToDevice, st));
+    return ENPROP_OK;
+  }
+  EP_NCCL(nccl().AllGather(D->ranks[0].seg_local, D->ranks[0].gathered, cnt, ncclDouble, D->comm, st));
+  return ENPROP_OK;
+}
+
+int fin_all(enprop_dist* D, int phase) {
+  const int s = D->desc.ensemble_size;
+  for (auto& d : D->ranks) {
+    EP_CUDA(launch_fin_gathered(s, D->N, d.gathered, d.plane_pos, phase, d.state, d.hist, nullptr,
+                                D->ctx->stream));
+    D->ctx->launches += 1;
+  }
+  return ENPROP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int enprop_nccl_unique_id(void* out, size_t bytes) {
+  if (!out || bytes < sizeof(ncclUniqueId)) return fail(ENPROP_ERR_INVALID, "enprop_nccl_unique_id: buffer too small");
+  if (!nccl().load()) return fail(ENPROP_ERR_CUDA, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  EP_NCCL(nccl().GetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+  return ENPROP_OK;
+}
+
+int enprop_dist_destroy(enprop_dist* D) {
+  if (!D) return ENPROP_OK;
+  for (auto& d : D->ranks) free_rank(d);
+  free_asm_setup(D->setup);
+  if (D->comm) nccl().CommDestroy(D->comm);
+  delete D;
+  return ENPROP_OK;
+}
+
+int enprop_dist_create(enprop_ctx* c, const enprop_problem_desc* desc, int nranks, int rank,
+                       const void* nccl_id, enprop_dist** out) {
+  if (!c || !desc || !out) return fail(ENPROP_ERR_INVALID, "enprop_dist_create: null argument");
+  if (!valid_width(desc->ensemble_size)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
+  const int n = desc->cells_per_axis;
+  if (n < 1) return fail(ENPROP_ERR_INVALID, "StructuredMesh: cells_per_axis must be at least 1");
+  if (nranks < 1 || nranks > n + 1)  // partition.cpp:35-38
+    return fail(ENPROP_ERR_INVALID, "partition: ranks must be in [1, node planes]");
+  if (rank < 0 || rank >= nranks) return fail(ENPROP_ERR_INVALID, "enprop_dist_create: bad rank");
+  auto* D = new (std::nothrow) enprop_dist();
+  if (!D) return fail(ENPROP_ERR_OOM, "out of host memory");
+  D->ctx = c;
+  D->desc = *desc;
+  D->nranks = nranks;
+  D->n = n;
+  D->N = n + 1;
+  D->plane = D->N * D->N;
+  D->maxplanes = (D->N + nranks - 1) / nranks;
+  D->emulated = nccl_id == nullptr;
+  auto bail = [&](int rc) {
+    enprop_dist_destroy(D);
+    return rc;
+  };
+  int rc = make_asm_setup(c, n, &desc->kl, &desc->coeffs, D->setup);
+  if (rc) return bail(rc);
+  if (!D->emulated) {
+    if (!nccl().load()) return bail(fail(ENPROP_ERR_CUDA, "libnccl.so.2 could not be loaded"));
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ncclResult_t r = nccl().CommInitRank(&D->comm, nranks, id, rank);
+    if (r != ncclSuccess) return bail(fail(ENPROP_ERR_CUDA, std::string("ncclCommInitRank: ") + nccl().GetErrorString(r)));
+  }
+  const int local = D->emulated ? nranks : 1;
+  D->ranks.resize(local);
+  for (int i = 0; i < local; ++i) {
+    rc = setup_rank(D, D->ranks[i], D->emulated ? i : rank);
+    if (rc) return bail(rc);
+  }
+  cudaError_t err = cudaStreamSynchronize(c->stream);
+  if (err != cudaSuccess) return bail(cuda_fail(err, "enprop_dist_create"));
+  *out = D;
+  return ENPROP_OK;
+}
+
+int enprop_dist_local_count(enprop_dist* D) { return D ? (int)D->ranks.size() : 0; }
+
+int enprop_dist_local(enprop_dist* D, int index, int* rank, int* row_begin, int* rows, double** x) {
+  if (!D || index < 0 || index >= (int)D->ranks.size()) return fail(ENPROP_ERR_INVALID, "enprop_dist_local: bad index");
+  const DistRank& d = D->ranks[index];
+  if (rank) *rank = d.rank;
+  if (row_begin) *row_begin = d.row_begin;
+  if (rows) *rows = d.rows;
+  if (x) *x = d.x;
+  return ENPROP_OK;
+}
+
+int enprop_dist_assemble(enprop_dist* D, const double* y) {
+  if (!D || !y) return fail(ENPROP_ERR_INVALID, "enprop_dist_assemble: null argument");
+  for (auto& d : D->ranks) {
+    AsmArgs a = D->setup.args;
+    a.rows = d.rows;
+    a.row_begin = d.row_begin;
+    a.u = nullptr;
+    a.y = y;
+    a.row_map = d.row_map;
+    a.values = d.values;
+    a.residual = d.residual;
+    a.dirichlet = 1;
+    a.bc0 = D->desc.bc.x0_value;
+    a.bc1 = D->desc.bc.x1_value;
+    EP_CUDA(launch_assemble(D->desc.ensemble_size, a, D->ctx->stream));
+    D->ctx->launches += 1;
+  }
+  return ENPROP_OK;
+}
+
+int enprop_dist_solve(enprop_dist* D, const enprop_cg_options* opt, int* iterations, int* lane_status) {
+  if (!D || !opt) return fail(ENPROP_ERR_INVALID, "enprop_dist_solve: null argument");
+  if (opt->dot_mode != ENPROP_DOT_CANONICAL)
+    return fail(ENPROP_ERR_INVALID, "enprop_dist_solve: the multi-GPU solve uses the canonical dot order");
+  if (opt->flavour != ENPROP_CG_COUPLED && opt->flavour != ENPROP_CG_UNCOUPLED)
+    return fail(ENPROP_ERR_INVALID, "enprop_cg: unknown CG flavour");
+  if (opt->max_iterations < 0) return fail(ENPROP_ERR_INVALID, "enprop_cg: negative max_iterations");
+  const int s = D->desc.ensemble_size;
+  cudaStream_t st = D->ctx->stream;
+  enprop_ctx* ctx = D->ctx;
+  if (D->maxit < opt->max_iterations) {
+    for (auto& d : D->ranks) {
+      if (d.hist) cudaFree(d.hist);
+      d.hist = nullptr;
+      EP_CUDA(cudaMalloc(&d.hist, (size_t)(opt->max_iterations + 1) * s * sizeof(double)));
+    }
+    D->maxit = opt->max_iterations;
+  }
+  CgState init;
+  std::memset(&init, 0, sizeof(init));
+  init.flavour = opt->flavour;
+  init.s = s;
+  init.maxit = opt->max_iterations;
+  init.tol = opt->tol;
+  for (auto& d : D->ranks) {
+    const size_t vec = (size_t)d.rows * s * sizeof(double);
+    EP_CUDA(cudaMemcpyAsync(d.state, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+    EP_CUDA(cudaMemsetAsync(d.x, 0, vec, st));
+    EP_CUDA(launch_negate((int64_t)d.rows * s, d.residual, d.r, st));  // b = -residual; r = b
+    EP_CUDA(launch_dot_tiles(s, d.tm, d.r, d.r, rank_fin(d, kPhaseInit), st));
+    ctx->launches += 2;
+  }
+  int rc = allgather(D);
+  if (rc) return rc;
+  rc = fin_all(D, kPhaseInit);
+  if (rc) return rc;
+
+  const int chunk = opt->check_every > 0 ? opt->check_every : 16;
+  const int limit = opt->max_iterations;
+  int launched = 0, slot = 0;
+  bool pending = false;
+  while (true) {
+    for (int c2 = 0; c2 < chunk && launched < limit; ++c2, ++launched) {
+      const int po = launched & 1, pn = (launched + 1) & 1;
+      for (auto& d : D->ranks) {
+        EP_CUDA(launch_cg_direction(s, d.rows, d.r, d.p[po] + (size_t)d.lo_rows * s,
+                                    d.p[pn] + (size_t)d.lo_rows * s, d.x, d.state, st));
+        ctx->launches += 1;
+      }
+      if ((rc = halo(D, pn))) return rc;
+      for (auto& d : D->ranks) {
+        EP_CUDA(launch_cg_spmv(s, true, false, false, d.tm, d.row_map, d.col_entry, d.values, d.r,
+                               d.p[po] + (size_t)d.lo_rows * s, d.p[pn] + (size_t)d.lo_rows * s, d.q,
+                               d.x, d.p[pn], rank_fin(d, kPhasePQ), st));
+        ctx->launches += 1;
+      }
+      if ((rc = allgather(D)) || (rc = fin_all(D, kPhasePQ))) return rc;
+      for (auto& d : D->ranks) {
+        EP_CUDA(launch_cg_update(s, true, d.tm, d.r, d.q, rank_fin(d, kPhaseRR), st));
+        ctx->launches += 1;
+      }
+      if ((rc = allgather(D)) || (rc = fin_all(D, kPhaseRR))) return rc;
+    }
+    EP_CUDA(cudaMemcpyAsync(&ctx->pinned_flags[slot], &D->ranks[0].state->done, sizeof(int),
+                            cudaMemcpyDeviceToHost, st));
+    EP_CUDA(cudaEventRecord(ctx->flag_ev[slot], st));
+    if (pending) {
+      EP_CUDA(cudaEventSynchronize(ctx->flag_ev[slot ^ 1]));
+      if (ctx->pinned_flags[slot ^ 1]) break;
+    }
+    if (launched >= limit) {
+      EP_CUDA(cudaEventSynchronize(ctx->flag_ev[slot]));
+      break;
+    }
+    pending = true;
+    slot ^= 1;
+  }
+  for (auto& d : D->ranks) {
+    double* pp[2] = {d.p[0] + (size_t)d.lo_rows * s, d.p[1] + (size_t)d.lo_rows * s};
+    EP_CUDA(launch_cg_flush(s, d.rows, d.x, pp, d.state, st));
+    ctx->launches += 1;
+  }
+  EP_CUDA(cudaStreamSynchronize(st));
+  CgState fin;
+  EP_CUDA(cudaMemcpy(&fin, D->ranks[0].state, sizeof(fin), cudaMemcpyDeviceToHost));
+  if (!fin.done) return fail(ENPROP_ERR_CUDA, "enprop_dist_solve: solver did not finish (internal)");
+  const int lanes = opt->flavour == ENPROP_CG_UNCOUPLED ? s : 1;
+  for (int l = 0; l < lanes; ++l) {
+    if (iterations) iterations[l] = fin.iters[l];
+    if (lane_status) lane_status[l] = opt->flavour == ENPROP_CG_UNCOUPLED ? fin.lane_status[l] : fin.status;
+  }
+  if (fin.status == ENPROP_ERR_NO_CONVERGENCE)
+    return fail(ENPROP_ERR_NO_CONVERGENCE, "pcg_solve: no convergence");
+  if (fin.status == ENPROP_ERR_INDEFINITE)
+    return fail(ENPROP_ERR_INDEFINITE, "pcg_solve: operator not positive definite (p'Ap <= 0)");
+  return ENPROP_OK;
+}
+
+}  // extern "C"

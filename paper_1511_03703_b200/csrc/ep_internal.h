@@ -1,0 +1,52 @@
+// Host internals shared by the C-ABI translation units (ep_capi.cu, ep_dist.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "enprop_b200.h"
+#include "ep_kernels.h"
+
+#define EP_CUDA(call)                                  \
+  do {                                                 \
+    cudaError_t _e = (call);                           \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+struct enprop_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  int* pinned_flags = nullptr;  // [2] convergence flags read back by the CG driver
+  cudaEvent_t flag_ev[2] = {nullptr, nullptr};
+  int spmv_pipeline = 0;    // ENPROP_OPT_SPMV_PIPELINE
+  int fused_direction = 0;  // ENPROP_OPT_FUSED_DIRECTION (split measured faster on B200)
+  // optional CUDA-event timing of the CG SpMV launches (bench roofline)
+  int profile = 0;
+  std::vector<cudaEvent_t> prof_ev;  // 5 events per profiled iteration, reused
+  size_t prof_used = 0;
+  double prof_ms = 0.0;       // CG SpMV phase (direction + SpMV)
+  int64_t prof_count = 0;     // profiled iterations that did work
+  double prof_detail[5] = {0, 0, 0, 0, 0};  // spmv, fin pq, update, fin rr, iteration
+};
+
+namespace ep_internal {
+
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t err, const char* where);
+bool valid_width(int s);
+
+// Device tables of one (mesh, field, coefficients) combination.
+struct AsmSetup {
+  double* F = nullptr;
+  ep::AsmTables* tab = nullptr;
+  ep::AsmArgs args{};
+};
+int make_asm_setup(enprop_ctx* c, int n, const enprop_kl_params* kl,
+                   const enprop_pde_coeffs* coeffs, AsmSetup& out);
+void free_asm_setup(AsmSetup& s);
+cudaError_t launch_negate(int64_t n, const double* a, double* b, cudaStream_t st);
+
+}  // namespace ep_internal

@@ -46,6 +46,39 @@ __global__ void k_build_graph(int n, int* __restrict__ row_map, int* __restrict_
       for (int ii = ilo; ii <= ihi; ++ii) col_entry[at++] = ii + N * (jj + N * kk);
 }
 
+__global__ void k_build_graph_range(int n, int row_begin, int nrows, int col_shift,
+                                    int* __restrict__ row_map, int* __restrict__ col_entry) {
+  const int N = n + 1;
+  const int W = 3 * N - 2;
+  const int lrow = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lrow >= nrows) return;
+  auto start_of = [&](int row) {
+    const int i = row % N, j = (row / N) % N, k = row / (N * N);
+    return axis_prefix(k) * W * W +
+           axis_count(k, N) * (axis_prefix(j) * W + axis_count(j, N) * axis_prefix(i));
+  };
+  const int row = row_begin + lrow;
+  const int i = row % N, j = (row / N) % N, k = row / (N * N);
+  const int base = start_of(row_begin);
+  const int start = start_of(row) - base;
+  if (lrow == 0) row_map[0] = 0;
+  row_map[lrow + 1] = start + axis_count(i, N) * axis_count(j, N) * axis_count(k, N);
+  int at = start;
+  const int ilo = i > 0 ? i - 1 : 0, ihi = i < N - 1 ? i + 1 : N - 1;
+  const int jlo = j > 0 ? j - 1 : 0, jhi = j < N - 1 ? j + 1 : N - 1;
+  const int klo = k > 0 ? k - 1 : 0, khi = k < N - 1 ? k + 1 : N - 1;
+  for (int kk = klo; kk <= khi; ++kk)
+    for (int jj = jlo; jj <= jhi; ++jj)
+      for (int ii = ilo; ii <= ihi; ++ii) col_entry[at++] = ii + N * (jj + N * kk) - col_shift;
+}
+
+cudaError_t launch_build_graph_range(int n, int row_begin, int rows, int col_shift, int* row_map,
+                                     int* col_entry, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  k_build_graph_range<<<(rows + 255) / 256, 256, 0, st>>>(n, row_begin, rows, col_shift, row_map, col_entry);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_build_graph(int n, int* row_map, int* col_entry, cudaStream_t st) {
   const int N = n + 1;
   const int rows = N * N * N;
@@ -311,6 +344,10 @@ __device__ void tiles_finish(const TileMap& tm, double* sprod, const FinArgs& f)
       __syncthreads();
     }
     if (threadIdx.x < S) f.seg_sums[(size_t)seg * S + threadIdx.x] = acc;
+    if (f.seg_only) {  // multi-GPU: the host all-gathers the segment sums
+      if (threadIdx.x == 0) f.seg_count[seg] = 0;
+      continue;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
       f.seg_count[seg] = 0;
@@ -543,6 +580,49 @@ __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hi
   }
 }
 
+// Multi-GPU canonical total: lanes[e] = 0.0 + seg_0 + seg_1 + ... over the
+// global planes in order, read from the all-gathered per-rank segment sums
+// (gathered[plane_pos[k]][e]); then the CG scalar phase. Every rank runs it on
+// identical data, so all ranks take identical decisions.
+template <int S>
+__global__ void __launch_bounds__(256) k_fin_gathered(int planes, const double* __restrict__ gathered,
+                                                      const int* __restrict__ plane_pos, int phase,
+                                                      CgState* cg, double* hist, double* lanes_out) {
+  if ((phase == kPhasePQ || phase == kPhaseRR) && cg->done) return;
+  constexpr int kChunk = 64;
+  __shared__ double sch[kChunk * S];
+  __shared__ double lanes[S];
+  double tot = 0.0;
+  for (int k0 = 0; k0 < planes; k0 += kChunk) {
+    const int cnt = min(kChunk, planes - k0);
+    for (int idx = threadIdx.x; idx < cnt * S; idx += blockDim.x) {
+      const int k = idx / S, e = idx - k * S;
+      sch[idx] = gathered[(size_t)plane_pos[k0 + k] * S + e];
+    }
+    __syncthreads();
+    if (threadIdx.x < S)
+      for (int k = 0; k < cnt; ++k) tot = EP_DADD(tot, sch[k * S + threadIdx.x]);
+    __syncthreads();
+  }
+  if (threadIdx.x < S) lanes[threadIdx.x] = tot;
+  __syncthreads();
+  if (threadIdx.x == 0) cg_phase<S>(phase, lanes, cg, hist, lanes_out);
+}
+
+template <int S>
+static cudaError_t fin_gathered_s(int planes, const double* gathered, const int* plane_pos,
+                                  int phase, CgState* cg, double* hist, double* lanes_out,
+                                  cudaStream_t st) {
+  k_fin_gathered<S><<<1, 256, 0, st>>>(planes, gathered, plane_pos, phase, cg, hist, lanes_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fin_gathered(int s, int planes, const double* gathered, const int* plane_pos,
+                                int phase, CgState* cg, double* hist, double* lanes_out,
+                                cudaStream_t st) {
+  EP_DISPATCH_S(s, fin_gathered_s, planes, gathered, plane_pos, phase, cg, hist, lanes_out, st);
+}
+
 // Serial finalize: the reference's own order (kernels.hpp:66-67), one chain
 // per sample: acc = 0; acc += u[row]*v[row] for row = 0, 1, ...  The chain is
 // latency-bound (one dependent DADD per row, ~8 cycles on B200), so the design
@@ -660,7 +740,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
     const TileMap tm, const int* __restrict__ row_map, const int* __restrict__ col_entry,
     const double* __restrict__ values, const double* __restrict__ r,
     const double* __restrict__ p_old, double* __restrict__ p_new, double* __restrict__ q,
-    double* __restrict__ x, const FinArgs f) {
+    double* __restrict__ x, const double* __restrict__ p_gather, const FinArgs f) {
   using Sh = TileShape<S, 1>;
   constexpr int V = Sh::V;
   const CgState* cg = f.cg;
@@ -692,7 +772,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
       }
       st_vec<V>(p_new + (size_t)row * S + lane0, pn);
     } else {
-      sum = row_product<S, V, SpmvShape<S>::U, false>(row, row_map, col_entry, values, p_new,
+      sum = row_product<S, V, SpmvShape<S>::U, false>(row, row_map, col_entry, values, p_gather,
                                                       nullptr, true, beta, lane0);
       pn = ld_vec<V>(p_new + (size_t)row * S + lane0);
     }
@@ -799,19 +879,34 @@ cudaError_t launch_cg_flush(int s, int rows, double* x, double* const* p, const 
 }
 
 template <int S>
-static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, const TileMap& tm, const int* row_map,
+static cudaError_t cg_direction_s(int rows, const double* r, const double* p_old, double* p_new,
+                                  double* x, const CgState* cg, cudaStream_t st) {
+  using Sd = TileShape<S, kDirPasses>;
+  if (rows <= 0) return cudaSuccess;
+  k_cg_direction<S><<<(rows + Sd::ROWS - 1) / Sd::ROWS, 256, 0, st>>>(rows, r, p_old, p_new, x, cg);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_direction(int s, int rows, const double* r, const double* p_old,
+                                double* p_new, double* x, const CgState* cg, cudaStream_t st) {
+  EP_DISPATCH_S(s, cg_direction_s, rows, r, p_old, p_new, x, cg, st);
+}
+
+template <int S>
+static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, bool run_direction, const TileMap& tm,
+                             const int* row_map,
                              const int* col_entry, const double* values, const double* r,
                              const double* p_old, double* p_new, double* q, double* x,
-                             const FinArgs& f, cudaStream_t st) {
+                             const double* p_gather, const FinArgs& f, cudaStream_t st) {
   using Sh = TileShape<S, 1>;
   const int blocks = tiles ? (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC : (tm.rows + Sh::ROWS - 1) / Sh::ROWS;
   if (blocks == 0) return cudaSuccess;
-  if (!fused_dir) {
+  if (!fused_dir && run_direction) {  // else the caller ran the direction pass (+ halo)
     using Sd = TileShape<S, kDirPasses>;
     k_cg_direction<S><<<(tm.rows + Sd::ROWS - 1) / Sd::ROWS, 256, 0, st>>>(tm.rows, r, p_old, p_new, x, f.cg);
   }
 #define EP_CG_SPMV(T, D) \
-  k_cg_spmv<S, T, D><<<blocks, 256, 0, st>>>(tm, row_map, col_entry, values, r, p_old, p_new, q, x, f)
+  k_cg_spmv<S, T, D><<<blocks, 256, 0, st>>>(tm, row_map, col_entry, values, r, p_old, p_new, q, x, p_gather, f)
   if (tiles) {
     if (fused_dir) EP_CG_SPMV(true, true);
     else EP_CG_SPMV(true, false);
@@ -823,12 +918,13 @@ static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, const TileMap& tm, cons
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, const TileMap& tm,
-                           const int* row_map, const int* col_entry, const double* values,
-                           const double* r, const double* p_old, double* p_new, double* q,
-                           double* x, const FinArgs& f, cudaStream_t st) {
-  EP_DISPATCH_S(s, cg_spmv_s, tiles, fused_dir, tm, row_map, col_entry, values, r, p_old, p_new, q,
-                x, f, st);
+cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, bool run_direction,
+                           const TileMap& tm, const int* row_map, const int* col_entry,
+                           const double* values, const double* r, const double* p_old,
+                           double* p_new, double* q, double* x, const double* p_gather,
+                           const FinArgs& f, cudaStream_t st) {
+  EP_DISPATCH_S(s, cg_spmv_s, tiles, fused_dir, run_direction, tm, row_map, col_entry, values, r,
+                p_old, p_new, q, x, p_gather, f, st);
 }
 
 // r = (-alpha)*q + 1.0*r on active lanes (pcg.hpp:95 via axpby,

@@ -21,7 +21,9 @@ struct AsmTables {
 
 struct AsmArgs {
   int n;                 // cells per axis
-  int rows;              // (n+1)^3
+  int rows;              // rows assembled by this launch ((n+1)^3 on one GPU)
+  int row_begin;         // global node id of local row 0 (a rank's slab; 0 on one GPU)
+  int u_shift;           // u is indexed by (global node - u_shift)
   int m;                 // KL terms
   double mean;           // kappa0
   const double* F;       // KL axis tables [m][2n]: f_t((c + off_b) * h)
@@ -65,9 +67,20 @@ struct FinArgs {
   CgState* cg;
   double* hist;
   double* lanes_out;  // [s + 1] for kPhaseNone
+  int seg_only;       // multi-GPU: stop at the segment sums (seg_sums) — the
+                      // total over all ranks' segments is k_fin_gathered's job
 };
 
 cudaError_t launch_build_graph(int n, int* row_map, int* col_entry, cudaStream_t st);
+// rows [row_begin, row_begin + rows) of the global node graph, entries
+// renumbered from 0 and columns shifted by -col_shift (a rank's slab)
+cudaError_t launch_build_graph_range(int n, int row_begin, int rows, int col_shift, int* row_map,
+                                     int* col_entry, cudaStream_t st);
+// multi-GPU finalize: total over all planes in global order from the
+// all-gathered per-rank segment sums, gathered[plane_pos[k]][s], then `phase`
+cudaError_t launch_fin_gathered(int s, int planes, const double* gathered, const int* plane_pos,
+                                int phase, CgState* cg, double* hist, double* lanes_out,
+                                cudaStream_t st);
 cudaError_t launch_assemble(int s, const AsmArgs& a, cudaStream_t st);
 cudaError_t launch_dirichlet(int s, int n, double bc0, double bc1, const int* row_map,
                              const int* col_entry, const double* u, double* values,
@@ -88,10 +101,17 @@ cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v,
 // p_new and q; with tiles, also the canonical p_new.q and its CG phase (f)
 // fused_dir = false: a separate k_cg_direction pass writes p_new first and the
 // SpMV gathers it directly (one gather per entry instead of two)
-cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, const TileMap& tm,
-                           const int* row_map, const int* col_entry, const double* values,
-                           const double* r, const double* p_old, double* p_new, double* q,
-                           double* x, const FinArgs& f, cudaStream_t st);
+// the split direction pass alone (multi-GPU: the halo goes between it and the SpMV)
+cudaError_t launch_cg_direction(int s, int rows, const double* r, const double* p_old,
+                                double* p_new, double* x, const CgState* cg, cudaStream_t st);
+// p_gather: base of the gathered p (the rank's ghost-extended layout; == p_new on
+// one GPU). run_direction (split schedule): launch the direction pass first;
+// false when the caller already ran it (multi-GPU: with the halo in between).
+cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, bool run_direction,
+                           const TileMap& tm, const int* row_map, const int* col_entry,
+                           const double* values, const double* r, const double* p_old,
+                           double* p_new, double* q, double* x, const double* p_gather,
+                           const FinArgs& f, cudaStream_t st);
 // r -= alpha q on active lanes; with tiles, also r.r and its phase
 cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* r, const double* q,
                              const FinArgs& f, cudaStream_t st);
