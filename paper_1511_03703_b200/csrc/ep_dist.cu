@@ -23,6 +23,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -180,6 +182,22 @@ int setup_rank(enprop_dist* D, DistRank& d, int r) {
   EP_CUDA(launch_build_graph_range(n, d.row_begin, d.rows, d.ext_begin, d.row_map, d.col_entry,
                                    D->ctx->stream));
   D->ctx->launches += 1;
+  if (getenv("EP_DIST_CHECK")) {  // debug: validate the graph slice on the host
+    EP_CUDA(cudaStreamSynchronize(D->ctx->stream));
+    std::vector<int> rm(d.rows + 1), ce(d.nnz);
+    EP_CUDA(cudaMemcpy(rm.data(), d.row_map, rm.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    EP_CUDA(cudaMemcpy(ce.data(), d.col_entry, ce.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    const int ext_rows = d.lo_rows + d.rows + d.hi_rows;
+    int bad = 0;
+    for (int i = 0; i < d.rows; ++i)
+      if (rm[i + 1] < rm[i]) ++bad;
+    if (rm[0] != 0 || rm[d.rows] != d.nnz) ++bad;
+    for (int64_t k = 0; k < d.nnz; ++k)
+      if (ce[k] < 0 || ce[k] >= ext_rows) ++bad;
+    fprintf(stderr, "rank %d: planes [%d,%d) row_begin %d rows %d lo %d hi %d ext_begin %d nnz %lld rm_end %d bad %d\n",
+            d.rank, d.k0, d.k1, d.row_begin, d.rows, d.lo_rows, d.hi_rows, d.ext_begin,
+            (long long)d.nnz, rm[d.rows], bad);
+  }
   return ENPROP_OK;
 }
 
