@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const int lrow = gt / S;  // local row
   const int row = a.row_begin + lrow;  // global node id
-  const int e = gt - row * S;
+  const int e = gt - lrow * S;
   if (lrow >= a.rows) return;
   const int n = a.n, N = n + 1, n2 = 2 * n;
   const int i = row % N, j = (row / N) % N, k = row / (N * N);
