@@ -302,6 +302,80 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
 
 
+def run_dd(args):
+    """cfg 4: ONE ensemble (s=32) on an n^3 mesh (default 256^3) domain-decomposed
+    into z-slabs over the N ranks (NCCL halo of p + all-gathered per-plane dot
+    sums); a step = assemble + Dirichlet + uncoupled CG to 1e-6.
+    Strong scaling: the work per step is fixed as N grows."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1511_03703_b200 as ep
+    from oracles import Oracle, pack_group
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("gloo")  # host plumbing only: broadcast the NCCL id, barrier, max
+        obj = [ep.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    n = args.dd_mesh
+    ctx = ep.Context(local)
+    kl = ep.KlField(M_TERMS, 1.0, SIGMA, 1.0)
+    d = ep.Dist(ctx, n, S, world, rank, nccl_id, kl=kl)
+    O = Oracle()
+    pool = O.draw_samples(0, S * (args.warmup + args.steps), M_TERMS)
+    ys = [torch.as_tensor(pack_group(pool, S, g)).cuda() for g in range(args.warmup + args.steps)]
+    cfg = ep.SolverConfig(tol=TOL, max_iterations=20000, flavour=ep.CG_UNCOUPLED, dot_mode=ep.DOT_CANONICAL)
+    for g in range(args.warmup):
+        d.assemble(ys[g])
+        d.solve(cfg)
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    e0.record(st)
+    iters = []
+    for k in range(args.steps):
+        d.assemble(ys[args.warmup + k])
+        it, status = d.solve(cfg)
+        iters.append(max(it))
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    launches = ctx.launches - launches0
+    if world > 1:
+        t = [None] * world
+        dist.all_gather_object(t, ms)
+        ms = max(t)
+        dist.barrier()
+    if rank == 0:
+        samples = args.steps * S
+        print(json.dumps({
+            "metric": "sample solves/sec (assembly+CG) at ensemble s=32", "value": round(samples / (ms / 1e3), 3),
+            "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"cfg4: {n}^3 mesh domain-decomposed into z-slabs over {world} GPU(s); "
+                                   "NCCL halo of p + all-gathered per-plane dot sums; s=32, KL m=3 "
+                                   "sigma=0.1, uncoupled CG tol 1e-6, canonical dot order",
+                       "mesh": n, "ensemble_size": S, "cg_iterations_max": iters,
+                       "parallelism": f"domain decomposition x {world}"},
+            "gpu_launches": int(launches), "clocks": clk}), flush=True)
+    d.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def bench_serial(torch, ep, workers, ys, args, cfg):
     """Throughput in the reference's own (serial) dot order, which reproduces
     pcg_solve bit for bit; its chains are latency-bound, so more sample groups
@@ -464,6 +538,9 @@ def main():
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-serial", action="store_true")
     ap.add_argument("--serial-groups", type=int, default=8)
+    ap.add_argument("--workload", choices=["groups", "dd"], default="groups",
+                    help="groups: cfg 2 sample groups (default); dd: cfg 4 domain decomposition")
+    ap.add_argument("--dd-mesh", type=int, default=256)
     ap.add_argument("--groups", type=int, default=3,
                     help="sample groups solved concurrently per step (one stream each)")
     ap.add_argument("--profile-only", action="store_true",
@@ -471,6 +548,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "dd":
+        run_dd(args)
     else:
         run_ours(args)
 
