@@ -1,0 +1,197 @@
+"""CPU, world_size 2 and 3 (torch.distributed gloo): the multi-rank protocol of
+the slab-decomposed solve (paper_1511_03703_b200/csrc/ep_dist.cu)
+restated in numpy and checked against the single-process C oracle.
+
+Each rank owns the z-planes partition.cpp:31-72 gives it, holds its rows of the
+assembled CRS with columns renumbered into the ghost-extended layout
+[lo ghost plane | owned planes | hi ghost plane], exchanges one ghost plane with
+each neighbour per SpMV (send/recv), and all-gathers its per-plane canonical
+dot sums; totals are summed in global plane order.  The result must equal the
+one-process canonical CG of the C oracle bit for bit (solution and iteration
+counts), for coupled and uncoupled CG.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+TILE = 16
+
+
+def plane_range(N, P, r):
+    base, extra = N // P, N % P
+    k0 = r * base + min(r, extra)
+    return k0, k0 + base + (1 if r < extra else 0)
+
+
+def tile_sum(prod):
+    t = np.zeros((TILE, prod.shape[1]))
+    t[:prod.shape[0]] = prod
+    h = TILE // 2
+    while h >= 1:
+        t[:h] = t[:h] + t[h:2 * h]
+        h //= 2
+    return t[0]
+
+
+def plane_sums(u, v, plane, s):
+    """Canonical per-segment (plane) sums of the owned rows: tiles of 16 rows,
+    stride-halving tree, then 0.0 + tile_0 + tile_1 + ... per plane."""
+    nplanes = u.shape[0] // plane
+    out = np.zeros((nplanes, s))
+    for k in range(nplanes):
+        seg = np.zeros(s)
+        for t0 in range(0, plane, TILE):
+            r0, r1 = k * plane + t0, k * plane + min(t0 + TILE, plane)
+            seg = seg + tile_sum(u[r0:r1] * v[r0:r1])
+        out[k] = seg
+    return out
+
+
+def spmv(rm, ce, vals, xe, s):
+    z = np.zeros((len(rm) - 1, s))
+    for row in range(len(rm) - 1):
+        acc = np.zeros(s)
+        for k in range(rm[row], rm[row + 1]):
+            acc = acc + vals[k] * xe[ce[k]]
+        z[row] = acc
+    return z
+
+
+def worker(rank, world, port, n, s, flavour, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from oracles import Oracle, pack_group
+    O = Oracle()
+    N, plane = n + 1, (n + 1) ** 2
+    y = pack_group(O.draw_samples(0, s, 3), s)
+    vals_g, res_g = O.assemble(s, n, O.kl(3, 1.0, 0.1, 1.0), y, dirichlet=True)
+    rm_g, ce_g = O.graph(n)
+    k0, k1 = plane_range(N, world, rank)
+    rb, re_ = k0 * plane, k1 * plane
+    lo = plane if k0 > 0 else 0
+    hi = plane if k1 < N else 0
+    ext_begin = rb - lo
+    rm = (rm_g[rb:re_ + 1] - rm_g[rb]).astype(np.int64)
+    ce = (ce_g[rm_g[rb]:rm_g[re_]] - ext_begin).astype(np.int64)
+    vals = vals_g[rm_g[rb]:rm_g[re_]]
+    rows = re_ - rb
+    maxplanes = (N + world - 1) // world
+    b = -res_g[rb:re_]
+
+    def total(u, v):
+        ps = np.zeros((maxplanes, s))
+        ps[:k1 - k0] = plane_sums(u, v, plane, s)
+        bufs = [torch.zeros((maxplanes, s), dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(bufs, torch.from_numpy(ps))
+        acc = np.zeros(s)
+        for q in range(world):
+            a, c = plane_range(N, world, q)
+            for k in range(c - a):
+                acc = acc + bufs[q].numpy()[k]
+        return acc
+
+    def halo(p_own):
+        pe = np.zeros((lo + rows + hi, s))
+        pe[lo:lo + rows] = p_own
+        reqs = []
+        lo_buf = torch.zeros((plane, s), dtype=torch.float64)
+        hi_buf = torch.zeros((plane, s), dtype=torch.float64)
+        if rank > 0:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(p_own[:plane])), rank - 1))
+            reqs.append(dist.irecv(lo_buf, rank - 1))
+        if rank + 1 < world:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(p_own[rows - plane:])), rank + 1))
+            reqs.append(dist.irecv(hi_buf, rank + 1))
+        for r_ in reqs:
+            r_.wait()
+        if lo:
+            pe[:plane] = lo_buf.numpy()
+        if hi:
+            pe[lo + rows:] = hi_buf.numpy()
+        return pe
+
+    # CG (pcg.hpp:52-103), canonical totals; coupled: one decision for all lanes
+    coupled = flavour == 0
+    red = (lambda d: np.full(s, sum_left(d))) if coupled else (lambda d: d)
+
+    def sum_left(d):
+        acc = 0.0
+        for e in range(s):
+            acc = acc + d[e]
+        return acc
+
+    tol, maxit = 1e-8, 500
+    x = np.zeros((rows, s))
+    r = b.copy()
+    dd = red(total(b, b))
+    bnorm = np.sqrt(dd)
+    rz = dd.copy()
+    active = (np.sqrt(dd) / bnorm >= tol)
+    iters = np.zeros(s, int)
+    p = r.copy()
+    it = 0
+    while active.any() and it < maxit:
+        q = spmv(rm, ce, vals, halo(p), s)
+        pq = red(total(p, q))
+        alpha = rz / pq
+        a = np.where(active, alpha, 0.0)
+        x = np.where(active, a * p + x, x)
+        r = np.where(active, (-a) * q + r, r)
+        rr = red(total(r, r))
+        beta = rr / rz
+        rz = np.where(active, rr, rz)
+        it += 1
+        rel = np.sqrt(rr) / bnorm
+        done_now = active & (rel < tol)
+        iters[done_now] = it
+        active = active & ~done_now
+        p = np.where(active, r + beta * p, p)
+    xs = [None] * world
+    dist.all_gather_object(xs, (rb, x))
+    if rank == 0:
+        xg = np.concatenate([v for _, v in sorted(xs, key=lambda t: t[0])])
+        out.put((xg, iters.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("flavour", [0, 1])
+def test_slab_protocol_equals_single_process_canonical_cg(world, flavour):
+    from oracles import DOT_CANONICAL, Oracle, bits, pack_group
+    n, s = 4, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, n, s, flavour, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    xg, iters = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    O = Oracle()
+    y = pack_group(O.draw_samples(0, s, 3), s)
+    vals, res = O.assemble(s, n, O.kl(3, 1.0, 0.1, 1.0), y, dirichlet=True)
+    rm, ce = O.graph(n)
+    ref = O.pcg(s, rm, ce, vals, -res, 1e-8, 500, flavour=flavour, mode=DOT_CANONICAL, tile=TILE,
+                seg=(n + 1) ** 2)
+    assert (bits(xg) == bits(ref["x"])).all()
+    if flavour == 1:
+        assert iters == list(ref["iterations"])
+    else:
+        assert iters[0] == ref["iterations"][0]
