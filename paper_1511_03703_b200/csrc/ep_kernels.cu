@@ -672,13 +672,25 @@ __global__ void __launch_bounds__(32 * SerialShape<S>::LG) k_fin_serial(
   for (int c = 0; c < nchunks; ++c) {
     if (c + 1 < nchunks) load(c + 1);  // in flight during the chain
     const int base = c * Sh::CHUNK;
-    for (int j = 0; j < 32; ++j) {
-      if (lane == j) {
+    if (base + Sh::CHUNK <= rows) {
+      // full chunk: every lane runs the same unpredicated chain on its own
+      // registers in lockstep (no divergence); the shuffle keeps lane j's
+      // result, which is the running sum through row base + (j+1)K - 1
+      for (int j = 0; j < 32; ++j) {
+        double t = acc;
+#pragma unroll
+        for (int k = 0; k < K; ++k) t = EP_DADD(t, cur[k]);
+        acc = __shfl_sync(0xffffffffu, t, j);
+      }
+    } else {
+      for (int j = 0; j < 32; ++j) {
+        double t = acc;
+        const int nv = rows - (base + j * K);  // rows of lane j in this chunk
 #pragma unroll
         for (int k = 0; k < K; ++k)
-          if (base + j * K + k < rows) acc = EP_DADD(acc, cur[k]);
+          if (k < nv) t = EP_DADD(t, cur[k]);
+        acc = __shfl_sync(0xffffffffu, t, j);
       }
-      acc = __shfl_sync(0xffffffffu, acc, j);
     }
     if (c + 1 < nchunks) {
 #pragma unroll
