@@ -67,9 +67,13 @@ int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
  *   ENPROP_OPT_FUSED_DIRECTION (default 0): 1 = form p = r + beta p inside the CG
  *   SpMV from gathers of r and p_old; 0 = separate direction pass, then an
  *   SpMV with a single gather.
+ *   ENPROP_OPT_SYMMETRIC_STORAGE (default 1): problems created afterwards store
+ *   only the diagonal + upper triangle of the (exactly symmetric) assembled
+ *   operator and read each lower entry from its transposed slot
+ *   (enprop_problem_expand_values rebuilds the full [nnz][s] values).
  *   ENPROP_OPT_SPMV_PIPELINE (default 0): 1 = enprop_spmv loads the next batch's
  *   column indices one batch ahead (software pipelining). */
-enum { ENPROP_OPT_FUSED_DIRECTION = 1, ENPROP_OPT_SPMV_PIPELINE = 2 };
+enum { ENPROP_OPT_FUSED_DIRECTION = 1, ENPROP_OPT_SPMV_PIPELINE = 2, ENPROP_OPT_SYMMETRIC_STORAGE = 3 };
 int enprop_ctx_set_option(enprop_ctx* ctx, int option, int value);
 /* Event timing of the CG SpMV kernel launches on the context stream (used by
  * bench.py for the roofline). Returns the totals accumulated since the last
@@ -191,6 +195,12 @@ int enprop_problem_destroy(enprop_problem* p);
 int enprop_problem_views(enprop_problem* p, int* num_rows, int64_t* nnz, const int** row_map,
                          const int** col_entry, double** values, double** residual,
                          double** solution);
+/* stored value entries (nnz, or (nnz + rows)/2 with symmetric storage) and the
+ * entry -> slot map (NULL for full storage); `values` of enprop_problem_views is
+ * the stored array */
+int enprop_problem_storage(enprop_problem* p, int64_t* nnz_stored, const int** vpos);
+/* full [nnz][s] values of the assembled operator into a device buffer */
+int enprop_problem_expand_values(enprop_problem* p, double* values_full);
 /* assemble + Dirichlet from device samples y [num_terms][s] (u = 0) */
 int enprop_problem_assemble(enprop_problem* p, const double* y);
 /* CG on the assembled system with rhs = -residual; solution in the problem */

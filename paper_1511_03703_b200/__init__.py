@@ -32,6 +32,7 @@ CG_COUPLED, CG_UNCOUPLED = 0, 1
 TILE_ROWS = 16
 OPT_FUSED_DIRECTION = 1
 OPT_SPMV_PIPELINE = 2
+OPT_SYMMETRIC_STORAGE = 3
 WIDTHS = (1, 2, 4, 8, 16, 32)
 
 _dp = C.POINTER(C.c_double)
@@ -167,6 +168,8 @@ def lib() -> C.CDLL:
                                        C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
                                        C.POINTER(_vp)]
     L.enprop_problem_assemble.argtypes = [_vp, _vp]
+    L.enprop_problem_storage.argtypes = [_vp, C.POINTER(C.c_int64), C.POINTER(_vp)]
+    L.enprop_problem_expand_values.argtypes = [_vp, _vp]
     L.enprop_problem_solve.argtypes = [_vp, C.POINTER(_CgOptions), _ip, _ip, _dp, _ip]
     L.enprop_problem_solve_host.argtypes = [_vp, _vp, _vp, C.POINTER(_CgOptions), _ip, _ip]
     L.enprop_nccl_unique_id.argtypes = [_vp, C.c_size_t]
@@ -469,7 +472,17 @@ class Problem:
 
     @property
     def values(self):
-        return self._view("values", self.nnz * self.s, torch.float64, (self.nnz, self.s))
+        """Full [nnz][s] values of the assembled operator (a copy when the
+        problem uses symmetric storage)."""
+        out = torch.empty((self.nnz, self.s), dtype=torch.float64, device=torch.device("cuda", self.ctx.device))
+        _check(lib().enprop_problem_expand_values(self.h, _ptr(out)), "expand_values")
+        return out
+
+    @property
+    def nnz_stored(self) -> int:
+        n = C.c_int64()
+        _check(lib().enprop_problem_storage(self.h, C.byref(n), None))
+        return n.value
 
     @property
     def residual(self):

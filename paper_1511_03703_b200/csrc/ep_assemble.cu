@@ -164,7 +164,11 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
     const int ox = t % 3 - 1, oy = (t / 3) % 3 - 1, oz = t / 9 - 1;
     const int ii = i + ox, jj = j + oy, kk = k + oz;
     if (ii < 0 || ii >= N || jj < 0 || jj >= N || kk < 0 || kk >= N) continue;
-    a.values[(size_t)(rs + pos) * S + e] = acc[t];
+    if (a.vpos == nullptr) {
+      a.values[(size_t)(rs + pos) * S + e] = acc[t];
+    } else if (t >= 13) {  // stencil slots are in column order; slot 13 is the diagonal
+      a.values[(size_t)a.vpos[rs + pos] * S + e] = acc[t];
+    }
     ++pos;
   }
   a.residual[(size_t)lrow * S + e] = res;

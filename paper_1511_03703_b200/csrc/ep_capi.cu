@@ -148,13 +148,15 @@ int prof_collect(enprop_ctx* c) {
 // never idles on the check. Kernels of iterations past convergence early-exit.
 int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_entry,
            const double* values, const double* b, double* x, const enprop_cg_options* opt,
-           CgWork& w, int* iterations, int* lane_status, double* history, int* hist_len) {
+           CgWork& w, int* iterations, int* lane_status, double* history, int* hist_len,
+           const int* vpos = nullptr) {
   const int seg = opt->seg_rows > 0 ? opt->seg_rows : 4096;
   const TileMap tm = make_tile_map(rows, seg);
   int rc = ensure_work(w, rows, s, opt->max_iterations, tm);
   if (rc) return rc;
   const bool canon = opt->dot_mode == ENPROP_DOT_CANONICAL;
   const int lanes = opt->flavour == ENPROP_CG_UNCOUPLED ? s : 1;
+  const bool fused = ctx->fused_direction != 0 && vpos == nullptr;  // symmetric storage: split only
   cudaStream_t st = ctx->stream;
 
   CgState init;
@@ -192,9 +194,8 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
         double* p_new = w.p[(launched + 1) & 1];
         cudaEvent_t* ev = ctx->profile ? prof_slot(ctx) : nullptr;
         if (ev) EP_CUDA(cudaEventRecord(ev[0], st));
-        EP_CUDA(launch_cg_spmv(s, canon, ctx->fused_direction != 0, ctx->fused_direction == 0, tm,
-                               row_map, col_entry, values, w.r, p_old, p_new, w.q, x, p_new, f_pq,
-                               st));
+        EP_CUDA(launch_cg_spmv(s, canon, fused, !fused, tm, row_map, col_entry, values, w.r, p_old,
+                               p_new, w.q, x, p_new, vpos, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[1], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[2], st));
@@ -202,7 +203,7 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
         if (ev) EP_CUDA(cudaEventRecord(ev[3], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, f_rr, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[4], st));
-        ctx->launches += (canon ? 2 : 4) + (ctx->fused_direction ? 0 : 1);
+        ctx->launches += (canon ? 2 : 4) + (fused ? 0 : 1);
       }
     }
     // flag of this chunk
@@ -328,6 +329,9 @@ int enprop_ctx_set_option(enprop_ctx* c, int option, int value) {
       return ENPROP_OK;
     case ENPROP_OPT_SPMV_PIPELINE:
       c->spmv_pipeline = value ? 1 : 0;
+      return ENPROP_OK;
+    case ENPROP_OPT_SYMMETRIC_STORAGE:
+      c->symmetric_storage = value ? 1 : 0;
       return ENPROP_OK;
     default:
       return fail(ENPROP_ERR_INVALID, "enprop_ctx_set_option: unknown option");
@@ -607,6 +611,8 @@ struct enprop_problem {
   double* rhs = nullptr;
   double* x = nullptr;
   double* y = nullptr;
+  int* vpos = nullptr;   // symmetric storage (ENPROP_OPT_SYMMETRIC_STORAGE): slot of each entry
+  int64_t nnz_stored = 0;
   AsmSetup setup;
   CgWork work;
 };
@@ -638,7 +644,6 @@ int enprop_problem_create(enprop_ctx* c, const enprop_problem_desc* d, enprop_pr
   cudaError_t err;
   if ((err = cudaMalloc(&p->row_map, (p->rows + 1) * sizeof(int))) != cudaSuccess ||
       (err = cudaMalloc(&p->col_entry, p->nnz * sizeof(int))) != cudaSuccess ||
-      (err = cudaMalloc(&p->values, (size_t)p->nnz * s * sizeof(double))) != cudaSuccess ||
       (err = cudaMalloc(&p->residual, vec)) != cudaSuccess ||
       (err = cudaMalloc(&p->rhs, vec)) != cudaSuccess ||
       (err = cudaMalloc(&p->x, vec)) != cudaSuccess ||
@@ -647,6 +652,15 @@ int enprop_problem_create(enprop_ctx* c, const enprop_problem_desc* d, enprop_pr
   if ((err = launch_build_graph(n, p->row_map, p->col_entry, c->stream)) != cudaSuccess)
     return cleanup(cuda_fail(err, "enprop_problem_create: graph"));
   c->launches += 1;
+  p->nnz_stored = p->nnz;
+  if (c->symmetric_storage) {  // the assembled operator is exactly symmetric
+    if ((err = cudaMalloc(&p->vpos, p->nnz * sizeof(int))) != cudaSuccess ||
+        (err = build_sym(p->rows, p->row_map, p->col_entry, p->vpos, &p->nnz_stored, c->stream)) != cudaSuccess)
+      return cleanup(cuda_fail(err, "enprop_problem_create: symmetric storage"));
+    c->launches += 2;
+  }
+  if ((err = cudaMalloc(&p->values, (size_t)p->nnz_stored * s * sizeof(double))) != cudaSuccess)
+    return cleanup(cuda_fail(err, "enprop_problem_create"));
   if ((err = cudaStreamSynchronize(c->stream)) != cudaSuccess)
     return cleanup(cuda_fail(err, "enprop_problem_create"));
   *out = p;
@@ -656,7 +670,7 @@ int enprop_problem_create(enprop_ctx* c, const enprop_problem_desc* d, enprop_pr
 int enprop_problem_destroy(enprop_problem* p) {
   if (!p) return ENPROP_OK;
   for (void* q : {(void*)p->row_map, (void*)p->col_entry, (void*)p->values, (void*)p->residual,
-                  (void*)p->rhs, (void*)p->x, (void*)p->y})
+                  (void*)p->rhs, (void*)p->x, (void*)p->y, (void*)p->vpos})
     if (q) cudaFree(q);
   free_asm_setup(p->setup);
   free_work(p->work);
@@ -678,6 +692,26 @@ int enprop_problem_views(enprop_problem* p, int* rows, int64_t* nnz, const int**
   return ENPROP_OK;
 }
 
+int enprop_problem_storage(enprop_problem* p, int64_t* nnz_stored, const int** vpos) {
+  if (!p) return fail(ENPROP_ERR_INVALID, "null problem");
+  if (nnz_stored) *nnz_stored = p->nnz_stored;
+  if (vpos) *vpos = p->vpos;
+  return ENPROP_OK;
+}
+
+int enprop_problem_expand_values(enprop_problem* p, double* values_full) {
+  if (!p || !values_full) return fail(ENPROP_ERR_INVALID, "enprop_problem_expand_values: null argument");
+  const int s = p->desc.ensemble_size;
+  if (!p->vpos) {
+    EP_CUDA(cudaMemcpyAsync(values_full, p->values, (size_t)p->nnz * s * sizeof(double),
+                            cudaMemcpyDeviceToDevice, p->ctx->stream));
+  } else {
+    EP_CUDA(launch_sym_expand(s, p->nnz, p->vpos, p->values, values_full, p->ctx->stream));
+    p->ctx->launches += 1;
+  }
+  return ENPROP_OK;
+}
+
 int enprop_problem_assemble(enprop_problem* p, const double* y) {
   if (!p || !y) return fail(ENPROP_ERR_INVALID, "enprop_problem_assemble: null argument");
   AsmArgs a = p->setup.args;
@@ -686,6 +720,7 @@ int enprop_problem_assemble(enprop_problem* p, const double* y) {
   a.row_map = p->row_map;
   a.values = p->values;
   a.residual = p->residual;
+  a.vpos = p->vpos;
   a.dirichlet = 1;
   a.bc0 = p->desc.bc.x0_value;
   a.bc1 = p->desc.bc.x1_value;
@@ -706,7 +741,7 @@ int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* i
   EP_CUDA(launch_negate(len, p->residual, p->rhs, p->ctx->stream));
   p->ctx->launches += 1;
   return run_cg(p->ctx, s, p->rows, p->row_map, p->col_entry, p->values, p->rhs, p->x, &o, p->work,
-                iterations, lane_status, history, hist_len);
+                iterations, lane_status, history, hist_len, p->vpos);
 }
 
 int enprop_problem_solve_host(enprop_problem* p, const double* y_host, double* x_host,

@@ -365,6 +365,7 @@ int enprop_dist_assemble(enprop_dist* D, const double* y) {
     a.row_map = d.row_map;
     a.values = d.values;
     a.residual = d.residual;
+    a.vpos = nullptr;  // slabs keep the full CRS (lower entries of boundary rows live on the neighbour)
     a.dirichlet = 1;
     a.bc0 = D->desc.bc.x0_value;
     a.bc1 = D->desc.bc.x1_value;
@@ -427,7 +428,7 @@ int enprop_dist_solve(enprop_dist* D, const enprop_cg_options* opt, int* iterati
       for (auto& d : D->ranks) {
         EP_CUDA(launch_cg_spmv(s, true, false, false, d.tm, d.row_map, d.col_entry, d.values, d.r,
                                d.p[po] + (size_t)d.lo_rows * s, d.p[pn] + (size_t)d.lo_rows * s, d.q,
-                               d.x, d.p[pn], rank_fin(d, kPhasePQ), st));
+                               d.x, d.p[pn], nullptr, rank_fin(d, kPhasePQ), st));
         ctx->launches += 1;
       }
       if ((rc = allgather(D)) || (rc = fin_all(D, kPhasePQ))) return rc;

@@ -102,13 +102,17 @@ struct SpmvShape {  // vector width per thread
   static constexpr int U = 4;  // entries per predicated batch
 };
 
-template <int S, int V, int U, bool kCg, bool kPipe = false>
+// kSym: values are the symmetric (diagonal + upper) storage and entry k's
+// value lives at vpos[k] (its own slot for col >= row, the transposed slot in
+// row col's upper part otherwise); the per-row summation order is unchanged.
+template <int S, int V, int U, bool kCg, bool kPipe = false, bool kSym = false>
 __device__ __forceinline__ VecD<V> row_product(int row, const int* __restrict__ row_map,
                                                const int* __restrict__ col_entry,
                                                const double* __restrict__ values,
                                                const double* __restrict__ x_or_r,
                                                const double* __restrict__ p_old, bool first,
-                                               const VecD<V>& beta, int lane0) {
+                                               const VecD<V>& beta, int lane0,
+                                               const int* __restrict__ vpos = nullptr) {
   const int rs = __ldg(row_map + row), re = __ldg(row_map + row + 1);
   VecD<V> sum;
 #pragma unroll
@@ -129,7 +133,8 @@ __device__ __forceinline__ VecD<V> row_product(int row, const int* __restrict__ 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (kb + u < re) {
-        av[u] = ld_stream<V>(values + (size_t)(kb + u) * S + lane0);
+        const size_t vi = kSym ? (size_t)ld_stream_i32(vpos + kb + u) : (size_t)(kb + u);
+        av[u] = ld_stream<V>(values + vi * S + lane0);
         xv[u] = ld_vec<V>(x_or_r + (size_t)c[u] * S + lane0);
         if (kCg && !first) pv[u] = ld_vec<V>(p_old + (size_t)c[u] * S + lane0);
       }
@@ -747,12 +752,13 @@ __device__ __forceinline__ int cg_row(const TileMap& tm, int slot) {
 // (saves the direction pass). Otherwise p_new was written by k_cg_direction
 // and is gathered directly (one gather per entry).  Both give the reference's
 // p = 1.0*z + beta*p (pcg.hpp:101) bit for bit.
-template <int S, bool kTiles, bool kFusedDir>
+template <int S, bool kTiles, bool kFusedDir, bool kSym = false>
 __global__ void __launch_bounds__(256, 4) k_cg_spmv(
     const TileMap tm, const int* __restrict__ row_map, const int* __restrict__ col_entry,
     const double* __restrict__ values, const double* __restrict__ r,
     const double* __restrict__ p_old, double* __restrict__ p_new, double* __restrict__ q,
-    double* __restrict__ x, const double* __restrict__ p_gather, const FinArgs f) {
+    double* __restrict__ x, const double* __restrict__ p_gather, const int* __restrict__ vpos,
+    const FinArgs f) {
   using Sh = TileShape<S, 1>;
   constexpr int V = Sh::V;
   const CgState* cg = f.cg;
@@ -784,8 +790,8 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
       }
       st_vec<V>(p_new + (size_t)row * S + lane0, pn);
     } else {
-      sum = row_product<S, V, SpmvShape<S>::U, false>(row, row_map, col_entry, values, p_gather,
-                                                      nullptr, true, beta, lane0);
+      sum = row_product<S, V, SpmvShape<S>::U, false, false, kSym>(
+          row, row_map, col_entry, values, p_gather, nullptr, true, beta, lane0, vpos);
       pn = ld_vec<V>(p_new + (size_t)row * S + lane0);
     }
     st_vec<V>(q + (size_t)row * S + lane0, sum);
@@ -909,7 +915,8 @@ static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, bool run_direction, con
                              const int* row_map,
                              const int* col_entry, const double* values, const double* r,
                              const double* p_old, double* p_new, double* q, double* x,
-                             const double* p_gather, const FinArgs& f, cudaStream_t st) {
+                             const double* p_gather, const int* vpos, const FinArgs& f,
+                             cudaStream_t st) {
   using Sh = TileShape<S, 1>;
   const int blocks = tiles ? (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC : (tm.rows + Sh::ROWS - 1) / Sh::ROWS;
   if (blocks == 0) return cudaSuccess;
@@ -917,14 +924,19 @@ static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, bool run_direction, con
     using Sd = TileShape<S, kDirPasses>;
     k_cg_direction<S><<<(tm.rows + Sd::ROWS - 1) / Sd::ROWS, 256, 0, st>>>(tm.rows, r, p_old, p_new, x, f.cg);
   }
-#define EP_CG_SPMV(T, D) \
-  k_cg_spmv<S, T, D><<<blocks, 256, 0, st>>>(tm, row_map, col_entry, values, r, p_old, p_new, q, x, p_gather, f)
-  if (tiles) {
-    if (fused_dir) EP_CG_SPMV(true, true);
-    else EP_CG_SPMV(true, false);
+#define EP_CG_SPMV(T, D, Y)                                                                   \
+  k_cg_spmv<S, T, D, Y><<<blocks, 256, 0, st>>>(tm, row_map, col_entry, values, r, p_old, p_new, q, \
+                                                x, p_gather, vpos, f)
+  if (vpos) {  // symmetric storage: split direction schedule only
+    if (fused_dir) return cudaErrorInvalidValue;
+    if (tiles) EP_CG_SPMV(true, false, true);
+    else EP_CG_SPMV(false, false, true);
+  } else if (tiles) {
+    if (fused_dir) EP_CG_SPMV(true, true, false);
+    else EP_CG_SPMV(true, false, false);
   } else {
-    if (fused_dir) EP_CG_SPMV(false, true);
-    else EP_CG_SPMV(false, false);
+    if (fused_dir) EP_CG_SPMV(false, true, false);
+    else EP_CG_SPMV(false, false, false);
   }
 #undef EP_CG_SPMV
   return cudaGetLastError();
@@ -934,9 +946,9 @@ cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, bool run_direction
                            const TileMap& tm, const int* row_map, const int* col_entry,
                            const double* values, const double* r, const double* p_old,
                            double* p_new, double* q, double* x, const double* p_gather,
-                           const FinArgs& f, cudaStream_t st) {
+                           const int* vpos, const FinArgs& f, cudaStream_t st) {
   EP_DISPATCH_S(s, cg_spmv_s, tiles, fused_dir, run_direction, tm, row_map, col_entry, values, r,
-                p_old, p_new, q, x, p_gather, f, st);
+                p_old, p_new, q, x, p_gather, vpos, f, st);
 }
 
 // r = (-alpha)*q + 1.0*r on active lanes (pcg.hpp:95 via axpby,
@@ -1008,6 +1020,121 @@ static cudaError_t cg_update_s(bool tiles, const TileMap& tm, double* r, const d
 cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* r, const double* q,
                              const FinArgs& f, cudaStream_t st) {
   EP_DISPATCH_S(s, cg_update_s, tiles, tm, r, q, f, st);
+}
+
+// =============================================================================
+// Symmetric storage. The assembled matrix is exactly symmetric
+// (G_qij == G_qji bitwise; Dirichlet keeps symmetry), so the device-resident
+// pipeline stores row r's entries with col >= r only ("upper", diagonal
+// included, in column order): nnz_up = (nnz + rows)/2 for a structurally
+// symmetric graph. vpos[k] maps every entry of the full CRS to its slot.
+// =============================================================================
+__global__ void k_sym_count(int rows, const int* __restrict__ row_map,
+                            const int* __restrict__ col_entry, int* __restrict__ cnt) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  int c = 0;
+  for (int k = row_map[r]; k < row_map[r + 1]; ++k) c += col_entry[k] >= r;
+  cnt[r] = c;
+}
+
+// first k in [lo, hi) with col_entry[k] >= v
+__device__ __forceinline__ int lower_bound_i(const int* a, int lo, int hi, int v) {
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void k_sym_vpos(int rows, const int* __restrict__ row_map,
+                           const int* __restrict__ col_entry, const int* __restrict__ up_start,
+                           int* __restrict__ vpos, int* __restrict__ bad) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int rs = row_map[r], re = row_map[r + 1];
+  const int first_up = lower_bound_i(col_entry, rs, re, r);
+  for (int k = rs; k < re; ++k) {
+    const int c = col_entry[k];
+    if (c >= r) {
+      vpos[k] = up_start[r] + (k - first_up);
+    } else {  // transposed entry (c, r) in row c's upper part
+      const int cs = row_map[c], ce = row_map[c + 1];
+      const int fu = lower_bound_i(col_entry, cs, ce, c);
+      const int t = lower_bound_i(col_entry, fu, ce, r);
+      if (t >= ce || col_entry[t] != r) {
+        atomicAdd(bad, 1);  // pattern not symmetric
+        vpos[k] = 0;
+      } else {
+        vpos[k] = up_start[c] + (t - fu);
+      }
+    }
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) k_sym_expand(int64_t nnz, const int* __restrict__ vpos,
+                                                    const double* __restrict__ up,
+                                                    double* __restrict__ full) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= nnz * S) return;
+  const int64_t k = g / S;
+  full[g] = up[(int64_t)vpos[k] * S + (g - k * S)];
+}
+
+template <int S>
+static cudaError_t sym_expand_s(int64_t nnz, const int* vpos, const double* up, double* full,
+                                cudaStream_t st) {
+  const int64_t t = nnz * S;
+  if (t == 0) return cudaSuccess;
+  k_sym_expand<S><<<(int)((t + 255) / 256), 256, 0, st>>>(nnz, vpos, up, full);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sym_expand(int s, int64_t nnz, const int* vpos, const double* up, double* full,
+                              cudaStream_t st) {
+  EP_DISPATCH_S(s, sym_expand_s, nnz, vpos, up, full, st);
+}
+
+}  // namespace ep
+
+#include <cub/device/device_scan.cuh>
+
+namespace ep {
+
+cudaError_t build_sym(int rows, const int* row_map, const int* col_entry, int* vpos,
+                      int64_t* nnz_up, cudaStream_t st) {
+  int *cnt = nullptr, *start = nullptr, *bad = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cudaError_t err = cudaMalloc(&cnt, (size_t)(rows + 1) * sizeof(int));
+  if (err == cudaSuccess) err = cudaMalloc(&start, (size_t)(rows + 1) * sizeof(int));
+  if (err == cudaSuccess) err = cudaMalloc(&bad, sizeof(int));
+  if (err == cudaSuccess) err = cudaMemsetAsync(bad, 0, sizeof(int), st);
+  if (err == cudaSuccess) err = cudaMemsetAsync(cnt + rows, 0, sizeof(int), st);
+  if (err == cudaSuccess && rows > 0) {
+    k_sym_count<<<(rows + 255) / 256, 256, 0, st>>>(rows, row_map, col_entry, cnt);
+    err = cudaGetLastError();
+  }
+  if (err == cudaSuccess) err = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, start, rows + 1, st);
+  if (err == cudaSuccess) err = cudaMalloc(&tmp, tmp_bytes ? tmp_bytes : 8);
+  if (err == cudaSuccess) err = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, start, rows + 1, st);
+  if (err == cudaSuccess && rows > 0) {
+    k_sym_vpos<<<(rows + 255) / 256, 256, 0, st>>>(rows, row_map, col_entry, start, vpos, bad);
+    err = cudaGetLastError();
+  }
+  int h_total = 0, h_bad = 0;
+  if (err == cudaSuccess) err = cudaMemcpyAsync(&h_total, start + rows, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (err == cudaSuccess) err = cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+  cudaFree(cnt);
+  cudaFree(start);
+  cudaFree(bad);
+  cudaFree(tmp);
+  if (err == cudaSuccess && h_bad) err = cudaErrorInvalidValue;
+  *nnz_up = h_total;
+  return err;
 }
 
 }  // namespace ep

@@ -33,6 +33,7 @@ struct AsmArgs {
   const double* y;       // [m][s]
   double* values;        // [nnz][s]
   double* residual;      // [rows][s]
+  const int* vpos;       // symmetric storage: write only col >= row, at vpos[entry]
   int dirichlet;         // fuse apply_dirichlet
   int nonlinear;         // alpha != 0 || beta != 0
   double bc0, bc1;
@@ -111,10 +112,18 @@ cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, bool run_direction
                            const TileMap& tm, const int* row_map, const int* col_entry,
                            const double* values, const double* r, const double* p_old,
                            double* p_new, double* q, double* x, const double* p_gather,
-                           const FinArgs& f, cudaStream_t st);
+                           const int* vpos, const FinArgs& f, cudaStream_t st);
 // r -= alpha q on active lanes; with tiles, also r.r and its phase
 cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* r, const double* q,
                              const FinArgs& f, cudaStream_t st);
+// Symmetric (diagonal + upper) value storage: vpos[nnz] maps each full-CRS entry
+// to its stored slot; nnz_up = stored entries. Fails (InvalidValue) if the
+// pattern is not structurally symmetric.
+cudaError_t build_sym(int rows, const int* row_map, const int* col_entry, int* vpos,
+                      int64_t* nnz_up, cudaStream_t st);
+// full[k] = up[vpos[k]] (views / checks)
+cudaError_t launch_sym_expand(int s, int64_t nnz, const int* vpos, const double* up, double* full,
+                              cudaStream_t st);
 // after the loop: apply the still-deferred x += alpha*p of the last iteration
 cudaError_t launch_cg_flush(int s, int rows, double* x, double* const* p, const CgState* cg,
                             cudaStream_t st);

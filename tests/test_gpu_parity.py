@@ -439,3 +439,33 @@ def test_cg_split_direction_option_is_bitwise_neutral(ctx, R, mode, s):
     finally:
         ctx.set_option(ep.OPT_FUSED_DIRECTION, 0)
     assert a.iterations == c.iterations and same(host(a.solution), host(c.solution))
+
+
+@pytest.mark.parametrize("mode", [DOT_SERIAL, DOT_CANONICAL])
+@pytest.mark.parametrize("s", [1, 4, 32])
+def test_symmetric_storage_is_bitwise_neutral(ctx, R, mode, s):
+    """ENPROP_OPT_SYMMETRIC_STORAGE: diagonal + upper values only, lower entries
+    read from their transposed slots; same operator, same bits."""
+    n, m = 9, 3
+    y = dev(pack_group(R.draw_samples(3, s, m), s))
+    kl = ep.KlField(m, 1.0, 0.2, 1.0)
+    cfg = ep.SolverConfig(tol=1e-8, flavour=ep.CG_UNCOUPLED, dot_mode=mode)
+    ps = ep.Problem(ctx, n, s, kl)  # default: symmetric storage
+    ctx.set_option(ep.OPT_SYMMETRIC_STORAGE, 0)
+    try:
+        pf = ep.Problem(ctx, n, s, kl)
+    finally:
+        ctx.set_option(ep.OPT_SYMMETRIC_STORAGE, 1)
+    N = n + 1
+    assert ps.nnz_stored == (ps.nnz + N ** 3) // 2 and pf.nnz_stored == pf.nnz
+    for p in (ps, pf):
+        p.assemble(y)
+    assert same(host(ps.values), host(pf.values))
+    a = ps.solve(cfg)
+    b = pf.solve(cfg)
+    assert a[0] == b[0]
+    assert same(host(ps.solution), host(pf.solution))
+    rv, _ = R.assemble(s, n, m, host(y), sigma=0.2)
+    assert same(host(ps.values), rv)
+    ps.close()
+    pf.close()
