@@ -25,14 +25,18 @@ def main():
     ap.add_argument("--s", type=int, default=32)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--spmv-only", action="store_true")
+    ap.add_argument("--sym", type=int, default=1, help="symmetric storage for the CG problems")
     args = ap.parse_args()
     n, s = args.n, args.s
     ctx = ep.Context(0)
     O = Oracle()
     y = torch.as_tensor(pack_group(O.draw_samples(0, s, 3), s)).cuda()
-    p = ep.Problem(ctx, n, s, ep.KlField(3, 1.0, 0.1, 1.0))
+    ctx.set_option(ep.OPT_SYMMETRIC_STORAGE, 0)
+    pfull = ep.Problem(ctx, n, s, ep.KlField(3, 1.0, 0.1, 1.0))
+    ctx.set_option(ep.OPT_SYMMETRIC_STORAGE, args.sym)
+    p = ep.Problem(ctx, n, s, ep.KlField(3, 1.0, 0.1, 1.0)) if args.sym else pfull
     st = torch.cuda.current_stream()
-    out = {"n": n, "s": s}
+    out = {"n": n, "s": s, "sym": args.sym}
     # assembly
     p.assemble(y)
     torch.cuda.synchronize()
@@ -44,17 +48,19 @@ def main():
     torch.cuda.synchronize()
     out["assemble_ms"] = a.elapsed_time(b) / 3
     # plain spmv on the assembled matrix
+    pfull.assemble(y)
+    vals_full = pfull.values
     x = torch.rand((p.rows, s), dtype=torch.float64, device="cuda")
     z = torch.empty_like(x)
     nnz, rows = p.nnz, p.rows
     for pipe in (1, 0):
         ctx.set_option(ep.OPT_SPMV_PIPELINE, pipe)
         for _ in range(3):
-            ep.spmv(ctx, s, p.row_map, p.col_entry, p.values, x, z)
+            ep.spmv(ctx, s, p.row_map, p.col_entry, vals_full, x, z)
         torch.cuda.synchronize()
         a.record(st)
         for _ in range(10):
-            ep.spmv(ctx, s, p.row_map, p.col_entry, p.values, x, z)
+            ep.spmv(ctx, s, p.row_map, p.col_entry, vals_full, x, z)
         b.record(st)
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / 10
