@@ -83,7 +83,7 @@ int ensure_work(CgWork& w, int rows, int s, int maxit, const TileMap& tm) {
   return ENPROP_OK;
 }
 
-FinArgs fin_args(const CgWork& w, const TileMap& tm, int phase) {
+FinArgs fin_args(const CgWork& w, const TileMap& tm, int phase, int defer = 1) {
   FinArgs f;
   f.partials = w.partials;
   f.seg_sums = w.seg_sums;
@@ -94,6 +94,7 @@ FinArgs fin_args(const CgWork& w, const TileMap& tm, int phase) {
   f.hist = w.hist;
   f.lanes_out = nullptr;
   f.seg_only = 0;
+  f.defer = defer;
   return f;
 }
 
@@ -171,12 +172,15 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
     EP_CUDA(cudaMemsetAsync(x, 0, vec, st));
     EP_CUDA(cudaMemcpyAsync(w.r, b, vec, cudaMemcpyDeviceToDevice, st));
   }
-  const FinArgs f_init = fin_args(w, tm, kPhaseInit);
-  const FinArgs f_pq = fin_args(w, tm, kPhasePQ);
-  const FinArgs f_rr = fin_args(w, tm, kPhaseRR);
+  const int defer = ctx->fused_finalize ? 0 : 1;
+  const FinArgs f_init = fin_args(w, tm, kPhaseInit, defer);
+  const FinArgs f_pq = fin_args(w, tm, kPhasePQ, defer);
+  const FinArgs f_rr = fin_args(w, tm, kPhaseRR, defer);
+  const bool fin_kernel = canon && defer;
   if (canon) {
     EP_CUDA(launch_dot_tiles(s, tm, w.r, w.r, f_init, st));
-    ctx->launches += 1;
+    if (fin_kernel) EP_CUDA(launch_fin_segments(s, tm, f_init, st));
+    ctx->launches += fin_kernel ? 2 : 1;
   } else {
     EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, f_init, st));
     ctx->launches += 1;
@@ -198,12 +202,14 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
                                p_new, w.q, x, p_new, vpos, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[1], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, f_pq, st));
+        if (fin_kernel) EP_CUDA(launch_fin_segments(s, tm, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[2], st));
         EP_CUDA(launch_cg_update(s, canon, tm, w.r, w.q, f_rr, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[3], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, f_rr, st));
+        if (fin_kernel) EP_CUDA(launch_fin_segments(s, tm, f_rr, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[4], st));
-        ctx->launches += (canon ? 2 : 4) + (fused ? 0 : 1);
+        ctx->launches += (canon ? 2 : 4) + (fused ? 0 : 1) + (fin_kernel ? 2 : 0);
       }
     }
     // flag of this chunk
@@ -332,6 +338,9 @@ int enprop_ctx_set_option(enprop_ctx* c, int option, int value) {
       return ENPROP_OK;
     case ENPROP_OPT_SYMMETRIC_STORAGE:
       c->symmetric_storage = value ? 1 : 0;
+      return ENPROP_OK;
+    case ENPROP_OPT_FUSED_FINALIZE:
+      c->fused_finalize = value ? 1 : 0;
       return ENPROP_OK;
     default:
       return fail(ENPROP_ERR_INVALID, "enprop_ctx_set_option: unknown option");
@@ -543,9 +552,14 @@ int enprop_dot(enprop_ctx* c, int s, int64_t n, const double* u, const double* v
   FinArgs f = fin_args(w, tm, kPhaseNone);
   f.lanes_out = out;
   if (err == cudaSuccess) {
-    if (dot_mode == ENPROP_DOT_CANONICAL && rows > 0) err = launch_dot_tiles(s, tm, u, v, f, c->stream);
-    else err = launch_fin_serial(s, rows, u, v, f, c->stream);
-    c->launches += 1;
+    if (dot_mode == ENPROP_DOT_CANONICAL && rows > 0) {
+      err = launch_dot_tiles(s, tm, u, v, f, c->stream);
+      if (err == cudaSuccess) err = launch_fin_segments(s, tm, f, c->stream);
+      c->launches += 2;
+    } else {
+      err = launch_fin_serial(s, rows, u, v, f, c->stream);
+      c->launches += 1;
+    }
   }
   std::vector<double> h(s + 1);
   if (err == cudaSuccess)

@@ -212,6 +212,7 @@ FinArgs rank_fin(const DistRank& d, int phase) {
   f.hist = d.hist;
   f.lanes_out = nullptr;
   f.seg_only = 1;
+  f.defer = 1;
   return f;
 }
 
@@ -405,7 +406,8 @@ int enprop_dist_solve(enprop_dist* D, const enprop_cg_options* opt, int* iterati
     EP_CUDA(cudaMemsetAsync(d.x, 0, vec, st));
     EP_CUDA(launch_negate((int64_t)d.rows * s, d.residual, d.r, st));  // b = -residual; r = b
     EP_CUDA(launch_dot_tiles(s, d.tm, d.r, d.r, rank_fin(d, kPhaseInit), st));
-    ctx->launches += 2;
+    EP_CUDA(launch_fin_segments(s, d.tm, rank_fin(d, kPhaseInit), st));
+    ctx->launches += 3;
   }
   int rc = allgather(D);
   if (rc) return rc;
@@ -429,12 +431,14 @@ int enprop_dist_solve(enprop_dist* D, const enprop_cg_options* opt, int* iterati
         EP_CUDA(launch_cg_spmv(s, true, false, false, d.tm, d.row_map, d.col_entry, d.values, d.r,
                                d.p[po] + (size_t)d.lo_rows * s, d.p[pn] + (size_t)d.lo_rows * s, d.q,
                                d.x, d.p[pn], nullptr, rank_fin(d, kPhasePQ), st));
-        ctx->launches += 1;
+        EP_CUDA(launch_fin_segments(s, d.tm, rank_fin(d, kPhasePQ), st));
+        ctx->launches += 2;
       }
       if ((rc = allgather(D)) || (rc = fin_all(D, kPhasePQ))) return rc;
       for (auto& d : D->ranks) {
         EP_CUDA(launch_cg_update(s, true, d.tm, d.r, d.q, rank_fin(d, kPhaseRR), st));
-        ctx->launches += 1;
+        EP_CUDA(launch_fin_segments(s, d.tm, rank_fin(d, kPhaseRR), st));
+        ctx->launches += 2;
       }
       if ((rc = allgather(D)) || (rc = fin_all(D, kPhaseRR))) return rc;
     }

@@ -306,6 +306,7 @@ __device__ void tiles_finish(const TileMap& tm, double* sprod, const FinArgs& f)
       if (nr > 0) f.partials[(size_t)tile * S + e] = sprod[lt * kTileRows * S + e];
     }
   }
+  if (f.defer) return;  // launch_fin_segments closes the dot
   __syncthreads();
   if (threadIdx.x == 0) {
     int nl = 0;
@@ -583,6 +584,69 @@ __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hi
     }
     if (!any) cg->done = 1;
   }
+}
+
+// Deferred canonical finalize (the default): block `seg` forms the segment sum
+// 0.0 + tile_0 + tile_1 + ... per sample from the tile partials (staged through
+// shared memory in chunks so the chain only waits on DADD latency); the last
+// block (acq_rel counter) forms 0.0 + seg_0 + seg_1 + ... and runs the phase.
+// Keeping this out of the SpMV / update kernels spares every one of their
+// blocks a global atomic round trip before it can retire.
+template <int S>
+__global__ void __launch_bounds__(256) k_fin_segments(const TileMap tm, const FinArgs f) {
+  if ((f.phase == kPhasePQ || f.phase == kPhaseRR) && f.cg->done) return;
+  constexpr int kChunk = 64;
+  __shared__ double sch[kChunk * S];
+  __shared__ double lanes[S];
+  __shared__ int s_final;
+  const int seg = blockIdx.x;
+  const int nt = tm.tiles_in_seg(seg);
+  const double* p = f.partials + (size_t)seg * tm.tiles_per_seg * S;
+  double acc = 0.0;
+  for (int t0 = 0; t0 < nt; t0 += kChunk) {
+    const int cnt = min(kChunk, nt - t0);
+    for (int idx = threadIdx.x; idx < cnt * S; idx += blockDim.x) sch[idx] = __ldcg(p + (size_t)t0 * S + idx);
+    __syncthreads();
+    if (threadIdx.x < S) {
+#pragma unroll 8
+      for (int t = 0; t < cnt; ++t) acc = EP_DADD(acc, sch[t * S + threadIdx.x]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < S) f.seg_sums[(size_t)seg * S + threadIdx.x] = acc;
+  if (f.seg_only) return;
+  __syncthreads();
+  if (threadIdx.x == 0) s_final = (atomic_add_acq_rel_gpu(f.seg_done, 1) == tm.num_segs - 1);
+  __syncthreads();
+  if (!s_final) return;
+  double tot = 0.0;
+  for (int g0 = 0; g0 < tm.num_segs; g0 += kChunk) {
+    const int cnt = min(kChunk, tm.num_segs - g0);
+    for (int idx = threadIdx.x; idx < cnt * S; idx += blockDim.x) sch[idx] = __ldcg(f.seg_sums + (size_t)g0 * S + idx);
+    __syncthreads();
+    if (threadIdx.x < S) {
+#pragma unroll 8
+      for (int g = 0; g < cnt; ++g) tot = EP_DADD(tot, sch[g * S + threadIdx.x]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < S) lanes[threadIdx.x] = tot;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *f.seg_done = 0;
+    cg_phase<S>(f.phase, lanes, f.cg, f.hist, f.lanes_out);
+  }
+}
+
+template <int S>
+static cudaError_t fin_segments_s(const TileMap& tm, const FinArgs& f, cudaStream_t st) {
+  if (tm.num_segs == 0) return cudaSuccess;
+  k_fin_segments<S><<<tm.num_segs, 256, 0, st>>>(tm, f);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fin_segments(int s, const TileMap& tm, const FinArgs& f, cudaStream_t st) {
+  EP_DISPATCH_S(s, fin_segments_s, tm, f, st);
 }
 
 // Multi-GPU canonical total: lanes[e] = 0.0 + seg_0 + seg_1 + ... over the

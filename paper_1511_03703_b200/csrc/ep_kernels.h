@@ -70,6 +70,8 @@ struct FinArgs {
   double* lanes_out;  // [s + 1] for kPhaseNone
   int seg_only;       // multi-GPU: stop at the segment sums (seg_sums) — the
                       // total over all ranks' segments is k_fin_gathered's job
+  int defer;          // producing kernels only write tile partials; a separate
+                      // launch_fin_segments forms the segment sums / total / phase
 };
 
 cudaError_t launch_build_graph(int n, int* row_map, int* col_entry, cudaStream_t st);
@@ -77,6 +79,9 @@ cudaError_t launch_build_graph(int n, int* row_map, int* col_entry, cudaStream_t
 // renumbered from 0 and columns shifted by -col_shift (a rank's slab)
 cudaError_t launch_build_graph_range(int n, int row_begin, int rows, int col_shift, int* row_map,
                                      int* col_entry, cudaStream_t st);
+// deferred canonical finalize: one block per segment forms 0.0 + tile_0 + ... from
+// f.partials; unless f.seg_only, the last block forms the total and runs f.phase
+cudaError_t launch_fin_segments(int s, const TileMap& tm, const FinArgs& f, cudaStream_t st);
 // multi-GPU finalize: total over all planes in global order from the
 // all-gathered per-rank segment sums, gathered[plane_pos[k]][s], then `phase`
 cudaError_t launch_fin_gathered(int s, int planes, const double* gathered, const int* plane_pos,
