@@ -71,15 +71,12 @@ int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
  *   only the diagonal + upper triangle of the (exactly symmetric) assembled
  *   operator and read each lower entry from its transposed slot
  *   (enprop_problem_expand_values rebuilds the full [nnz][s] values).
- *   ENPROP_OPT_FUSED_FINALIZE (default 0): 1 = close canonical dots inside the
- *   producing kernels (last-block pattern) instead of a per-segment kernel.
  *   ENPROP_OPT_SPMV_PIPELINE (default 0): 1 = enprop_spmv loads the next batch's
  *   column indices one batch ahead (software pipelining). */
 enum {
   ENPROP_OPT_FUSED_DIRECTION = 1,
   ENPROP_OPT_SPMV_PIPELINE = 2,
-  ENPROP_OPT_SYMMETRIC_STORAGE = 3,
-  ENPROP_OPT_FUSED_FINALIZE = 4
+  ENPROP_OPT_SYMMETRIC_STORAGE = 3
 };
 int enprop_ctx_set_option(enprop_ctx* ctx, int option, int value);
 /* Event timing of the CG SpMV kernel launches on the context stream (used by

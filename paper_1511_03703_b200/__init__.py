@@ -33,7 +33,6 @@ TILE_ROWS = 16
 OPT_FUSED_DIRECTION = 1
 OPT_SPMV_PIPELINE = 2
 OPT_SYMMETRIC_STORAGE = 3
-OPT_FUSED_FINALIZE = 4
 WIDTHS = (1, 2, 4, 8, 16, 32)
 
 _dp = C.POINTER(C.c_double)

@@ -83,7 +83,7 @@ int ensure_work(CgWork& w, int rows, int s, int maxit, const TileMap& tm) {
   return ENPROP_OK;
 }
 
-FinArgs fin_args(const CgWork& w, const TileMap& tm, int phase, int defer = 1) {
+FinArgs fin_args(const CgWork& w, const TileMap& tm, int phase) {
   FinArgs f;
   f.partials = w.partials;
   f.seg_sums = w.seg_sums;
@@ -94,7 +94,7 @@ FinArgs fin_args(const CgWork& w, const TileMap& tm, int phase, int defer = 1) {
   f.hist = w.hist;
   f.lanes_out = nullptr;
   f.seg_only = 0;
-  f.defer = defer;
+  f.defer = 1;
   return f;
 }
 
@@ -172,11 +172,10 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
     EP_CUDA(cudaMemsetAsync(x, 0, vec, st));
     EP_CUDA(cudaMemcpyAsync(w.r, b, vec, cudaMemcpyDeviceToDevice, st));
   }
-  const int defer = ctx->fused_finalize ? 0 : 1;
-  const FinArgs f_init = fin_args(w, tm, kPhaseInit, defer);
-  const FinArgs f_pq = fin_args(w, tm, kPhasePQ, defer);
-  const FinArgs f_rr = fin_args(w, tm, kPhaseRR, defer);
-  const bool fin_kernel = canon && defer;
+  const FinArgs f_init = fin_args(w, tm, kPhaseInit);
+  const FinArgs f_pq = fin_args(w, tm, kPhasePQ);
+  const FinArgs f_rr = fin_args(w, tm, kPhaseRR);
+  const bool fin_kernel = canon;
   if (canon) {
     EP_CUDA(launch_dot_tiles(s, tm, w.r, w.r, f_init, st));
     if (fin_kernel) EP_CUDA(launch_fin_segments(s, tm, f_init, st));
@@ -339,9 +338,7 @@ int enprop_ctx_set_option(enprop_ctx* c, int option, int value) {
     case ENPROP_OPT_SYMMETRIC_STORAGE:
       c->symmetric_storage = value ? 1 : 0;
       return ENPROP_OK;
-    case ENPROP_OPT_FUSED_FINALIZE:
-      c->fused_finalize = value ? 1 : 0;
-      return ENPROP_OK;
+
     default:
       return fail(ENPROP_ERR_INVALID, "enprop_ctx_set_option: unknown option");
   }

@@ -24,7 +24,6 @@ struct enprop_ctx {
   int spmv_pipeline = 0;    // ENPROP_OPT_SPMV_PIPELINE
   int fused_direction = 0;  // ENPROP_OPT_FUSED_DIRECTION (split measured faster on B200)
   int symmetric_storage = 1;  // ENPROP_OPT_SYMMETRIC_STORAGE (problems created afterwards)
-  int fused_finalize = 0;     // ENPROP_OPT_FUSED_FINALIZE
   // optional CUDA-event timing of the CG SpMV launches (bench roofline)
   int profile = 0;
   std::vector<cudaEvent_t> prof_ev;  // 5 events per profiled iteration, reused

@@ -256,6 +256,56 @@ template <int S>
 __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hist,
                          double* lanes_out);
 
+__device__ __forceinline__ int atomic_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Sequential left-to-right sum acc + a_0 + a_1 + ... + a_{n-1} of a
+// strided array by one warp at DADD latency: lane j holds the K values
+// [jK, jK+K) of each chunk in registers, every lane runs the same chain on its
+// own registers in lockstep and a shuffle keeps lane j's running sum; the next
+// chunk's loads are in flight meanwhile. Returns the sum in every lane.
+template <int K>
+__device__ __forceinline__ double warp_chain_sum(double acc, const double* __restrict__ a,
+                                                 int n, size_t stride) {
+  const int lane = threadIdx.x & 31;
+  constexpr int CH = 32 * K;
+  const int nch = (n + CH - 1) / CH;
+  double cur[K], nxt[K];
+  auto load = [&](int c, double* dst) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int i = c * CH + lane * K + k;
+      dst[k] = i < n ? __ldcg(a + (size_t)i * stride) : 0.0;
+    }
+  };
+  if (nch > 0) load(0, cur);
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) load(c + 1, nxt);
+    const int base = c * CH;
+    for (int j = 0; j < 32; ++j) {
+      double t = acc;
+      const int nv = n - (base + j * K);
+      if (nv >= K) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) t = EP_DADD(t, cur[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+          if (k < nv) t = EP_DADD(t, cur[k]);
+      }
+      acc = __shfl_sync(0xffffffffu, t, j);
+    }
+    if (c + 1 < nch) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) cur[k] = nxt[k];
+    }
+  }
+  return acc;
+}
+
 // Row of block slot `slot` in canonical tiling (-1: none).
 template <int S, int P>
 __device__ __forceinline__ int tile_row(const TileMap& tm, int slot) {
@@ -268,118 +318,30 @@ __device__ __forceinline__ int tile_row(const TileMap& tm, int slot) {
   return ri < nr ? r0 + ri : -1;
 }
 
-__device__ __forceinline__ int atomic_add_acq_rel_gpu(int* p, int v) {
-  int old;
-  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-
-// Tile trees + fused finalize. Ordering: threads write partials, bar.sync, then
-// one thread's acq_rel atomic publishes them (release is cumulative over the
-// CTA barrier) and, for the block completing a segment, acquires everyone
-// else's partials; partials are then read with ld.global.cg (L2).
+// Tile trees: every thread has stored its rows' products in sprod[slot][S];
+// after one barrier, thread (tile, sample) folds the tile's 16 rows in
+// registers in the canonical order (v[i] += v[i+h], h = 8,4,2,1; rows past the
+// tile end hold +0.0) and writes the tile partial. The dot is closed by
+// k_fin_segments, so blocks retire right after this (no global round trip).
 template <int S, int P>
-__device__ void tiles_finish(const TileMap& tm, double* sprod, const FinArgs& f) {
+__device__ __forceinline__ void tiles_finish(const TileMap& tm, const double* sprod, const FinArgs& f) {
   using Sh = TileShape<S, P>;
-  constexpr int kChunk = Sh::ROWS;  // tile partials staged per step (reuses sprod)
-  double* schunk = sprod;
-  __shared__ double lanes[S];
-  __shared__ int s_last[Sh::TPC];
-  __shared__ int s_nlast, s_final;
   __syncthreads();
-#pragma unroll
-  for (int half = kTileRows / 2; half >= 1; half >>= 1) {
-    for (int idx = threadIdx.x; idx < Sh::TPC * half * S; idx += Sh::NT) {
-      const int lt = idx / (half * S);
-      const int rem = idx - lt * half * S;
-      double* base = sprod + lt * kTileRows * S;
-      base[rem] = EP_DADD(base[rem], base[rem + half * S]);
-    }
-    __syncthreads();
-  }
   for (int idx = threadIdx.x; idx < Sh::TPC * S; idx += Sh::NT) {
     const int lt = idx / S, e = idx - lt * S;
     const int tile = blockIdx.x * Sh::TPC + lt;
+    if (tile >= tm.num_tiles()) continue;
     int r0, nr;
-    if (tile < tm.num_tiles()) {
-      tm.tile(tile, r0, nr);
-      if (nr > 0) f.partials[(size_t)tile * S + e] = sprod[lt * kTileRows * S + e];
-    }
-  }
-  if (f.defer) return;  // launch_fin_segments closes the dot
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int nl = 0;
-    int cur = -1, cnt = 0;
-    auto flush = [&]() {
-      if (cnt == 0) return;
-      const int old = atomic_add_acq_rel_gpu(&f.seg_count[cur], cnt);
-      if (old + cnt == tm.tiles_in_seg(cur)) s_last[nl++] = cur;
-    };
-    for (int lt = 0; lt < Sh::TPC; ++lt) {
-      const int tile = blockIdx.x * Sh::TPC + lt;
-      if (tile >= tm.num_tiles()) break;
-      int r0, nr;
-      tm.tile(tile, r0, nr);
-      if (nr <= 0) continue;
-      const int seg = tile / tm.tiles_per_seg;
-      if (seg != cur) {
-        flush();
-        cur = seg;
-        cnt = 0;
-      }
-      ++cnt;
-    }
-    flush();
-    s_nlast = nl;
-  }
-  __syncthreads();
-  for (int k = 0; k < s_nlast; ++k) {
-    const int seg = s_last[k];
-    const int nt = tm.tiles_in_seg(seg);
-    const double* p = f.partials + (size_t)seg * tm.tiles_per_seg * S;
-    double acc = 0.0;
-    for (int t0 = 0; t0 < nt; t0 += kChunk) {
-      const int cnt = min(kChunk, nt - t0);
-      for (int idx = threadIdx.x; idx < cnt * S; idx += Sh::NT) schunk[idx] = __ldcg(p + (size_t)t0 * S + idx);
-      __syncthreads();
-      if (threadIdx.x < S) {
-#pragma unroll 8
-        for (int t = 0; t < cnt; ++t) acc = EP_DADD(acc, schunk[t * S + threadIdx.x]);
-      }
-      __syncthreads();
-    }
-    if (threadIdx.x < S) f.seg_sums[(size_t)seg * S + threadIdx.x] = acc;
-    if (f.seg_only) {  // multi-GPU: the host all-gathers the segment sums
-      if (threadIdx.x == 0) f.seg_count[seg] = 0;
-      continue;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      f.seg_count[seg] = 0;
-      s_final = (atomic_add_acq_rel_gpu(f.seg_done, 1) == tm.num_segs - 1);
-    }
-    __syncthreads();
-    if (s_final) {
-      double tot = 0.0;
-      for (int g0 = 0; g0 < tm.num_segs; g0 += kChunk) {
-        const int cnt = min(kChunk, tm.num_segs - g0);
-        for (int idx = threadIdx.x; idx < cnt * S; idx += Sh::NT)
-          schunk[idx] = __ldcg(f.seg_sums + (size_t)g0 * S + idx);
-        __syncthreads();
-        if (threadIdx.x < S) {
-#pragma unroll 8
-          for (int g = 0; g < cnt; ++g) tot = EP_DADD(tot, schunk[g * S + threadIdx.x]);
-        }
-        __syncthreads();
-      }
-      if (threadIdx.x < S) lanes[threadIdx.x] = tot;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        *f.seg_done = 0;
-        cg_phase<S>(f.phase, lanes, f.cg, f.hist, f.lanes_out);
-      }
-    }
+    tm.tile(tile, r0, nr);
+    if (nr <= 0) continue;
+    double v[kTileRows];
+#pragma unroll
+    for (int i = 0; i < kTileRows; ++i) v[i] = sprod[(lt * kTileRows + i) * S + e];
+#pragma unroll
+    for (int h = kTileRows / 2; h >= 1; h >>= 1)
+#pragma unroll
+      for (int i = 0; i < h; ++i) v[i] = EP_DADD(v[i], v[i + h]);
+    f.partials[(size_t)tile * S + e] = v[0];
   }
 }
 
@@ -586,51 +548,28 @@ __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hi
   }
 }
 
-// Deferred canonical finalize (the default): block `seg` forms the segment sum
-// 0.0 + tile_0 + tile_1 + ... per sample from the tile partials (staged through
-// shared memory in chunks so the chain only waits on DADD latency); the last
-// block (acq_rel counter) forms 0.0 + seg_0 + seg_1 + ... and runs the phase.
-// Keeping this out of the SpMV / update kernels spares every one of their
-// blocks a global atomic round trip before it can retire.
+// Canonical finalize: block `seg` has one warp per sample; warp e forms the
+// segment sum 0.0 + tile_0 + tile_1 + ... of sample e from the tile partials
+// (warp_chain_sum, DADD-latency bound); the last block (acq_rel counter) forms
+// 0.0 + seg_0 + seg_1 + ... the same way and runs the CG phase. With seg_only
+// (multi-GPU) the per-segment sums are the output.
 template <int S>
-__global__ void __launch_bounds__(256) k_fin_segments(const TileMap tm, const FinArgs f) {
+__global__ void __launch_bounds__(32 * S) k_fin_segments(const TileMap tm, const FinArgs f) {
   if ((f.phase == kPhasePQ || f.phase == kPhaseRR) && f.cg->done) return;
-  constexpr int kChunk = 64;
-  __shared__ double sch[kChunk * S];
   __shared__ double lanes[S];
   __shared__ int s_final;
   const int seg = blockIdx.x;
-  const int nt = tm.tiles_in_seg(seg);
-  const double* p = f.partials + (size_t)seg * tm.tiles_per_seg * S;
-  double acc = 0.0;
-  for (int t0 = 0; t0 < nt; t0 += kChunk) {
-    const int cnt = min(kChunk, nt - t0);
-    for (int idx = threadIdx.x; idx < cnt * S; idx += blockDim.x) sch[idx] = __ldcg(p + (size_t)t0 * S + idx);
-    __syncthreads();
-    if (threadIdx.x < S) {
-#pragma unroll 8
-      for (int t = 0; t < cnt; ++t) acc = EP_DADD(acc, sch[t * S + threadIdx.x]);
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x < S) f.seg_sums[(size_t)seg * S + threadIdx.x] = acc;
+  const int e = threadIdx.x >> 5;
+  const double* p = f.partials + (size_t)seg * tm.tiles_per_seg * S + e;
+  const double acc = warp_chain_sum<8>(0.0, p, tm.tiles_in_seg(seg), S);
+  if ((threadIdx.x & 31) == 0) f.seg_sums[(size_t)seg * S + e] = acc;
   if (f.seg_only) return;
   __syncthreads();
   if (threadIdx.x == 0) s_final = (atomic_add_acq_rel_gpu(f.seg_done, 1) == tm.num_segs - 1);
   __syncthreads();
   if (!s_final) return;
-  double tot = 0.0;
-  for (int g0 = 0; g0 < tm.num_segs; g0 += kChunk) {
-    const int cnt = min(kChunk, tm.num_segs - g0);
-    for (int idx = threadIdx.x; idx < cnt * S; idx += blockDim.x) sch[idx] = __ldcg(f.seg_sums + (size_t)g0 * S + idx);
-    __syncthreads();
-    if (threadIdx.x < S) {
-#pragma unroll 8
-      for (int g = 0; g < cnt; ++g) tot = EP_DADD(tot, sch[g * S + threadIdx.x]);
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x < S) lanes[threadIdx.x] = tot;
+  const double tot = warp_chain_sum<8>(0.0, f.seg_sums + e, tm.num_segs, S);
+  if ((threadIdx.x & 31) == 0) lanes[e] = tot;
   __syncthreads();
   if (threadIdx.x == 0) {
     *f.seg_done = 0;
@@ -641,7 +580,7 @@ __global__ void __launch_bounds__(256) k_fin_segments(const TileMap tm, const Fi
 template <int S>
 static cudaError_t fin_segments_s(const TileMap& tm, const FinArgs& f, cudaStream_t st) {
   if (tm.num_segs == 0) return cudaSuccess;
-  k_fin_segments<S><<<tm.num_segs, 256, 0, st>>>(tm, f);
+  k_fin_segments<S><<<tm.num_segs, 32 * S, 0, st>>>(tm, f);
   return cudaGetLastError();
 }
 

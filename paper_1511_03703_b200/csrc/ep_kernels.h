@@ -70,8 +70,8 @@ struct FinArgs {
   double* lanes_out;  // [s + 1] for kPhaseNone
   int seg_only;       // multi-GPU: stop at the segment sums (seg_sums) — the
                       // total over all ranks' segments is k_fin_gathered's job
-  int defer;          // producing kernels only write tile partials; a separate
-                      // launch_fin_segments forms the segment sums / total / phase
+  int defer;          // producing kernels only write tile partials (always 1:
+                      // launch_fin_segments forms the segment sums / total / phase)
 };
 
 cudaError_t launch_build_graph(int n, int* row_map, int* col_entry, cudaStream_t st);

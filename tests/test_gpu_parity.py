@@ -469,21 +469,3 @@ def test_symmetric_storage_is_bitwise_neutral(ctx, R, mode, s):
     assert same(host(ps.values), rv)
     ps.close()
     pf.close()
-
-
-@pytest.mark.parametrize("flavour", [CG_COUPLED, CG_UNCOUPLED])
-@pytest.mark.parametrize("s", [1, 32])
-def test_fused_finalize_option_is_bitwise_neutral(ctx, R, flavour, s):
-    n = 11
-    rm, ce, v, b = mesh_system(R, s, n, seed=6)
-    cfg = ep.SolverConfig(tol=1e-8, flavour=flavour, dot_mode=ep.DOT_CANONICAL, seg_rows=(n + 1) ** 2)
-    args = (ctx, s, dev(rm, torch.int32), dev(ce, torch.int32), dev(v), dev(b), cfg)
-    a = ep.pcg_solve(*args)
-    ctx.set_option(ep.OPT_FUSED_FINALIZE, 1)
-    try:
-        c = ep.pcg_solve(*args)
-    finally:
-        ctx.set_option(ep.OPT_FUSED_FINALIZE, 0)
-    assert a.iterations == c.iterations and same(host(a.solution), host(c.solution))
-    o = O.pcg(s, rm, ce, v, b, 1e-8, 1000, flavour=flavour, mode=DOT_CANONICAL, seg=(n + 1) ** 2)
-    assert same(host(a.solution), o["x"])
