@@ -48,6 +48,8 @@ enum { ENPROP_CG_COUPLED = 0, ENPROP_CG_UNCOUPLED = 1 };
 
 /* Rows per canonical reduction tile. */
 #define ENPROP_TILE_ROWS 16
+/* Tiles per canonical reduction block. */
+#define ENPROP_BLOCK_TILES 16
 
 const char* enprop_last_error(void);
 int enprop_abi_version(void);

@@ -359,9 +359,17 @@ void or_spmv(int S, int rows, const int* row_map, const int* col_entry, const do
  * CANONICAL (the product's fast order, documented in DESIGN.md §4):
  *   rows are cut into segments of seg_rows (for a mesh: one z-plane of nodes),
  *   each segment into tiles of tile_rows (power of two) aligned at the segment
- *   start; a tile's products are padded with +0.0 to tile_rows and folded by
- *   v[i] = v[i] + v[i + half] for half = tile_rows/2, ..., 1; the segment sum
- *   is 0.0 + tile_0 + tile_1 + ... and the lane total 0.0 + seg_0 + seg_1 + ... */
+ *   start, and the tiles into blocks of OR_BLOCK_TILES consecutive tiles.
+ *   A tile's products are padded with +0.0 to tile_rows and folded by
+ *   v[i] = v[i] + v[i + half] for half = tile_rows/2, ..., 1; a block's tile sums
+ *   are padded with +0.0 to OR_BLOCK_TILES and folded the same way; the segment
+ *   sum is 0.0 + block_0 + block_1 + ... and the lane total 0.0 + seg_0 + ... */
+static double fold(double* t, int n) {
+  for (int half = n / 2; half >= 1; half /= 2)
+    for (int i = 0; i < half; ++i) t[i] = t[i] + t[i + half];
+  return t[0];
+}
+
 void or_dot_lanes(int S, int64_t n, const double* u, const double* v, int mode, int tile_rows,
                   int seg_rows, double* lanes) {
   if (mode == OR_DOT_SERIAL) {
@@ -371,19 +379,23 @@ void or_dot_lanes(int S, int64_t n, const double* u, const double* v, int mode, 
     return;
   }
   double* t = (double*)malloc(sizeof(double) * (size_t)tile_rows);
+  double blk[OR_BLOCK_TILES];
+  const int64_t block_rows = (int64_t)tile_rows * OR_BLOCK_TILES;
   for (int e = 0; e < S; ++e) {
     double total = 0.0;
     for (int64_t r0 = 0; r0 < n; r0 += seg_rows) {
       const int64_t r1 = r0 + seg_rows < n ? r0 + seg_rows : n;
       double seg = 0.0;
-      for (int64_t t0 = r0; t0 < r1; t0 += tile_rows) {
-        for (int i = 0; i < tile_rows; ++i) {
-          const int64_t row = t0 + i;
-          t[i] = row < r1 ? u[row * S + e] * v[row * S + e] : 0.0;
+      for (int64_t b0 = r0; b0 < r1; b0 += block_rows) {
+        for (int k = 0; k < OR_BLOCK_TILES; ++k) {
+          const int64_t t0 = b0 + (int64_t)k * tile_rows;
+          for (int i = 0; i < tile_rows; ++i) {
+            const int64_t row = t0 + i;
+            t[i] = row < r1 ? u[row * S + e] * v[row * S + e] : 0.0;
+          }
+          blk[k] = t0 < r1 ? fold(t, tile_rows) : 0.0;
         }
-        for (int half = tile_rows / 2; half >= 1; half /= 2)
-          for (int i = 0; i < half; ++i) t[i] = t[i] + t[i + half];
-        seg = seg + t[0];
+        seg = seg + fold(blk, OR_BLOCK_TILES);
       }
       total = total + seg;
     }

@@ -22,6 +22,7 @@ extern "C" {
 #endif
 
 #define OR_MAX_TERMS 64
+#define OR_BLOCK_TILES 16 /* canonical order: tiles per block */
 
 typedef struct {
   int m;

@@ -262,50 +262,6 @@ __device__ __forceinline__ int atomic_add_acq_rel_gpu(int* p, int v) {
   return old;
 }
 
-// Sequential left-to-right sum acc + a_0 + a_1 + ... + a_{n-1} of a
-// strided array by one warp at DADD latency: lane j holds the K values
-// [jK, jK+K) of each chunk in registers, every lane runs the same chain on its
-// own registers in lockstep and a shuffle keeps lane j's running sum; the next
-// chunk's loads are in flight meanwhile. Returns the sum in every lane.
-template <int K>
-__device__ __forceinline__ double warp_chain_sum(double acc, const double* __restrict__ a,
-                                                 int n, size_t stride) {
-  const int lane = threadIdx.x & 31;
-  constexpr int CH = 32 * K;
-  const int nch = (n + CH - 1) / CH;
-  double cur[K], nxt[K];
-  auto load = [&](int c, double* dst) {
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int i = c * CH + lane * K + k;
-      dst[k] = i < n ? __ldcg(a + (size_t)i * stride) : 0.0;
-    }
-  };
-  if (nch > 0) load(0, cur);
-  for (int c = 0; c < nch; ++c) {
-    if (c + 1 < nch) load(c + 1, nxt);
-    const int base = c * CH;
-    for (int j = 0; j < 32; ++j) {
-      double t = acc;
-      const int nv = n - (base + j * K);
-      if (nv >= K) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) t = EP_DADD(t, cur[k]);
-      } else {
-#pragma unroll
-        for (int k = 0; k < K; ++k)
-          if (k < nv) t = EP_DADD(t, cur[k]);
-      }
-      acc = __shfl_sync(0xffffffffu, t, j);
-    }
-    if (c + 1 < nch) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) cur[k] = nxt[k];
-    }
-  }
-  return acc;
-}
-
 // Row of block slot `slot` in canonical tiling (-1: none).
 template <int S, int P>
 __device__ __forceinline__ int tile_row(const TileMap& tm, int slot) {
@@ -548,28 +504,64 @@ __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hi
   }
 }
 
-// Canonical finalize: block `seg` has one warp per sample; warp e forms the
-// segment sum 0.0 + tile_0 + tile_1 + ... of sample e from the tile partials
-// (warp_chain_sum, DADD-latency bound); the last block (acq_rel counter) forms
-// 0.0 + seg_0 + seg_1 + ... the same way and runs the CG phase. With seg_only
-// (multi-GPU) the per-segment sums are the output.
+// Canonical finalize, one CTA per segment. Thread (block b, sample e) folds the
+// block's kBlockTiles tile partials in registers (v[i] += v[i+h], h = 8..1;
+// missing tiles are +0.0) -- a warp covers 32 consecutive samples, so every
+// load is one coalesced 256-byte row of partials -- and thread e then forms
+// the segment sum 0.0 + block_0 + block_1 + ... from shared memory. The last
+// CTA (acq_rel counter) forms 0.0 + seg_0 + seg_1 + ... and runs the CG phase.
+// With seg_only (multi-GPU) the per-segment sums are the output.
+constexpr int kFinThreads = 256;
+constexpr int kFinChunk = 64;  // blocks (resp. segments) staged per pass
+
 template <int S>
-__global__ void __launch_bounds__(32 * S) k_fin_segments(const TileMap tm, const FinArgs f) {
+__global__ void __launch_bounds__(kFinThreads) k_fin_segments(const TileMap tm, const FinArgs f) {
   if ((f.phase == kPhasePQ || f.phase == kPhaseRR) && f.cg->done) return;
+  __shared__ double sblk[kFinChunk * S];
   __shared__ double lanes[S];
   __shared__ int s_final;
   const int seg = blockIdx.x;
-  const int e = threadIdx.x >> 5;
-  const double* p = f.partials + (size_t)seg * tm.tiles_per_seg * S + e;
-  const double acc = warp_chain_sum<8>(0.0, p, tm.tiles_in_seg(seg), S);
-  if ((threadIdx.x & 31) == 0) f.seg_sums[(size_t)seg * S + e] = acc;
+  const int ntiles = tm.tiles_in_seg(seg);
+  const int nblk = (ntiles + kBlockTiles - 1) / kBlockTiles;
+  const double* part = f.partials + (size_t)seg * tm.tiles_per_seg * S;
+  double acc = 0.0;
+  for (int b0 = 0; b0 < nblk; b0 += kFinChunk) {
+    const int cnt = min(kFinChunk, nblk - b0);
+    for (int idx = threadIdx.x; idx < cnt * S; idx += kFinThreads) {
+      const int b = idx / S, e = idx - b * S;
+      const int t0 = (b0 + b) * kBlockTiles;
+      double v[kBlockTiles];
+#pragma unroll
+      for (int i = 0; i < kBlockTiles; ++i)
+        v[i] = t0 + i < ntiles ? part[(size_t)(t0 + i) * S + e] : 0.0;
+#pragma unroll
+      for (int h = kBlockTiles / 2; h >= 1; h >>= 1)
+#pragma unroll
+        for (int i = 0; i < h; ++i) v[i] = EP_DADD(v[i], v[i + h]);
+      sblk[idx] = v[0];
+    }
+    __syncthreads();
+    if (threadIdx.x < S)
+      for (int b = 0; b < cnt; ++b) acc = EP_DADD(acc, sblk[b * S + threadIdx.x]);
+    __syncthreads();
+  }
+  if (threadIdx.x < S) f.seg_sums[(size_t)seg * S + threadIdx.x] = acc;
   if (f.seg_only) return;
   __syncthreads();
   if (threadIdx.x == 0) s_final = (atomic_add_acq_rel_gpu(f.seg_done, 1) == tm.num_segs - 1);
   __syncthreads();
   if (!s_final) return;
-  const double tot = warp_chain_sum<8>(0.0, f.seg_sums + e, tm.num_segs, S);
-  if ((threadIdx.x & 31) == 0) lanes[e] = tot;
+  double tot = 0.0;
+  for (int k0 = 0; k0 < tm.num_segs; k0 += kFinChunk) {
+    const int cnt = min(kFinChunk, tm.num_segs - k0);
+    for (int idx = threadIdx.x; idx < cnt * S; idx += kFinThreads)
+      sblk[idx] = __ldcg(f.seg_sums + (size_t)k0 * S + idx);
+    __syncthreads();
+    if (threadIdx.x < S)
+      for (int k = 0; k < cnt; ++k) tot = EP_DADD(tot, sblk[k * S + threadIdx.x]);
+    __syncthreads();
+  }
+  if (threadIdx.x < S) lanes[threadIdx.x] = tot;
   __syncthreads();
   if (threadIdx.x == 0) {
     *f.seg_done = 0;
@@ -580,7 +572,7 @@ __global__ void __launch_bounds__(32 * S) k_fin_segments(const TileMap tm, const
 template <int S>
 static cudaError_t fin_segments_s(const TileMap& tm, const FinArgs& f, cudaStream_t st) {
   if (tm.num_segs == 0) return cudaSuccess;
-  k_fin_segments<S><<<tm.num_segs, 32 * S, 0, st>>>(tm, f);
+  k_fin_segments<S><<<tm.num_segs, kFinThreads, 0, st>>>(tm, f);
   return cudaGetLastError();
 }
 

@@ -5,9 +5,11 @@
 namespace ep {
 
 constexpr int kTileRows = 16;
+constexpr int kBlockTiles = 16;  // tiles per canonical block
 
 // Canonical tile map: rows are cut into segments of seg_rows, each segment into
-// tiles of kTileRows aligned at the segment start.
+// tiles of kTileRows aligned at the segment start, and the tiles into blocks of
+// kBlockTiles.
 __host__ __device__ inline int imin(int a, int b) { return a < b ? a : b; }
 
 struct TileMap {

@@ -28,10 +28,8 @@ def plane_range(N, P, r):
     return k0, k0 + base + (1 if r < extra else 0)
 
 
-def tile_sum(prod):
-    t = np.zeros((TILE, prod.shape[1]))
-    t[:prod.shape[0]] = prod
-    h = TILE // 2
+def fold(t):
+    h = t.shape[0] // 2
     while h >= 1:
         t[:h] = t[:h] + t[h:2 * h]
         h //= 2
@@ -39,15 +37,25 @@ def tile_sum(prod):
 
 
 def plane_sums(u, v, plane, s):
-    """Canonical per-segment (plane) sums of the owned rows: tiles of 16 rows,
-    stride-halving tree, then 0.0 + tile_0 + tile_1 + ... per plane."""
+    """Canonical per-segment (plane) sums of the owned rows:
+    tiles of 16 rows and blocks of 16 tiles folded by stride halving (+0.0
+    padding), then 0.0 + block_0 + block_1 + ... per plane."""
     nplanes = u.shape[0] // plane
     out = np.zeros((nplanes, s))
     for k in range(nplanes):
+        r0, r1 = k * plane, (k + 1) * plane
         seg = np.zeros(s)
-        for t0 in range(0, plane, TILE):
-            r0, r1 = k * plane + t0, k * plane + min(t0 + TILE, plane)
-            seg = seg + tile_sum(u[r0:r1] * v[r0:r1])
+        for b0 in range(r0, r1, 16 * TILE):
+            blk = np.zeros((16, s))
+            for j in range(16):
+                t0 = b0 + j * TILE
+                if t0 >= r1:
+                    continue
+                t = np.zeros((TILE, s))
+                m = min(TILE, r1 - t0)
+                t[:m] = u[t0:t0 + m] * v[t0:t0 + m]
+                blk[j] = fold(t)
+            seg = seg + fold(blk)
         out[k] = seg
     return out
 

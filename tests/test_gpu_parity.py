@@ -208,7 +208,7 @@ def test_dot_serial_equals_reference(ctx, R, s):
 @pytest.mark.parametrize("s", WIDTHS)
 def test_dot_canonical_equals_restatement(ctx, s):
     rng = np.random.default_rng(60 + s)
-    for n, seg in ((1, 4096), (300, 64), (4225, 4225), (70001, 4225)):
+    for n, seg in ((1, 4096), (300, 64), (4225, 4225), (70001, 4225), (70001, 70001), (70001, 300)):
         u, v = rng.uniform(-1, 1, (n, s)), rng.uniform(-1, 1, (n, s))
         lanes, coupled = ep.dot_lanes(ctx, s, dev(u), dev(v), ep.DOT_CANONICAL, seg)
         assert lanes == list(O.dot_lanes(s, u, v, DOT_CANONICAL, TILE_ROWS, seg))

@@ -98,29 +98,48 @@ def test_pcg_golden_coupled_and_uncoupled():
 
 
 # --------------------------------------------------------- canonical order itself
+def fold(t):
+    t = t.copy()
+    h = len(t) // 2
+    while h >= 1:
+        t[:h] = t[:h] + t[h:2 * h]
+        h //= 2
+    return t[0]
+
+
+def canonical_lane(u, v, seg, e):
+    """The canonical order in numpy: tiles of TILE_ROWS rows,
+    blocks of 16 tiles, both stride-halving folds with +0.0 padding; segment
+    and total sums sequential."""
+    n = u.shape[0]
+    total = 0.0
+    for r0 in range(0, n, seg):
+        r1 = min(r0 + seg, n)
+        sg = 0.0
+        for b0 in range(r0, r1, 16 * TILE_ROWS):
+            blk = np.zeros(16)
+            for k in range(16):
+                t0 = b0 + k * TILE_ROWS
+                if t0 >= r1:
+                    continue
+                t = np.zeros(TILE_ROWS)
+                m = min(TILE_ROWS, r1 - t0)
+                t[:m] = u[t0:t0 + m, e] * v[t0:t0 + m, e]
+                blk[k] = fold(t)
+            sg = sg + fold(blk)
+        total = total + sg
+    return total
+
+
 def test_canonical_dot_definition():
-    """The canonical order (DESIGN.md §4) restated in numpy agrees with the C oracle."""
+    """The canonical order restated in numpy agrees with the C oracle."""
     rng = np.random.default_rng(5)
-    for n, seg in ((1, 7), (200, 64), (1000, 137), (4225, 4225)):
+    for n, seg in ((1, 7), (200, 64), (1000, 137), (4225, 4225), (9000, 4225)):
         u = rng.uniform(-1, 1, (n, 4))
         v = rng.uniform(-1, 1, (n, 4))
         lanes = O.dot_lanes(4, u, v, DOT_CANONICAL, TILE_ROWS, seg)
         for e in range(4):
-            total = 0.0
-            for r0 in range(0, n, seg):
-                r1 = min(r0 + seg, n)
-                sg = 0.0
-                for t0 in range(r0, r1, TILE_ROWS):
-                    t = np.zeros(TILE_ROWS)
-                    k = min(TILE_ROWS, r1 - t0)
-                    t[:k] = u[t0:t0 + k, e] * v[t0:t0 + k, e]
-                    h = TILE_ROWS // 2
-                    while h >= 1:
-                        t[:h] = t[:h] + t[h:2 * h]
-                        h //= 2
-                    sg = sg + t[0]
-                total = total + sg
-            assert total == lanes[e]
+            assert canonical_lane(u, v, seg, e) == lanes[e]
 
 
 def test_serial_dot_is_sequential():
