@@ -85,9 +85,11 @@ int enprop_ctx_set_option(enprop_ctx* ctx, int option, int value);
  * bench.py for the roofline). Returns the totals accumulated since the last
  * reset; enable = 1/0 turns timing on/off and resets, enable = -1 only reads. */
 int enprop_ctx_profile(enprop_ctx* ctx, int enable, double* spmv_ms, int64_t* spmv_launches);
-/* Per-phase totals of the profiled CG iterations: ms[0] SpMV phase, ms[1] PQ
- * finalize (serial order only), ms[2] update, ms[3] RR finalize (serial order
- * only), ms[4] whole iterations. */
+/* Per-phase totals of the profiled CG iterations, ms[9]: [0] SpMV phase
+ * (direction + SpMV), [1] PQ finalize, [2] update, [3] RR finalize, [4] whole
+ * working iterations; per profiled solve: [5] whole solve on the GPU, [6] setup
+ * and initial residual, [7] iteration loop (incl. early-exit iterations),
+ * [8] iterations enqueued past convergence (early-exit). */
 int enprop_ctx_profile_detail(enprop_ctx* ctx, double* ms, int64_t* iterations);
 
 int enprop_malloc(enprop_ctx* ctx, size_t bytes, void** dptr);

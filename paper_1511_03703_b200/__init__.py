@@ -249,11 +249,11 @@ class Context:
 
     def profile_detail(self):
         """Per-phase CG totals since the last profile(1): dict of ms and count."""
-        ms = (C.c_double * 5)()
+        ms = (C.c_double * 9)()
         n = C.c_int64()
         _check(lib().enprop_ctx_profile_detail(self.h, ms, C.byref(n)))
         return dict(spmv=ms[0], fin_pq=ms[1], update=ms[2], fin_rr=ms[3], iteration=ms[4],
-                    iterations=n.value)
+                    solve=ms[5], init=ms[6], loop=ms[7], early_exit=ms[8], iterations=n.value)
 
     def close(self):
         if getattr(self, "h", None):

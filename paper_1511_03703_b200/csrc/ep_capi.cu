@@ -125,18 +125,19 @@ cudaEvent_t* prof_slot(enprop_ctx* c) {
   return p;
 }
 
-// Accumulate the recorded iterations. Iterations enqueued past convergence
-// early-exit in every kernel (a few microseconds); they are excluded by a
-// 5-microsecond threshold on the SpMV phase, far below any real SpMV here.
-int prof_collect(enprop_ctx* c) {
-  for (size_t i = 0; i + 4 < c->prof_used + 0 && i + 5 <= c->prof_used; i += 5) {
+// Accumulate the recorded iterations: the first `working` did work; the rest
+// were enqueued past convergence and early-exited (their time goes to [8]).
+int prof_collect(enprop_ctx* c, int working) {
+  for (size_t i = 0; i + 5 <= c->prof_used; i += 5) {
     float t[4];
     for (int k = 0; k < 4; ++k) EP_CUDA(cudaEventElapsedTime(&t[k], c->prof_ev[i + k], c->prof_ev[i + k + 1]));
-    if (t[0] > 0.005f) {
+    if ((int)(i / 5) < working) {
       c->prof_ms += t[0];
       c->prof_count += 1;
       for (int k = 0; k < 4; ++k) c->prof_detail[k] += t[k];
       c->prof_detail[4] += t[0] + t[1] + t[2] + t[3];
+    } else {
+      c->prof_detail[8] += t[0] + t[1] + t[2] + t[3];
     }
   }
   c->prof_used = 0;
@@ -159,6 +160,13 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
   const int lanes = opt->flavour == ENPROP_CG_UNCOUPLED ? s : 1;
   const bool fused = ctx->fused_direction != 0 && vpos == nullptr;  // symmetric storage: split only
   cudaStream_t st = ctx->stream;
+  cudaEvent_t* sev = nullptr;  // profiled: solve start, loop start, loop end, solve end
+  if (ctx->profile) {
+    if (!ctx->prof_solve_ev[0])
+      for (int k = 0; k < 4; ++k) EP_CUDA(cudaEventCreate(&ctx->prof_solve_ev[k]));
+    sev = ctx->prof_solve_ev;
+    EP_CUDA(cudaEventRecord(sev[0], st));
+  }
 
   CgState init;
   std::memset(&init, 0, sizeof(init));
@@ -185,6 +193,7 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
     ctx->launches += 1;
   }
 
+  if (sev) EP_CUDA(cudaEventRecord(sev[1], st));
   const int chunk = opt->check_every > 0 ? opt->check_every : 16;
   int launched = 0;
   int slot = 0;
@@ -226,37 +235,40 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
     pending = true;
     slot ^= 1;
   }
+  if (sev) EP_CUDA(cudaEventRecord(sev[2], st));
   // the last finished iteration's x += alpha*p is still deferred
   EP_CUDA(launch_cg_flush(s, rows, x, w.p, w.state, st));
   ctx->launches += 1;
+  if (sev) EP_CUDA(cudaEventRecord(sev[3], st));
   EP_CUDA(cudaStreamSynchronize(st));
-  if (ctx->profile) {
-    rc = prof_collect(ctx);
-    if (rc) return rc;
-  }
 
   CgState fin;
   EP_CUDA(cudaMemcpy(&fin, w.state, sizeof(fin), cudaMemcpyDeviceToHost));
+  if (ctx->profile) {
+    rc = prof_collect(ctx, fin.it);
+    if (rc) return rc;
+    float t[3];
+    EP_CUDA(cudaEventElapsedTime(&t[0], sev[0], sev[3]));
+    EP_CUDA(cudaEventElapsedTime(&t[1], sev[0], sev[1]));
+    EP_CUDA(cudaEventElapsedTime(&t[2], sev[1], sev[2]));
+    for (int k = 0; k < 3; ++k) ctx->prof_detail[5 + k] += t[k];
+  }
   if (!fin.done) return fail(ENPROP_ERR_CUDA, "enprop_cg: solver did not finish (internal)");
   for (int l = 0; l < lanes; ++l) {
     if (iterations) iterations[l] = fin.iters[l];
     if (lane_status) lane_status[l] = opt->flavour == ENPROP_CG_UNCOUPLED ? fin.lane_status[l] : fin.status;
     if (hist_len) hist_len[l] = fin.hist_len[l];
   }
-  if (history) {
-    const size_t count = (size_t)(opt->max_iterations + 1) * lanes;
-    if (lanes == 1) {
-      std::vector<double> h((size_t)opt->max_iterations + 1);
-      EP_CUDA(cudaMemcpy(h.data(), w.hist, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
-      for (size_t i = 0; i < h.size(); ++i) history[i] = (int)i < fin.hist_len[0] ? h[i] : NAN;
-    } else {
-      std::vector<double> h(count);
-      EP_CUDA(cudaMemcpy(h.data(), w.hist, count * sizeof(double), cudaMemcpyDeviceToHost));
-      for (int it = 0; it <= opt->max_iterations; ++it)
-        for (int e = 0; e < s; ++e)
-          history[(size_t)it * s + e] = it < fin.hist_len[e] ? h[(size_t)it * s + e] : NAN;
-    }
+  if (history) {  // copy only the recorded rows; NaN past each lane's end
+    int len = 0;
+    for (int l = 0; l < lanes; ++l) len = fin.hist_len[l] > len ? fin.hist_len[l] : len;
+    std::vector<double> h((size_t)len * lanes);
+    if (len) EP_CUDA(cudaMemcpy(h.data(), w.hist, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int it = 0; it <= opt->max_iterations; ++it)
+      for (int l = 0; l < lanes; ++l)
+        history[(size_t)it * lanes + l] = it < fin.hist_len[l] ? h[(size_t)it * lanes + l] : NAN;
   }
+
   if (fin.status == ENPROP_ERR_NO_CONVERGENCE)
     return fail(ENPROP_ERR_NO_CONVERGENCE, "pcg_solve: no convergence within " +
                                                std::to_string(opt->max_iterations) + " iterations");
@@ -305,6 +317,8 @@ int enprop_ctx_destroy(enprop_ctx* c) {
   if (c->flag_ev[1]) cudaEventDestroy(c->flag_ev[1]);
   if (c->pinned_flags) cudaFreeHost(c->pinned_flags);
   for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->prof_solve_ev)
+    if (e) cudaEventDestroy(e);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return ENPROP_OK;
@@ -359,7 +373,7 @@ int enprop_ctx_profile(enprop_ctx* c, int enable, double* spmv_ms, int64_t* spmv
 
 int enprop_ctx_profile_detail(enprop_ctx* c, double* ms, int64_t* iterations) {
   if (!c || !ms) return fail(ENPROP_ERR_INVALID, "enprop_ctx_profile_detail: null argument");
-  for (int k = 0; k < 5; ++k) ms[k] = c->prof_detail[k];
+  for (int k = 0; k < 9; ++k) ms[k] = c->prof_detail[k];
   if (iterations) *iterations = c->prof_count;
   return ENPROP_OK;
 }

@@ -30,7 +30,9 @@ struct enprop_ctx {
   size_t prof_used = 0;
   double prof_ms = 0.0;       // CG SpMV phase (direction + SpMV)
   int64_t prof_count = 0;     // profiled iterations that did work
-  double prof_detail[5] = {0, 0, 0, 0, 0};  // spmv, fin pq, update, fin rr, iteration
+  // spmv, fin pq, update, fin rr, iteration, solve, init, loop, early-exit (enprop_b200.h)
+  double prof_detail[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  cudaEvent_t prof_solve_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace ep_internal {

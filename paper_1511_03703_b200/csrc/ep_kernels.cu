@@ -803,6 +803,171 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
   }
 }
 
+// -----------------------------------------------------------------------------
+// Warp-per-tile CG SpMV (split-direction schedule, the default): q = A p and
+// the canonical p.q tile partials with no shared memory and no barrier.
+//
+// A warp owns TILES whole tiles (or, in serial order, 16 contiguous rows) and
+// walks them in PASSES passes of R = 32/TPR rows; thread (g, sub) handles row
+// g of each pass, lanes [sub*V, sub*V+V). Tile row r = ps*R + g, so the tree
+// levels h >= R of the canonical tile fold (v[r] += v[r+h], h = 8,4,2,1) pair
+// rows held by the same thread (register adds) and the levels h < R pair
+// threads h*TPR apart (shuffles).
+//
+// Row products load the row's column indices (and symmetric slots)
+// cooperatively -- each of the row's TPR threads loads E of the window's
+// W = TPR*E entries -- and broadcast them by shuffle, so each batch of U
+// gathers waits on one memory latency instead of two.
+// -----------------------------------------------------------------------------
+template <int S>
+struct WarpTile {
+  static constexpr int V = SpmvShape<S>::V;
+  static constexpr int TPR = S / V;                                  // threads per row
+  static constexpr int R = 32 / TPR;                                 // rows per warp pass
+  static constexpr int PASSES = R >= kTileRows ? 1 : kTileRows / R;  // passes per tile
+  static constexpr int TILES = R >= kTileRows ? R / kTileRows : 1;   // tiles per warp
+  static constexpr int E = TPR >= 4 ? 32 / TPR : 0;                  // index loads per thread
+  static constexpr int W = TPR * E;                                  // window (entries)
+};
+
+template <int S, bool kSym>
+__device__ __forceinline__ VecD<SpmvShape<S>::V> row_product_coop(
+    int row, const int* __restrict__ row_map, const int* __restrict__ col_entry,
+    const double* __restrict__ values, const double* __restrict__ x, const int* __restrict__ vpos,
+    int sub) {
+  using Sh = WarpTile<S>;
+  constexpr int V = Sh::V, TPR = Sh::TPR, E = Sh::E, W = Sh::W, U = 4;
+  const int lane0 = sub * V;
+  int rs = 0, n = 0;
+  if (row >= 0) {
+    rs = __ldg(row_map + row);
+    n = __ldg(row_map + row + 1) - rs;
+  }
+  VecD<V> sum;
+#pragma unroll
+  for (int j = 0; j < V; ++j) sum.v[j] = 0.0;
+  if constexpr (E == 0) {  // narrow rows (TPR < 4): plain per-thread loop
+    if (row >= 0) {
+      VecD<V> beta;
+      sum = row_product<S, V, U, false, false, kSym>(row, row_map, col_entry, values, x, nullptr,
+                                                     true, beta, lane0, vpos);
+    }
+    return sum;
+  } else {
+    const int nmax = __reduce_max_sync(0xffffffffu, n);
+    for (int w0 = 0; w0 < nmax; w0 += W) {
+      int mc[E], mv[E];
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const int k = w0 + i * TPR + sub;
+        mc[i] = k < n ? ld_stream_i32(col_entry + rs + k) : 0;
+        if constexpr (kSym) mv[i] = k < n ? ld_stream_i32(vpos + rs + k) : 0;
+      }
+#pragma unroll
+      for (int kb = 0; kb < W; kb += U) {
+        if (w0 + kb >= nmax) break;
+        int c[U], vi[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int idx = kb + u;  // compile-time: register selects are static
+          c[u] = __shfl_sync(0xffffffffu, mc[idx / TPR], idx % TPR, TPR);
+          if constexpr (kSym) vi[u] = __shfl_sync(0xffffffffu, mv[idx / TPR], idx % TPR, TPR);
+          else vi[u] = rs + w0 + idx;
+        }
+        VecD<V> av[U], xv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (w0 + kb + u < n) {
+            av[u] = ld_stream<V>(values + (size_t)vi[u] * S + lane0);
+            xv[u] = ld_vec<V>(x + (size_t)c[u] * S + lane0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (w0 + kb + u < n) {
+#pragma unroll
+            for (int j = 0; j < V; ++j) sum.v[j] = EP_DADD(sum.v[j], EP_DMUL(av[u].v[j], xv[u].v[j]));
+          }
+        }
+      }
+    }
+    return sum;
+  }
+}
+
+template <int S, bool kTiles, bool kSym>
+__global__ void __launch_bounds__(256, 4) k_cg_spmv_warp(
+    const TileMap tm, const int* __restrict__ row_map, const int* __restrict__ col_entry,
+    const double* __restrict__ values, const double* __restrict__ p_new, double* __restrict__ q,
+    const double* __restrict__ p_gather, const int* __restrict__ vpos, const FinArgs f) {
+  using Sh = WarpTile<S>;
+  constexpr int V = Sh::V, TPR = Sh::TPR, R = Sh::R;
+  if (f.cg->done) return;
+  const int lane = threadIdx.x & 31;
+  const int g = lane / TPR, sub = lane % TPR;
+  const int lane0 = sub * V;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  // tile (or 16-row chunk) of this thread and its first row / row count
+  const int unit = warp * Sh::TILES + (Sh::TILES > 1 ? g / kTileRows : 0);
+  int r0, nr;
+  if constexpr (kTiles) {
+    if (unit < tm.num_tiles()) tm.tile(unit, r0, nr);
+    else r0 = 0, nr = 0;
+  } else {
+    r0 = unit * kTileRows;
+    nr = imin(kTileRows, tm.rows - r0);
+  }
+  const int g16 = Sh::TILES > 1 ? g % kTileRows : g;  // row within the tile at pass 0
+  // HALF > 0: the top tree level (h = 8 >= R) pairs pass ps with ps + HALF and
+  // is applied as soon as pass ps + HALF is known (fewer live registers).
+  constexpr int HALF = Sh::PASSES / 2;
+  double prod[HALF > 0 ? HALF : 1][V];
+#pragma unroll
+  for (int ps = 0; ps < Sh::PASSES; ++ps) {
+    const int tr = ps * R + g16;
+    const int row = tr < nr ? r0 + tr : -1;
+    const VecD<V> sum = row_product_coop<S, kSym>(row, row_map, col_entry, values, p_gather, vpos, sub);
+    double cur[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) cur[j] = 0.0;
+    if (row >= 0) {
+      st_vec<V>(q + (size_t)row * S + lane0, sum);
+      if constexpr (kTiles) {
+        const VecD<V> pn = ld_vec<V>(p_new + (size_t)row * S + lane0);
+#pragma unroll
+        for (int j = 0; j < V; ++j) cur[j] = EP_DMUL(pn.v[j], sum.v[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) {
+      if (HALF == 0) prod[0][j] = cur[j];
+      else if (ps < HALF) prod[ps % (HALF > 0 ? HALF : 1)][j] = cur[j];
+      else prod[(ps - HALF) % (HALF > 0 ? HALF : 1)][j] = EP_DADD(prod[(ps - HALF) % (HALF > 0 ? HALF : 1)][j], cur[j]);
+    }
+  }
+  if constexpr (kTiles) {
+    // remaining register levels h with R <= h < 8: rows r and r+h are slots ps, ps + h/R
+#pragma unroll
+    for (int h = kTileRows / 4; h >= R && h >= 1; h >>= 1)
+#pragma unroll
+      for (int ps = 0; ps < h / R; ++ps)
+#pragma unroll
+        for (int j = 0; j < V; ++j) prod[ps][j] = EP_DADD(prod[ps][j], prod[ps + h / R][j]);
+    // levels h < R: row g16 + h lives h*TPR lanes up
+#pragma unroll
+    for (int h = (R < kTileRows ? R : kTileRows) / 2; h >= 1; h >>= 1)
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const double o = __shfl_down_sync(0xffffffffu, prod[0][j], h * TPR);
+        prod[0][j] = EP_DADD(prod[0][j], o);
+      }
+    if (g16 == 0 && nr > 0) {
+#pragma unroll
+      for (int j = 0; j < V; ++j) f.partials[(size_t)unit * S + lane0 + j] = prod[0][j];
+    }
+  }
+}
+
 // Direction pass (split variant), every row:
 //   x     = alpha_prev*p_old + x   on lanes that owe it (pcg.hpp:94, deferred
 //                                  from the previous iteration's update)
@@ -922,6 +1087,24 @@ static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, bool run_direction, con
 #define EP_CG_SPMV(T, D, Y)                                                                   \
   k_cg_spmv<S, T, D, Y><<<blocks, 256, 0, st>>>(tm, row_map, col_entry, values, r, p_old, p_new, q, \
                                                 x, p_gather, vpos, f)
+  if (!fused_dir) {  // warp-per-tile kernel (split direction schedule)
+    using Sw = WarpTile<S>;
+    const int units = tiles ? tm.num_tiles() : (tm.rows + kTileRows - 1) / kTileRows;
+    const int warps = (units + Sw::TILES - 1) / Sw::TILES;
+    const int wblocks = (warps + 7) / 8;
+#define EP_CG_SPMV_W(T, Y)                                                                    \
+  k_cg_spmv_warp<S, T, Y><<<wblocks, 256, 0, st>>>(tm, row_map, col_entry, values, p_new, q,  \
+                                                   p_gather, vpos, f)
+    if (vpos) {
+      if (tiles) EP_CG_SPMV_W(true, true);
+      else EP_CG_SPMV_W(false, true);
+    } else {
+      if (tiles) EP_CG_SPMV_W(true, false);
+      else EP_CG_SPMV_W(false, false);
+    }
+#undef EP_CG_SPMV_W
+    return cudaGetLastError();
+  }
   if (vpos) {  // symmetric storage: split direction schedule only
     if (fused_dir) return cudaErrorInvalidValue;
     if (tiles) EP_CG_SPMV(true, false, true);

@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--spmv-only", action="store_true")
     ap.add_argument("--sym", type=int, default=1, help="symmetric storage for the CG problems")
+    ap.add_argument("--modes", default="canonical,serial")
+    ap.add_argument("--fused", default="1,0", help="fused-direction settings to time")
     args = ap.parse_args()
     n, s = args.n, args.s
     ctx = ep.Context(0)
@@ -70,8 +72,10 @@ def main():
     if args.spmv_only:
         print(json.dumps(out, indent=1))
         return
-    for mode_name, mode in (("canonical", ep.DOT_CANONICAL), ("serial", ep.DOT_SERIAL)):
-        for fused in (1, 0):
+    modes = {"canonical": ep.DOT_CANONICAL, "serial": ep.DOT_SERIAL}
+    for mode_name in args.modes.split(","):
+        mode = modes[mode_name]
+        for fused in (int(v) for v in args.fused.split(",")):
             ctx.set_option(ep.OPT_FUSED_DIRECTION, fused)
             cfg = ep.SolverConfig(tol=1e-6, max_iterations=10000, flavour=ep.CG_UNCOUPLED, dot_mode=mode)
             p.solve(cfg)
@@ -91,7 +95,11 @@ def main():
             out[key] = {"solve_ms": round(ms, 3), "iters": its, "ms_per_iter": round(ms / its[-1], 4),
                         "spmv_phase_ms": round(sp_ms / max(sp_n, 1), 4),
                         "per_iter_ms": {k: round(v / max(det["iterations"], 1), 4)
-                                        for k, v in det.items() if k != "iterations"}}
+                                        for k, v in det.items()
+                                        if k not in ("iterations", "solve", "init", "loop", "early_exit")},
+                        "counted_iterations": det["iterations"],
+                        "per_solve_ms": {k: round(det[k] / args.steps, 3)
+                                         for k in ("solve", "init", "loop", "early_exit")}}
             if mode_name == "serial" and args.steps > 1:
                 pass
     ctx.set_option(ep.OPT_FUSED_DIRECTION, 0)
