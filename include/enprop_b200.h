@@ -74,11 +74,18 @@ int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
  *   operator and read each lower entry from its transposed slot
  *   (enprop_problem_expand_values rebuilds the full [nnz][s] values).
  *   ENPROP_OPT_SPMV_PIPELINE (default 0): 1 = enprop_spmv loads the next batch's
- *   column indices one batch ahead (software pipelining). */
+ *   column indices one batch ahead (software pipelining).
+ *   ENPROP_OPT_L2_HINTS (default 0, process-wide): L2 priority of the CG SpMV
+ *   streams: 0 all evict_normal; 1 single-use streams (indices, transposed and
+ *   diagonal value slots, q) evict_first; 2 upper value slots evict_last.
+ *   ENPROP_OPT_SPMV_VARIANT (default 0, process-wide): CG SpMV schedule; bit 0
+ *   prefetches the next pass's index window, bit 1 gathers 8 entries per batch. */
 enum {
   ENPROP_OPT_FUSED_DIRECTION = 1,
   ENPROP_OPT_SPMV_PIPELINE = 2,
-  ENPROP_OPT_SYMMETRIC_STORAGE = 3
+  ENPROP_OPT_SYMMETRIC_STORAGE = 3,
+  ENPROP_OPT_L2_HINTS = 4,
+  ENPROP_OPT_SPMV_VARIANT = 5
 };
 int enprop_ctx_set_option(enprop_ctx* ctx, int option, int value);
 /* Event timing of the CG SpMV kernel launches on the context stream (used by

@@ -33,6 +33,8 @@ TILE_ROWS = 16
 OPT_FUSED_DIRECTION = 1
 OPT_SPMV_PIPELINE = 2
 OPT_SYMMETRIC_STORAGE = 3
+OPT_L2_HINTS = 4
+OPT_SPMV_VARIANT = 5
 WIDTHS = (1, 2, 4, 8, 16, 32)
 
 _dp = C.POINTER(C.c_double)

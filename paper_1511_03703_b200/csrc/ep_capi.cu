@@ -352,6 +352,12 @@ int enprop_ctx_set_option(enprop_ctx* c, int option, int value) {
     case ENPROP_OPT_SYMMETRIC_STORAGE:
       c->symmetric_storage = value ? 1 : 0;
       return ENPROP_OK;
+    case ENPROP_OPT_L2_HINTS:
+      set_l2_hints(value);
+      return ENPROP_OK;
+    case ENPROP_OPT_SPMV_VARIANT:
+      set_spmv_variant(value);
+      return ENPROP_OK;
 
     default:
       return fail(ENPROP_ERR_INVALID, "enprop_ctx_set_option: unknown option");

@@ -86,6 +86,54 @@ __device__ __forceinline__ int ld_stream_i32(const int* p) {
   return r;
 }
 
+// ---- L2 eviction-priority hints (createpolicy + .L2::cache_hint) ----------
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+template <int V>
+__device__ __forceinline__ VecD<V> ld_stream_hint(const double* p, uint64_t pol) {
+  VecD<V> r;
+  if constexpr (V == 1) {
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r.v[0]) : "l"(p), "l"(pol));
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; i += 2)
+      asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+          : "=d"(r.v[i]), "=d"(r.v[i + 1])
+          : "l"(p + i), "l"(pol));
+  }
+  return r;
+}
+__device__ __forceinline__ int ld_stream_i32_hint(const int* p, uint64_t pol) {
+  int r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+template <int V>
+__device__ __forceinline__ void st_vec_hint(double* p, const VecD<V>& a, uint64_t pol) {
+  if constexpr (V == 1) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(a.v[0]), "l"(pol) : "memory");
+  } else {
+#pragma unroll
+    for (int i = 0; i < V; i += 2)
+      asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p + i), "d"(a.v[i]),
+                   "d"(a.v[i + 1]), "l"(pol)
+                   : "memory");
+  }
+}
+
 // ---- mbarrier + 1D bulk copy (TMA engine, cp.async.bulk) -------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

@@ -254,7 +254,7 @@ struct TileShape {
 
 template <int S>
 __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hist,
-                         double* lanes_out);
+                         double* lanes_out);  // executed by all 32 lanes of one warp
 
 __device__ __forceinline__ int atomic_add_acq_rel_gpu(int* p, int v) {
   int old;
@@ -351,98 +351,107 @@ cudaError_t launch_dot_tiles(int s, const TileMap& tm, const double* u, const do
 // dot products are known.  Coupled solves keep their scalars replicated across
 // lanes; uncoupled solves run s independent copies of pcg_solve<double>.
 // =============================================================================
+// One warp runs the phase; lane e owns sample lane e (e < S). Scalars shared by
+// the lanes (it, done, status, coupled reductions) are formed by lane 0 after
+// warp votes, so per-lane work (sqrt, divisions) runs in parallel.
 template <int S>
 __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hist,
                          double* lanes_out) {
+  const int e = threadIdx.x & 31;
+  const bool mine = e < S;
   if (phase == kPhaseNone) {
-    double acc = 0.0;  // reduce_sum (ensemble.hpp:240-244)
-    for (int e = 0; e < S; ++e) {
-      lanes_out[e] = lanes[e];
-      acc = EP_DADD(acc, lanes[e]);
+    if (mine) lanes_out[e] = lanes[e];
+    if (e == 0) {
+      double acc = 0.0;  // reduce_sum (ensemble.hpp:240-244)
+      for (int k = 0; k < S; ++k) acc = EP_DADD(acc, lanes[k]);
+      lanes_out[S] = acc;
     }
-    lanes_out[S] = acc;
     return;
   }
   const double tol = cg->tol;
   const int maxit = cg->maxit;
+  const int it0 = cg->it;
   // Deferred x updates: RR records which lanes updated r (and so owe
   // x += alpha*p); the next direction pass pays them, so PQ clears the record.
-  if (phase == kPhaseRR) {
-    for (int e = 0; e < S; ++e) cg->pending[e] = cg->active[e];
-  } else {
-    for (int e = 0; e < S; ++e) cg->pending[e] = 0;
-  }
+  const int was_active = mine ? cg->active[e] : 0;
+  if (mine) cg->pending[e] = phase == kPhaseRR ? was_active : 0;
   if (cg->flavour == 0) {  // ---------------------------------------------- coupled
-    double d = 0.0;
-    for (int e = 0; e < S; ++e) d = EP_DADD(d, lanes[e]);
+    double d = 0.0;  // reduce_sum over lanes, left to right
+#pragma unroll 1
+    for (int k = 0; k < S; ++k) d = EP_DADD(d, lanes[k]);
     if (phase == kPhaseInit) {  // b_norm = norm2(b); r = b; p = z = r; rz = dot(r, z)
-      cg->it = 0;
       const double bn = sqrt(d);
-      cg->bnorm[0] = bn;
-      cg->status = 0;
-      cg->iters[0] = 0;
+      if (e == 0) {
+        cg->it = 0;
+        cg->bnorm[0] = bn;
+        cg->status = 0;
+        cg->iters[0] = 0;
+      }
       if (bn == 0.0) {  // pcg.hpp:62-66
-        hist[0] = 0.0;
-        cg->hist_len[0] = 1;
-        cg->done = 1;
+        if (e == 0) {
+          hist[0] = 0.0;
+          cg->hist_len[0] = 1;
+          cg->done = 1;
+        }
         return;
       }
-      for (int e = 0; e < S; ++e) cg->rz[e] = d;
+      if (mine) cg->rz[e] = d;
       const double rel = sqrt(d) / bn;
-      hist[0] = rel;
-      cg->hist_len[0] = 1;
-      if (rel < tol) {
-        cg->done = 1;
-      } else if (0 >= maxit) {
-        cg->status = 2;
-        cg->done = 1;
-      } else {
-        cg->done = 0;
+      int done = 0;
+      if (rel < tol) done = 1;
+      else if (0 >= maxit) done = 2;
+      if (e == 0) {
+        hist[0] = rel;
+        cg->hist_len[0] = 1;
+        if (done == 2) cg->status = 2;
+        cg->done = done ? 1 : 0;
       }
-      for (int e = 0; e < S; ++e) cg->active[e] = !cg->done;
+      if (mine) cg->active[e] = done ? 0 : 1;
     } else if (phase == kPhasePQ) {  // pq = dot(p, q); alpha = rz / pq
       if (d <= 0.0) {
-        cg->status = 3;
-        cg->iters[0] = cg->it;
-        cg->done = 1;
+        if (e == 0) {
+          cg->status = 3;
+          cg->iters[0] = it0;
+          cg->done = 1;
+        }
         return;
       }
       const double alpha = cg->rz[0] / d;
-      for (int e = 0; e < S; ++e) cg->alpha[e] = alpha;
+      if (mine) cg->alpha[e] = alpha;
     } else {  // kPhaseRR: rz_next = dot(r, z); beta; next relative residual
       const double beta = d / cg->rz[0];
-      for (int e = 0; e < S; ++e) {
+      const int it = it0 + 1;
+      const double rel = sqrt(d) / cg->bnorm[0];
+      __syncwarp();  // every lane has read rz[0] before it is replaced
+      if (mine) {
         cg->beta[e] = beta;
         cg->rz[e] = d;
       }
-      const int it = ++cg->it;
-      const double rel = sqrt(d) / cg->bnorm[0];
-      hist[it] = rel;
-      cg->hist_len[0] = it + 1;
-      if (rel < tol) {
-        cg->iters[0] = it;
-        cg->done = 1;
-      } else if (it >= maxit) {
-        cg->iters[0] = it;
-        cg->status = 2;
-        cg->done = 1;
+      if (e == 0) {
+        cg->it = it;
+        hist[it] = rel;
+        cg->hist_len[0] = it + 1;
+        if (rel < tol) {
+          cg->iters[0] = it;
+          cg->done = 1;
+        } else if (it >= maxit) {
+          cg->iters[0] = it;
+          cg->status = 2;
+          cg->done = 1;
+        }
       }
     }
     return;
   }
   // ------------------------------------------------------------------ uncoupled
+  int st = 0, act = 0;
   if (phase == kPhaseInit) {
-    cg->it = 0;
-    cg->status = 0;
-    int any = 0;
-    for (int e = 0; e < S; ++e) {
+    if (mine) {
       const double d = lanes[e];
       const double bn = sqrt(d);
       cg->bnorm[e] = bn;
       cg->iters[e] = 0;
-      cg->lane_status[e] = 0;
       cg->hist_len[e] = 1;
-      int act = 0;
       if (bn == 0.0) {
         hist[e] = 0.0;
       } else {
@@ -451,37 +460,43 @@ __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hi
         hist[e] = rel;
         if (rel < tol) {
         } else if (0 >= maxit) {
-          cg->lane_status[e] = 2;
+          st = 2;
         } else {
           act = 1;
         }
       }
+      cg->lane_status[e] = st;
       cg->active[e] = act;
-      any |= act;
-      if (cg->lane_status[e] > cg->status) cg->status = cg->lane_status[e];
     }
-    cg->done = !any;
+    const int any = __any_sync(0xffffffffu, act);
+    const int worst = __reduce_max_sync(0xffffffffu, st);
+    if (e == 0) {
+      cg->it = 0;
+      cg->status = worst;
+      cg->done = !any;
+    }
   } else if (phase == kPhasePQ) {
-    int any = 0;
-    for (int e = 0; e < S; ++e) {
-      if (!cg->active[e]) continue;
+    if (mine && was_active) {
       const double d = lanes[e];
       if (d <= 0.0) {
         cg->lane_status[e] = 3;
-        cg->iters[e] = cg->it;
+        cg->iters[e] = it0;
         cg->active[e] = 0;
-        if (3 > cg->status) cg->status = 3;
-        continue;
+        st = 3;
+      } else {
+        cg->alpha[e] = cg->rz[e] / d;
+        act = 1;
       }
-      cg->alpha[e] = cg->rz[e] / d;
-      any = 1;
     }
-    if (!any) cg->done = 1;
+    const int any = __any_sync(0xffffffffu, act);
+    const int worst = __reduce_max_sync(0xffffffffu, st);
+    if (e == 0) {
+      if (worst > cg->status) cg->status = worst;
+      if (!any) cg->done = 1;
+    }
   } else {
-    const int it = ++cg->it;
-    int any = 0;
-    for (int e = 0; e < S; ++e) {
-      if (!cg->active[e]) continue;
+    const int it = it0 + 1;
+    if (mine && was_active) {
       const double d = lanes[e];
       cg->beta[e] = d / cg->rz[e];
       cg->rz[e] = d;
@@ -495,29 +510,37 @@ __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hi
         cg->iters[e] = it;
         cg->lane_status[e] = 2;
         cg->active[e] = 0;
-        if (2 > cg->status) cg->status = 2;
+        st = 2;
       } else {
-        any = 1;
+        act = 1;
       }
     }
-    if (!any) cg->done = 1;
+    const int any = __any_sync(0xffffffffu, act);
+    const int worst = __reduce_max_sync(0xffffffffu, st);
+    if (e == 0) {
+      cg->it = it;
+      if (worst > cg->status) cg->status = worst;
+      if (!any) cg->done = 1;
+    }
   }
 }
 
 // Canonical finalize, one CTA per segment. Thread (block b, sample e) folds the
 // block's kBlockTiles tile partials in registers (v[i] += v[i+h], h = 8..1;
 // missing tiles are +0.0) -- a warp covers 32 consecutive samples, so every
-// load is one coalesced 256-byte row of partials -- and thread e then forms
-// the segment sum 0.0 + block_0 + block_1 + ... from shared memory. The last
-// CTA (acq_rel counter) forms 0.0 + seg_0 + seg_1 + ... and runs the CG phase.
-// With seg_only (multi-GPU) the per-segment sums are the output.
+// load is one coalesced row of partials, and a thread's FIN_ITEMS blocks are
+// loaded together -- and thread e then forms the segment sum
+// 0.0 + block_0 + block_1 + ... from shared memory. The last CTA (acq_rel
+// counter) forms 0.0 + seg_0 + seg_1 + ... and warp 0 runs the CG phase. With
+// seg_only (multi-GPU) the per-segment sums are the output.
 constexpr int kFinThreads = 256;
-constexpr int kFinChunk = 64;  // blocks (resp. segments) staged per pass
+constexpr int kFinItems = 2;  // (block, sample) items per thread per round
 
 template <int S>
 __global__ void __launch_bounds__(kFinThreads) k_fin_segments(const TileMap tm, const FinArgs f) {
   if ((f.phase == kPhasePQ || f.phase == kPhaseRR) && f.cg->done) return;
-  __shared__ double sblk[kFinChunk * S];
+  constexpr int CHUNK = kFinThreads * kFinItems / S;  // blocks (resp. segments) per round
+  __shared__ double sblk[CHUNK * S];
   __shared__ double lanes[S];
   __shared__ int s_final;
   const int seg = blockIdx.x;
@@ -525,20 +548,27 @@ __global__ void __launch_bounds__(kFinThreads) k_fin_segments(const TileMap tm, 
   const int nblk = (ntiles + kBlockTiles - 1) / kBlockTiles;
   const double* part = f.partials + (size_t)seg * tm.tiles_per_seg * S;
   double acc = 0.0;
-  for (int b0 = 0; b0 < nblk; b0 += kFinChunk) {
-    const int cnt = min(kFinChunk, nblk - b0);
-    for (int idx = threadIdx.x; idx < cnt * S; idx += kFinThreads) {
+  for (int b0 = 0; b0 < nblk; b0 += CHUNK) {
+    const int cnt = min(CHUNK, nblk - b0);
+    double v[kFinItems][kBlockTiles];
+#pragma unroll
+    for (int it = 0; it < kFinItems; ++it) {
+      const int idx = threadIdx.x + it * kFinThreads;
       const int b = idx / S, e = idx - b * S;
       const int t0 = (b0 + b) * kBlockTiles;
-      double v[kBlockTiles];
+      const bool ok = idx < cnt * S;
 #pragma unroll
       for (int i = 0; i < kBlockTiles; ++i)
-        v[i] = t0 + i < ntiles ? part[(size_t)(t0 + i) * S + e] : 0.0;
+        v[it][i] = ok && t0 + i < ntiles ? part[(size_t)(t0 + i) * S + e] : 0.0;
+    }
+#pragma unroll
+    for (int it = 0; it < kFinItems; ++it) {
 #pragma unroll
       for (int h = kBlockTiles / 2; h >= 1; h >>= 1)
 #pragma unroll
-        for (int i = 0; i < h; ++i) v[i] = EP_DADD(v[i], v[i + h]);
-      sblk[idx] = v[0];
+        for (int i = 0; i < h; ++i) v[it][i] = EP_DADD(v[it][i], v[it][i + h]);
+      const int idx = threadIdx.x + it * kFinThreads;
+      if (idx < cnt * S) sblk[idx] = v[it][0];
     }
     __syncthreads();
     if (threadIdx.x < S)
@@ -552,10 +582,19 @@ __global__ void __launch_bounds__(kFinThreads) k_fin_segments(const TileMap tm, 
   __syncthreads();
   if (!s_final) return;
   double tot = 0.0;
-  for (int k0 = 0; k0 < tm.num_segs; k0 += kFinChunk) {
-    const int cnt = min(kFinChunk, tm.num_segs - k0);
-    for (int idx = threadIdx.x; idx < cnt * S; idx += kFinThreads)
-      sblk[idx] = __ldcg(f.seg_sums + (size_t)k0 * S + idx);
+  for (int k0 = 0; k0 < tm.num_segs; k0 += CHUNK) {
+    const int cnt = min(CHUNK, tm.num_segs - k0);
+    double w[kFinItems];
+#pragma unroll
+    for (int it = 0; it < kFinItems; ++it) {
+      const int idx = threadIdx.x + it * kFinThreads;
+      w[it] = idx < cnt * S ? __ldcg(f.seg_sums + (size_t)k0 * S + idx) : 0.0;
+    }
+#pragma unroll
+    for (int it = 0; it < kFinItems; ++it) {
+      const int idx = threadIdx.x + it * kFinThreads;
+      if (idx < cnt * S) sblk[idx] = w[it];
+    }
     __syncthreads();
     if (threadIdx.x < S)
       for (int k = 0; k < cnt; ++k) tot = EP_DADD(tot, sblk[k * S + threadIdx.x]);
@@ -563,10 +602,8 @@ __global__ void __launch_bounds__(kFinThreads) k_fin_segments(const TileMap tm, 
   }
   if (threadIdx.x < S) lanes[threadIdx.x] = tot;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    *f.seg_done = 0;
-    cg_phase<S>(f.phase, lanes, f.cg, f.hist, f.lanes_out);
-  }
+  if (threadIdx.x == 0) *f.seg_done = 0;
+  if (threadIdx.x < 32) cg_phase<S>(f.phase, lanes, f.cg, f.hist, f.lanes_out);
 }
 
 template <int S>
@@ -606,7 +643,7 @@ __global__ void __launch_bounds__(256) k_fin_gathered(int planes, const double* 
   }
   if (threadIdx.x < S) lanes[threadIdx.x] = tot;
   __syncthreads();
-  if (threadIdx.x == 0) cg_phase<S>(phase, lanes, cg, hist, lanes_out);
+  if (threadIdx.x < 32) cg_phase<S>(phase, lanes, cg, hist, lanes_out);
 }
 
 template <int S>
@@ -704,10 +741,8 @@ __global__ void __launch_bounds__(32 * SerialShape<S>::LG) k_fin_serial(
   if (s_final) {
     if (threadIdx.x < S) lanes[threadIdx.x] = __ldcg(f.seg_sums + threadIdx.x);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      *f.seg_done = 0;
-      cg_phase<S>(f.phase, lanes, f.cg, f.hist, f.lanes_out);
-    }
+    if (threadIdx.x == 0) *f.seg_done = 0;
+    if (threadIdx.x < 32) cg_phase<S>(f.phase, lanes, f.cg, f.hist, f.lanes_out);
   }
 }
 
@@ -819,6 +854,11 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
 // W = TPR*E entries -- and broadcast them by shuffle, so each batch of U
 // gathers waits on one memory latency instead of two.
 // -----------------------------------------------------------------------------
+static int g_l2_hints = 0;      // ENPROP_OPT_L2_HINTS (process-wide; 0/1/2, see k_cg_spmv_warp)
+static int g_spmv_variant = 0;  // ENPROP_OPT_SPMV_VARIANT (process-wide; see SpmvVariant)
+void set_l2_hints(int v) { g_l2_hints = v; }
+void set_spmv_variant(int v) { g_spmv_variant = v & 3; }
+
 template <int S>
 struct WarpTile {
   static constexpr int V = SpmvShape<S>::V;
@@ -830,38 +870,78 @@ struct WarpTile {
   static constexpr int W = TPR * E;                                  // window (entries)
 };
 
+// Index window of one row: its CRS range and the first W column indices (and
+// symmetric slots), E per thread, loaded by the row's TPR threads together.
+template <int S>
+struct RowIdx {
+  static constexpr int E = WarpTile<S>::E > 0 ? WarpTile<S>::E : 1;
+  int rs, n;
+  int mc[E], mv[E];
+};
+
 template <int S, bool kSym>
-__device__ __forceinline__ VecD<SpmvShape<S>::V> row_product_coop(
-    int row, const int* __restrict__ row_map, const int* __restrict__ col_entry,
-    const double* __restrict__ values, const double* __restrict__ x, const int* __restrict__ vpos,
-    int sub) {
+__device__ __forceinline__ void row_index(int row, const int* __restrict__ row_map,
+                                          const int* __restrict__ col_entry,
+                                          const int* __restrict__ vpos, int sub, uint64_t pol,
+                                          RowIdx<S>& ix) {
   using Sh = WarpTile<S>;
-  constexpr int V = Sh::V, TPR = Sh::TPR, E = Sh::E, W = Sh::W, U = 4;
-  const int lane0 = sub * V;
-  int rs = 0, n = 0;
+  ix.rs = 0;
+  ix.n = 0;
   if (row >= 0) {
-    rs = __ldg(row_map + row);
-    n = __ldg(row_map + row + 1) - rs;
+    ix.rs = __ldg(row_map + row);
+    ix.n = __ldg(row_map + row + 1) - ix.rs;
   }
+  if constexpr (Sh::E > 0) {
+#pragma unroll
+    for (int i = 0; i < Sh::E; ++i) {
+      const int k = i * Sh::TPR + sub;
+      ix.mc[i] = k < ix.n ? ld_stream_i32_hint(col_entry + ix.rs + k, pol) : 0;
+      if constexpr (kSym) ix.mv[i] = k < ix.n ? ld_stream_i32_hint(vpos + ix.rs + k, pol) : 0;
+    }
+  }
+}
+
+// Row product from a loaded index window: batches of U entries, each batch's
+// value and vector gathers issued together (the indices come by shuffle), so a
+// batch waits on one memory latency. Every lane of the warp must call this
+// (warp-uniform trip counts via __reduce_max_sync).
+// L2 policy: all streams are read with an explicit cache policy -- the default
+// for ld.global.nc.L1::no_allocate let the upper slots fall out of L2 before
+// their transposed re-read (1.68 vs 1.29 GB DRAM per SpMV at 64^3, s = 32).
+template <int S, bool kSym, int U>
+__device__ __forceinline__ VecD<SpmvShape<S>::V> row_compute(
+    int row, const RowIdx<S>& ix, const int* __restrict__ row_map,
+    const int* __restrict__ col_entry, const double* __restrict__ values,
+    const double* __restrict__ x, const int* __restrict__ vpos, int sub, uint64_t pol_first,
+    uint64_t pol_keep) {
+  using Sh = WarpTile<S>;
+  constexpr int V = Sh::V, TPR = Sh::TPR, E = Sh::E, W = Sh::W;
+  const int lane0 = sub * V;
   VecD<V> sum;
 #pragma unroll
   for (int j = 0; j < V; ++j) sum.v[j] = 0.0;
   if constexpr (E == 0) {  // narrow rows (TPR < 4): plain per-thread loop
     if (row >= 0) {
       VecD<V> beta;
-      sum = row_product<S, V, U, false, false, kSym>(row, row_map, col_entry, values, x, nullptr,
+      sum = row_product<S, V, 4, false, false, kSym>(row, row_map, col_entry, values, x, nullptr,
                                                      true, beta, lane0, vpos);
     }
     return sum;
   } else {
+    const int rs = ix.rs, n = ix.n;
     const int nmax = __reduce_max_sync(0xffffffffu, n);
     for (int w0 = 0; w0 < nmax; w0 += W) {
       int mc[E], mv[E];
 #pragma unroll
       for (int i = 0; i < E; ++i) {
-        const int k = w0 + i * TPR + sub;
-        mc[i] = k < n ? ld_stream_i32(col_entry + rs + k) : 0;
-        if constexpr (kSym) mv[i] = k < n ? ld_stream_i32(vpos + rs + k) : 0;
+        if (w0 == 0) {
+          mc[i] = ix.mc[i];
+          mv[i] = ix.mv[i];
+        } else {  // rows longer than one window (general graphs)
+          const int k = w0 + i * TPR + sub;
+          mc[i] = k < n ? ld_stream_i32_hint(col_entry + rs + k, pol_first) : 0;
+          if constexpr (kSym) mv[i] = k < n ? ld_stream_i32_hint(vpos + rs + k, pol_first) : 0;
+        }
       }
 #pragma unroll
       for (int kb = 0; kb < W; kb += U) {
@@ -878,7 +958,8 @@ __device__ __forceinline__ VecD<SpmvShape<S>::V> row_product_coop(
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           if (w0 + kb + u < n) {
-            av[u] = ld_stream<V>(values + (size_t)vi[u] * S + lane0);
+            const uint64_t pol = (!kSym || c[u] <= row) ? pol_first : pol_keep;
+            av[u] = ld_stream_hint<V>(values + (size_t)vi[u] * S + lane0, pol);
             xv[u] = ld_vec<V>(x + (size_t)c[u] * S + lane0);
           }
         }
@@ -895,14 +976,29 @@ __device__ __forceinline__ VecD<SpmvShape<S>::V> row_product_coop(
   }
 }
 
-template <int S, bool kTiles, bool kSym>
-__global__ void __launch_bounds__(256, 4) k_cg_spmv_warp(
+// Variants (ENPROP_OPT_SPMV_VARIANT): bit 0 = load the next pass's index
+// window before computing this pass; bit 1 = batches of 8 entries (2 CTAs/SM)
+// instead of 4 (4 CTAs/SM).
+template <int kVar>
+struct SpmvVariant {
+  static constexpr bool kPrefetch = (kVar & 1) != 0;
+  static constexpr int U = (kVar & 2) ? 8 : 4;
+  static constexpr int kMinBlocks = (kVar & 2) ? 2 : 4;
+};
+
+template <int S, bool kTiles, bool kSym, int kVar>
+__global__ void __launch_bounds__(256, SpmvVariant<kVar>::kMinBlocks) k_cg_spmv_warp(
     const TileMap tm, const int* __restrict__ row_map, const int* __restrict__ col_entry,
     const double* __restrict__ values, const double* __restrict__ p_new, double* __restrict__ q,
-    const double* __restrict__ p_gather, const int* __restrict__ vpos, const FinArgs f) {
+    const double* __restrict__ p_gather, const int* __restrict__ vpos, const FinArgs f, int hints) {
   using Sh = WarpTile<S>;
+  using Var = SpmvVariant<kVar>;
   constexpr int V = Sh::V, TPR = Sh::TPR, R = Sh::R;
   if (f.cg->done) return;
+  // hints: 0 all evict_normal; 1 single-use evict_first; 2 upper slots evict_last
+  const uint64_t pol_norm = l2_policy_evict_normal();
+  const uint64_t pol_keep = hints == 2 ? l2_policy_evict_last() : pol_norm;
+  const uint64_t pol_first = hints == 1 ? l2_policy_evict_first() : pol_norm;
   const int lane = threadIdx.x & 31;
   const int g = lane / TPR, sub = lane % TPR;
   const int lane0 = sub * V;
@@ -922,16 +1018,30 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv_warp(
   // is applied as soon as pass ps + HALF is known (fewer live registers).
   constexpr int HALF = Sh::PASSES / 2;
   double prod[HALF > 0 ? HALF : 1][V];
+  RowIdx<S> ix;
+  if constexpr (Var::kPrefetch)
+    row_index<S, kSym>(g16 < nr ? r0 + g16 : -1, row_map, col_entry, vpos, sub, pol_first, ix);
 #pragma unroll
   for (int ps = 0; ps < Sh::PASSES; ++ps) {
     const int tr = ps * R + g16;
     const int row = tr < nr ? r0 + tr : -1;
-    const VecD<V> sum = row_product_coop<S, kSym>(row, row_map, col_entry, values, p_gather, vpos, sub);
+    RowIdx<S> rix;
+    if constexpr (Var::kPrefetch) {
+      rix = ix;
+      if (ps + 1 < Sh::PASSES) {
+        const int tn = tr + R;
+        row_index<S, kSym>(tn < nr ? r0 + tn : -1, row_map, col_entry, vpos, sub, pol_first, ix);
+      }
+    } else {
+      row_index<S, kSym>(row, row_map, col_entry, vpos, sub, pol_first, rix);
+    }
+    const VecD<V> sum = row_compute<S, kSym, Var::U>(row, rix, row_map, col_entry, values, p_gather,
+                                                     vpos, sub, pol_first, pol_keep);
     double cur[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) cur[j] = 0.0;
     if (row >= 0) {
-      st_vec<V>(q + (size_t)row * S + lane0, sum);
+      st_vec_hint<V>(q + (size_t)row * S + lane0, sum, pol_first);
       if constexpr (kTiles) {
         const VecD<V> pn = ld_vec<V>(p_new + (size_t)row * S + lane0);
 #pragma unroll
@@ -1092,16 +1202,24 @@ static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, bool run_direction, con
     const int units = tiles ? tm.num_tiles() : (tm.rows + kTileRows - 1) / kTileRows;
     const int warps = (units + Sw::TILES - 1) / Sw::TILES;
     const int wblocks = (warps + 7) / 8;
-#define EP_CG_SPMV_W(T, Y)                                                                    \
-  k_cg_spmv_warp<S, T, Y><<<wblocks, 256, 0, st>>>(tm, row_map, col_entry, values, p_new, q,  \
-                                                   p_gather, vpos, f)
+#define EP_CG_SPMV_W(T, Y, K)                                                                 \
+  k_cg_spmv_warp<S, T, Y, K><<<wblocks, 256, 0, st>>>(tm, row_map, col_entry, values, p_new, q, \
+                                                      p_gather, vpos, f, g_l2_hints)
+#define EP_CG_SPMV_WV(T, Y)                 \
+  switch (g_spmv_variant) {                 \
+    case 1: EP_CG_SPMV_W(T, Y, 1); break;   \
+    case 2: EP_CG_SPMV_W(T, Y, 2); break;   \
+    case 3: EP_CG_SPMV_W(T, Y, 3); break;   \
+    default: EP_CG_SPMV_W(T, Y, 0); break;  \
+  }
     if (vpos) {
-      if (tiles) EP_CG_SPMV_W(true, true);
-      else EP_CG_SPMV_W(false, true);
+      if (tiles) EP_CG_SPMV_WV(true, true)
+      else EP_CG_SPMV_WV(false, true)
     } else {
-      if (tiles) EP_CG_SPMV_W(true, false);
-      else EP_CG_SPMV_W(false, false);
+      if (tiles) EP_CG_SPMV_WV(true, false)
+      else EP_CG_SPMV_WV(false, false)
     }
+#undef EP_CG_SPMV_WV
 #undef EP_CG_SPMV_W
     return cudaGetLastError();
   }

@@ -27,10 +27,14 @@ def main():
     ap.add_argument("--spmv-only", action="store_true")
     ap.add_argument("--sym", type=int, default=1, help="symmetric storage for the CG problems")
     ap.add_argument("--modes", default="canonical,serial")
+    ap.add_argument("--l2-hints", type=int, default=0)
+    ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--fused", default="1,0", help="fused-direction settings to time")
     args = ap.parse_args()
     n, s = args.n, args.s
     ctx = ep.Context(0)
+    ctx.set_option(ep.OPT_L2_HINTS, args.l2_hints)
+    ctx.set_option(ep.OPT_SPMV_VARIANT, args.variant)
     O = Oracle()
     y = torch.as_tensor(pack_group(O.draw_samples(0, s, 3), s)).cuda()
     ctx.set_option(ep.OPT_SYMMETRIC_STORAGE, 0)
