@@ -95,17 +95,34 @@ def spmv_bytes(nnz, rows, s):
     return nnz * (8 * s + 4) + 4 * (rows + 1) + 16 * s * rows
 
 
-def cg_iter_bytes(nnz, rows, s):
-    """Algorithmic bytes of one CG iteration in this schedule:
-    direction 5 vector passes, SpMV values/cols/row_map + 2 passes, update 3."""
-    return nnz * (8 * s + 4) + 4 * (rows + 1) + 10 * 8 * s * rows
+def cg_spmv_bytes(nnz, nnz_stored, rows, s):
+    """Algorithmic bytes of one CG SpMV launch (k_cg_spmv_warp):
+    the stored value slots once (symmetric storage: diagonal + upper), column
+    indices, the slot map (symmetric storage only), row_map, the direction
+    vector gathered once and q written once. The transposed re-reads of the
+    upper slots are not algorithmic bytes."""
+    sym = nnz_stored < nnz
+    return nnz_stored * 8 * s + nnz * (8 if sym else 4) + 4 * (rows + 1) + 16 * s * rows
 
 
-def cg_spmv_bytes(nnz, rows, s):
-    """Algorithmic bytes of the CG SpMV phase, split-direction
-    schedule: direction pass (read r, p_old, x; write p_new, x) + SpMV (values,
-    cols, row_map, p_new gathered once, q written once)."""
-    return 5 * 8 * s * rows + nnz * (8 * s + 4) + 4 * (rows + 1) + 16 * s * rows
+def direction_bytes(rows, s):
+    """k_cg_direction: read r, p_old, x; write p_new, x."""
+    return 5 * 8 * s * rows
+
+
+def measured_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full capture (profiles/*/traffic.json), else None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "traffic.json")), reverse=True):
+        try:
+            with open(path) as fh:
+                d = json.load(fh)
+            if kernel in d:
+                return d[kernel]
+        except (OSError, ValueError):
+            pass
+    return None
 
 
 # --------------------------------------------------------------------------- ours
@@ -248,18 +265,27 @@ def run_ours(args):
     w0.prob.solve(cfg)
     det = w0.ctx.profile_detail()
     spmv_ms, spmv_n = w0.ctx.profile(0)
-    nnz, rows = w0.prob.nnz, w0.prob.rows
+    nnz, nnz_st, rows = w0.prob.nnz, w0.prob.nnz_stored, w0.prob.rows
     avg_spmv_ms = spmv_ms / max(spmv_n, 1)
-    achieved = cg_spmv_bytes(nnz, rows, S) / (avg_spmv_ms / 1e3) / 1e9
-    it_ms = det["iteration"] / max(det["iterations"], 1)
-    roofline = {"bound": "hbm", "kernel": "k_cg_direction<32> + k_cg_spmv<32,true,false>",
+    nit = max(det["iterations"], 1)
+    byt = cg_spmv_bytes(nnz, nnz_st, rows, S)
+    achieved = byt / (avg_spmv_ms / 1e3) / 1e9
+    it_ms = det["iteration"] / nit
+    kname = "k_cg_spmv_warp<32,true,%s>" % ("true" if nnz_st < nnz else "false")
+    dir_ms = det["direction"] / nit
+    it_bytes = byt + direction_bytes(rows, S) + 3 * 8 * S * rows  # + update (r, q -> r)
+    roofline = {"bound": "hbm", "kernel": kname,
                 "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": None,
-                "bytes_per_launch": cg_spmv_bytes(nnz, rows, S), "avg_launch_ms": round(avg_spmv_ms, 4),
+                "frac": round(achieved / hbm, 4), "traffic": measured_traffic(kname),
+                "bytes_per_launch": byt, "avg_launch_ms": round(avg_spmv_ms, 4),
                 "launches_timed": spmv_n,
                 "share_of_iteration": round(avg_spmv_ms / it_ms, 3) if it_ms else None,
-                "iteration_bytes": cg_iter_bytes(nnz, rows, S),
-                "iteration_gbs": round(cg_iter_bytes(nnz, rows, S) / (it_ms / 1e3) / 1e9, 1) if it_ms else None,
+                "per_iteration_ms": {k: round(det[k] / nit, 4) for k in
+                                     ("direction", "spmv_kernel", "fin_pq", "update", "fin_rr", "iteration")},
+                "direction": {"kernel": "k_cg_direction<32>", "bytes": direction_bytes(rows, S),
+                              "achieved": round(direction_bytes(rows, S) / (dir_ms / 1e3) / 1e9, 1) if dir_ms else None},
+                "iteration_bytes": it_bytes,
+                "iteration_gbs": round(it_bytes / (it_ms / 1e3) / 1e9, 1) if it_ms else None,
                 "timing": "CUDA events on the solve's stream, single-stream solve"}
 
     extra = {}

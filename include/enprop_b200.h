@@ -75,16 +75,14 @@ int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
  *   (enprop_problem_expand_values rebuilds the full [nnz][s] values).
  *   ENPROP_OPT_SPMV_PIPELINE (default 0): 1 = enprop_spmv loads the next batch's
  *   column indices one batch ahead (software pipelining).
- *   ENPROP_OPT_L2_HINTS (default 0, process-wide): L2 priority of the CG SpMV
- *   streams: 0 all evict_normal; 1 single-use streams (indices, transposed and
- *   diagonal value slots, q) evict_first; 2 upper value slots evict_last.
- *   ENPROP_OPT_SPMV_VARIANT (default 0, process-wide): CG SpMV schedule; bit 0
- *   prefetches the next pass's index window, bit 1 gathers 8 entries per batch. */
+ *   ENPROP_OPT_SPMV_VARIANT (default -1 = auto, process-wide): CG SpMV schedule
+ *   (entries per gather batch / CTAs per SM): 0: 4/4, 1: 4/4 + index prefetch,
+ *   2: 8/2, 3: 8/2 + index prefetch, 4: 4/4 zero-padded, 5: 8/3, 6: 16/1;
+ *   auto = 2 with symmetric storage, 0 otherwise. */
 enum {
   ENPROP_OPT_FUSED_DIRECTION = 1,
   ENPROP_OPT_SPMV_PIPELINE = 2,
   ENPROP_OPT_SYMMETRIC_STORAGE = 3,
-  ENPROP_OPT_L2_HINTS = 4,
   ENPROP_OPT_SPMV_VARIANT = 5
 };
 int enprop_ctx_set_option(enprop_ctx* ctx, int option, int value);
@@ -92,11 +90,12 @@ int enprop_ctx_set_option(enprop_ctx* ctx, int option, int value);
  * bench.py for the roofline). Returns the totals accumulated since the last
  * reset; enable = 1/0 turns timing on/off and resets, enable = -1 only reads. */
 int enprop_ctx_profile(enprop_ctx* ctx, int enable, double* spmv_ms, int64_t* spmv_launches);
-/* Per-phase totals of the profiled CG iterations, ms[9]: [0] SpMV phase
+/* Per-phase totals of the profiled CG iterations, ms[11]: [0] SpMV phase
  * (direction + SpMV), [1] PQ finalize, [2] update, [3] RR finalize, [4] whole
  * working iterations; per profiled solve: [5] whole solve on the GPU, [6] setup
  * and initial residual, [7] iteration loop (incl. early-exit iterations),
- * [8] iterations enqueued past convergence (early-exit). */
+ * [8] iterations enqueued past convergence (early-exit); per iteration again:
+ * [9] direction pass, [10] SpMV kernel. */
 int enprop_ctx_profile_detail(enprop_ctx* ctx, double* ms, int64_t* iterations);
 
 int enprop_malloc(enprop_ctx* ctx, size_t bytes, void** dptr);

@@ -33,7 +33,6 @@ TILE_ROWS = 16
 OPT_FUSED_DIRECTION = 1
 OPT_SPMV_PIPELINE = 2
 OPT_SYMMETRIC_STORAGE = 3
-OPT_L2_HINTS = 4
 OPT_SPMV_VARIANT = 5
 WIDTHS = (1, 2, 4, 8, 16, 32)
 
@@ -251,11 +250,12 @@ class Context:
 
     def profile_detail(self):
         """Per-phase CG totals since the last profile(1): dict of ms and count."""
-        ms = (C.c_double * 9)()
+        ms = (C.c_double * 11)()
         n = C.c_int64()
         _check(lib().enprop_ctx_profile_detail(self.h, ms, C.byref(n)))
         return dict(spmv=ms[0], fin_pq=ms[1], update=ms[2], fin_rr=ms[3], iteration=ms[4],
-                    solve=ms[5], init=ms[6], loop=ms[7], early_exit=ms[8], iterations=n.value)
+                    solve=ms[5], init=ms[6], loop=ms[7], early_exit=ms[8], direction=ms[9],
+                    spmv_kernel=ms[10], iterations=n.value)
 
     def close(self):
         if getattr(self, "h", None):

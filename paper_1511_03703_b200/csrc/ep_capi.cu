@@ -109,35 +109,43 @@ int validate_cg_options(const enprop_cg_options* opt, int s) {
   return ENPROP_OK;
 }
 
-// Five events per profiled iteration (grown on demand, reused across solves):
-// before the SpMV phase, after it, after the PQ finalize, after the update,
-// after the RR finalize (the finalizes are separate launches in serial order).
+// Six events per profiled iteration (grown on demand, reused across solves):
+// before the direction pass, before the SpMV, after it, after the PQ finalize,
+// after the update, after the RR finalize.
+constexpr int kProfEv = 6;
 cudaEvent_t* prof_slot(enprop_ctx* c) {
-  if (c->prof_used + 5 > c->prof_ev.size()) {
-    for (int k = 0; k < 160; ++k) {
+  if (c->prof_used + kProfEv > c->prof_ev.size()) {
+    for (int k = 0; k < 32 * kProfEv; ++k) {
       cudaEvent_t e;
       if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
       c->prof_ev.push_back(e);
     }
   }
   cudaEvent_t* p = &c->prof_ev[c->prof_used];
-  c->prof_used += 5;
+  c->prof_used += kProfEv;
   return p;
 }
 
 // Accumulate the recorded iterations: the first `working` did work; the rest
 // were enqueued past convergence and early-exited (their time goes to [8]).
 int prof_collect(enprop_ctx* c, int working) {
-  for (size_t i = 0; i + 5 <= c->prof_used; i += 5) {
-    float t[4];
-    for (int k = 0; k < 4; ++k) EP_CUDA(cudaEventElapsedTime(&t[k], c->prof_ev[i + k], c->prof_ev[i + k + 1]));
-    if ((int)(i / 5) < working) {
-      c->prof_ms += t[0];
+  for (size_t i = 0; i + kProfEv <= c->prof_used; i += kProfEv) {
+    float t[kProfEv - 1];
+    for (int k = 0; k + 1 < kProfEv; ++k)
+      EP_CUDA(cudaEventElapsedTime(&t[k], c->prof_ev[i + k], c->prof_ev[i + k + 1]));
+    const float all = t[0] + t[1] + t[2] + t[3] + t[4];
+    if ((int)(i / kProfEv) < working) {
+      c->prof_ms += t[1];
       c->prof_count += 1;
-      for (int k = 0; k < 4; ++k) c->prof_detail[k] += t[k];
-      c->prof_detail[4] += t[0] + t[1] + t[2] + t[3];
+      c->prof_detail[0] += t[0] + t[1];
+      c->prof_detail[1] += t[2];
+      c->prof_detail[2] += t[3];
+      c->prof_detail[3] += t[4];
+      c->prof_detail[4] += all;
+      c->prof_detail[9] += t[0];
+      c->prof_detail[10] += t[1];
     } else {
-      c->prof_detail[8] += t[0] + t[1] + t[2] + t[3];
+      c->prof_detail[8] += all;
     }
   }
   c->prof_used = 0;
@@ -206,17 +214,19 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
         double* p_new = w.p[(launched + 1) & 1];
         cudaEvent_t* ev = ctx->profile ? prof_slot(ctx) : nullptr;
         if (ev) EP_CUDA(cudaEventRecord(ev[0], st));
-        EP_CUDA(launch_cg_spmv(s, canon, fused, !fused, tm, row_map, col_entry, values, w.r, p_old,
-                               p_new, w.q, x, p_new, vpos, f_pq, st));
+        if (!fused) EP_CUDA(launch_cg_direction(s, rows, w.r, p_old, p_new, x, w.state, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[1], st));
+        EP_CUDA(launch_cg_spmv(s, canon, fused, false, tm, row_map, col_entry, values, w.r, p_old,
+                               p_new, w.q, x, p_new, vpos, f_pq, st));
+        if (ev) EP_CUDA(cudaEventRecord(ev[2], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, f_pq, st));
         if (fin_kernel) EP_CUDA(launch_fin_segments(s, tm, f_pq, st));
-        if (ev) EP_CUDA(cudaEventRecord(ev[2], st));
-        EP_CUDA(launch_cg_update(s, canon, tm, w.r, w.q, f_rr, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[3], st));
+        EP_CUDA(launch_cg_update(s, canon, tm, w.r, w.q, f_rr, st));
+        if (ev) EP_CUDA(cudaEventRecord(ev[4], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, f_rr, st));
         if (fin_kernel) EP_CUDA(launch_fin_segments(s, tm, f_rr, st));
-        if (ev) EP_CUDA(cudaEventRecord(ev[4], st));
+        if (ev) EP_CUDA(cudaEventRecord(ev[5], st));
         ctx->launches += (canon ? 2 : 4) + (fused ? 0 : 1) + (fin_kernel ? 2 : 0);
       }
     }
@@ -352,9 +362,6 @@ int enprop_ctx_set_option(enprop_ctx* c, int option, int value) {
     case ENPROP_OPT_SYMMETRIC_STORAGE:
       c->symmetric_storage = value ? 1 : 0;
       return ENPROP_OK;
-    case ENPROP_OPT_L2_HINTS:
-      set_l2_hints(value);
-      return ENPROP_OK;
     case ENPROP_OPT_SPMV_VARIANT:
       set_spmv_variant(value);
       return ENPROP_OK;
@@ -379,7 +386,7 @@ int enprop_ctx_profile(enprop_ctx* c, int enable, double* spmv_ms, int64_t* spmv
 
 int enprop_ctx_profile_detail(enprop_ctx* c, double* ms, int64_t* iterations) {
   if (!c || !ms) return fail(ENPROP_ERR_INVALID, "enprop_ctx_profile_detail: null argument");
-  for (int k = 0; k < 9; ++k) ms[k] = c->prof_detail[k];
+  for (int k = 0; k < 11; ++k) ms[k] = c->prof_detail[k];
   if (iterations) *iterations = c->prof_count;
   return ENPROP_OK;
 }

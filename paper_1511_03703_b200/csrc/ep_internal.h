@@ -28,10 +28,11 @@ struct enprop_ctx {
   int profile = 0;
   std::vector<cudaEvent_t> prof_ev;  // 5 events per profiled iteration, reused
   size_t prof_used = 0;
-  double prof_ms = 0.0;       // CG SpMV phase (direction + SpMV)
+  double prof_ms = 0.0;       // CG SpMV kernel (without the direction pass)
   int64_t prof_count = 0;     // profiled iterations that did work
-  // spmv, fin pq, update, fin rr, iteration, solve, init, loop, early-exit (enprop_b200.h)
-  double prof_detail[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  // spmv phase, fin pq, update, fin rr, iteration, solve, init, loop, early-exit,
+  // direction, spmv kernel (enprop_b200.h)
+  double prof_detail[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   cudaEvent_t prof_solve_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 

@@ -534,13 +534,16 @@ __device__ void cg_phase(int phase, const double* lanes, CgState* cg, double* hi
 // counter) forms 0.0 + seg_0 + seg_1 + ... and warp 0 runs the CG phase. With
 // seg_only (multi-GPU) the per-segment sums are the output.
 constexpr int kFinThreads = 256;
-constexpr int kFinItems = 2;  // (block, sample) items per thread per round
+constexpr int kFinItems = 3;   // (block, sample) items per thread per round
+constexpr int kFinItems2 = 12;  // (segment, sample) items per thread per round (total)
 
 template <int S>
 __global__ void __launch_bounds__(kFinThreads) k_fin_segments(const TileMap tm, const FinArgs f) {
   if ((f.phase == kPhasePQ || f.phase == kPhaseRR) && f.cg->done) return;
-  constexpr int CHUNK = kFinThreads * kFinItems / S;  // blocks (resp. segments) per round
+  constexpr int CHUNK = kFinThreads * kFinItems / S;    // blocks per round
+  constexpr int CHUNK2 = kFinThreads * kFinItems2 / S;  // segments per round
   __shared__ double sblk[CHUNK * S];
+  __shared__ double stot[CHUNK2 * S];
   __shared__ double lanes[S];
   __shared__ int s_final;
   const int seg = blockIdx.x;
@@ -571,8 +574,10 @@ __global__ void __launch_bounds__(kFinThreads) k_fin_segments(const TileMap tm, 
       if (idx < cnt * S) sblk[idx] = v[it][0];
     }
     __syncthreads();
-    if (threadIdx.x < S)
+    if (threadIdx.x < S) {
+#pragma unroll 8
       for (int b = 0; b < cnt; ++b) acc = EP_DADD(acc, sblk[b * S + threadIdx.x]);
+    }
     __syncthreads();
   }
   if (threadIdx.x < S) f.seg_sums[(size_t)seg * S + threadIdx.x] = acc;
@@ -582,22 +587,24 @@ __global__ void __launch_bounds__(kFinThreads) k_fin_segments(const TileMap tm, 
   __syncthreads();
   if (!s_final) return;
   double tot = 0.0;
-  for (int k0 = 0; k0 < tm.num_segs; k0 += CHUNK) {
-    const int cnt = min(CHUNK, tm.num_segs - k0);
-    double w[kFinItems];
+  for (int k0 = 0; k0 < tm.num_segs; k0 += CHUNK2) {
+    const int cnt = min(CHUNK2, tm.num_segs - k0);
+    double w[kFinItems2];
 #pragma unroll
-    for (int it = 0; it < kFinItems; ++it) {
+    for (int it = 0; it < kFinItems2; ++it) {
       const int idx = threadIdx.x + it * kFinThreads;
       w[it] = idx < cnt * S ? __ldcg(f.seg_sums + (size_t)k0 * S + idx) : 0.0;
     }
 #pragma unroll
-    for (int it = 0; it < kFinItems; ++it) {
+    for (int it = 0; it < kFinItems2; ++it) {
       const int idx = threadIdx.x + it * kFinThreads;
-      if (idx < cnt * S) sblk[idx] = w[it];
+      if (idx < cnt * S) stot[idx] = w[it];
     }
     __syncthreads();
-    if (threadIdx.x < S)
-      for (int k = 0; k < cnt; ++k) tot = EP_DADD(tot, sblk[k * S + threadIdx.x]);
+    if (threadIdx.x < S) {
+#pragma unroll 8
+      for (int k = 0; k < cnt; ++k) tot = EP_DADD(tot, stot[k * S + threadIdx.x]);
+    }
     __syncthreads();
   }
   if (threadIdx.x < S) lanes[threadIdx.x] = tot;
@@ -854,10 +861,8 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
 // W = TPR*E entries -- and broadcast them by shuffle, so each batch of U
 // gathers waits on one memory latency instead of two.
 // -----------------------------------------------------------------------------
-static int g_l2_hints = 0;      // ENPROP_OPT_L2_HINTS (process-wide; 0/1/2, see k_cg_spmv_warp)
-static int g_spmv_variant = 0;  // ENPROP_OPT_SPMV_VARIANT (process-wide; see SpmvVariant)
-void set_l2_hints(int v) { g_l2_hints = v; }
-void set_spmv_variant(int v) { g_spmv_variant = v & 3; }
+static int g_spmv_variant = -1;  // ENPROP_OPT_SPMV_VARIANT (process-wide; -1 auto, see SpmvVariant)
+void set_spmv_variant(int v) { g_spmv_variant = (v >= 0 && v <= 6) ? v : -1; }
 
 template <int S>
 struct WarpTile {
@@ -908,12 +913,11 @@ __device__ __forceinline__ void row_index(int row, const int* __restrict__ row_m
 // L2 policy: all streams are read with an explicit cache policy -- the default
 // for ld.global.nc.L1::no_allocate let the upper slots fall out of L2 before
 // their transposed re-read (1.68 vs 1.29 GB DRAM per SpMV at 64^3, s = 32).
-template <int S, bool kSym, int U>
+template <int S, bool kSym, int U, bool kPadZero>
 __device__ __forceinline__ VecD<SpmvShape<S>::V> row_compute(
     int row, const RowIdx<S>& ix, const int* __restrict__ row_map,
     const int* __restrict__ col_entry, const double* __restrict__ values,
-    const double* __restrict__ x, const int* __restrict__ vpos, int sub, uint64_t pol_first,
-    uint64_t pol_keep) {
+    const double* __restrict__ x, const int* __restrict__ vpos, int sub, uint64_t pol) {
   using Sh = WarpTile<S>;
   constexpr int V = Sh::V, TPR = Sh::TPR, E = Sh::E, W = Sh::W;
   const int lane0 = sub * V;
@@ -930,6 +934,7 @@ __device__ __forceinline__ VecD<SpmvShape<S>::V> row_compute(
   } else {
     const int rs = ix.rs, n = ix.n;
     const int nmax = __reduce_max_sync(0xffffffffu, n);
+    const int gbase = (threadIdx.x & 31) - sub;  // first lane of this row's group
     for (int w0 = 0; w0 < nmax; w0 += W) {
       int mc[E], mv[E];
 #pragma unroll
@@ -939,8 +944,8 @@ __device__ __forceinline__ VecD<SpmvShape<S>::V> row_compute(
           mv[i] = ix.mv[i];
         } else {  // rows longer than one window (general graphs)
           const int k = w0 + i * TPR + sub;
-          mc[i] = k < n ? ld_stream_i32_hint(col_entry + rs + k, pol_first) : 0;
-          if constexpr (kSym) mv[i] = k < n ? ld_stream_i32_hint(vpos + rs + k, pol_first) : 0;
+          mc[i] = k < n ? ld_stream_i32_hint(col_entry + rs + k, pol) : 0;
+          if constexpr (kSym) mv[i] = k < n ? ld_stream_i32_hint(vpos + rs + k, pol) : 0;
         }
       }
 #pragma unroll
@@ -950,22 +955,25 @@ __device__ __forceinline__ VecD<SpmvShape<S>::V> row_compute(
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int idx = kb + u;  // compile-time: register selects are static
-          c[u] = __shfl_sync(0xffffffffu, mc[idx / TPR], idx % TPR, TPR);
-          if constexpr (kSym) vi[u] = __shfl_sync(0xffffffffu, mv[idx / TPR], idx % TPR, TPR);
+          c[u] = __shfl_sync(0xffffffffu, mc[idx / TPR], gbase + idx % TPR);
+          if constexpr (kSym) vi[u] = __shfl_sync(0xffffffffu, mv[idx / TPR], gbase + idx % TPR);
           else vi[u] = rs + w0 + idx;
         }
         VecD<V> av[U], xv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+          if constexpr (kPadZero) {
+#pragma unroll
+            for (int j = 0; j < V; ++j) av[u].v[j] = xv[u].v[j] = 0.0;
+          }
           if (w0 + kb + u < n) {
-            const uint64_t pol = (!kSym || c[u] <= row) ? pol_first : pol_keep;
             av[u] = ld_stream_hint<V>(values + (size_t)vi[u] * S + lane0, pol);
             xv[u] = ld_vec<V>(x + (size_t)c[u] * S + lane0);
           }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          if (w0 + kb + u < n) {
+          if (kPadZero || w0 + kb + u < n) {
 #pragma unroll
             for (int j = 0; j < V; ++j) sum.v[j] = EP_DADD(sum.v[j], EP_DMUL(av[u].v[j], xv[u].v[j]));
           }
@@ -976,29 +984,30 @@ __device__ __forceinline__ VecD<SpmvShape<S>::V> row_compute(
   }
 }
 
-// Variants (ENPROP_OPT_SPMV_VARIANT): bit 0 = load the next pass's index
-// window before computing this pass; bit 1 = batches of 8 entries (2 CTAs/SM)
-// instead of 4 (4 CTAs/SM).
+// Variants (ENPROP_OPT_SPMV_VARIANT), batch U entries / min CTAs per SM:
+// 0: 4/4; 1: 4/4 + next pass's index window loaded before this pass; 2: 8/2;
+// 3: 8/2 + index prefetch; 4: 4/4 with entries past the row end entering the
+// sum as +0.0 * +0.0 instead of predicated off (bitwise identical: the running
+// sum starts at +0.0, so it is never -0.0 and sum + 0.0 == sum); 5: 8/3;
+// 6: 16/1.
 template <int kVar>
 struct SpmvVariant {
-  static constexpr bool kPrefetch = (kVar & 1) != 0;
-  static constexpr int U = (kVar & 2) ? 8 : 4;
-  static constexpr int kMinBlocks = (kVar & 2) ? 2 : 4;
+  static constexpr bool kPrefetch = kVar == 1 || kVar == 3;
+  static constexpr bool kPadZero = kVar == 4;
+  static constexpr int U = (kVar == 2 || kVar == 3 || kVar == 5) ? 8 : (kVar == 6 ? 16 : 4);
+  static constexpr int kMinBlocks = kVar == 5 ? 3 : (kVar == 6 ? 1 : ((kVar & 2) ? 2 : 4));
 };
 
 template <int S, bool kTiles, bool kSym, int kVar>
 __global__ void __launch_bounds__(256, SpmvVariant<kVar>::kMinBlocks) k_cg_spmv_warp(
     const TileMap tm, const int* __restrict__ row_map, const int* __restrict__ col_entry,
     const double* __restrict__ values, const double* __restrict__ p_new, double* __restrict__ q,
-    const double* __restrict__ p_gather, const int* __restrict__ vpos, const FinArgs f, int hints) {
+    const double* __restrict__ p_gather, const int* __restrict__ vpos, const FinArgs f) {
   using Sh = WarpTile<S>;
   using Var = SpmvVariant<kVar>;
   constexpr int V = Sh::V, TPR = Sh::TPR, R = Sh::R;
   if (f.cg->done) return;
-  // hints: 0 all evict_normal; 1 single-use evict_first; 2 upper slots evict_last
-  const uint64_t pol_norm = l2_policy_evict_normal();
-  const uint64_t pol_keep = hints == 2 ? l2_policy_evict_last() : pol_norm;
-  const uint64_t pol_first = hints == 1 ? l2_policy_evict_first() : pol_norm;
+  const uint64_t pol = l2_policy_evict_normal();
   const int lane = threadIdx.x & 31;
   const int g = lane / TPR, sub = lane % TPR;
   const int lane0 = sub * V;
@@ -1020,7 +1029,7 @@ __global__ void __launch_bounds__(256, SpmvVariant<kVar>::kMinBlocks) k_cg_spmv_
   double prod[HALF > 0 ? HALF : 1][V];
   RowIdx<S> ix;
   if constexpr (Var::kPrefetch)
-    row_index<S, kSym>(g16 < nr ? r0 + g16 : -1, row_map, col_entry, vpos, sub, pol_first, ix);
+    row_index<S, kSym>(g16 < nr ? r0 + g16 : -1, row_map, col_entry, vpos, sub, pol, ix);
 #pragma unroll
   for (int ps = 0; ps < Sh::PASSES; ++ps) {
     const int tr = ps * R + g16;
@@ -1030,18 +1039,18 @@ __global__ void __launch_bounds__(256, SpmvVariant<kVar>::kMinBlocks) k_cg_spmv_
       rix = ix;
       if (ps + 1 < Sh::PASSES) {
         const int tn = tr + R;
-        row_index<S, kSym>(tn < nr ? r0 + tn : -1, row_map, col_entry, vpos, sub, pol_first, ix);
+        row_index<S, kSym>(tn < nr ? r0 + tn : -1, row_map, col_entry, vpos, sub, pol, ix);
       }
     } else {
-      row_index<S, kSym>(row, row_map, col_entry, vpos, sub, pol_first, rix);
+      row_index<S, kSym>(row, row_map, col_entry, vpos, sub, pol, rix);
     }
-    const VecD<V> sum = row_compute<S, kSym, Var::U>(row, rix, row_map, col_entry, values, p_gather,
-                                                     vpos, sub, pol_first, pol_keep);
+    const VecD<V> sum = row_compute<S, kSym, Var::U, Var::kPadZero>(row, rix, row_map, col_entry, values, p_gather,
+                                                     vpos, sub, pol);
     double cur[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) cur[j] = 0.0;
     if (row >= 0) {
-      st_vec_hint<V>(q + (size_t)row * S + lane0, sum, pol_first);
+      st_vec<V>(q + (size_t)row * S + lane0, sum);
       if constexpr (kTiles) {
         const VecD<V> pn = ld_vec<V>(p_new + (size_t)row * S + lane0);
 #pragma unroll
@@ -1204,12 +1213,19 @@ static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, bool run_direction, con
     const int wblocks = (warps + 7) / 8;
 #define EP_CG_SPMV_W(T, Y, K)                                                                 \
   k_cg_spmv_warp<S, T, Y, K><<<wblocks, 256, 0, st>>>(tm, row_map, col_entry, values, p_new, q, \
-                                                      p_gather, vpos, f, g_l2_hints)
+                                                      p_gather, vpos, f)
+    // auto: 8-entry batches at 2 CTAs/SM for symmetric storage, 4 at 4 CTAs/SM
+    // for full storage (same-process A/B at 64^3, s = 32: 0.301 vs 0.332 ms and
+    // 0.366 vs 0.391 ms; tools/kernel_bench.py --ab)
+    const int var = g_spmv_variant >= 0 ? g_spmv_variant : (vpos ? 2 : 0);
 #define EP_CG_SPMV_WV(T, Y)                 \
-  switch (g_spmv_variant) {                 \
+  switch (var) {                            \
     case 1: EP_CG_SPMV_W(T, Y, 1); break;   \
     case 2: EP_CG_SPMV_W(T, Y, 2); break;   \
     case 3: EP_CG_SPMV_W(T, Y, 3); break;   \
+    case 4: EP_CG_SPMV_W(T, Y, 4); break;   \
+    case 5: EP_CG_SPMV_W(T, Y, 5); break;   \
+    case 6: EP_CG_SPMV_W(T, Y, 6); break;   \
     default: EP_CG_SPMV_W(T, Y, 0); break;  \
   }
     if (vpos) {

@@ -113,7 +113,6 @@ cudaError_t launch_cg_direction(int s, int rows, const double* r, const double* 
 // p_gather: base of the gathered p (the rank's ghost-extended layout; == p_new on
 // one GPU). run_direction (split schedule): launch the direction pass first;
 // false when the caller already ran it (multi-GPU: with the halo in between).
-void set_l2_hints(int v);       // ENPROP_OPT_L2_HINTS
 void set_spmv_variant(int v);   // ENPROP_OPT_SPMV_VARIANT
 cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, bool run_direction,
                            const TileMap& tm, const int* row_map, const int* col_entry,

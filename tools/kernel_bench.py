@@ -27,13 +27,13 @@ def main():
     ap.add_argument("--spmv-only", action="store_true")
     ap.add_argument("--sym", type=int, default=1, help="symmetric storage for the CG problems")
     ap.add_argument("--modes", default="canonical,serial")
-    ap.add_argument("--l2-hints", type=int, default=0)
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--ab", default="", help="comma list of SpMV variants timed alternately (CG SpMV kernel only)")
+    ap.add_argument("--ab-rounds", type=int, default=5)
     ap.add_argument("--fused", default="1,0", help="fused-direction settings to time")
     args = ap.parse_args()
     n, s = args.n, args.s
     ctx = ep.Context(0)
-    ctx.set_option(ep.OPT_L2_HINTS, args.l2_hints)
     ctx.set_option(ep.OPT_SPMV_VARIANT, args.variant)
     O = Oracle()
     y = torch.as_tensor(pack_group(O.draw_samples(0, s, 3), s)).cuda()
@@ -76,6 +76,27 @@ def main():
     if args.spmv_only:
         print(json.dumps(out, indent=1))
         return
+    if args.ab:
+        # same process, same box: alternate the variants, median SpMV kernel time
+        import statistics
+        cfg = ep.SolverConfig(tol=1e-6, max_iterations=10000, flavour=ep.CG_UNCOUPLED,
+                              dot_mode=ep.DOT_CANONICAL)
+        vs = [int(v) for v in args.ab.split(",")]
+        res = {v: [] for v in vs}
+        for v in vs:
+            ctx.set_option(ep.OPT_SPMV_VARIANT, v)
+            p.solve(cfg)
+        for _ in range(args.ab_rounds):
+            for v in vs:
+                ctx.set_option(ep.OPT_SPMV_VARIANT, v)
+                ctx.profile(1)
+                p.solve(cfg)
+                sp_ms, sp_n = ctx.profile(0)
+                res[v].append(sp_ms / max(sp_n, 1))
+        out["ab_spmv_kernel_ms"] = {v: round(statistics.median(r), 4) for v, r in res.items()}
+        out["ab_all"] = {v: [round(t, 4) for t in r] for v, r in res.items()}
+        print(json.dumps(out, indent=1))
+        return
     modes = {"canonical": ep.DOT_CANONICAL, "serial": ep.DOT_SERIAL}
     for mode_name in args.modes.split(","):
         mode = modes[mode_name]
@@ -97,7 +118,7 @@ def main():
             ms = a.elapsed_time(b) / args.steps
             key = f"{mode_name}_fused{fused}"
             out[key] = {"solve_ms": round(ms, 3), "iters": its, "ms_per_iter": round(ms / its[-1], 4),
-                        "spmv_phase_ms": round(sp_ms / max(sp_n, 1), 4),
+                        "spmv_kernel_ms": round(sp_ms / max(sp_n, 1), 4),
                         "per_iter_ms": {k: round(v / max(det["iterations"], 1), 4)
                                         for k, v in det.items()
                                         if k not in ("iterations", "solve", "init", "loop", "early_exit")},
