@@ -271,7 +271,7 @@ def run_ours(args):
     byt = cg_spmv_bytes(nnz, nnz_st, rows, S)
     achieved = byt / (avg_spmv_ms / 1e3) / 1e9
     it_ms = det["iteration"] / nit
-    kname = "k_cg_spmv_warp<32,true,%s>" % ("true" if nnz_st < nnz else "false")
+    kname = "k_cg_spmv_warp<32,true,true,2>" if nnz_st < nnz else "k_cg_spmv_warp<32,true,false,0>"
     dir_ms = det["direction"] / nit
     it_bytes = byt + direction_bytes(rows, S) + 3 * 8 * S * rows  # + update (r, q -> r)
     roofline = {"bound": "hbm", "kernel": kname,

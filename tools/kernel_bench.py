@@ -27,7 +27,7 @@ def main():
     ap.add_argument("--spmv-only", action="store_true")
     ap.add_argument("--sym", type=int, default=1, help="symmetric storage for the CG problems")
     ap.add_argument("--modes", default="canonical,serial")
-    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--variant", type=int, default=-1, help="CG SpMV variant (-1 auto)")
     ap.add_argument("--ab", default="", help="comma list of SpMV variants timed alternately (CG SpMV kernel only)")
     ap.add_argument("--ab-rounds", type=int, default=5)
     ap.add_argument("--fused", default="1,0", help="fused-direction settings to time")
