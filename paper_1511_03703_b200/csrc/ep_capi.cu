@@ -159,7 +159,7 @@ int prof_collect(enprop_ctx* c, int working) {
 int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_entry,
            const double* values, const double* b, double* x, const enprop_cg_options* opt,
            CgWork& w, int* iterations, int* lane_status, double* history, int* hist_len,
-           const int* vpos = nullptr) {
+           const int* vpos = nullptr, const StageMap* stage = nullptr) {
   const int seg = opt->seg_rows > 0 ? opt->seg_rows : 4096;
   const TileMap tm = make_tile_map(rows, seg);
   int rc = ensure_work(w, rows, s, opt->max_iterations, tm);
@@ -216,8 +216,11 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
         if (ev) EP_CUDA(cudaEventRecord(ev[0], st));
         if (!fused) EP_CUDA(launch_cg_direction(s, rows, w.r, p_old, p_new, x, w.state, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[1], st));
-        EP_CUDA(launch_cg_spmv(s, canon, fused, false, tm, row_map, col_entry, values, w.r, p_old,
-                               p_new, w.q, x, p_new, vpos, f_pq, st));
+        if (stage)
+          EP_CUDA(launch_cg_spmv_staged(s, canon, *stage, values, p_new, w.q, f_pq, st));
+        else
+          EP_CUDA(launch_cg_spmv(s, canon, fused, false, tm, row_map, col_entry, values, w.r, p_old,
+                                 p_new, w.q, x, p_new, vpos, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[2], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, f_pq, st));
         if (fin_kernel) EP_CUDA(launch_fin_segments(s, tm, f_pq, st));
@@ -650,7 +653,10 @@ struct enprop_problem {
   double* x = nullptr;
   double* y = nullptr;
   int* vpos = nullptr;   // symmetric storage (ENPROP_OPT_SYMMETRIC_STORAGE): slot of each entry
+  int* up_start = nullptr;  // first stored slot of each row (rows + 1)
   int64_t nnz_stored = 0;
+  StageMap stage;           // stage-pipelined CG SpMV (ep_staged.cu), built on first solve
+  int stage_failed = 0;
   AsmSetup setup;
   CgWork work;
 };
@@ -693,7 +699,9 @@ int enprop_problem_create(enprop_ctx* c, const enprop_problem_desc* d, enprop_pr
   p->nnz_stored = p->nnz;
   if (c->symmetric_storage) {  // the assembled operator is exactly symmetric
     if ((err = cudaMalloc(&p->vpos, p->nnz * sizeof(int))) != cudaSuccess ||
-        (err = build_sym(p->rows, p->row_map, p->col_entry, p->vpos, &p->nnz_stored, c->stream)) != cudaSuccess)
+        (err = cudaMalloc(&p->up_start, (p->rows + 1) * sizeof(int))) != cudaSuccess ||
+        (err = build_sym(p->rows, p->row_map, p->col_entry, p->vpos, &p->nnz_stored, c->stream,
+                         p->up_start)) != cudaSuccess)
       return cleanup(cuda_fail(err, "enprop_problem_create: symmetric storage"));
     c->launches += 2;
   }
@@ -708,8 +716,9 @@ int enprop_problem_create(enprop_ctx* c, const enprop_problem_desc* d, enprop_pr
 int enprop_problem_destroy(enprop_problem* p) {
   if (!p) return ENPROP_OK;
   for (void* q : {(void*)p->row_map, (void*)p->col_entry, (void*)p->values, (void*)p->residual,
-                  (void*)p->rhs, (void*)p->x, (void*)p->y, (void*)p->vpos})
+                  (void*)p->rhs, (void*)p->x, (void*)p->y, (void*)p->vpos, (void*)p->up_start})
     if (q) cudaFree(q);
+  free_stage_map(p->stage);
   free_asm_setup(p->setup);
   free_work(p->work);
   delete p;
@@ -778,8 +787,28 @@ int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* i
   const int64_t len = (int64_t)p->rows * s;  // rhs = -residual (bench.cpp:298-299)
   EP_CUDA(launch_negate(len, p->residual, p->rhs, p->ctx->stream));
   p->ctx->launches += 1;
+  // stage-pipelined SpMV (ep_staged.cu): structured graph + symmetric storage,
+  // s in {16, 32}, automatic variant selection
+  const StageMap* stage = nullptr;
+  const int N = p->desc.cells_per_axis + 1;
+  if (p->vpos && spmv_variant() < 0 && staged_supported(s, N) && !p->stage_failed) {
+    if (!p->stage.desc || p->stage.tm.seg_rows != o.seg_rows) {
+      const TileMap tm = make_tile_map(p->rows, o.seg_rows);
+      const cudaError_t err = build_stage_map(s, tm, N, p->row_map, p->col_entry, p->vpos,
+                                              p->up_start, p->stage, p->ctx->stream);
+      if (err == cudaErrorInvalidValue) {
+        p->stage_failed = 1;  // not representable: the warp-per-tile kernel runs instead
+        cudaGetLastError();
+      } else if (err != cudaSuccess) {
+        return cuda_fail(err, "enprop_problem_solve: stage map");
+      } else {
+        p->ctx->launches += 1;
+      }
+    }
+    if (p->stage.desc) stage = &p->stage;
+  }
   return run_cg(p->ctx, s, p->rows, p->row_map, p->col_entry, p->values, p->rhs, p->x, &o, p->work,
-                iterations, lane_status, history, hist_len, p->vpos);
+                iterations, lane_status, history, hist_len, p->vpos, stage);
 }
 
 int enprop_problem_solve_host(enprop_problem* p, const double* y_host, double* x_host,

@@ -863,6 +863,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
 // -----------------------------------------------------------------------------
 static int g_spmv_variant = -1;  // ENPROP_OPT_SPMV_VARIANT (process-wide; -1 auto, see SpmvVariant)
 void set_spmv_variant(int v) { g_spmv_variant = (v >= 0 && v <= 6) ? v : -1; }
+int spmv_variant() { return g_spmv_variant; }
 
 template <int S>
 struct WarpTile {
@@ -1416,7 +1417,7 @@ cudaError_t launch_sym_expand(int s, int64_t nnz, const int* vpos, const double*
 namespace ep {
 
 cudaError_t build_sym(int rows, const int* row_map, const int* col_entry, int* vpos,
-                      int64_t* nnz_up, cudaStream_t st) {
+                      int64_t* nnz_up, cudaStream_t st, int* up_start) {
   int *cnt = nullptr, *start = nullptr, *bad = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
@@ -1436,6 +1437,8 @@ cudaError_t build_sym(int rows, const int* row_map, const int* col_entry, int* v
     k_sym_vpos<<<(rows + 255) / 256, 256, 0, st>>>(rows, row_map, col_entry, start, vpos, bad);
     err = cudaGetLastError();
   }
+  if (err == cudaSuccess && up_start)
+    err = cudaMemcpyAsync(up_start, start, (size_t)(rows + 1) * sizeof(int), cudaMemcpyDeviceToDevice, st);
   int h_total = 0, h_bad = 0;
   if (err == cudaSuccess) err = cudaMemcpyAsync(&h_total, start + rows, sizeof(int), cudaMemcpyDeviceToHost, st);
   if (err == cudaSuccess) err = cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);

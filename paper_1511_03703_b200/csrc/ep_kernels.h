@@ -125,11 +125,46 @@ cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* r, co
 // Symmetric (diagonal + upper) value storage: vpos[nnz] maps each full-CRS entry
 // to its stored slot; nnz_up = stored entries. Fails (InvalidValue) if the
 // pattern is not structurally symmetric.
+// up_start (optional, rows + 1 ints): first stored slot of each row.
 cudaError_t build_sym(int rows, const int* row_map, const int* col_entry, int* vpos,
-                      int64_t* nnz_up, cudaStream_t st);
+                      int64_t* nnz_up, cudaStream_t st, int* up_start = nullptr);
 // full[k] = up[vpos[k]] (views / checks)
 cudaError_t launch_sym_expand(int s, int64_t nnz, const int* vpos, const double* up, double* full,
                               cudaStream_t st);
+// ---- stage-pipelined CG SpMV (ep_staged.cu): structured 27-point graph, symmetric storage
+constexpr int kStageMaxUpper = 14;   // stored slots per row (diagonal + 13 upper)
+constexpr int kStageMaxRow = 27;     // entries per row
+constexpr int kStageMaxGlobal = 13;  // leading entries that may live in an earlier stage
+
+struct StageDesc {
+  int R0, R1;        // rows [R0, R1) of the stage
+  int slot0, slot1;  // stored slots of those rows (symmetric storage)
+  int64_t blk_off;   // index block (bytes, 16-aligned)
+  int blk_bytes, pad;
+};
+
+struct StageMap {
+  int nstages = 0, s = 0, N = 0;
+  TileMap tm{};
+  StageDesc* desc = nullptr;
+  unsigned char* blk = nullptr;
+  int64_t blk_bytes = 0;
+};
+
+bool staged_supported(int s, int N);
+// N = mesh nodes per axis (rows == N^3, the k_build_graph numbering); up_start =
+// first stored slot of each row (rows + 1). Fails (InvalidValue) for graphs
+// that are not the structured 27-point pattern.
+cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
+                            const int* col_entry, const int* vpos, const int* up_start,
+                            StageMap& sm, cudaStream_t st);
+void free_stage_map(StageMap& sm);
+// q = A p and (tiles) the canonical p.q tile partials; bitwise equal to the
+// warp-per-tile kernel
+cudaError_t launch_cg_spmv_staged(int s, bool tiles, const StageMap& sm, const double* values,
+                                  const double* p, double* q, const FinArgs& f, cudaStream_t st);
+int spmv_variant();  // ENPROP_OPT_SPMV_VARIANT (-1 = auto)
+
 // after the loop: apply the still-deferred x += alpha*p of the last iteration
 cudaError_t launch_cg_flush(int s, int rows, double* x, double* const* p, const CgState* cg,
                             cudaStream_t st);

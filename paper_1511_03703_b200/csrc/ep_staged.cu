@@ -1,0 +1,463 @@
+// Stage-pipelined CG SpMV for structured-mesh problems with symmetric storage
+// ("staged SpMV").
+//
+// Same arithmetic as k_cg_spmv_warp (ep_kernels.cu): row sums in column order,
+// z = ((0 + a_0 x_0) + a_1 x_1) + ... per sample (kernels.hpp:15-26), and the
+// same canonical 16-row tile trees for p.q, so the two kernels are bitwise
+// interchangeable.  What changes is how the bytes reach the SM.
+//
+// A stage is T = 32/S consecutive canonical tiles (16 T rows, a contiguous row
+// range [R0, R1)).  One persistent CTA per SM walks the stages round-robin
+// (CTA c takes stages c, c + grid, ...: the SMs sweep the matrix together, so a
+// plane's upper slots are still in L2 when the next plane re-reads them
+// transposed) through a two-deep ring of shared-memory stage buffers.  Thread 0
+// fills a buffer with cp.async.bulk (TMA engine) copies completing on an
+// mbarrier:
+//   * the stage's stored slots (diagonal + upper of its rows): one contiguous
+//     range of the symmetric value array, up to 16 T x 14 x 8S = 57 KB;
+//   * the direction vector around the stage: the 27-point neighbours of rows
+//     [R0, R1) lie in 9 contiguous row runs [R0-1 + dj N + dk N^2, R1+1 + ...),
+//     dj, dk in {-1,0,1} (x-fastest numbering, mesh.hpp:24-26), 9 x 18 x 8S
+//     bytes at S = 32 instead of 16 x 27 gathers;
+//   * a precomputed index block (k_stage_fill): per row the local entry start,
+//     per entry the smem row of its x operand and where its value lives.
+// Only the lower entries whose transposed slot belongs to an earlier stage
+// (<= 13 per row, all in the row's leading entries) are gathered from global
+// memory into registers, issued together as soon as the buffer is ready.
+// The register file therefore only holds the transposed gathers; the streamed
+// bytes are in flight in the TMA engine, a stage ahead of the compute.
+#include <cstdio>
+#include <vector>
+
+#include "ep_common.cuh"
+#include "ep_kernels.h"
+
+namespace ep {
+
+template <int S>
+struct StagedShape {
+  static constexpr int V = 2;
+  static constexpr int TPR = S / V;                 // threads per row
+  static constexpr int T = 32 / S;                  // canonical tiles per stage
+  static constexpr int RS = kTileRows * T;          // row slots per stage
+  static constexpr int L = RS + 2;                  // rows per x run
+  static constexpr int CH = 8 * S;                  // bytes per chunk (one entry's / row's s values)
+  static constexpr int ROWE = 28;                   // sa entries per row slot (27 padded to int4)
+  static constexpr int ROWX = 32;                   // sx entries per row slot (27 padded to 4 x uint4)
+  static constexpr int UP_CHUNKS = RS * kStageMaxUpper;
+  static constexpr int X_CHUNKS = 9 * L;
+  static constexpr int ZC = UP_CHUNKS + X_CHUNKS;   // the zero chunk (padding entries)
+  static constexpr int BIG_BYTES = (ZC + 1) * CH;
+  static constexpr int IDX_BYTES = 2 * RS * 4 + RS * ROWE * 4 + RS * ROWX * 2;
+  static constexpr int NIDX = 4;                    // index blocks in flight (ring depth)
+  static constexpr int RED_BYTES = RS * S * 8;
+  static constexpr int SMEM = 2 * BIG_BYTES + NIDX * IDX_BYTES + 2 * RED_BYTES + 64;
+  static_assert(RS * TPR == 256, "one thread per (row slot, sample pair)");
+  static_assert(BIG_BYTES % 128 == 0 && IDX_BYTES % 16 == 0, "alignment");
+  static_assert(SMEM <= 232448, "stage ring exceeds shared memory");
+  static_assert(ZC < 65536, "chunk indices are 16-bit");
+};
+
+// the transposed gathers of one stage (the first kStageMaxGlobal entries of a
+// row may live in an earlier stage) and the codes of entries 0..15
+struct StageGather {
+  int code[16];
+  double2 v[kStageMaxGlobal];
+};
+
+template <int S>
+struct StagedCta {
+  using Sh = StagedShape<S>;
+  const TileMap& tm;
+  int N, nstages;
+  const StageDesc* __restrict__ desc;
+  const unsigned char* __restrict__ blk;
+  const double* __restrict__ values;
+  const double* __restrict__ p;
+  double* __restrict__ q;
+  const FinArgs& f;
+  unsigned char* smem;
+  uint64_t* bar;  // [0,2): big buffers, [2,6): index ring
+  double* red;
+  uint64_t pol;
+  int rr, lane0;
+
+  __device__ __forceinline__ int stage_of(int it) const { return (int)blockIdx.x + it * (int)gridDim.x; }
+  __device__ __forceinline__ bool has(int it) const { return stage_of(it) < nstages; }
+  __device__ __forceinline__ unsigned char* big(int it) const { return smem + (it & 1) * Sh::BIG_BYTES; }
+  __device__ __forceinline__ const int* idx(int it) const {
+    return reinterpret_cast<const int*>(smem + 2 * Sh::BIG_BYTES + (it & (Sh::NIDX - 1)) * Sh::IDX_BYTES);
+  }
+
+  // producer (thread 0)
+  __device__ __forceinline__ void issue_big(int it, const StageDesc& d) const {
+    unsigned char* sb = big(it);
+    uint64_t* b = &bar[it & 1];
+    const int rows = tm.rows, NN = N * N;
+    const int L = d.R1 - d.R0 + 2;
+    const uint32_t upb = (uint32_t)(d.slot1 - d.slot0) * Sh::CH;
+    uint32_t total = upb;
+#pragma unroll
+    for (int run = 0; run < 9; ++run) {
+      const int a = d.R0 - 1 + (run % 3 - 1) * N + (run / 3 - 1) * NN;
+      const int lo = a > 0 ? a : 0, hi = a + L < rows ? a + L : rows;
+      if (hi > lo) total += (uint32_t)(hi - lo) * Sh::CH;
+    }
+    mbar_arrive_expect_tx(b, total);
+    bulk_g2s(sb, values + (size_t)d.slot0 * S, upb, b);
+#pragma unroll
+    for (int run = 0; run < 9; ++run) {
+      const int a = d.R0 - 1 + (run % 3 - 1) * N + (run / 3 - 1) * NN;
+      const int lo = a > 0 ? a : 0, hi = a + L < rows ? a + L : rows;
+      if (hi > lo)
+        bulk_g2s(sb + (size_t)(Sh::UP_CHUNKS + run * Sh::L + (lo - a)) * Sh::CH, p + (size_t)lo * S,
+                 (uint32_t)(hi - lo) * Sh::CH, b);
+    }
+  }
+  __device__ __forceinline__ void issue_idx(int it) const {
+    uint64_t* b = &bar[2 + (it & (Sh::NIDX - 1))];
+    mbar_arrive_expect_tx(b, Sh::IDX_BYTES);
+    bulk_g2s((void*)idx(it), blk + (size_t)stage_of(it) * Sh::IDX_BYTES, Sh::IDX_BYTES, b);
+  }
+
+  __device__ __forceinline__ void gather(int it, StageGather& G) const {
+    const int4* sa = reinterpret_cast<const int4*>(idx(it) + 2 * Sh::RS + rr * Sh::ROWE);
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int4 w = sa[v];
+      G.code[4 * v] = w.x, G.code[4 * v + 1] = w.y, G.code[4 * v + 2] = w.z, G.code[4 * v + 3] = w.w;
+    }
+#pragma unroll
+    for (int k = 0; k < kStageMaxGlobal; ++k) {
+      if (G.code[k] >= 0) {
+        const VecD<2> v = ld_stream_hint<2>(values + (size_t)G.code[k] * S + lane0, pol);
+        G.v[k] = make_double2(v.v[0], v.v[1]);
+      }
+    }
+  }
+
+  __device__ __forceinline__ double2 chunk(const unsigned char* sb, int c) const {
+    return *reinterpret_cast<const double2*>(sb + c * Sh::CH + lane0 * 8);
+  }
+
+  template <bool kTiles>
+  __device__ __forceinline__ void stage(int it, StageGather& Gc, StageGather& Gn) const {
+    StageDesc dn;  // producer: descriptor of stage it + 2, loaded early
+    const bool prod = threadIdx.x == 0 && has(it + 2);
+    if (prod) dn = desc[stage_of(it + 2)];
+    if (has(it + 1)) {  // the next stage's transposed gathers fly during this stage
+      mbar_wait(&bar[2 + ((it + 1) & (Sh::NIDX - 1))], ((it + 1) >> 2) & 1);
+      gather(it + 1, Gn);
+    }
+    const int* ib = idx(it);
+    const int row = ib[rr];
+    const int pch = ib[Sh::RS + rr];
+    int ca[12];  // codes of entries 16..27
+    {
+      const int4* sa = reinterpret_cast<const int4*>(ib + 2 * Sh::RS + rr * Sh::ROWE) + 4;
+#pragma unroll
+      for (int v = 0; v < 3; ++v) {
+        const int4 w = sa[v];
+        ca[4 * v] = w.x, ca[4 * v + 1] = w.y, ca[4 * v + 2] = w.z, ca[4 * v + 3] = w.w;
+      }
+    }
+    int cx[kStageMaxRow];
+    {
+      const uint4* sx = reinterpret_cast<const uint4*>(ib + 2 * Sh::RS + Sh::RS * Sh::ROWE) + rr * 4;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const uint4 w = sx[v];
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int h = 0; h < 8; ++h)
+          if (8 * v + h < kStageMaxRow) cx[8 * v + h] = (int)((ww[h / 2] >> (16 * (h & 1))) & 0xffffu);
+      }
+    }
+    mbar_wait(&bar[it & 1], (it >> 1) & 1);
+    const unsigned char* sb = big(it);
+    // all 27 entries: entries past the row end point at the zero chunk and add
+    // +0.0 * +0.0 (the running sum starts at +0.0 and never becomes -0.0, so
+    // adding +0.0 changes no bit)
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < kStageMaxRow; ++k) {
+      const int c = k < 16 ? Gc.code[k] : ca[k - 16];
+      double2 a;
+      if (k < kStageMaxGlobal) {
+        a = Gc.v[k];
+        if (c < 0) a = chunk(sb, -c - 1);
+      } else {
+        a = chunk(sb, -c - 1);
+      }
+      const double2 xv = chunk(sb, cx[k]);
+      s0 = EP_DADD(s0, EP_DMUL(a.x, xv.x));
+      s1 = EP_DADD(s1, EP_DMUL(a.y, xv.y));
+    }
+    if (row >= 0) *reinterpret_cast<double2*>(q + (size_t)row * S + lane0) = make_double2(s0, s1);
+    double* rb = red + (it & 1) * (Sh::RS * S);
+    if constexpr (kTiles) {
+      double c0 = 0.0, c1 = 0.0;
+      if (row >= 0) {  // own p (x run (dj, dk) = (0, 0))
+        const double2 pn = chunk(sb, pch);
+        c0 = EP_DMUL(pn.x, s0);
+        c1 = EP_DMUL(pn.y, s1);
+      }
+      *reinterpret_cast<double2*>(rb + rr * S + lane0) = make_double2(c0, c1);
+    }
+    __syncthreads();  // big buffer and index slot of stage it consumed, products in rb
+    if (threadIdx.x == 0) {
+      fence_proxy_async_smem();
+      if (prod) issue_big(it + 2, dn);
+      if (has(it + Sh::NIDX)) issue_idx(it + Sh::NIDX);
+    }
+    if constexpr (kTiles) {
+      if (threadIdx.x < 32) {  // tile trees: lane -> (tile, sample); v[i] += v[i+h], h = 8,4,2,1
+        const int tt = threadIdx.x / S, e = threadIdx.x % S;
+        const int b2 = stage_of(it) * Sh::T + tt;
+        if (ib[tt * kTileRows] >= 0) {  // the tile exists (its first row slot is a row)
+          double v[kTileRows];
+#pragma unroll
+          for (int h = 0; h < kTileRows; ++h) v[h] = rb[(tt * kTileRows + h) * S + e];
+#pragma unroll
+          for (int h = kTileRows / 2; h >= 1; h >>= 1)
+#pragma unroll
+            for (int k = 0; k < h; ++k) v[k] = EP_DADD(v[k], v[k + h]);
+          f.partials[(size_t)b2 * S + e] = v[0];
+        }
+      }
+    }
+  }
+};
+
+template <int S, bool kTiles>
+__global__ void __launch_bounds__(256, 1) k_cg_spmv_staged(
+    const TileMap tm, int N, int nstages, const StageDesc* __restrict__ desc,
+    const unsigned char* __restrict__ blk, const double* __restrict__ values,
+    const double* __restrict__ p, double* __restrict__ q, const FinArgs f) {
+  using Sh = StagedShape<S>;
+  if (f.cg->done) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int tid = threadIdx.x;
+  StagedCta<S> c{tm, N, nstages, desc, blk, values, p, q, f, smem,
+                 reinterpret_cast<uint64_t*>(smem + 2 * Sh::BIG_BYTES + Sh::NIDX * Sh::IDX_BYTES + 2 * Sh::RED_BYTES),
+                 reinterpret_cast<double*>(smem + 2 * Sh::BIG_BYTES + Sh::NIDX * Sh::IDX_BYTES),
+                 l2_policy_evict_normal(), tid / Sh::TPR, (tid % Sh::TPR) * Sh::V};
+  if (tid == 0) {
+    for (int k = 0; k < 2 + Sh::NIDX; ++k) mbar_init(&c.bar[k], 1);
+    fence_mbar_init();
+  }
+  if (tid < Sh::CH / 8) {  // zero chunks (never written by the copies)
+    reinterpret_cast<double*>(smem + Sh::ZC * Sh::CH)[tid] = 0.0;
+    reinterpret_cast<double*>(smem + Sh::BIG_BYTES + Sh::ZC * Sh::CH)[tid] = 0.0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int it = 0; it < Sh::NIDX; ++it)
+      if (c.has(it)) c.issue_idx(it);
+    for (int it = 0; it < 2; ++it)
+      if (c.has(it)) c.issue_big(it, desc[c.stage_of(it)]);
+  }
+  if (!c.has(0)) return;
+  StageGather ga, gb;
+  mbar_wait(&c.bar[2], 0);
+  c.gather(0, ga);
+  for (int it = 0;;) {
+    c.template stage<kTiles>(it, ga, gb);
+    if (!c.has(++it)) break;
+    c.template stage<kTiles>(it, gb, ga);
+    if (!c.has(++it)) break;
+  }
+}
+
+// ---- stage map ---------------------------------------------------------------
+// Index block of stage g at blk + g * IDX_BYTES, by row slot rr = ti*16 + t
+// (tile ti of the stage, row t of the tile):
+//   int srow[RS]       the slot's row, -1 if none
+//   int spch[RS]       chunk of the row's own p in the stage buffer
+//   int sa[RS][28]     value of entry k: >= 0 global slot (transposed entry of an
+//                      earlier stage's row), < 0: -(chunk + 1) in the stage buffer
+//   u16 sx[RS][32]     chunk of entry k's x operand: UP_CHUNKS + run*L + lr + di + 1,
+//                      run = (dk+1)*3 + (dj+1), lr = row - R0
+// Entries past a row's end (and empty slots) point both operands at the zero chunk.
+__global__ void k_stage_fill(const TileMap tm, int nstages, int T, int N, int L, int RS,
+                             int up_chunks, int zc, int idx_bytes,
+                             const StageDesc* __restrict__ desc, const int* __restrict__ row_map,
+                             const int* __restrict__ col_entry, const int* __restrict__ vpos,
+                             unsigned char* __restrict__ blk, int* __restrict__ bad) {
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= nstages * RS) return;
+  const int g = gid / RS, rr = gid % RS;
+  const StageDesc d = desc[g];
+  int* ib = reinterpret_cast<int*>(blk + (size_t)g * idx_bytes);
+  int* sa = ib + 2 * RS + rr * 28;
+  uint16_t* sx = reinterpret_cast<uint16_t*>(ib + 2 * RS + RS * 28) + rr * 32;
+  const int b = g * T + rr / kTileRows, t = rr % kTileRows;
+  int r0 = 0, nr = 0;
+  if (b < tm.num_tiles()) tm.tile(b, r0, nr);
+  const int r = t < nr ? r0 + t : -1;
+  int n = 0;
+  if (r >= 0) {
+    const int ks = row_map[r], ke = row_map[r + 1];
+    n = ke - ks;
+    const int lr = r - d.R0;
+    if (n > kStageMaxRow || lr < 0 || lr >= RS) {
+      atomicAdd(bad, 1);
+      return;
+    }
+    const int NN = N * N;
+    for (int k = ks; k < ke; ++k) {
+      const int c = col_entry[k], v = vpos[k];
+      int code;
+      if (c >= d.R0) {
+        const int a = v - d.slot0;
+        if (a < 0 || a >= up_chunks) atomicAdd(bad, 1);
+        code = -(a + 1);
+      } else {
+        if (k - ks >= kStageMaxGlobal) atomicAdd(bad, 1);
+        code = v;
+      }
+      const int dl = c - r;
+      const int dk = dl > NN / 2 ? 1 : (dl < -(NN / 2) ? -1 : 0);
+      const int rem = dl - dk * NN;
+      const int dj = rem > N / 2 ? 1 : (rem < -(N / 2) ? -1 : 0);
+      const int di = rem - dj * N;
+      if (di < -1 || di > 1) atomicAdd(bad, 1);
+      sa[k - ks] = code;
+      sx[k - ks] = (uint16_t)(up_chunks + ((dk + 1) * 3 + (dj + 1)) * L + lr + di + 1);
+    }
+    ib[rr] = r;
+    ib[RS + rr] = up_chunks + 4 * L + lr + 1;
+  } else {
+    ib[rr] = -1;
+    ib[RS + rr] = zc;
+  }
+  for (int k = n; k < 28; ++k) sa[k] = -(zc + 1);
+  for (int k = n; k < 32; ++k) sx[k] = (uint16_t)zc;
+}
+
+template <int S>
+static int stage_shape(int& T, int& L, int& RS, int& max_upper, int& idx_bytes, int& zc) {
+  using Sh = StagedShape<S>;
+  T = Sh::T;
+  L = Sh::L;
+  RS = Sh::RS;
+  max_upper = Sh::UP_CHUNKS;
+  idx_bytes = Sh::IDX_BYTES;
+  zc = Sh::ZC;
+  return 0;
+}
+
+bool staged_supported(int s, int N) { return (s == 16 || s == 32) && N >= 8; }
+
+cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
+                            const int* col_entry, const int* vpos, const int* up_start,
+                            StageMap& sm, cudaStream_t st) {
+  free_stage_map(sm);
+  if (!staged_supported(s, N) || tm.rows != N * N * N) return cudaErrorInvalidValue;
+  int T = 0, L = 0, RS = 0, max_upper = 0, idx_bytes = 0, zc = 0;
+  if (s == 32) stage_shape<32>(T, L, RS, max_upper, idx_bytes, zc);
+  else stage_shape<16>(T, L, RS, max_upper, idx_bytes, zc);
+  const int rows = tm.rows;
+  std::vector<int> hup(rows + 1);
+  cudaError_t err = cudaMemcpyAsync(hup.data(), up_start, (rows + 1) * sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+  if (err != cudaSuccess) return err;
+  const int tiles = tm.num_tiles();
+  std::vector<StageDesc> hd;
+  hd.reserve((tiles + T - 1) / T);
+  int64_t off = 0;
+  for (int b0 = 0; b0 < tiles; b0 += T) {
+    int R0 = -1, R1 = -1;
+    for (int ti = 0; ti < T && b0 + ti < tiles; ++ti) {
+      int r0, nr;
+      tm.tile(b0 + ti, r0, nr);
+      if (nr > 0) {
+        if (R0 < 0) R0 = r0;
+        else if (r0 != R1) return cudaErrorInvalidValue;  // stages must be contiguous
+        R1 = r0 + nr;
+      }
+    }
+    if (R0 < 0) break;  // only trailing tiles of the last segment are empty
+    StageDesc d{};
+    d.R0 = R0;
+    d.R1 = R1;
+    d.slot0 = hup[R0];
+    d.slot1 = hup[R1];
+    if (d.slot1 - d.slot0 > max_upper) return cudaErrorInvalidValue;
+    d.blk_off = off;
+    d.blk_bytes = idx_bytes;
+    off += idx_bytes;
+    hd.push_back(d);
+  }
+  sm.nstages = (int)hd.size();
+  sm.s = s;
+  sm.N = N;
+  sm.tm = tm;
+  sm.blk_bytes = off;
+  int* bad = nullptr;
+  err = cudaMalloc(&sm.desc, hd.size() * sizeof(StageDesc) + 16);
+  if (err == cudaSuccess) err = cudaMalloc(&sm.blk, off + 16);
+  if (err == cudaSuccess) err = cudaMalloc(&bad, sizeof(int));
+  if (err == cudaSuccess) err = cudaMemsetAsync(bad, 0, sizeof(int), st);
+  if (err == cudaSuccess)
+    err = cudaMemcpyAsync(sm.desc, hd.data(), hd.size() * sizeof(StageDesc), cudaMemcpyHostToDevice, st);
+  if (err == cudaSuccess) {
+    const int work = sm.nstages * RS;
+    k_stage_fill<<<(work + 255) / 256, 256, 0, st>>>(tm, sm.nstages, T, N, L, RS, max_upper, zc,
+                                                     idx_bytes, sm.desc, row_map, col_entry, vpos,
+                                                     sm.blk, bad);
+    err = cudaGetLastError();
+  }
+  int hbad = 0;
+  if (err == cudaSuccess) err = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+  if (bad) cudaFree(bad);
+  if (err == cudaSuccess && hbad) err = cudaErrorInvalidValue;  // not the structured 27-point graph
+  if (err != cudaSuccess) free_stage_map(sm);
+  return err;
+}
+
+void free_stage_map(StageMap& sm) {
+  if (sm.desc) cudaFree(sm.desc);
+  if (sm.blk) cudaFree(sm.blk);
+  sm = StageMap{};
+}
+
+template <int S>
+static cudaError_t cg_spmv_staged_s(bool tiles, const StageMap& sm, const double* values,
+                                    const double* p, double* q, const FinArgs& f, cudaStream_t st) {
+  using Sh = StagedShape<S>;
+  static int sms[64] = {0};  // per device: SM count, and the smem opt-in done
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  if (!sms[dev]) {
+    cudaError_t err = cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(k_cg_spmv_staged<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(k_cg_spmv_staged<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM);
+    if (err != cudaSuccess) {
+      sms[dev] = 0;
+      return err;
+    }
+  }
+  if (sm.nstages == 0) return cudaSuccess;
+  const int grid = sm.nstages < sms[dev] ? sm.nstages : sms[dev];
+  if (tiles)
+    k_cg_spmv_staged<S, true><<<grid, 256, Sh::SMEM, st>>>(sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
+                                                           values, p, q, f);
+  else
+    k_cg_spmv_staged<S, false><<<grid, 256, Sh::SMEM, st>>>(sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
+                                                            values, p, q, f);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_spmv_staged(int s, bool tiles, const StageMap& sm, const double* values,
+                                  const double* p, double* q, const FinArgs& f, cudaStream_t st) {
+  if (s == 32) return cg_spmv_staged_s<32>(tiles, sm, values, p, q, f, st);
+  if (s == 16) return cg_spmv_staged_s<16>(tiles, sm, values, p, q, f, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace ep

@@ -469,3 +469,31 @@ def test_symmetric_storage_is_bitwise_neutral(ctx, R, mode, s):
     assert same(host(ps.values), rv)
     ps.close()
     pf.close()
+
+
+@pytest.mark.parametrize("mode", [DOT_SERIAL, DOT_CANONICAL])
+@pytest.mark.parametrize("s,n,seg", [(32, 7, 0), (32, 12, 0), (32, 23, 0), (16, 8, 0), (16, 19, 0),
+                                     (32, 12, 1000), (16, 12, 77)])
+def test_staged_spmv_is_bitwise_equal_to_warp_kernel(ctx, mode, s, n, seg):
+    """The stage-pipelined CG SpMV (ep_staged.cu; auto-selected for structured
+    problems with symmetric storage at s in {16, 32}) gives the same bits as the
+    warp-per-tile kernel: solution, iteration counts and residual histories,
+    coupled and uncoupled, for plane-aligned and arbitrary canonical segments."""
+    m = 3
+    y = dev(pack_group(O.draw_samples(11, s, m), s))
+    kl = ep.KlField(m, 1.0, 0.25, 1.0)
+    p = ep.Problem(ctx, n, s, kl)
+    p.assemble(y)
+    for flavour in (ep.CG_UNCOUPLED, ep.CG_COUPLED):
+        cfg = ep.SolverConfig(tol=1e-9, flavour=flavour, dot_mode=mode, seg_rows=seg)
+        a = p.solve(cfg)
+        xa = host(p.solution).copy()
+        ctx.set_option(ep.OPT_SPMV_VARIANT, 2)
+        try:
+            b = p.solve(cfg)
+        finally:
+            ctx.set_option(ep.OPT_SPMV_VARIANT, -1)
+        assert a[0] == b[0]
+        assert a[1] == b[1]  # residual histories
+        assert same(xa, host(p.solution))
+    p.close()
