@@ -788,10 +788,13 @@ int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* i
   EP_CUDA(launch_negate(len, p->residual, p->rhs, p->ctx->stream));
   p->ctx->launches += 1;
   // stage-pipelined SpMV (ep_staged.cu): structured graph + symmetric storage,
-  // s in {16, 32}, automatic variant selection
+  // s in {16, 32}, canonical dots, automatic variant selection. (The serial
+  // order keeps the warp kernel: its latency-bound dot chains need other
+  // groups' kernels alongside, and the persistent staged kernel fills the SMs.)
   const StageMap* stage = nullptr;
   const int N = p->desc.cells_per_axis + 1;
-  if (p->vpos && spmv_variant() < 0 && staged_supported(s, N) && !p->stage_failed) {
+  if (p->vpos && o.dot_mode == ENPROP_DOT_CANONICAL && spmv_variant() < 0 && staged_supported(s, N) &&
+      !p->stage_failed) {
     if (!p->stage.desc || p->stage.tm.seg_rows != o.seg_rows) {
       const TileMap tm = make_tile_map(p->rows, o.seg_rows);
       const cudaError_t err = build_stage_map(s, tm, N, p->row_map, p->col_entry, p->vpos,
