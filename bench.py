@@ -96,7 +96,7 @@ def spmv_bytes(nnz, rows, s):
 
 
 def cg_spmv_bytes(nnz, nnz_stored, rows, s):
-    """Algorithmic bytes of one CG SpMV launch (k_cg_spmv_warp):
+    """Algorithmic bytes of one CG SpMV launch (k_cg_spmv_staged / k_cg_spmv_warp):
     the stored value slots once (symmetric storage: diagonal + upper), column
     indices, the slot map (symmetric storage only), row_map, the direction
     vector gathered once and q written once. The transposed re-reads of the
@@ -271,7 +271,12 @@ def run_ours(args):
     byt = cg_spmv_bytes(nnz, nnz_st, rows, S)
     achieved = byt / (avg_spmv_ms / 1e3) / 1e9
     it_ms = det["iteration"] / nit
-    kname = "k_cg_spmv_warp<32,true,true,2>" if nnz_st < nnz else "k_cg_spmv_warp<32,true,false,0>"
+    # the library's auto choice (ep_capi.cu enprop_problem_solve): the staged
+    # kernel for symmetric storage + canonical dots at s in {16, 32}
+    if nnz_st < nnz and args.dot == "canonical" and S in (16, 32):
+        kname = f"k_cg_spmv_staged<{S},true>"
+    else:
+        kname = "k_cg_spmv_warp<32,true,true,2>" if nnz_st < nnz else "k_cg_spmv_warp<32,true,false,0>"
     dir_ms = det["direction"] / nit
     it_bytes = byt + direction_bytes(rows, S) + 3 * 8 * S * rows  # + update (r, q -> r)
     roofline = {"bound": "hbm", "kernel": kname,
