@@ -461,8 +461,54 @@ def bench_spmv(ctx, ep, torch, pack_group, O, hbm, peak_kind, reps=20):
                         "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                         "frac": round(byt / (med / 1e3) / 1e9 / hbm, 4), "traffic": None},
            "l2": "matrix 14.6 GB >> L2", "reps": reps}
+    out["layouts"] = bench_spmv_layouts(ctx, ep, torch, p, x, z, byt, med, reps=max(5, reps // 4))
     p.close()
     return out
+
+
+def bench_spmv_layouts(ctx, ep, torch, p, x, z, byt, commuted_ms, reps=5):
+    """The paper's SpMV layout comparison (bench.cpp:73-238, acceptance.cpp:377-408)
+    on the same matrix: commuted = ensemble layout (enprop_spmv); outer =
+    sample-major OuterEnsembleMatrix (enprop_spmv_outer); scalar = s back-to-back
+    s = 1 products over the shared graph. Gate: outer and scalar equal the
+    commuted product bitwise. Median of reps, CUDA events."""
+    s = S
+    rm, ce = p.row_map, p.col_entry
+    vo = p.values.t().contiguous()          # [s][nnz]
+    xo = x.t().contiguous()                 # [s][rows]
+    zo = torch.empty_like(xo)
+    zs = torch.empty_like(xo)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    def scalar():
+        for e in range(s):
+            ep.spmv(ctx, 1, rm, ce, vo[e], xo[e], zs[e])
+
+    outer_ms = timed(lambda: ep.spmv_outer(ctx, s, rm, ce, vo, xo, zo))
+    scalar_ms = timed(scalar)
+    gate = bool(torch.equal(zo.view(torch.int64), z.t().contiguous().view(torch.int64)) and
+                torch.equal(zs.view(torch.int64), zo.view(torch.int64)))
+    del vo
+    gbs = lambda ms: round(byt / (ms / 1e3) / 1e9, 1)
+    return {"commuted": {"ms": round(commuted_ms, 4), "gbs": gbs(commuted_ms), "kernel": "k_spmv<32>"},
+            "outer": {"ms": round(outer_ms, 4), "gbs": gbs(outer_ms), "kernel": "k_spmv_outer"},
+            "scalar": {"ms": round(scalar_ms, 4), "gbs": gbs(scalar_ms), "kernel": "32 x k_spmv<1>"},
+            "speedup_commuted_vs_scalar": round(scalar_ms / commuted_ms, 3),
+            "speedup_commuted_vs_outer": round(outer_ms / commuted_ms, 3),
+            "gate_bitwise": gate}
 
 
 def cpu_baseline_sample(max_cg=10):

@@ -157,6 +157,14 @@ int enprop_apply_dirichlet(enprop_ctx* ctx, int s, int cells_per_axis,
 int enprop_spmv(enprop_ctx* ctx, int s, int num_rows, int num_cols, const int* row_map,
                 const int* col_entry, const double* values, const double* x, double* z);
 
+/* spmv_outer (kernels.hpp:38-56) on the sample-major layout of
+ * OuterEnsembleMatrix (crs.hpp:138-147): values[e*nnz + k], x[e*num_cols + c],
+ * z[e*num_rows + row] for e < ensemble_size; any ensemble_size >= 1. Each
+ * component is bitwise the reference's scalar product. (Device pointers.) */
+int enprop_spmv_outer(enprop_ctx* ctx, int ensemble_size, int num_rows, int num_cols, int64_t nnz,
+                      const int* row_map, const int* col_entry, const double* values,
+                      const double* x, double* z);
+
 /* dot (kernels.hpp:62-69): per-lane sums lanes_host[s] (may be NULL) and the
  * coupled reduce_sum coupled_host (may be NULL) in the given order.
  * seg_rows is the canonical segment length (ignored for SERIAL). */

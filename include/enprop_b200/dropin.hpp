@@ -173,6 +173,30 @@ Vector spmv(const Matrix& a, const Vector& x) {
   return z;
 }
 
+/// z = A x on the sample-major layout (spmv_outer, kernels.hpp:38-56): any
+/// matrix with num_rows / num_cols / ensemble_size / row_map / col_entry /
+/// values (OuterEnsembleMatrix, crs.hpp:138-147). z is resized to
+/// num_rows * ensemble_size.
+template <class OuterMatrix>
+void spmv_outer(const OuterMatrix& a, const std::vector<double>& x, std::vector<double>& z) {
+  const long long nnz = static_cast<long long>(a.col_entry.size());
+  const long long cols = static_cast<long long>(a.num_cols);
+  if (static_cast<long long>(x.size()) != cols * a.ensemble_size)
+    throw std::invalid_argument("spmv_outer: x length must equal num_cols*ensemble_size");
+  z.resize(static_cast<std::size_t>(a.num_rows) * a.ensemble_size);
+  if (a.num_rows == 0 || a.ensemble_size == 0) return;
+  detail::Buf rm(a.row_map.data(), a.row_map.size() * sizeof(int));
+  detail::Buf ce(a.col_entry.data(), a.col_entry.size() * sizeof(int));
+  detail::Buf va(a.values.data(), a.values.size() * sizeof(double));
+  detail::Buf dx(x.data(), x.size() * sizeof(double));
+  detail::Buf dz(z.size() * sizeof(double));
+  detail::check(enprop_spmv_outer(detail::Runtime::get().ctx, a.ensemble_size, a.num_rows,
+                                  a.num_cols, nnz, rm.as<int>(), ce.as<int>(), va.as<double>(),
+                                  dx.as<double>(), dz.as<double>()),
+                "spmv_outer");
+  dz.down(z.data(), z.size() * sizeof(double));
+}
+
 // ------------------------------------------------------------- dot, axpby
 /// Coupled inner product (kernels.hpp:62-69).
 template <class Vector>

@@ -354,6 +354,22 @@ void or_spmv(int S, int rows, const int* row_map, const int* col_entry, const do
     }
 }
 
+/* spmv_outer, proj/include/enprop/kernels.hpp:38-56: sample-major layout,
+ * component e sweeps the shared graph against values[e*nnz ...]. */
+void or_spmv_outer(int S, int rows, int cols, const int* row_map, const int* col_entry,
+                   const double* values, const double* x, double* z) {
+  const size_t nnz = (size_t)row_map[rows];
+  for (int e = 0; e < S; ++e) {
+    const double* ve = values + (size_t)e * nnz;
+    const double* xe = x + (size_t)e * cols;
+    for (int row = 0; row < rows; ++row) {
+      double sum = 0.0;
+      for (int k = row_map[row]; k < row_map[row + 1]; ++k) sum += ve[k] * xe[col_entry[k]];
+      z[(size_t)e * rows + row] = sum;
+    }
+  }
+}
+
 /* Per-lane dot in one of two orders.
  * SERIAL: proj/include/enprop/kernels.hpp:66-67 — acc = 0; acc += u*v row by row.
  * CANONICAL (the product's fast order, documented in DESIGN.md §4):

@@ -63,6 +63,9 @@ void or_apply_dirichlet(int S, int n, double bc_x0, double bc_x1, const int* row
 /* kernels.hpp:15-26 */
 void or_spmv(int S, int rows, const int* row_map, const int* col_entry, const double* values,
              const double* x, double* z);
+/* kernels.hpp:38-56 (sample-major: values[e*nnz+k], x[e*cols+c], z[e*rows+row]) */
+void or_spmv_outer(int S, int rows, int cols, const int* row_map, const int* col_entry,
+                   const double* values, const double* x, double* z);
 /* per-lane sums of u.v in the chosen order; kernels.hpp:62-69 for SERIAL */
 void or_dot_lanes(int S, int64_t n, const double* u, const double* v, int mode, int tile_rows,
                   int seg_rows, double* lanes /*[S]*/);

@@ -242,6 +242,23 @@ int ref_spmv(int s, int rows, int cols, const int* row_map, const int* col_entry
   });
 }
 
+// spmv_outer on OuterEnsembleMatrix (kernels.hpp:38-56, crs.hpp:138-147).
+int ref_spmv_outer(int s, int rows, int cols, const int* row_map, const int* col_entry,
+                   const double* values, const double* x, double* z) {
+  return guarded([&] {
+    OuterEnsembleMatrix a;
+    a.num_rows = rows;
+    a.num_cols = cols;
+    a.ensemble_size = s;
+    a.row_map.assign(row_map, row_map + rows + 1);
+    a.col_entry.assign(col_entry, col_entry + row_map[rows]);
+    a.values.assign(values, values + (size_t)row_map[rows] * s);
+    DenseVector<double> xx(x, x + (size_t)cols * s), zz;
+    spmv_outer(a, xx, zz);
+    std::copy(zz.begin(), zz.end(), z);
+  });
+}
+
 // Coupled dot (kernels.hpp:62-69).
 int ref_dot(int s, int64_t n, const double* u, const double* v, double* out) {
   return guarded([&] {

@@ -340,6 +340,25 @@ def spmv(ctx: Context, s: int, row_map, col_entry, values, x, z=None, num_cols=N
     return z
 
 
+def spmv_outer(ctx: Context, ensemble_size: int, row_map, col_entry, values, x, z=None, num_cols=None):
+    """z = A x on the sample-major layout (spmv_outer, kernels.hpp:38-56):
+    values [s][nnz], x [s][num_cols], z [s][num_rows]; bitwise equal to the
+    reference per component."""
+    s = ensemble_size
+    rows = row_map.numel() - 1
+    cols = rows if num_cols is None else num_cols
+    nnz = col_entry.numel()
+    if x.numel() != cols * s:
+        raise ValueError("spmv_outer: x length must equal num_cols*ensemble_size")
+    if values.numel() != nnz * s:
+        raise ValueError("spmv_outer: values length must equal nnz*ensemble_size")
+    if z is None:
+        z = torch.empty((s, rows), dtype=torch.float64, device=x.device)
+    _check(lib().enprop_spmv_outer(ctx.h, s, rows, cols, nnz, _ptr(row_map), _ptr(col_entry),
+                                   _ptr(values), _ptr(x), _ptr(z)), "spmv_outer")
+    return z
+
+
 def dot_lanes(ctx: Context, s: int, u, v, mode: int = DOT_SERIAL, seg_rows: int = 4096):
     if u.numel() != v.numel():
         raise ValueError("dot: length mismatch")

@@ -560,6 +560,19 @@ int enprop_spmv(enprop_ctx* c, int s, int rows, int cols, const int* row_map,
   return ENPROP_OK;
 }
 
+int enprop_spmv_outer(enprop_ctx* c, int s, int rows, int cols, int64_t nnz, const int* row_map,
+                      const int* col_entry, const double* values, const double* x, double* z) {
+  if (!c) return fail(ENPROP_ERR_INVALID, "null context");
+  if (s < 1) return fail(ENPROP_ERR_INVALID, "spmv_outer: ensemble_size must be at least 1");
+  if (rows < 0 || cols < 0 || nnz < 0) return fail(ENPROP_ERR_INVALID, "spmv_outer: negative dimension");
+  if (rows == 0) return ENPROP_OK;
+  if (!row_map || !z || (cols > 0 && !x) || (nnz > 0 && (!col_entry || !values)))
+    return fail(ENPROP_ERR_INVALID, "spmv_outer: null argument");
+  EP_CUDA(launch_spmv_outer(s, rows, cols, nnz, row_map, col_entry, values, x, z, c->stream));
+  c->launches += 1;
+  return ENPROP_OK;
+}
+
 int enprop_dot(enprop_ctx* c, int s, int64_t n, const double* u, const double* v, int dot_mode,
                int seg_rows, double* lanes_host, double* coupled_host) {
   if (!c) return fail(ENPROP_ERR_INVALID, "null context");

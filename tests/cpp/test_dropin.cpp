@@ -79,6 +79,27 @@ static void spmv_dot_axpby() {
   CHECK(same_bits(y1, y2));
 }
 
+// sample-major layout (test_kernels.cpp:127-143): spmv_outer on OuterEnsembleMatrix
+static void spmv_outer_layout(int s) {
+  for (int trial = 0; trial < 10; ++trial) {
+    const int rows = 1 + static_cast<int>(rng() % 60), cols = 1 + static_cast<int>(rng() % 60);
+    CrsMatrix<double> base = testutil::random_crs(rng, rows, cols, 0.15);
+    OuterEnsembleMatrix a;
+    a.num_rows = rows;
+    a.num_cols = cols;
+    a.ensemble_size = s;
+    a.row_map = base.row_map;
+    a.col_entry = base.col_entry;
+    a.values.resize(base.col_entry.size() * s);
+    for (auto& v : a.values) v = testutil::uniform_pm1(rng);
+    DenseVector<double> x(static_cast<std::size_t>(cols) * s), z1, z2;
+    for (auto& v : x) v = testutil::uniform_pm1(rng);
+    enprop::spmv_outer(a, x, z1);
+    enprop_b200::spmv_outer(a, x, z2);
+    CHECK(same_bits(z1, z2));
+  }
+}
+
 template <class Scalar>
 static void assembly_and_cg(int n) {
   StructuredMesh mesh(n);
@@ -155,6 +176,7 @@ int main() {
   spmv_dot_axpby<8>();
   spmv_dot_axpby<16>();
   spmv_dot_axpby<32>();
+  for (int s : {1, 3, 4, 32}) spmv_outer_layout(s);
 
   for (int n : {1, 3, 9}) {
     std::vector<int> rm, ce;

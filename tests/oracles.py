@@ -64,6 +64,7 @@ class Oracle:
                                   _dp, _dp, _dp, C.c_int, C.c_double, C.c_double, _dp, _dp]
         L.or_apply_dirichlet.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _ip, _ip, _dp, _dp, _dp]
         L.or_spmv.argtypes = [C.c_int, C.c_int, _ip, _ip, _dp, _dp, _dp]
+        L.or_spmv_outer.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip, _dp, _dp, _dp]
         L.or_dot_lanes.argtypes = [C.c_int, C.c_int64, _dp, _dp, C.c_int, C.c_int, C.c_int, _dp]
         L.or_dot.argtypes = [C.c_int, C.c_int64, _dp, _dp, C.c_int, C.c_int, C.c_int]
         L.or_axpby.argtypes = [C.c_int, C.c_int64, C.c_int, _dp, _dp, _dp, _dp]
@@ -111,6 +112,14 @@ class Oracle:
         self.lib.or_spmv(s, rows, iptr(row_map), iptr(col_entry), dptr(values), dptr(x), dptr(z))
         return z
 
+    def spmv_outer(self, s, row_map, col_entry, values, x, cols=None):
+        """values [s][nnz], x [s][cols] -> z [s][rows] (kernels.hpp:38-56)."""
+        rows = len(row_map) - 1
+        cols = rows if cols is None else cols
+        z = np.empty((s, rows))
+        self.lib.or_spmv_outer(s, rows, cols, iptr(row_map), iptr(col_entry), dptr(values), dptr(x), dptr(z))
+        return z
+
     def dot_lanes(self, s, u, v, mode=DOT_SERIAL, tile=TILE_ROWS, seg=4096):
         out = np.empty(s)
         self.lib.or_dot_lanes(s, u.shape[0], dptr(u), dptr(v), mode, tile, seg, dptr(out))
@@ -152,6 +161,7 @@ class RefLib:
                                       _dp, _dp]
         L.ref_apply_dirichlet.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _dp, _dp, _dp]
         L.ref_spmv.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip, _dp, _dp, _dp]
+        L.ref_spmv_outer.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip, _dp, _dp, _dp]
         L.ref_dot.argtypes = [C.c_int, C.c_int64, _dp, _dp, _dp]
         L.ref_axpby.argtypes = [C.c_int, C.c_int64, C.c_int, _dp, _dp, _dp, _dp]
         L.ref_pcg.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip, _dp, _dp, C.c_double, C.c_int,
@@ -215,6 +225,14 @@ class RefLib:
         z = np.empty((rows, s))
         self._check(self.lib.ref_spmv(s, rows, cols, iptr(row_map), iptr(col_entry),
                                       dptr(values), dptr(x), dptr(z)))
+        return z
+
+    def spmv_outer(self, s, row_map, col_entry, values, x, cols=None):
+        rows = len(row_map) - 1
+        cols = rows if cols is None else cols
+        z = np.empty((s, rows))
+        self._check(self.lib.ref_spmv_outer(s, rows, cols, iptr(row_map), iptr(col_entry),
+                                            dptr(values), dptr(x), dptr(z)))
         return z
 
     def dot(self, s, u, v):

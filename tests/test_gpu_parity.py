@@ -497,3 +497,41 @@ def test_staged_spmv_is_bitwise_equal_to_warp_kernel(ctx, mode, s, n, seg):
         assert a[1] == b[1]  # residual histories
         assert same(xa, host(p.solution))
     p.close()
+
+
+# ------------------------------------------------- sample-major (outer) layout
+@pytest.mark.parametrize("s", [1, 3, 4, 32])
+def test_spmv_outer_random_crs_bitwise(ctx, R, s):
+    """enprop_spmv_outer == the reference's spmv_outer (kernels.hpp:38-56)
+    bitwise on random CRS (empty rows, rectangular) and a long-row matrix that
+    exceeds the staging capacity (direct-read path)."""
+    rng = np.random.default_rng(40 + s)
+    shapes = [(int(rng.integers(1, 300)), int(rng.integers(1, 300)), 0.05) for _ in range(6)]
+    shapes.append((130, 200, 0.9))  # ~180 entries per row: > 28 * 128 per block
+    for rows, cols, dens in shapes:
+        rm, ce = random_crs(rng, rows, cols, dens)
+        vals = rng.uniform(-1, 1, (s, len(ce)))
+        x = rng.uniform(-1, 1, (s, cols))
+        z = ep.spmv_outer(ctx, s, dev(rm, torch.int32), dev(ce, torch.int32), dev(vals), dev(x), num_cols=cols)
+        assert same(host(z), R.spmv_outer(s, rm, ce, vals, x, cols))
+
+
+def test_spmv_outer_mesh_matrix_equals_ensemble_layout(ctx, R):
+    """On the assembled mesh matrix (16^3, s = 8): the sample-major product of the
+    transposed values equals the ensemble-layout product transposed, bitwise."""
+    s, n = 8, 16
+    rm, ce, v, _ = mesh_system(R, s, n)
+    x = np.random.default_rng(1).uniform(-1, 1, (len(rm) - 1, s))
+    zc = ep.spmv(ctx, s, dev(rm, torch.int32), dev(ce, torch.int32), dev(v), dev(x))
+    zo = ep.spmv_outer(ctx, s, dev(rm, torch.int32), dev(ce, torch.int32), dev(np.ascontiguousarray(v.T)),
+                       dev(np.ascontiguousarray(x.T)))
+    assert same(host(zo), host(zc).T)
+
+
+def test_spmv_outer_rejects_bad_lengths(ctx):
+    rm = dev(np.arange(5, dtype=np.int32), torch.int32)
+    ce = dev(np.arange(4, dtype=np.int32), torch.int32)
+    with pytest.raises(ValueError):
+        ep.spmv_outer(ctx, 2, rm, ce, dev(np.ones(8)), dev(np.ones(7)))
+    with pytest.raises(ValueError):
+        ep.spmv_outer(ctx, 2, rm, ce, dev(np.ones(7)), dev(np.ones(8)))

@@ -223,3 +223,33 @@ def test_oracle_matches_reference_cg_failures():
     b2 = np.array([[0.0], [1.0]])
     assert R.pcg(1, rm2, ce2, vals2, b2, 1e-8, 100, scalar=True)["status"] == 3
     assert O.pcg(1, rm2, ce2, vals2, b2, 1e-8, 100)["status"] == 3
+
+
+def _random_crs(rng, rows, cols, density):
+    """testutil::random_crs (tests/oracles.hpp:25-34): per-coordinate Bernoulli."""
+    mask = rng.uniform(0, 1, (rows, cols)) < density
+    rm = np.zeros(rows + 1, np.int32)
+    rm[1:] = np.cumsum(mask.sum(axis=1))
+    return rm, np.nonzero(mask)[1].astype(np.int32)
+
+
+@needs_ref
+@pytest.mark.parametrize("s", [1, 3, 4, 32])
+def test_spmv_outer_oracle_equals_reference(s):
+    """or_spmv_outer (the C restatement of kernels.hpp:38-56) == the reference's
+    spmv_outer bitwise, and each component == the scalar spmv of that component
+    (test_kernels.cpp:127-143)."""
+    R = RefLib()
+    rng = np.random.default_rng(3 + s)
+    for trial in range(10):
+        rows, cols = int(rng.integers(1, 60)), int(rng.integers(1, 60))
+        rm, ce = _random_crs(rng, rows, cols, 0.15)
+        nnz = len(ce)
+        vals = rng.uniform(-1, 1, (s, nnz))
+        x = rng.uniform(-1, 1, (s, cols))
+        zr = R.spmv_outer(s, rm, ce, vals, x, cols)
+        zo = O.spmv_outer(s, rm, ce, vals, x, cols)
+        assert same(zr, zo)
+        for e in range(s):
+            ze = R.spmv(1, rm, ce, np.ascontiguousarray(vals[e][:, None]), np.ascontiguousarray(x[e][:, None]), cols)
+            assert same(ze[:, 0], zr[e])
