@@ -463,7 +463,43 @@ def bench_spmv(ctx, ep, torch, pack_group, O, hbm, peak_kind, reps=20):
            "l2": "matrix 14.6 GB >> L2", "reps": reps}
     out["layouts"] = bench_spmv_layouts(ctx, ep, torch, p, x, z, byt, med, reps=max(5, reps // 4))
     p.close()
+    del vals, x, z
+    out["widths"] = bench_spmv_widths(ctx, ep, torch, pack_group, O, hbm, n, out["value"])
     return out
+
+
+def bench_spmv_widths(ctx, ep, torch, pack_group, O, hbm, n, gbs32, reps=10):
+    """Ensemble SpMV GB/s at s = 1, 4, 8, 16 on the same 128^3 matrix family
+    (north_star: throughput at ensemble sizes 1/4/8/16/32); s = 32 is cfg 3."""
+    res = {}
+    stream = torch.cuda.current_stream()
+    for s in (1, 4, 8, 16):
+        y = torch.as_tensor(pack_group(O.draw_samples(0, s, M_TERMS), s)).cuda()
+        p = ep.Problem(ctx, n, s, ep.KlField(M_TERMS, 1.0, SIGMA, 1.0))
+        p.assemble(y)
+        vals = p.values
+        g = torch.Generator(device="cuda").manual_seed(0)
+        x = torch.rand((p.rows, s), dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+        z = torch.empty_like(x)
+        for _ in range(3):
+            ep.spmv(ctx, s, p.row_map, p.col_entry, vals, x, z)
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            ep.spmv(ctx, s, p.row_map, p.col_entry, vals, x, z)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        med = statistics.median(ts)
+        byt = spmv_bytes(p.nnz, p.rows, s)
+        res[str(s)] = {"ms": round(med, 4), "gbs": round(byt / (med / 1e3) / 1e9, 1),
+                       "frac": round(byt / (med / 1e3) / 1e9 / hbm, 4),
+                       "kernel": f"k_spmv_small<{s}>" if s <= 8 else f"k_spmv<{s}>"}
+        p.close()
+        del vals, x, z
+    res["32"] = {"gbs": gbs32, "frac": round(gbs32 / hbm, 4), "kernel": "k_spmv<32>"}
+    return res
 
 
 def bench_spmv_layouts(ctx, ep, torch, p, x, z, byt, commuted_ms, reps=5):

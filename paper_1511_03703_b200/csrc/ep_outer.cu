@@ -60,6 +60,67 @@ __global__ void __launch_bounds__(kOuterRows) k_spmv_outer(int rows, int cols, i
   }
 }
 
+// Ensemble-layout SpMV for narrow ensembles (s <= 8): a row's s values are only
+// 8s <= 64 bytes, so one thread per (row, sample) walking its row would issue
+// strided, uncoalesced loads. Instead a CTA stages its row block's contiguous
+// column-index and value ranges in shared memory with coalesced loads, then
+// thread (row, sample e) sums its row in entry order from shared memory
+// (kernels.hpp:15-26, bitwise). Falls back to direct reads for blocks whose
+// entries exceed the staging capacity.
+template <int S>
+__global__ void __launch_bounds__(kOuterRows) k_spmv_small(int rows, const int* __restrict__ row_map,
+                                                           const int* __restrict__ col_entry,
+                                                           const double* __restrict__ values,
+                                                           const double* __restrict__ x,
+                                                           double* __restrict__ z) {
+  constexpr int RB = kOuterRows / S;   // rows per CTA
+  constexpr int CAP = RB * 28;         // staged entries
+  __shared__ int scol[CAP];
+  __shared__ double sval[CAP * S];
+  const int r0 = blockIdx.x * RB;
+  const int r1 = imin(r0 + RB, rows);
+  const int row = r0 + threadIdx.x / S, e = threadIdx.x % S;
+  const int k0 = __ldg(row_map + r0), k1 = __ldg(row_map + r1);
+  const int n = k1 - k0;
+  const bool staged = n <= CAP;
+  if (staged) {
+    for (int i = threadIdx.x; i < n; i += kOuterRows) scol[i] = ld_stream_i32(col_entry + k0 + i);
+    const double* v0 = values + (size_t)k0 * S;
+    for (int i = threadIdx.x; i < n * S; i += kOuterRows) sval[i] = ld_stream<1>(v0 + i).v[0];
+    __syncthreads();
+  }
+  if (row >= rows) return;
+  const int ks = __ldg(row_map + row) - k0, ke = __ldg(row_map + row + 1) - k0;
+  double sum = 0.0;
+  if (staged) {
+    for (int k = ks; k < ke; ++k) sum = EP_DADD(sum, EP_DMUL(sval[k * S + e], __ldg(x + (size_t)scol[k] * S + e)));
+  } else {
+    for (int k = k0 + ks; k < k0 + ke; ++k)
+      sum = EP_DADD(sum, EP_DMUL(__ldg(values + (size_t)k * S + e), __ldg(x + (size_t)__ldg(col_entry + k) * S + e)));
+  }
+  z[(size_t)row * S + e] = sum;
+}
+
+template <int S>
+static cudaError_t spmv_small_s(int rows, const int* row_map, const int* col_entry,
+                                const double* values, const double* x, double* z, cudaStream_t st) {
+  constexpr int RB = kOuterRows / S;
+  if (rows <= 0) return cudaSuccess;
+  k_spmv_small<S><<<(rows + RB - 1) / RB, kOuterRows, 0, st>>>(rows, row_map, col_entry, values, x, z);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spmv_small(int s, int rows, const int* row_map, const int* col_entry,
+                              const double* values, const double* x, double* z, cudaStream_t st) {
+  switch (s) {
+    case 1: return spmv_small_s<1>(rows, row_map, col_entry, values, x, z, st);
+    case 2: return spmv_small_s<2>(rows, row_map, col_entry, values, x, z, st);
+    case 4: return spmv_small_s<4>(rows, row_map, col_entry, values, x, z, st);
+    case 8: return spmv_small_s<8>(rows, row_map, col_entry, values, x, z, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_spmv_outer(int s, int rows, int cols, int64_t nnz, const int* row_map,
                               const int* col_entry, const double* values, const double* x,
                               double* z, cudaStream_t st) {

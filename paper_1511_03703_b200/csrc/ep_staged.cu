@@ -26,7 +26,9 @@
 // memory into registers, issued together as soon as the buffer is ready.
 // The register file therefore only holds the transposed gathers; the streamed
 // bytes are in flight in the TMA engine, a stage ahead of the compute.
+#include <atomic>
 #include <cstdio>
+#include <mutex>
 #include <vector>
 
 #include "ep_common.cuh"
@@ -427,23 +429,29 @@ template <int S>
 static cudaError_t cg_spmv_staged_s(bool tiles, const StageMap& sm, const double* values,
                                     const double* p, double* q, const FinArgs& f, cudaStream_t st) {
   using Sh = StagedShape<S>;
-  static int sms[64] = {0};  // per device: SM count, and the smem opt-in done
+  // per device: SM count, published only after the shared-memory opt-in is
+  // done (solves on several host threads launch concurrently)
+  static std::atomic<int> sms[64];
+  static std::mutex init_mu;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
-  if (!sms[dev]) {
-    cudaError_t err = cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
-    if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(k_cg_spmv_staged<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM);
-    if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(k_cg_spmv_staged<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM);
-    if (err != cudaSuccess) {
-      sms[dev] = 0;
-      return err;
+  if (!sms[dev].load(std::memory_order_acquire)) {
+    std::lock_guard<std::mutex> lock(init_mu);
+    if (!sms[dev].load(std::memory_order_relaxed)) {
+      int count = 0;
+      cudaError_t err = cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev);
+      if (err == cudaSuccess)
+        err = cudaFuncSetAttribute(k_cg_spmv_staged<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM);
+      if (err == cudaSuccess)
+        err = cudaFuncSetAttribute(k_cg_spmv_staged<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM);
+      if (err != cudaSuccess) return err;
+      sms[dev].store(count, std::memory_order_release);
     }
   }
+  const int nsm = sms[dev].load(std::memory_order_acquire);
   if (sm.nstages == 0) return cudaSuccess;
-  const int grid = sm.nstages < sms[dev] ? sm.nstages : sms[dev];
+  const int grid = sm.nstages < nsm ? sm.nstages : nsm;
   if (tiles)
     k_cg_spmv_staged<S, true><<<grid, 256, Sh::SMEM, st>>>(sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
                                                            values, p, q, f);
