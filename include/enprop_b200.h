@@ -232,6 +232,28 @@ int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* i
 int enprop_problem_solve_host(enprop_problem* p, const double* y_host, double* x_host,
                               const enprop_cg_options* opt, int* iterations, int* lane_status);
 
+/* NewtonOptions (fem.hpp:244-249) without the multigrid block: the linear
+ * solves use the identity preconditioner (IdentityPreconditioner, pcg.hpp:40-46). */
+typedef struct {
+  double tol;          /* on the coupled residual norm, relative to the first (default 1e-8) */
+  int max_iterations;  /* Newton steps (default 20) */
+  enprop_cg_options linear;
+} enprop_newton_options;
+
+/* newton_solve (fem.hpp:265-302) on the device-resident problem: from u = 0,
+ * assemble residual and Jacobian at u (nonlinear terms of the problem's
+ * PdeCoefficients), impose Dirichlet, stop when the coupled residual norm is
+ * below tol x the first (or the first is 0), else solve J du = -f by CG and
+ * u = 1.0*du + 1.0*u (axpby). y: device [num_terms][s]. The converged iterate is
+ * left in the problem's `solution` view. residual_norms (host, may be NULL,
+ * max_iterations + 1 entries) receives the norm before each step, num_norms
+ * their count; total_cg_iterations sums each linear solve's iterations (the
+ * maximum over lanes for uncoupled solves). Errors: NO_CONVERGENCE after
+ * max_iterations steps (norms filled), or the linear solver's failure. */
+int enprop_problem_newton(enprop_problem* p, const double* y, const enprop_newton_options* opt,
+                          int* newton_iterations, int* total_cg_iterations,
+                          double* residual_norms, int* num_norms);
+
 /* ------------------------------------ multi-GPU: slab domain decomposition */
 /* The node planes z = k of the mesh are split over nranks like the
  * reference's partition (partition.cpp:31-72; lower ranks take the extra

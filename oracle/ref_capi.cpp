@@ -324,6 +324,67 @@ int ref_pcg(int s, int scalar, int rows, const int* row_map, const int* col_entr
   });
 }
 
+// newton_solve (fem.hpp:265-302) composed from the reference's own pieces with
+// the multigrid preconditioner replaced by IdentityPreconditioner (the loop
+// below is fem.hpp:273-301 line for line otherwise): coupled ensemble CG.
+int ref_newton_identity(int s, int scalar, int n, int m, double mean, double sigma, double L,
+                        double alpha, double beta, const double* velocity, const double* y,
+                        double bc_x0, double bc_x1, double tol, int max_newton, double lin_tol,
+                        int lin_maxit, double* u_out, int* iterations, int* total_cg,
+                        double* norms, int* num_norms) {
+  *iterations = 0;
+  *total_cg = 0;
+  *num_norms = 0;
+  return guarded([&] {
+    StructuredMesh mesh(n);
+    AssemblyContext ctx(mesh);
+    KlField field(m, mean, sigma, L);
+    PdeCoefficients coeffs;
+    coeffs.alpha = alpha;
+    coeffs.beta = beta;
+    if (velocity) coeffs.velocity = {velocity[0], velocity[1], velocity[2]};
+    DirichletBc bc{bc_x0, bc_x1};
+    SolverConfig linear;
+    linear.tol = lin_tol;
+    linear.max_iterations = lin_maxit;
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      auto yy = from_raw<T>(y, m);
+      DenseVector<T> sol(mesh.num_nodes(), T(0.0));
+      AssembledSystem<T> system;
+      double initial_norm = 0.0;
+      auto out = [&] {
+        to_raw(sol, u_out);
+      };
+      for (int step = 0;; ++step) {
+        assemble<T>(ctx, field, coeffs, sol, std::span<const T>(yy), system);
+        apply_dirichlet(system, mesh, bc, sol);
+        const double residual_norm = norm2(system.residual);
+        norms[(*num_norms)++] = residual_norm;
+        if (step == 0) {
+          initial_norm = residual_norm;
+          if (initial_norm == 0.0) return out();
+        } else if (residual_norm < tol * initial_norm) {
+          *iterations = step;
+          return out();
+        }
+        if (step >= max_newton) {
+          *iterations = step;
+          out();
+          throw SolverError("newton_solve: no convergence", {});
+        }
+        DenseVector<T> rhs(system.residual.size());
+        for (std::size_t i = 0; i < rhs.size(); ++i) rhs[i] = -system.residual[i];
+        SolveResult<T> lin = pcg_solve(system.matrix, rhs, IdentityPreconditioner{}, linear);
+        *total_cg += lin.iterations;
+        axpby(1.0, lin.solution, 1.0, sol);
+      }
+    };
+    if (scalar && s == 1) run(double{});
+    else with_width(s, [&](auto w) { run(E<decltype(w)::value>{}); });
+  });
+}
+
 // draw_samples(seed, count, m) (samples.cpp:7-18) -> out[count][m].
 int ref_draw_samples(uint64_t seed, int count, int m, double* out) {
   return guarded([&] {

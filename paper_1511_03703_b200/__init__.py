@@ -76,6 +76,10 @@ class _CgOptions(C.Structure):
                 ("tol", C.c_double), ("max_iterations", C.c_int), ("check_every", C.c_int)]
 
 
+class _NewtonOptions(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iterations", C.c_int), ("linear", _CgOptions)]
+
+
 class _ProblemDesc(C.Structure):
     _fields_ = [("cells_per_axis", C.c_int), ("ensemble_size", C.c_int), ("kl", _KlParams),
                 ("coeffs", _Coeffs), ("bc", _Bc)]
@@ -125,6 +129,27 @@ class SolverConfig:
     def _c(self):
         return _CgOptions(self.flavour, self.dot_mode, self.seg_rows, self.tol,
                           self.max_iterations, self.check_every)
+
+
+@dataclass
+class NewtonOptions:
+    """NewtonOptions (fem.hpp:244-249); the linear solves use the identity
+    preconditioner (no multigrid block)."""
+    tol: float = 1e-8
+    max_iterations: int = 20
+    linear: SolverConfig = None
+
+    def _c(self):
+        return _NewtonOptions(self.tol, self.max_iterations, (self.linear or SolverConfig())._c())
+
+
+@dataclass
+class NewtonResult:
+    """NewtonResult (fem.hpp:251-257); the solution stays on the device
+    (Problem.solution)."""
+    iterations: int
+    total_cg_iterations: int
+    residual_norms: list
 
 
 _lib = None
@@ -476,6 +501,26 @@ class Problem:
         else:
             _check(rc, "solve")
         return iters, history, lstat
+
+    def newton(self, y: torch.Tensor, options: NewtonOptions = None,
+               raise_on_failure: bool = True) -> NewtonResult:
+        """newton_solve (fem.hpp:265-302) from u = 0 with this problem's
+        PdeCoefficients; the iterate ends in self.solution."""
+        _need_cuda(y, torch.float64, "y")
+        if y.numel() != self.kl.num_terms * self.s:
+            raise ValueError("newton: sample vector length mismatch")
+        opt = options or NewtonOptions()
+        it, cg, nn = C.c_int(), C.c_int(), C.c_int()
+        norms = (C.c_double * (max(opt.max_iterations, 0) + 1))()
+        rc = lib().enprop_problem_newton(self.h, _ptr(y), C.byref(opt._c()), C.byref(it), C.byref(cg),
+                                         norms, C.byref(nn))
+        res = NewtonResult(it.value, cg.value, [norms[i] for i in range(nn.value)])
+        if rc in (ERR_NO_CONVERGENCE, ERR_INDEFINITE):
+            if raise_on_failure:
+                raise SolverError(_err(), res.residual_norms, rc, res.iterations)
+        else:
+            _check(rc, "newton")
+        return res
 
     def solve_host(self, y_host: torch.Tensor, x_host: torch.Tensor, config: SolverConfig = None):
         """End to end from host buffers (pinned for speed)."""

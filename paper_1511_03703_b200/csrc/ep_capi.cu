@@ -671,6 +671,7 @@ struct enprop_problem {
   int* vpos = nullptr;   // symmetric storage (ENPROP_OPT_SYMMETRIC_STORAGE): slot of each entry
   int* up_start = nullptr;  // first stored slot of each row (rows + 1)
   int64_t nnz_stored = 0;
+  double* u = nullptr;      // Newton iterate (enprop_problem_newton)
   StageMap stage;           // stage-pipelined CG SpMV (ep_staged.cu), built on first solve
   int stage_failed = 0;
   AsmSetup setup;
@@ -713,7 +714,9 @@ int enprop_problem_create(enprop_ctx* c, const enprop_problem_desc* d, enprop_pr
     return cleanup(cuda_fail(err, "enprop_problem_create: graph"));
   c->launches += 1;
   p->nnz_stored = p->nnz;
-  if (c->symmetric_storage) {  // the assembled operator is exactly symmetric
+  // the assembled operator is exactly symmetric unless the
+  // advection term (alpha != 0, fem.hpp:167-191) is on
+  if (c->symmetric_storage && d->coeffs.alpha == 0.0) {
     if ((err = cudaMalloc(&p->vpos, p->nnz * sizeof(int))) != cudaSuccess ||
         (err = cudaMalloc(&p->up_start, (p->rows + 1) * sizeof(int))) != cudaSuccess ||
         (err = build_sym(p->rows, p->row_map, p->col_entry, p->vpos, &p->nnz_stored, c->stream,
@@ -732,7 +735,7 @@ int enprop_problem_create(enprop_ctx* c, const enprop_problem_desc* d, enprop_pr
 int enprop_problem_destroy(enprop_problem* p) {
   if (!p) return ENPROP_OK;
   for (void* q : {(void*)p->row_map, (void*)p->col_entry, (void*)p->values, (void*)p->residual,
-                  (void*)p->rhs, (void*)p->x, (void*)p->y, (void*)p->vpos, (void*)p->up_start})
+                  (void*)p->rhs, (void*)p->x, (void*)p->y, (void*)p->vpos, (void*)p->up_start, (void*)p->u})
     if (q) cudaFree(q);
   free_stage_map(p->stage);
   free_asm_setup(p->setup);
@@ -828,6 +831,83 @@ int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* i
   }
   return run_cg(p->ctx, s, p->rows, p->row_map, p->col_entry, p->values, p->rhs, p->x, &o, p->work,
                 iterations, lane_status, history, hist_len, p->vpos, stage);
+}
+
+int enprop_problem_newton(enprop_problem* p, const double* y, const enprop_newton_options* opt,
+                          int* newton_iterations, int* total_cg_iterations, double* residual_norms,
+                          int* num_norms) {
+  if (!p || !y || !opt) return fail(ENPROP_ERR_INVALID, "enprop_problem_newton: null argument");
+  if (opt->max_iterations < 0) return fail(ENPROP_ERR_INVALID, "newton_solve: negative max_iterations");
+  const int s = p->desc.ensemble_size;
+  int rc = validate_cg_options(&opt->linear, s);
+  if (rc) return rc;
+  enprop_ctx* c = p->ctx;
+  cudaStream_t st = c->stream;
+  const int64_t len = (int64_t)p->rows * s;
+  const size_t vec = (size_t)len * sizeof(double);
+  if (!p->u) EP_CUDA(cudaMalloc(&p->u, vec));
+  EP_CUDA(cudaMemsetAsync(p->u, 0, vec, st));  // result.solution = 0 (fem.hpp:271)
+  const int seg = (p->desc.cells_per_axis + 1) * (p->desc.cells_per_axis + 1);
+  int steps = 0, cg_total = 0, nn = 0;
+  double initial = 0.0;
+  auto finish = [&](int code) {
+    if (newton_iterations) *newton_iterations = steps;
+    if (total_cg_iterations) *total_cg_iterations = cg_total;
+    if (num_norms) *num_norms = nn;
+    cudaError_t err = cudaMemcpyAsync(p->x, p->u, vec, cudaMemcpyDeviceToDevice, st);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    if (err != cudaSuccess) return cuda_fail(err, "enprop_problem_newton");
+    return code;
+  };
+  for (int step = 0;; ++step) {
+    AsmArgs a = p->setup.args;  // assemble at u, Dirichlet fused (fem.hpp:275-276)
+    a.u = p->u;
+    a.y = y;
+    a.row_map = p->row_map;
+    a.values = p->values;
+    a.residual = p->residual;
+    a.vpos = p->vpos;
+    a.dirichlet = 1;
+    a.bc0 = p->desc.bc.x0_value;
+    a.bc1 = p->desc.bc.x1_value;
+    EP_CUDA(launch_assemble(s, a, st));
+    c->launches += 1;
+    double dot = 0.0;  // norm2(system.residual) (fem.hpp:277), coupled
+    rc = enprop_dot(c, s, len / s, p->residual, p->residual, opt->linear.dot_mode, seg, nullptr, &dot);
+    if (rc) return rc;
+    const double norm = std::sqrt(dot);
+    if (residual_norms && nn <= opt->max_iterations) residual_norms[nn] = norm;
+    ++nn;
+    if (step == 0) {
+      initial = norm;
+      if (initial == 0.0) return finish(ENPROP_OK);
+    } else if (norm < opt->tol * initial) {
+      steps = step;
+      return finish(ENPROP_OK);
+    }
+    if (step >= opt->max_iterations) {
+      steps = step;
+      finish(ENPROP_OK);
+      return fail(ENPROP_ERR_NO_CONVERGENCE, "newton_solve: no convergence within " +
+                                                 std::to_string(opt->max_iterations) + " iterations");
+    }
+    // rhs = -residual; J du = rhs by CG; u = 1.0*du + 1.0*u (fem.hpp:294-300)
+    const int lanes = opt->linear.flavour == ENPROP_CG_UNCOUPLED ? s : 1;
+    std::vector<int> its(lanes, 0), ls(lanes, 0);
+    rc = enprop_problem_solve(p, &opt->linear, its.data(), ls.data(), nullptr, nullptr);
+    int mx = 0;
+    for (int l = 0; l < lanes; ++l) mx = its[l] > mx ? its[l] : mx;
+    cg_total += mx;
+    if (rc) {
+      steps = step;
+      const std::string msg = g_last_error;
+      finish(ENPROP_OK);
+      return fail(rc, msg);
+    }
+    const double one = 1.0;
+    rc = enprop_axpby(c, s, len / s, 0, &one, p->x, &one, p->u);
+    if (rc) return rc;
+  }
 }
 
 int enprop_problem_solve_host(enprop_problem* p, const double* y_host, double* x_host,

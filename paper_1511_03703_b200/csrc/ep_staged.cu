@@ -206,6 +206,9 @@ struct StagedCta {
       }
       *reinterpret_cast<double2*>(rb + rr * S + lane0) = make_double2(c0, c1);
     }
+    // tile existence (first row slot of each tile), read before the barrier:
+    // thread 0 refills this index slot right after it
+    const bool tile_exists = threadIdx.x < 32 && ib[(threadIdx.x / S) * kTileRows] >= 0;
     __syncthreads();  // big buffer and index slot of stage it consumed, products in rb
     if (threadIdx.x == 0) {
       fence_proxy_async_smem();
@@ -216,7 +219,7 @@ struct StagedCta {
       if (threadIdx.x < 32) {  // tile trees: lane -> (tile, sample); v[i] += v[i+h], h = 8,4,2,1
         const int tt = threadIdx.x / S, e = threadIdx.x % S;
         const int b2 = stage_of(it) * Sh::T + tt;
-        if (ib[tt * kTileRows] >= 0) {  // the tile exists (its first row slot is a row)
+        if (tile_exists) {
           double v[kTileRows];
 #pragma unroll
           for (int h = 0; h < kTileRows; ++h) v[h] = rb[(tt * kTileRows + h) * S + e];

@@ -162,6 +162,10 @@ class RefLib:
         L.ref_apply_dirichlet.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _dp, _dp, _dp]
         L.ref_spmv.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip, _dp, _dp, _dp]
         L.ref_spmv_outer.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip, _dp, _dp, _dp]
+        L.ref_newton_identity.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                          C.c_double, C.c_double, C.c_double, _dp, _dp, C.c_double,
+                                          C.c_double, C.c_double, C.c_int, C.c_double, C.c_int, _dp,
+                                          _ip, _ip, _dp, _ip]
         L.ref_dot.argtypes = [C.c_int, C.c_int64, _dp, _dp, _dp]
         L.ref_axpby.argtypes = [C.c_int, C.c_int64, C.c_int, _dp, _dp, _dp, _dp]
         L.ref_pcg.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip, _dp, _dp, C.c_double, C.c_int,
@@ -234,6 +238,22 @@ class RefLib:
         self._check(self.lib.ref_spmv_outer(s, rows, cols, iptr(row_map), iptr(col_entry),
                                             dptr(values), dptr(x), dptr(z)))
         return z
+
+    def newton_identity(self, s, n, m, y, sigma=0.2, mean=1.0, L=1.0, alpha=0.0, beta=0.0,
+                        velocity=(1.0, 0.0, 0.0), bc=(1.0, 0.0), tol=1e-8, max_newton=20,
+                        lin_tol=1e-8, lin_maxit=1000):
+        """fem.hpp:265-302 with IdentityPreconditioner, from the reference's pieces
+        (oracle/ref_capi.cpp ref_newton_identity). Returns (rc, u, its, cg, norms)."""
+        rows = (n + 1) ** 3
+        u = np.zeros((rows, s))
+        it, cg, nn = (np.zeros(1, np.int32) for _ in range(3))
+        norms = np.zeros(max_newton + 2)
+        vel = np.array(velocity, dtype=np.float64)
+        rc = self.lib.ref_newton_identity(s, 0, n, m, mean, sigma, L, alpha, beta, dptr(vel),
+                                          dptr(np.ascontiguousarray(y, dtype=np.float64)), bc[0], bc[1],
+                                          tol, max_newton, lin_tol, lin_maxit, dptr(u), iptr(it),
+                                          iptr(cg), dptr(norms), iptr(nn))
+        return rc, u, int(it[0]), int(cg[0]), list(norms[:nn[0]])
 
     def dot(self, s, u, v):
         out = C.c_double()

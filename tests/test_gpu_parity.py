@@ -535,3 +535,64 @@ def test_spmv_outer_rejects_bad_lengths(ctx):
         ep.spmv_outer(ctx, 2, rm, ce, dev(np.ones(8)), dev(np.ones(7)))
     with pytest.raises(ValueError):
         ep.spmv_outer(ctx, 2, rm, ce, dev(np.ones(7)), dev(np.ones(8)))
+
+
+# ---------------------------------------------------------------- Newton (f.3)
+@pytest.mark.parametrize("s", [1, 4, 32])
+@pytest.mark.parametrize("beta", [0.0, 1.0])
+def test_newton_matches_reference_composition_bitwise(ctx, R, s, beta):
+    """enprop_problem_newton == newton_solve (fem.hpp:265-302) composed from the
+    reference's assemble / apply_dirichlet / norm2 / pcg_solve(Identity) / axpby
+    (oracle/ref_capi.cpp), serial dots, coupled CG: iterate, Newton steps, total
+    CG iterations and residual norms bitwise (reaction term on and off;
+    symmetric storage stays valid with the reaction term)."""
+    n, m = 5, 5
+    y = pack_group(R.draw_samples(19, s, m), s)
+    coeffs = ep.PdeCoefficients(0.0, beta)
+    p = ep.Problem(ctx, n, s, ep.KlField(m, 1.0, 0.2, 1.0), coeffs=coeffs)
+    opt = ep.NewtonOptions(tol=1e-8, max_iterations=20,
+                           linear=ep.SolverConfig(tol=1e-10, max_iterations=1000, dot_mode=DOT_SERIAL))
+    res = p.newton(dev(y), opt)
+    rc, u, its, cg, norms = R.newton_identity(s, n, m, y, sigma=0.2, beta=beta, lin_tol=1e-10)
+    assert rc == 0
+    assert res.iterations == its and res.total_cg_iterations == cg
+    assert same(np.array(res.residual_norms), np.array(norms))
+    assert same(host(p.solution), u)
+    assert its == (1 if beta == 0.0 else its) and (beta == 0.0 or its >= 2)
+    p.close()
+
+
+def test_newton_exhaustion_raises_with_norms(ctx, R):
+    n, m, s = 4, 5, 2
+    y = pack_group(R.draw_samples(19, s, m), s)
+    p = ep.Problem(ctx, n, s, ep.KlField(m, 1.0, 0.2, 1.0), coeffs=ep.PdeCoefficients(0.0, 1.0))
+    opt = ep.NewtonOptions(tol=1e-30, max_iterations=2,
+                           linear=ep.SolverConfig(tol=1e-10, dot_mode=DOT_SERIAL))
+    with pytest.raises(ep.SolverError) as e:
+        p.newton(dev(y), opt)
+    assert len(e.value.history()) == 3  # norms before steps 0, 1, 2
+    p.close()
+
+
+@pytest.mark.parametrize("variant", [-1, 2])
+def test_problem_canonical_cg_equals_restatement_straddling_stages(ctx, R, variant):
+    """30^3, s = 16: a plane is 61 canonical tiles (60 full + 1 row), so the
+    staged kernel's two-tile stages straddle planes with a one-row first tile,
+    and each CTA cycles its stage rings several times. Both SpMV kernels must
+    reproduce the C restatement of canonical CG bitwise (coupled)."""
+    n, s, m = 30, 16, 3
+    N = n + 1
+    rm, ce, v, b = mesh_system(R, s, n)
+    y = pack_group(R.draw_samples(0, s, m), s)
+    p = ep.Problem(ctx, n, s, ep.KlField(m, 1.0, 0.1, 1.0))
+    p.assemble(dev(y))
+    cfg = ep.SolverConfig(tol=1e-6, max_iterations=1000, flavour=CG_COUPLED, dot_mode=DOT_CANONICAL)
+    ctx.set_option(ep.OPT_SPMV_VARIANT, variant)
+    try:
+        it, _, _ = p.solve(cfg)
+    finally:
+        ctx.set_option(ep.OPT_SPMV_VARIANT, -1)
+    o = O.pcg(s, rm, ce, v, b, 1e-6, 1000, flavour=CG_COUPLED, mode=DOT_CANONICAL, seg=N * N)
+    assert it == o["iterations"][0]
+    assert same(host(p.solution), o["x"])
+    p.close()

@@ -253,3 +253,24 @@ def test_spmv_outer_oracle_equals_reference(s):
         for e in range(s):
             ze = R.spmv(1, rm, ce, np.ascontiguousarray(vals[e][:, None]), np.ascontiguousarray(x[e][:, None]), cols)
             assert same(ze[:, 0], zr[e])
+
+
+@needs_ref
+def test_newton_identity_oracle_properties():
+    """The reference-composed Newton (fem.hpp:265-302 with the identity
+    preconditioner, oracle/ref_capi.cpp) on test_mesh_fem.cpp:240-258's
+    reaction-diffusion case: 2..6 steps, residual down by 1e-8, iterate in the
+    boundary band; and one step on the linear problem with the exact 1 - x
+    profile (test_mesh_fem.cpp:220-237)."""
+    R = RefLib()
+    y = O.draw_samples(19, 1, 5).reshape(5, 1)
+    rc, u, its, cg, norms = R.newton_identity(1, 4, 5, y, sigma=0.2, beta=1.0)
+    assert rc == 0 and 2 <= its <= 6 and cg > 0
+    assert norms[-1] < 1e-8 * norms[0]
+    assert (u > -0.05).all() and (u < 1.05).all()
+    for n in (2, 4):
+        rc, u, its, cg, norms = R.newton_identity(1, n, 1, np.zeros((1, 1)), sigma=0.0, lin_tol=1e-13)
+        assert rc == 0 and its == 1
+        N = n + 1
+        x = (np.arange(N ** 3) % N) / n
+        assert np.abs(u[:, 0] - (1 - x)).max() < 1e-10
