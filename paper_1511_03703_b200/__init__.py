@@ -24,7 +24,7 @@ from typing import Optional, Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libenprop_b200.so")
+LIB_PATH = os.environ.get("ENPROP_B200_LIB") or os.path.join(_HERE, "lib", "libenprop_b200.so")  # override: A/B builds
 
 OK, ERR_INVALID, ERR_NO_CONVERGENCE, ERR_INDEFINITE, ERR_CUDA, ERR_OOM = range(6)
 DOT_SERIAL, DOT_CANONICAL = 0, 1

@@ -147,7 +147,8 @@ struct StageDesc {
   int R0, R1;        // rows [R0, R1) of the stage
   int slot0, slot1;  // stored slots of those rows (symmetric storage)
   int64_t blk_off;   // index block (bytes, 16-aligned)
-  int blk_bytes, pad;
+  int blk_bytes;
+  int g;             // canonical stage id (tiles g*T ...); desc is stored in sweep order
 };
 
 struct StageMap {

@@ -26,8 +26,10 @@
 // memory into registers, issued together as soon as the buffer is ready.
 // The register file therefore only holds the transposed gathers; the streamed
 // bytes are in flight in the TMA engine, a stage ahead of the compute.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -50,7 +52,8 @@ struct StagedShape {
   static constexpr int X_CHUNKS = 9 * L;
   static constexpr int ZC = UP_CHUNKS + X_CHUNKS;   // the zero chunk (padding entries)
   static constexpr int BIG_BYTES = (ZC + 1) * CH;
-  static constexpr int IDX_BYTES = 2 * RS * 4 + RS * ROWE * 4 + RS * ROWX * 2;
+  static constexpr int HDR = 2 * RS + 4;            // ints: srow[RS], spch[RS], stage id, pad
+  static constexpr int IDX_BYTES = HDR * 4 + RS * ROWE * 4 + RS * ROWX * 2;
   static constexpr int NIDX = 4;                    // index blocks in flight (ring depth)
   static constexpr int RED_BYTES = RS * S * 8;
   static constexpr int SMEM = 2 * BIG_BYTES + NIDX * IDX_BYTES + 2 * RED_BYTES + 64;
@@ -84,6 +87,9 @@ struct StagedCta {
   uint64_t pol;
   int rr, lane0;
 
+  // the it-th stage of this CTA: position blockIdx.x + it*grid of the sweep
+  // order (desc and index blocks are stored in sweep order; desc[pos].g is the
+  // stage's canonical id)
   __device__ __forceinline__ int stage_of(int it) const { return (int)blockIdx.x + it * (int)gridDim.x; }
   __device__ __forceinline__ bool has(int it) const { return stage_of(it) < nstages; }
   __device__ __forceinline__ unsigned char* big(int it) const { return smem + (it & 1) * Sh::BIG_BYTES; }
@@ -123,7 +129,7 @@ struct StagedCta {
   }
 
   __device__ __forceinline__ void gather(int it, StageGather& G) const {
-    const int4* sa = reinterpret_cast<const int4*>(idx(it) + 2 * Sh::RS + rr * Sh::ROWE);
+    const int4* sa = reinterpret_cast<const int4*>(idx(it) + Sh::HDR + rr * Sh::ROWE);
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const int4 w = sa[v];
@@ -156,7 +162,7 @@ struct StagedCta {
     const int pch = ib[Sh::RS + rr];
     int ca[12];  // codes of entries 16..27
     {
-      const int4* sa = reinterpret_cast<const int4*>(ib + 2 * Sh::RS + rr * Sh::ROWE) + 4;
+      const int4* sa = reinterpret_cast<const int4*>(ib + Sh::HDR + rr * Sh::ROWE) + 4;
 #pragma unroll
       for (int v = 0; v < 3; ++v) {
         const int4 w = sa[v];
@@ -165,7 +171,7 @@ struct StagedCta {
     }
     int cx[kStageMaxRow];
     {
-      const uint4* sx = reinterpret_cast<const uint4*>(ib + 2 * Sh::RS + Sh::RS * Sh::ROWE) + rr * 4;
+      const uint4* sx = reinterpret_cast<const uint4*>(ib + Sh::HDR + Sh::RS * Sh::ROWE) + rr * 4;
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
         const uint4 w = sx[v];
@@ -209,6 +215,7 @@ struct StagedCta {
     // tile existence (first row slot of each tile), read before the barrier:
     // thread 0 refills this index slot right after it
     const bool tile_exists = threadIdx.x < 32 && ib[(threadIdx.x / S) * kTileRows] >= 0;
+    const int gid = ib[2 * Sh::RS];  // canonical stage id (tile trees)
     __syncthreads();  // big buffer and index slot of stage it consumed, products in rb
     if (threadIdx.x == 0) {
       fence_proxy_async_smem();
@@ -218,7 +225,7 @@ struct StagedCta {
     if constexpr (kTiles) {
       if (threadIdx.x < 32) {  // tile trees: lane -> (tile, sample); v[i] += v[i+h], h = 8,4,2,1
         const int tt = threadIdx.x / S, e = threadIdx.x % S;
-        const int b2 = stage_of(it) * Sh::T + tt;
+        const int b2 = gid * Sh::T + tt;
         if (tile_exists) {
           double v[kTileRows];
 #pragma unroll
@@ -275,10 +282,12 @@ __global__ void __launch_bounds__(256, 1) k_cg_spmv_staged(
 }
 
 // ---- stage map ---------------------------------------------------------------
-// Index block of stage g at blk + g * IDX_BYTES, by row slot rr = ti*16 + t
-// (tile ti of the stage, row t of the tile):
+// Index block of the stage at sweep position pos (blk + pos * IDX_BYTES; the
+// stage's canonical id g = desc[pos].g), by row slot rr = ti*16 + t (tile ti
+// of the stage, row t of the tile):
 //   int srow[RS]       the slot's row, -1 if none
 //   int spch[RS]       chunk of the row's own p in the stage buffer
+//   int g, pad[3]      canonical stage id (tiles g*T + ti)
 //   int sa[RS][28]     value of entry k: >= 0 global slot (transposed entry of an
 //                      earlier stage's row), < 0: -(chunk + 1) in the stage buffer
 //   u16 sx[RS][32]     chunk of entry k's x operand: UP_CHUNKS + run*L + lr + di + 1,
@@ -291,11 +300,14 @@ __global__ void k_stage_fill(const TileMap tm, int nstages, int T, int N, int L,
                              unsigned char* __restrict__ blk, int* __restrict__ bad) {
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= nstages * RS) return;
-  const int g = gid / RS, rr = gid % RS;
-  const StageDesc d = desc[g];
-  int* ib = reinterpret_cast<int*>(blk + (size_t)g * idx_bytes);
-  int* sa = ib + 2 * RS + rr * 28;
-  uint16_t* sx = reinterpret_cast<uint16_t*>(ib + 2 * RS + RS * 28) + rr * 32;
+  const int pos = gid / RS, rr = gid % RS;  // sweep position, row slot
+  const StageDesc d = desc[pos];
+  const int g = d.g;                          // canonical stage id
+  int* ib = reinterpret_cast<int*>(blk + (size_t)pos * idx_bytes);
+  const int hdr = 2 * RS + 4;
+  int* sa = ib + hdr + rr * 28;
+  uint16_t* sx = reinterpret_cast<uint16_t*>(ib + hdr + RS * 28) + rr * 32;
+  if (rr == 0) ib[2 * RS] = g;  // stage id for the tile trees
   const int b = g * T + rr / kTileRows, t = rr % kTileRows;
   int r0 = 0, nr = 0;
   if (b < tm.num_tiles()) tm.tile(b, r0, nr);
@@ -395,12 +407,42 @@ cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
     hd.push_back(d);
   }
   sm.nstages = (int)hd.size();
+  // Sweep order: stages grouped by bands of B mesh lines (B*N ~ 4096 rows per
+  // plane), each band swept through all planes. A row's transposed (lower)
+  // slots live one plane back in the same band, ~4096 rows of stored slots
+  // (~15 MB at s = 32) earlier in the sweep: still in L2 even when a whole
+  // plane is not (256^3: 237 MB of stored slots per plane).
+  std::vector<int> ord(hd.size());
+  {
+    const int NN = N * N;
+    const int B = 4096 / N > 1 ? 4096 / N : 1;
+    std::vector<int64_t> key(hd.size());
+    for (size_t g = 0; g < hd.size(); ++g) {
+      const int r = hd[g].R0;
+      const int k = r / NN, j = (r - k * NN) / N;
+      key[g] = ((int64_t)(j / B) * N + k) * (int64_t)NN + (r - k * NN);
+      ord[g] = (int)g;
+    }
+    const char* env = getenv("ENPROP_STAGED_ORDER");  // "0": plain round-robin (A/B)
+    if (!env || atoi(env) != 0)
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return key[a] < key[b]; });
+  }
+  {  // store descriptors and index blocks in sweep order
+    std::vector<StageDesc> sorted(hd.size());
+    for (size_t q = 0; q < hd.size(); ++q) {
+      sorted[q] = hd[ord[q]];
+      sorted[q].g = ord[q];
+      sorted[q].blk_off = (int64_t)q * idx_bytes;
+    }
+    hd.swap(sorted);
+  }
   sm.s = s;
   sm.N = N;
   sm.tm = tm;
   sm.blk_bytes = off;
   int* bad = nullptr;
   err = cudaMalloc(&sm.desc, hd.size() * sizeof(StageDesc) + 16);
+
   if (err == cudaSuccess) err = cudaMalloc(&sm.blk, off + 16);
   if (err == cudaSuccess) err = cudaMalloc(&bad, sizeof(int));
   if (err == cudaSuccess) err = cudaMemsetAsync(bad, 0, sizeof(int), st);

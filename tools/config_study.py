@@ -3,6 +3,8 @@
   cfg1  32^3, m=3, sigma=0.1, s=16, tol 1e-6 (the reference's CPU case)
   cfg2  64^3, m=3, sigma=0.1, tol 1e-6, s in {1,4,8,16,32}: samples/s, coupled and uncoupled
   cfg5  128^3, m=10, sigma=0.25, s=32, tol 1e-6: coupled vs uncoupled iterations and samples/s
+  cfg4  256^3, m=3, sigma=0.1, s=32, tol 1e-6 on ONE GPU through the device-resident
+        problem (symmetric storage, staged SpMV); the slab path is bench.py --workload dd
 
 Each line: one sample group (seed 0, group 0) assembled + solved on the device,
 timed with CUDA events (one stream; no inter-group concurrency), canonical dot
@@ -65,6 +67,9 @@ def main():
         for s in (1, 4, 8, 16, 32):
             for fl in (ep.CG_COUPLED, ep.CG_UNCOUPLED):
                 print(json.dumps(solve_line(ctx, O, 64, s, 3, 0.1, fl, args.dot, tag="cfg2")), flush=True)
+    if "4" in which:
+        print(json.dumps(solve_line(ctx, O, 256, 32, 3, 0.1, ep.CG_UNCOUPLED, args.dot, reps=1, tag="cfg4-1gpu")),
+              flush=True)
     if "5" in which:
         for fl in (ep.CG_COUPLED, ep.CG_UNCOUPLED):
             print(json.dumps(solve_line(ctx, O, 128, 32, 10, 0.25, fl, args.dot, reps=1, tag="cfg5")), flush=True)
