@@ -79,11 +79,15 @@ int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
  *   (entries per gather batch / CTAs per SM): 0: 4/4, 1: 4/4 + index prefetch,
  *   2: 8/2, 3: 8/2 + index prefetch, 4: 4/4 zero-padded, 5: 8/3, 6: 16/1;
  *   auto = 2 with symmetric storage, 0 otherwise. */
+/*   ENPROP_OPT_PDL (default 1, process-wide): launch the CG loop's kernels with
+ *   programmatic dependent launch (the next kernel is scheduled while the
+ *   previous one drains; it waits for its completion before reading). */
 enum {
   ENPROP_OPT_FUSED_DIRECTION = 1,
   ENPROP_OPT_SPMV_PIPELINE = 2,
   ENPROP_OPT_SYMMETRIC_STORAGE = 3,
-  ENPROP_OPT_SPMV_VARIANT = 5
+  ENPROP_OPT_SPMV_VARIANT = 5,
+  ENPROP_OPT_PDL = 6
 };
 int enprop_ctx_set_option(enprop_ctx* ctx, int option, int value);
 /* Event timing of the CG SpMV kernel launches on the context stream (used by

@@ -34,6 +34,7 @@ OPT_FUSED_DIRECTION = 1
 OPT_SPMV_PIPELINE = 2
 OPT_SYMMETRIC_STORAGE = 3
 OPT_SPMV_VARIANT = 5
+OPT_PDL = 6
 WIDTHS = (1, 2, 4, 8, 16, 32)
 
 _dp = C.POINTER(C.c_double)

@@ -368,6 +368,9 @@ int enprop_ctx_set_option(enprop_ctx* c, int option, int value) {
     case ENPROP_OPT_SPMV_VARIANT:
       set_spmv_variant(value);
       return ENPROP_OK;
+    case ENPROP_OPT_PDL:
+      set_pdl_enabled(value ? 1 : 0);
+      return ENPROP_OK;
 
     default:
       return fail(ENPROP_ERR_INVALID, "enprop_ctx_set_option: unknown option");

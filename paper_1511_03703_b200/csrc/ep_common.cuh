@@ -7,6 +7,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "ep_tilemap.h"
 
@@ -180,6 +181,68 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// Kernels of the CG loop are launched with programmatic stream serialization
+// (launch_k): the next kernel's CTAs may be scheduled while this one drains.
+// Every such kernel starts with EP_PDL_ENTRY(): allow the dependent grid to be
+// scheduled (once all of this grid's CTAs have started, so it never takes SMs
+// from them), then wait until the preceding grid has completed and its memory
+// is visible -- before any read of its results. Without the launch attribute
+// both instructions are no-ops.
+#define EP_PDL_ENTRY()                                                  \
+  do {                                                                  \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");     \
+    asm volatile("griddepcontrol.wait;" ::: "memory");                  \
+  } while (0)
+
+// process-wide switch (ENPROP_OPT_PDL, default on)
+inline int& pdl_enabled() {
+  static int on = 1;
+  return on;
+}
+
+// ENPROP_PDL_MASK (env, tuning): kernel kinds launched with PDL (1 direction,
+// 2 SpMV, 4 finalize, 8 update, 16 other); default all
+inline int pdl_mask() {
+  static int m = [] {
+    const char* e = getenv("ENPROP_PDL_MASK");
+    return e ? atoi(e) : 31;
+  }();
+  return m;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_kk(int kind, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl_enabled() && (pdl_mask() & kind)) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 }  // namespace ep

@@ -306,6 +306,7 @@ constexpr int kStreamPasses = 4;  // rows per thread in the streaming (dot/updat
 template <int S>
 __global__ void __launch_bounds__(256) k_dot_tiles(const TileMap tm, const double* __restrict__ u,
                                                    const double* __restrict__ v, const FinArgs f) {
+  EP_PDL_ENTRY();
   constexpr int P = kStreamPasses;
   using Sh = TileShape<S, P>;
   constexpr int V = Sh::V;
@@ -337,7 +338,7 @@ static cudaError_t dot_tiles_s(const TileMap& tm, const double* u, const double*
   using Sh = TileShape<S, kStreamPasses>;
   const int blocks = (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC;
   if (blocks == 0) return cudaSuccess;
-  k_dot_tiles<S><<<blocks, Sh::NT, 0, st>>>(tm, u, v, f);
+  launch_kk(16, k_dot_tiles<S>, dim3(blocks), dim3(Sh::NT), 0, st, tm, u, v, f);
   return cudaGetLastError();
 }
 
@@ -539,6 +540,7 @@ constexpr int kFinItems2 = 12;  // (segment, sample) items per thread per round 
 
 template <int S>
 __global__ void __launch_bounds__(kFinThreads) k_fin_segments(const TileMap tm, const FinArgs f) {
+  EP_PDL_ENTRY();
   if ((f.phase == kPhasePQ || f.phase == kPhaseRR) && f.cg->done) return;
   constexpr int CHUNK = kFinThreads * kFinItems / S;    // blocks per round
   constexpr int CHUNK2 = kFinThreads * kFinItems2 / S;  // segments per round
@@ -616,7 +618,7 @@ __global__ void __launch_bounds__(kFinThreads) k_fin_segments(const TileMap tm, 
 template <int S>
 static cudaError_t fin_segments_s(const TileMap& tm, const FinArgs& f, cudaStream_t st) {
   if (tm.num_segs == 0) return cudaSuccess;
-  k_fin_segments<S><<<tm.num_segs, kFinThreads, 0, st>>>(tm, f);
+  launch_kk(4, k_fin_segments<S>, dim3(tm.num_segs), dim3(kFinThreads), 0, st, tm, f);
   return cudaGetLastError();
 }
 
@@ -632,6 +634,7 @@ template <int S>
 __global__ void __launch_bounds__(256) k_fin_gathered(int planes, const double* __restrict__ gathered,
                                                       const int* __restrict__ plane_pos, int phase,
                                                       CgState* cg, double* hist, double* lanes_out) {
+  EP_PDL_ENTRY();
   if ((phase == kPhasePQ || phase == kPhaseRR) && cg->done) return;
   constexpr int kChunk = 64;
   __shared__ double sch[kChunk * S];
@@ -657,7 +660,7 @@ template <int S>
 static cudaError_t fin_gathered_s(int planes, const double* gathered, const int* plane_pos,
                                   int phase, CgState* cg, double* hist, double* lanes_out,
                                   cudaStream_t st) {
-  k_fin_gathered<S><<<1, 256, 0, st>>>(planes, gathered, plane_pos, phase, cg, hist, lanes_out);
+  launch_kk(4, k_fin_gathered<S>, dim3(1), dim3(256), 0, st, planes, gathered, plane_pos, phase, cg, hist, lanes_out);
   return cudaGetLastError();
 }
 
@@ -688,6 +691,7 @@ struct SerialShape {
 template <int S>
 __global__ void __launch_bounds__(32 * SerialShape<S>::LG) k_fin_serial(
     int rows, const double* __restrict__ u, const double* __restrict__ v, const FinArgs f) {
+  EP_PDL_ENTRY();
   using Sh = SerialShape<S>;
   constexpr int K = kSerialK;
   if ((f.phase == kPhasePQ || f.phase == kPhaseRR) && f.cg->done) return;
@@ -757,7 +761,7 @@ template <int S>
 static cudaError_t fin_serial_s(int rows, const double* u, const double* v, const FinArgs& f,
                                 cudaStream_t st) {
   using Sh = SerialShape<S>;
-  k_fin_serial<S><<<Sh::GROUPS, 32 * Sh::LG, 0, st>>>(rows, u, v, f);
+  launch_kk(4, k_fin_serial<S>, dim3(Sh::GROUPS), dim3(32 * Sh::LG), 0, st, rows, u, v, f);
   return cudaGetLastError();
 }
 
@@ -796,6 +800,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
     const double* __restrict__ p_old, double* __restrict__ p_new, double* __restrict__ q,
     double* __restrict__ x, const double* __restrict__ p_gather, const int* __restrict__ vpos,
     const FinArgs f) {
+  EP_PDL_ENTRY();
   using Sh = TileShape<S, 1>;
   constexpr int V = Sh::V;
   const CgState* cg = f.cg;
@@ -1004,6 +1009,7 @@ __global__ void __launch_bounds__(256, SpmvVariant<kVar>::kMinBlocks) k_cg_spmv_
     const TileMap tm, const int* __restrict__ row_map, const int* __restrict__ col_entry,
     const double* __restrict__ values, const double* __restrict__ p_new, double* __restrict__ q,
     const double* __restrict__ p_gather, const int* __restrict__ vpos, const FinArgs f) {
+  EP_PDL_ENTRY();
   using Sh = WarpTile<S>;
   using Var = SpmvVariant<kVar>;
   constexpr int V = Sh::V, TPR = Sh::TPR, R = Sh::R;
@@ -1102,6 +1108,7 @@ __global__ void __launch_bounds__(256) k_cg_direction(int rows, const double* __
                                                       double* __restrict__ p_new,
                                                       double* __restrict__ x,
                                                       const CgState* __restrict__ cg) {
+  EP_PDL_ENTRY();
   constexpr int P = kDirPasses;
   using Sh = TileShape<S, P>;
   constexpr int V = Sh::V;
@@ -1154,6 +1161,7 @@ __global__ void __launch_bounds__(256) k_cg_flush(int rows, double* __restrict__
                                                   const double* __restrict__ p0,
                                                   const double* __restrict__ p1,
                                                   const CgState* __restrict__ cg) {
+  EP_PDL_ENTRY();
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= (int64_t)rows * S) return;
   const int e = (int)(g % S);
@@ -1167,7 +1175,7 @@ static cudaError_t cg_flush_s(int rows, double* x, double* const* p, const CgSta
                               cudaStream_t st) {
   const int64_t t = (int64_t)rows * S;
   if (t == 0) return cudaSuccess;
-  k_cg_flush<S><<<(int)((t + 255) / 256), 256, 0, st>>>(rows, x, p[0], p[1], cg);
+  launch_kk(16, k_cg_flush<S>, dim3((int)((t + 255) / 256)), dim3(256), 0, st, rows, x, p[0], p[1], cg);
   return cudaGetLastError();
 }
 
@@ -1181,7 +1189,7 @@ static cudaError_t cg_direction_s(int rows, const double* r, const double* p_old
                                   double* x, const CgState* cg, cudaStream_t st) {
   using Sd = TileShape<S, kDirPasses>;
   if (rows <= 0) return cudaSuccess;
-  k_cg_direction<S><<<(rows + Sd::ROWS - 1) / Sd::ROWS, 256, 0, st>>>(rows, r, p_old, p_new, x, cg);
+  launch_kk(1, k_cg_direction<S>, dim3((rows + Sd::ROWS - 1) / Sd::ROWS), dim3(256), 0, st, rows, r, p_old, p_new, x, cg);
   return cudaGetLastError();
 }
 
@@ -1202,10 +1210,10 @@ static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, bool run_direction, con
   if (blocks == 0) return cudaSuccess;
   if (!fused_dir && run_direction) {  // else the caller ran the direction pass (+ halo)
     using Sd = TileShape<S, kDirPasses>;
-    k_cg_direction<S><<<(tm.rows + Sd::ROWS - 1) / Sd::ROWS, 256, 0, st>>>(tm.rows, r, p_old, p_new, x, f.cg);
+    launch_kk(1, k_cg_direction<S>, dim3((tm.rows + Sd::ROWS - 1) / Sd::ROWS), dim3(256), 0, st, tm.rows, r, p_old, p_new, x, f.cg);
   }
 #define EP_CG_SPMV(T, D, Y)                                                                   \
-  k_cg_spmv<S, T, D, Y><<<blocks, 256, 0, st>>>(tm, row_map, col_entry, values, r, p_old, p_new, q, \
+  launch_kk(2, k_cg_spmv<S, T, D, Y>, dim3(blocks), dim3(256), 0, st, tm, row_map, col_entry, values, r, p_old, p_new, q, \
                                                 x, p_gather, vpos, f)
   if (!fused_dir) {  // warp-per-tile kernel (split direction schedule)
     using Sw = WarpTile<S>;
@@ -1213,7 +1221,7 @@ static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, bool run_direction, con
     const int warps = (units + Sw::TILES - 1) / Sw::TILES;
     const int wblocks = (warps + 7) / 8;
 #define EP_CG_SPMV_W(T, Y, K)                                                                 \
-  k_cg_spmv_warp<S, T, Y, K><<<wblocks, 256, 0, st>>>(tm, row_map, col_entry, values, p_new, q, \
+  launch_kk(2, k_cg_spmv_warp<S, T, Y, K>, dim3(wblocks), dim3(256), 0, st, tm, row_map, col_entry, values, p_new, q, \
                                                       p_gather, vpos, f)
     // auto: 8-entry batches at 2 CTAs/SM for symmetric storage, 4 at 4 CTAs/SM
     // for full storage (same-process A/B at 64^3, s = 32: 0.301 vs 0.332 ms and
@@ -1271,6 +1279,7 @@ cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, bool run_direction
 template <int S, bool kTiles>
 __global__ void __launch_bounds__(256) k_cg_update(const TileMap tm, double* __restrict__ r,
                                                    const double* __restrict__ q, const FinArgs f) {
+  EP_PDL_ENTRY();
   constexpr int P = kStreamPasses;
   using Sh = TileShape<S, P>;
   constexpr int V = Sh::V;
@@ -1325,8 +1334,8 @@ static cudaError_t cg_update_s(bool tiles, const TileMap& tm, double* r, const d
   using Sh = TileShape<S, kStreamPasses>;
   const int blocks = tiles ? (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC : (tm.rows + Sh::ROWS - 1) / Sh::ROWS;
   if (blocks == 0) return cudaSuccess;
-  if (tiles) k_cg_update<S, true><<<blocks, 256, 0, st>>>(tm, r, q, f);
-  else k_cg_update<S, false><<<blocks, 256, 0, st>>>(tm, r, q, f);
+  if (tiles) launch_kk(8, k_cg_update<S, true>, dim3(blocks), dim3(256), 0, st, tm, r, q, f);
+  else launch_kk(8, k_cg_update<S, false>, dim3(blocks), dim3(256), 0, st, tm, r, q, f);
   return cudaGetLastError();
 }
 

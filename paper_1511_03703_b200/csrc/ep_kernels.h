@@ -172,6 +172,7 @@ void free_stage_map(StageMap& sm);
 cudaError_t launch_cg_spmv_staged(int s, bool tiles, const StageMap& sm, const double* values,
                                   const double* p, double* q, const FinArgs& f, cudaStream_t st);
 int spmv_variant();  // ENPROP_OPT_SPMV_VARIANT (-1 = auto)
+void set_pdl_enabled(int on);  // ENPROP_OPT_PDL
 
 // after the loop: apply the still-deferred x += alpha*p of the last iteration
 cudaError_t launch_cg_flush(int s, int rows, double* x, double* const* p, const CgState* cg,

@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(256, 1) k_cg_spmv_staged(
     const unsigned char* __restrict__ blk, const double* __restrict__ values,
     const double* __restrict__ p, double* __restrict__ q, const FinArgs f) {
   using Sh = StagedShape<S>;
+  EP_PDL_ENTRY();
   if (f.cg->done) return;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
@@ -363,6 +364,8 @@ static int stage_shape(int& T, int& L, int& RS, int& max_upper, int& idx_bytes, 
   zc = Sh::ZC;
   return 0;
 }
+
+void set_pdl_enabled(int on) { pdl_enabled() = on; }
 
 bool staged_supported(int s, int N) { return (s == 16 || s == 32) && N >= 8; }
 
@@ -498,10 +501,10 @@ static cudaError_t cg_spmv_staged_s(bool tiles, const StageMap& sm, const double
   if (sm.nstages == 0) return cudaSuccess;
   const int grid = sm.nstages < nsm ? sm.nstages : nsm;
   if (tiles)
-    k_cg_spmv_staged<S, true><<<grid, 256, Sh::SMEM, st>>>(sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
+    launch_kk(2, k_cg_spmv_staged<S, true>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
                                                            values, p, q, f);
   else
-    k_cg_spmv_staged<S, false><<<grid, 256, Sh::SMEM, st>>>(sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
+    launch_kk(2, k_cg_spmv_staged<S, false>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
                                                             values, p, q, f);
   return cudaGetLastError();
 }
