@@ -301,6 +301,8 @@ def run_ours(args):
         for w in workers:
             w.prob.close()
         spmv_obj = bench_spmv(ep.Context(local), ep, torch, pack_group, O, hbm, peak_kind)
+    if rank == 0 and world == 1 and not args.skip_spmv:
+        extra["halo_model"] = bench_halo_model(ep, torch)
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         cpu = cpu_baseline_sample()
@@ -545,6 +547,28 @@ def bench_spmv_layouts(ctx, ep, torch, p, x, z, byt, commuted_ms, reps=5):
             "speedup_commuted_vs_scalar": round(scalar_ms / commuted_ms, 3),
             "speedup_commuted_vs_outer": round(outer_ms / commuted_ms, 3),
             "gate_bitwise": gate}
+
+
+def bench_halo_model(ep, torch, n=128, nranks=2, reps=50):
+    """T(s) = a + b*s fitted (enprop_fit_halo_model =
+    halo.cpp:156-181) to the slab solver's MEASURED halo exchange (one plane of
+    s values per neighbour, 128^3 mesh) at s = 1..32, and predicted_speedup
+    (halo.cpp:183-188). On one GPU the transport is the emulated one (device
+    copies inside HBM); NVLink needs two GPUs."""
+    ctx = ep.Context(0)
+    samples = []
+    for s in (1, 2, 4, 8, 16, 32):
+        d = ep.Dist(ctx, n, s, nranks=nranks, kl=ep.KlField(M_TERMS, 1.0, SIGMA, 1.0))
+        samples.append((s, d.time_halo(reps)))
+        del d
+        torch.cuda.synchronize()
+    a, b, rss = ep.fit_halo_model(samples)
+    return {"transport": f"emulated ({nranks} ranks on one GPU: device-to-device copies)",
+            "mesh": n, "plane_bytes_per_component": (n + 1) ** 2 * 8,
+            "measured_us": {str(s): round(t * 1e6, 3) for s, t in samples},
+            "fit": {"a_us": round(a * 1e6, 4), "b_us_per_component": round(b * 1e6, 5),
+                    "rss": rss},
+            "predicted_speedup": {str(s): round(ep.predicted_speedup(a, b, s), 3) for s in (4, 16, 32)}}
 
 
 def cpu_baseline_sample(max_cg=10):

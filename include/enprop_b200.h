@@ -283,6 +283,19 @@ int enprop_dist_solve(enprop_dist* d, const enprop_cg_options* opt, int* iterati
 int enprop_dist_local_count(enprop_dist* d);
 int enprop_dist_local(enprop_dist* d, int index, int* rank, int* row_begin, int* rows,
                       double** x);
+/* Measured halo exchange (the solver's own exchange of one p buffer: one plane
+ * of s values to each neighbour, NCCL or the emulated device copies), mean
+ * seconds per exchange over `reps`, CUDA events on the context's stream. */
+int enprop_dist_time_halo(enprop_dist* d, int reps, double* seconds);
+
+/* ------------------------------------------------ halo timing model (host) */
+/* fit_halo_model (halo.cpp:156-181): least-squares T(s) = a + b*s through
+ * (s[i], t[i]), i < n; INVALID for n < 2 or all s equal (singular). */
+int enprop_fit_halo_model(int n, const double* s, const double* t, double* a, double* b,
+                          double* residual_sum_of_squares);
+/* predicted_speedup (halo.cpp:183-188): s*(a + b)/(a + b*s); INVALID for s < 1
+ * or a zero exchange time. */
+int enprop_predicted_speedup(double a, double b, double s, double* speedup);
 
 #ifdef __cplusplus
 }

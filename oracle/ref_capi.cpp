@@ -385,6 +385,27 @@ int ref_newton_identity(int s, int scalar, int n, int m, double mean, double sig
   });
 }
 
+// fit_halo_model / predicted_speedup (halo.cpp:156-188).
+int ref_fit_halo_model(int n, const double* s, const double* t, double* a, double* b, double* rss) {
+  return guarded([&] {
+    std::vector<std::pair<double, double>> samples;
+    for (int i = 0; i < n; ++i) samples.emplace_back(s[i], t[i]);
+    const HaloFit fit = fit_halo_model(samples);
+    *a = fit.model.a;
+    *b = fit.model.b;
+    *rss = fit.residual_sum_of_squares;
+  });
+}
+
+int ref_predicted_speedup(double a, double b, double s, double* out) {
+  return guarded([&] {
+    HaloModel m;
+    m.a = a;
+    m.b = b;
+    *out = predicted_speedup(m, s);
+  });
+}
+
 // draw_samples(seed, count, m) (samples.cpp:7-18) -> out[count][m].
 int ref_draw_samples(uint64_t seed, int count, int m, double* out) {
   return guarded([&] {

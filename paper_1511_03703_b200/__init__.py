@@ -597,6 +597,25 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def fit_halo_model(samples):
+    """fit_halo_model (halo.cpp:156-181): least squares T(s) = a + b*s through
+    [(s, seconds), ...]; returns (a, b, residual_sum_of_squares)."""
+    n = len(samples)
+    s = (C.c_double * max(n, 1))(*[float(p[0]) for p in samples])
+    t = (C.c_double * max(n, 1))(*[float(p[1]) for p in samples])
+    a, b, r = C.c_double(), C.c_double(), C.c_double()
+    _check(lib().enprop_fit_halo_model(n, s, t, C.byref(a), C.byref(b), C.byref(r)), "fit_halo_model")
+    return a.value, b.value, r.value
+
+
+def predicted_speedup(a: float, b: float, s: float) -> float:
+    """predicted_speedup (halo.cpp:183-188): s*(a + b)/(a + b*s)."""
+    out = C.c_double()
+    _check(lib().enprop_predicted_speedup(C.c_double(a), C.c_double(b), C.c_double(s), C.byref(out)),
+           "predicted_speedup")
+    return out.value
+
+
 class Dist:
     """Ensemble problem domain-decomposed into z-slabs of node planes over
     `nranks` (partition.cpp:31-72 rule).  nccl_id=None emulates all ranks in
@@ -634,6 +653,13 @@ class Dist:
         else:
             _check(rc, "solve")
         return (list(it) if cfg.flavour == CG_UNCOUPLED else it[0]), list(ls)
+
+    def time_halo(self, reps: int = 20) -> float:
+        """Mean seconds of one halo exchange of the solver's p buffer (one plane
+        of s values to each neighbour; NCCL, or the emulated device copies)."""
+        sec = C.c_double()
+        _check(lib().enprop_dist_time_halo(self.h, reps, C.byref(sec)), "time_halo")
+        return sec.value
 
     def local(self):
         """[(rank, row_begin, rows, x view [rows][s])] of the ranks in this process."""

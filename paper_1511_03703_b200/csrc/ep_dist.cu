@@ -343,6 +343,69 @@ int enprop_dist_create(enprop_ctx* c, const enprop_problem_desc* desc, int nrank
   return ENPROP_OK;
 }
 
+int enprop_dist_time_halo(enprop_dist* D, int reps, double* seconds) {
+  if (!D || !seconds || reps < 1) return fail(ENPROP_ERR_INVALID, "enprop_dist_time_halo: bad argument");
+  cudaStream_t st = D->ctx->stream;
+  cudaEvent_t e0, e1;
+  EP_CUDA(cudaEventCreate(&e0));
+  EP_CUDA(cudaEventCreate(&e1));
+  int rc = halo(D, 0);  // warm-up (NCCL connection setup)
+  if (!rc) {
+    cudaEventRecord(e0, st);
+    for (int i = 0; i < reps && !rc; ++i) rc = halo(D, 0);
+    cudaEventRecord(e1, st);
+  }
+  float ms = 0.0f;
+  cudaError_t err = cudaEventSynchronize(e1);
+  if (err == cudaSuccess) err = cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc) return rc;
+  if (err != cudaSuccess) return cuda_fail(err, "enprop_dist_time_halo");
+  *seconds = (double)ms / 1e3 / reps;
+  return ENPROP_OK;
+}
+
+int enprop_fit_halo_model(int n, const double* s, const double* t, double* a, double* b,
+                          double* rss) {
+  // halo.cpp:156-181, same operations in the same order
+  if (n < 2 || !s || !t) return fail(ENPROP_ERR_INVALID, "fit_halo_model: need at least two points");
+  double mean_s = 0.0, mean_t = 0.0;
+  for (int i = 0; i < n; ++i) {
+    mean_s += s[i];
+    mean_t += t[i];
+  }
+  mean_s /= static_cast<double>(n);
+  mean_t /= static_cast<double>(n);
+  double ss = 0.0, st = 0.0;
+  for (int i = 0; i < n; ++i) {
+    ss += (s[i] - mean_s) * (s[i] - mean_s);
+    st += (s[i] - mean_s) * (t[i] - mean_t);
+  }
+  if (ss == 0.0) return fail(ENPROP_ERR_INVALID, "fit_halo_model: all ensemble sizes equal, fit is singular");
+  const double fb = st / ss;
+  const double fa = mean_t - fb * mean_s;
+  double r2 = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double r = t[i] - fa - fb * s[i];
+    r2 += r * r;
+  }
+  if (a) *a = fa;
+  if (b) *b = fb;
+  if (rss) *rss = r2;
+  return ENPROP_OK;
+}
+
+int enprop_predicted_speedup(double a, double b, double s, double* speedup) {
+  // halo.cpp:183-188
+  if (!speedup) return fail(ENPROP_ERR_INVALID, "predicted_speedup: null output");
+  if (s < 1.0) return fail(ENPROP_ERR_INVALID, "predicted_speedup: s must be at least 1");
+  const double denom = a + b * s;
+  if (denom == 0.0) return fail(ENPROP_ERR_INVALID, "predicted_speedup: zero exchange time");
+  *speedup = s * (a + b) / denom;
+  return ENPROP_OK;
+}
+
 int enprop_dist_local_count(enprop_dist* D) { return D ? (int)D->ranks.size() : 0; }
 
 int enprop_dist_local(enprop_dist* D, int index, int* rank, int* row_begin, int* rows, double** x) {

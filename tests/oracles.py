@@ -162,6 +162,8 @@ class RefLib:
         L.ref_apply_dirichlet.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, _dp, _dp, _dp]
         L.ref_spmv.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip, _dp, _dp, _dp]
         L.ref_spmv_outer.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip, _dp, _dp, _dp]
+        L.ref_fit_halo_model.argtypes = [C.c_int, _dp, _dp, _dp, _dp, _dp]
+        L.ref_predicted_speedup.argtypes = [C.c_double, C.c_double, C.c_double, _dp]
         L.ref_newton_identity.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                           C.c_double, C.c_double, C.c_double, _dp, _dp, C.c_double,
                                           C.c_double, C.c_double, C.c_int, C.c_double, C.c_int, _dp,
@@ -254,6 +256,17 @@ class RefLib:
                                           tol, max_newton, lin_tol, lin_maxit, dptr(u), iptr(it),
                                           iptr(cg), dptr(norms), iptr(nn))
         return rc, u, int(it[0]), int(cg[0]), list(norms[:nn[0]])
+
+    def fit_halo_model(self, s, t):
+        s, t = np.ascontiguousarray(s, dtype=np.float64), np.ascontiguousarray(t, dtype=np.float64)
+        out = np.zeros(3)
+        rc = self.lib.ref_fit_halo_model(len(s), dptr(s), dptr(t), dptr(out[0:1]), dptr(out[1:2]), dptr(out[2:3]))
+        return rc, tuple(out)
+
+    def predicted_speedup(self, a, b, s):
+        out = np.zeros(1)
+        rc = self.lib.ref_predicted_speedup(a, b, s, dptr(out))
+        return rc, float(out[0])
 
     def dot(self, s, u, v):
         out = C.c_double()

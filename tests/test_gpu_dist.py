@@ -67,3 +67,15 @@ def test_dist_rejects_serial_order_and_too_many_ranks(ctx):
     with pytest.raises(ValueError):
         d.solve(ep.SolverConfig(dot_mode=ep.DOT_SERIAL))
     d.close()
+
+
+def test_time_halo_measures_the_exchange(ctx):
+    """enprop_dist_time_halo: the solver's own halo exchange, timed; larger
+    ensembles move more bytes (one plane of s values per neighbour)."""
+    times = {}
+    for s in (1, 32):
+        d = ep.Dist(ctx, 24, s, nranks=3, kl=ep.KlField(3, 1.0, 0.1, 1.0))
+        times[s] = d.time_halo(20)
+        assert times[s] > 0
+    a, b, _ = ep.fit_halo_model([(1, times[1]), (32, times[32])])
+    assert b > 0 or abs(times[32] - times[1]) < 2e-6
