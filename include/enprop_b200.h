@@ -79,9 +79,12 @@ int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
  *   (entries per gather batch / CTAs per SM): 0: 4/4, 1: 4/4 + index prefetch,
  *   2: 8/2, 3: 8/2 + index prefetch, 4: 4/4 zero-padded, 5: 8/3, 6: 16/1;
  *   auto = 2 with symmetric storage, 0 otherwise. */
-/*   ENPROP_OPT_PDL (default 1, process-wide): launch the CG loop's kernels with
+/*   ENPROP_OPT_PDL (default 0, process-wide): launch the CG loop's kernels with
  *   programmatic dependent launch (the next kernel is scheduled while the
- *   previous one drains; it waits for its completion before reading). */
+ *   previous one drains; it waits for its completion before reading).
+ *   Measured: +2-4% on single-stream s = 4 / 16 solves, -1% with three
+ *   concurrent s = 32 groups (early-scheduled CTAs hold SMs other streams
+ *   could use). */
 enum {
   ENPROP_OPT_FUSED_DIRECTION = 1,
   ENPROP_OPT_SPMV_PIPELINE = 2,

@@ -31,7 +31,7 @@ def main():
     ap.add_argument("--ab", default="", help="comma list of SpMV variants timed alternately (CG SpMV kernel only)")
     ap.add_argument("--ab-rounds", type=int, default=5)
     ap.add_argument("--fused", default="1,0", help="fused-direction settings to time")
-    ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch (ENPROP_OPT_PDL)")
+    ap.add_argument("--pdl", type=int, default=0, help="programmatic dependent launch (ENPROP_OPT_PDL)")
     args = ap.parse_args()
     n, s = args.n, args.s
     ctx = ep.Context(0)
