@@ -24,16 +24,27 @@ def main():
     ap.add_argument("--groups", default="1,2,3,4")
     ap.add_argument("--rounds", type=int, default=2)
     ap.add_argument("--n", type=int, default=64)
+    ap.add_argument("--torch-streams", action="store_true", help="bench.py's setup: torch streams, 3 shared y")
+    ap.add_argument("--pdl", type=int, default=0)
     args = ap.parse_args()
     n, s = args.n, 32
     O = Oracle()
     Gmax = max(int(g) for g in args.groups.split(","))
     pool = O.draw_samples(0, s * Gmax * (args.rounds + 1), 3)
     workers = []
+    shared = [torch.as_tensor(pack_group(pool, s, g)).cuda() for g in range(3)]
     for g in range(Gmax):
         ctx = ep.Context(0, use_torch_stream=False)
+        if args.torch_streams:
+            stream = torch.cuda.Stream()
+            ctx.set_stream(stream.cuda_stream)
+            ctx._keep = stream
+        ctx.set_option(ep.OPT_PDL, args.pdl)
         p = ep.Problem(ctx, n, s, ep.KlField(3, 1.0, 0.1, 1.0))
-        ys = [torch.as_tensor(pack_group(pool, s, r * Gmax + g)).cuda() for r in range(args.rounds + 1)]
+        if args.torch_streams:
+            ys = [shared[g % 3] for r in range(args.rounds + 1)]
+        else:
+            ys = [torch.as_tensor(pack_group(pool, s, r * Gmax + g)).cuda() for r in range(args.rounds + 1)]
         workers.append((ctx, p, ys))
     torch.cuda.synchronize()
     mode = ep.DOT_CANONICAL if args.dot == "canonical" else ep.DOT_SERIAL
@@ -63,7 +74,7 @@ def main():
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         samples = G * args.rounds * s
-        print(f"dot={args.dot} G={G}: {samples / dt:8.1f} samples/s  ({dt / args.rounds * 1e3:.1f} ms per round of {G} groups) iters={out[0]}", flush=True)
+        print(f"dot={args.dot} G={G}: {samples / dt:8.1f} samples/s  ({dt / args.rounds * 1e3:.1f} ms per round of {G} groups) iters={[o[0] for o in out]}", flush=True)
 
 
 if __name__ == "__main__":
