@@ -192,6 +192,8 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
   const FinArgs f_pq = fin_args(w, tm, kPhasePQ);
   const FinArgs f_rr = fin_args(w, tm, kPhaseRR);
   const bool fin_kernel = canon;
+  // the staged SpMV finalizes p.q itself (grid barrier; needs >= 2 counters)
+  const bool fuse_pq = stage && canon && staged_fuse_fin() && tm.num_segs >= 2;
   if (canon) {
     EP_CUDA(launch_dot_tiles(s, tm, w.r, w.r, f_init, st));
     if (fin_kernel) EP_CUDA(launch_fin_segments(s, tm, f_init, st));
@@ -217,20 +219,20 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
         if (!fused) EP_CUDA(launch_cg_direction(s, rows, w.r, p_old, p_new, x, w.state, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[1], st));
         if (stage)
-          EP_CUDA(launch_cg_spmv_staged(s, canon, *stage, values, p_new, w.q, f_pq, st));
+          EP_CUDA(launch_cg_spmv_staged(s, canon, fuse_pq, *stage, values, p_new, w.q, f_pq, st));
         else
           EP_CUDA(launch_cg_spmv(s, canon, fused, false, tm, row_map, col_entry, values, w.r, p_old,
                                  p_new, w.q, x, p_new, vpos, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[2], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, f_pq, st));
-        if (fin_kernel) EP_CUDA(launch_fin_segments(s, tm, f_pq, st));
+        if (fin_kernel && !fuse_pq) EP_CUDA(launch_fin_segments(s, tm, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[3], st));
         EP_CUDA(launch_cg_update(s, canon, tm, w.r, w.q, f_rr, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[4], st));
         if (!canon) EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, f_rr, st));
         if (fin_kernel) EP_CUDA(launch_fin_segments(s, tm, f_rr, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[5], st));
-        ctx->launches += (canon ? 2 : 4) + (fused ? 0 : 1) + (fin_kernel ? 2 : 0);
+        ctx->launches += (canon ? 2 : 4) + (fused ? 0 : 1) + (fin_kernel ? 2 : 0) - (fuse_pq ? 1 : 0);
       }
     }
     // flag of this chunk

@@ -169,8 +169,13 @@ cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
 void free_stage_map(StageMap& sm);
 // q = A p and (tiles) the canonical p.q tile partials; bitwise equal to the
 // warp-per-tile kernel
-cudaError_t launch_cg_spmv_staged(int s, bool tiles, const StageMap& sm, const double* values,
-                                  const double* p, double* q, const FinArgs& f, cudaStream_t st);
+// fuse_fin (tiles only): the kernel also runs the canonical finalize of p.q
+// (k_fin_segments' work and order) after a grid barrier, so no separate
+// finalize launch follows. Needs f.seg_count[0..1] zero between launches.
+cudaError_t launch_cg_spmv_staged(int s, bool tiles, bool fuse_fin, const StageMap& sm,
+                                  const double* values, const double* p, double* q, const FinArgs& f,
+                                  cudaStream_t st);
+bool staged_fuse_fin();  // ENPROP_STAGED_FUSE (env, default 1)
 int spmv_variant();  // ENPROP_OPT_SPMV_VARIANT (-1 = auto)
 void set_pdl_enabled(int on);  // ENPROP_OPT_PDL
 

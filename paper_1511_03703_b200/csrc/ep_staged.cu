@@ -35,6 +35,7 @@
 
 #include "ep_common.cuh"
 #include "ep_kernels.h"
+#include "ep_fin.cuh"
 
 namespace ep {
 
@@ -46,14 +47,13 @@ struct StagedShape {
   static constexpr int RS = kTileRows * T;          // row slots per stage
   static constexpr int L = RS + 2;                  // rows per x run
   static constexpr int CH = 8 * S;                  // bytes per chunk (one entry's / row's s values)
-  static constexpr int ROWE = 28;                   // sa entries per row slot (27 padded to int4)
-  static constexpr int ROWX = 32;                   // sx entries per row slot (27 padded to 4 x uint4)
+  static constexpr int ROWE = 28;                   // value codes per row slot: 27 stencil slots + pad
   static constexpr int UP_CHUNKS = RS * kStageMaxUpper;
   static constexpr int X_CHUNKS = 9 * L;
   static constexpr int ZC = UP_CHUNKS + X_CHUNKS;   // the zero chunk (padding entries)
   static constexpr int BIG_BYTES = (ZC + 1) * CH;
-  static constexpr int HDR = 2 * RS + 4;            // ints: srow[RS], spch[RS], stage id, pad
-  static constexpr int IDX_BYTES = HDR * 4 + RS * ROWE * 4 + RS * ROWX * 2;
+  static constexpr int HDR = 2 * RS + 4;            // ints: srow[RS], slr[RS], stage id, pad
+  static constexpr int IDX_BYTES = HDR * 4 + RS * ROWE * 4;
   static constexpr int NIDX = 4;                    // index blocks in flight (ring depth)
   static constexpr int RED_BYTES = RS * S * 8;
   static constexpr int SMEM = 2 * BIG_BYTES + NIDX * IDX_BYTES + 2 * RED_BYTES + 64;
@@ -159,8 +159,8 @@ struct StagedCta {
     }
     const int* ib = idx(it);
     const int row = ib[rr];
-    const int pch = ib[Sh::RS + rr];
-    int ca[12];  // codes of entries 16..27
+    const int lr = ib[Sh::RS + rr];  // local row (x-run positions)
+    int ca[12];  // codes of stencil slots 16..27
     {
       const int4* sa = reinterpret_cast<const int4*>(ib + Sh::HDR + rr * Sh::ROWE) + 4;
 #pragma unroll
@@ -169,46 +169,61 @@ struct StagedCta {
         ca[4 * v] = w.x, ca[4 * v + 1] = w.y, ca[4 * v + 2] = w.z, ca[4 * v + 3] = w.w;
       }
     }
-    int cx[kStageMaxRow];
-    {
-      const uint4* sx = reinterpret_cast<const uint4*>(ib + Sh::HDR + Sh::RS * Sh::ROWE) + rr * 4;
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const uint4 w = sx[v];
-        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int h = 0; h < 8; ++h)
-          if (8 * v + h < kStageMaxRow) cx[8 * v + h] = (int)((ww[h / 2] >> (16 * (h & 1))) & 0xffffu);
-      }
-    }
     mbar_wait(&bar[it & 1], (it >> 1) & 1);
     const unsigned char* sb = big(it);
-    // all 27 entries: entries past the row end point at the zero chunk and add
-    // +0.0 * +0.0 (the running sum starts at +0.0 and never becomes -0.0, so
-    // adding +0.0 changes no bit)
+    // Stencil slots k = run*3 + di + 1 in column order, run = (dk+1)*3 + dj+1;
+    // absent neighbours (and empty row slots) point the value at the zero chunk
+    // and add +0.0 * x (the running sum starts at +0.0 and never becomes
+    // -0.0, so adding a signed zero changes no bit).  x of slot (run, di) sits
+    // at position lr + di + 1 of x run `run`.
+    //   s = 32: the two rows of a warp (half h, local rows lr0 + h) share two of
+    //   their three x positions per run: both halves load lr0+1 and lr0+2 from
+    //   the same addresses (one 256-byte wavefront pair), then lr0 resp. lr0+3.
     double s0 = 0.0, s1 = 0.0;
+    double2 pown = make_double2(0.0, 0.0);
+    const unsigned char* xb = sb + Sh::UP_CHUNKS * Sh::CH + lane0 * 8;
+    const int h = (S == 32) ? ((threadIdx.x >> 4) & 1) : 0;
+    const int lr0 = lr - h;
 #pragma unroll
-    for (int k = 0; k < kStageMaxRow; ++k) {
-      const int c = k < 16 ? Gc.code[k] : ca[k - 16];
-      double2 a;
-      if (k < kStageMaxGlobal) {
-        a = Gc.v[k];
-        if (c < 0) a = chunk(sb, -c - 1);
+    for (int run = 0; run < 9; ++run) {
+      const unsigned char* xr = xb + run * Sh::L * Sh::CH;
+      double2 xm, x0, xp;
+      if constexpr (S == 32) {
+        const double2 A = *reinterpret_cast<const double2*>(xr + (lr0 + 1) * Sh::CH);
+        const double2 B = *reinterpret_cast<const double2*>(xr + (lr0 + 2) * Sh::CH);
+        const double2 C = *reinterpret_cast<const double2*>(xr + (h ? lr0 + 3 : lr0) * Sh::CH);
+        xm = h ? A : C;
+        x0 = h ? B : A;
+        xp = h ? C : B;
       } else {
-        a = chunk(sb, -c - 1);
+        xm = *reinterpret_cast<const double2*>(xr + lr * Sh::CH);
+        x0 = *reinterpret_cast<const double2*>(xr + (lr + 1) * Sh::CH);
+        xp = *reinterpret_cast<const double2*>(xr + (lr + 2) * Sh::CH);
       }
-      const double2 xv = chunk(sb, cx[k]);
-      s0 = EP_DADD(s0, EP_DMUL(a.x, xv.x));
-      s1 = EP_DADD(s1, EP_DMUL(a.y, xv.y));
+      if (run == 4) pown = x0;  // the row's own p
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int k = run * 3 + d;
+        const int c = k < 16 ? Gc.code[k] : ca[k - 16];
+        double2 a;
+        if (k < kStageMaxGlobal) {
+          a = Gc.v[k];
+          if (c < 0) a = chunk(sb, -c - 1);
+        } else {
+          a = chunk(sb, -c - 1);
+        }
+        const double2 xv = d == 0 ? xm : (d == 1 ? x0 : xp);
+        s0 = EP_DADD(s0, EP_DMUL(a.x, xv.x));
+        s1 = EP_DADD(s1, EP_DMUL(a.y, xv.y));
+      }
     }
     if (row >= 0) *reinterpret_cast<double2*>(q + (size_t)row * S + lane0) = make_double2(s0, s1);
     double* rb = red + (it & 1) * (Sh::RS * S);
     if constexpr (kTiles) {
       double c0 = 0.0, c1 = 0.0;
       if (row >= 0) {  // own p (x run (dj, dk) = (0, 0))
-        const double2 pn = chunk(sb, pch);
-        c0 = EP_DMUL(pn.x, s0);
-        c1 = EP_DMUL(pn.y, s1);
+        c0 = EP_DMUL(pown.x, s0);
+        c1 = EP_DMUL(pown.y, s1);
       }
       *reinterpret_cast<double2*>(rb + rr * S + lane0) = make_double2(c0, c1);
     }
@@ -241,11 +256,32 @@ struct StagedCta {
   }
 };
 
+// Grid-wide barrier of the persistent staged kernel: its grid is one CTA per
+// SM (at most), so all CTAs are resident or become resident as other streams'
+// kernels retire. Self-resetting counter + monotonic generation.
+__device__ __forceinline__ void grid_barrier(int* count, int* gen, int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile int* vgen = gen;
+    const int g = *vgen;
+    __threadfence();
+    if (atomicAdd(count, 1) == nblocks - 1) {
+      *count = 0;
+      __threadfence();
+      atomicAdd(gen, 1);
+    } else {
+      while (*vgen == g) __nanosleep(64);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 template <int S, bool kTiles>
 __global__ void __launch_bounds__(256, 1) k_cg_spmv_staged(
     const TileMap tm, int N, int nstages, const StageDesc* __restrict__ desc,
     const unsigned char* __restrict__ blk, const double* __restrict__ values,
-    const double* __restrict__ p, double* __restrict__ q, const FinArgs f) {
+    const double* __restrict__ p, double* __restrict__ q, const FinArgs f, int fuse_fin) {
   using Sh = StagedShape<S>;
   EP_PDL_ENTRY();
   if (f.cg->done) return;
@@ -259,12 +295,16 @@ __global__ void __launch_bounds__(256, 1) k_cg_spmv_staged(
     for (int k = 0; k < 2 + Sh::NIDX; ++k) mbar_init(&c.bar[k], 1);
     fence_mbar_init();
   }
-  if (tid < Sh::CH / 8) {  // zero chunks (never written by the copies)
-    reinterpret_cast<double*>(smem + Sh::ZC * Sh::CH)[tid] = 0.0;
-    reinterpret_cast<double*>(smem + Sh::BIG_BYTES + Sh::ZC * Sh::CH)[tid] = 0.0;
+  // zero chunks (never written by the copies) and x-run areas: positions a
+  // copy does not reach (clipped runs) are read for absent neighbours only,
+  // times a zero value, so they must hold finite numbers
+  for (int b = 0; b < 2; ++b) {
+    double2* z = reinterpret_cast<double2*>(smem + b * Sh::BIG_BYTES + Sh::UP_CHUNKS * Sh::CH);
+    for (int i = tid; i < (Sh::X_CHUNKS + 1) * Sh::CH / 16; i += blockDim.x) z[i] = make_double2(0.0, 0.0);
   }
   __syncthreads();
   if (tid == 0) {
+    fence_proxy_async_smem();  // the zero-filled x areas are rewritten by the copies
     for (int it = 0; it < Sh::NIDX; ++it)
       if (c.has(it)) c.issue_idx(it);
     for (int it = 0; it < 2; ++it)
@@ -280,6 +320,22 @@ __global__ void __launch_bounds__(256, 1) k_cg_spmv_staged(
     c.template stage<kTiles>(it, gb, ga);
     if (!c.has(++it)) break;
   }
+  if constexpr (kTiles) {
+    if (fuse_fin) {
+      // Fused canonical finalize (the k_fin_segments work, same order): once
+      // every tile partial is written, CTA c folds segments c, c + grid, ...
+      // and the last CTA to finish its folds forms the total and runs the CG
+      // phase. The stage buffers are free now and serve as scratch.
+      grid_barrier(f.seg_count, f.seg_count + 1, gridDim.x);
+      double* scratch = reinterpret_cast<double*>(smem);
+      double* lanes = scratch + FinShape<S>::CHUNK * S + FinShape<S>::CHUNK2 * S;
+      int* s_final = reinterpret_cast<int*>(lanes + S);
+      int folds = 0;
+      for (int seg = blockIdx.x; seg < tm.num_segs; seg += gridDim.x, ++folds)
+        fin_segment_fold<S>(tm, f, seg, scratch);
+      if (folds) fin_total_phase<S>(tm, f, scratch + FinShape<S>::CHUNK * S, lanes, s_final, folds);
+    }
+  }
 }
 
 // ---- stage map ---------------------------------------------------------------
@@ -287,13 +343,15 @@ __global__ void __launch_bounds__(256, 1) k_cg_spmv_staged(
 // stage's canonical id g = desc[pos].g), by row slot rr = ti*16 + t (tile ti
 // of the stage, row t of the tile):
 //   int srow[RS]       the slot's row, -1 if none
-//   int spch[RS]       chunk of the row's own p in the stage buffer
+//   int slr[RS]        its local row lr = row - R0 (x-run positions lr .. lr+2);
+//                      empty slots: rr for s = 32 (the warp's row pair stays
+//                      consecutive), 0 otherwise
 //   int g, pad[3]      canonical stage id (tiles g*T + ti)
-//   int sa[RS][28]     value of entry k: >= 0 global slot (transposed entry of an
-//                      earlier stage's row), < 0: -(chunk + 1) in the stage buffer
-//   u16 sx[RS][32]     chunk of entry k's x operand: UP_CHUNKS + run*L + lr + di + 1,
-//                      run = (dk+1)*3 + (dj+1), lr = row - R0
-// Entries past a row's end (and empty slots) point both operands at the zero chunk.
+//   int sa[RS][28]     value of stencil slot k = run*3 + di + 1, run =
+//                      (dk+1)*3 + dj+1 (column order): >= 0 global slot (the
+//                      transposed entry of an earlier stage's row), < 0:
+//                      -(chunk + 1) in the stage buffer; absent neighbours and
+//                      empty slots point at the zero chunk
 __global__ void k_stage_fill(const TileMap tm, int nstages, int T, int N, int L, int RS,
                              int up_chunks, int zc, int idx_bytes,
                              const StageDesc* __restrict__ desc, const int* __restrict__ row_map,
@@ -307,50 +365,48 @@ __global__ void k_stage_fill(const TileMap tm, int nstages, int T, int N, int L,
   int* ib = reinterpret_cast<int*>(blk + (size_t)pos * idx_bytes);
   const int hdr = 2 * RS + 4;
   int* sa = ib + hdr + rr * 28;
-  uint16_t* sx = reinterpret_cast<uint16_t*>(ib + hdr + RS * 28) + rr * 32;
   if (rr == 0) ib[2 * RS] = g;  // stage id for the tile trees
+  for (int k = 0; k < 28; ++k) sa[k] = -(zc + 1);
   const int b = g * T + rr / kTileRows, t = rr % kTileRows;
   int r0 = 0, nr = 0;
   if (b < tm.num_tiles()) tm.tile(b, r0, nr);
   const int r = t < nr ? r0 + t : -1;
-  int n = 0;
-  if (r >= 0) {
-    const int ks = row_map[r], ke = row_map[r + 1];
-    n = ke - ks;
-    const int lr = r - d.R0;
-    if (n > kStageMaxRow || lr < 0 || lr >= RS) {
-      atomicAdd(bad, 1);
-      return;
-    }
-    const int NN = N * N;
-    for (int k = ks; k < ke; ++k) {
-      const int c = col_entry[k], v = vpos[k];
-      int code;
-      if (c >= d.R0) {
-        const int a = v - d.slot0;
-        if (a < 0 || a >= up_chunks) atomicAdd(bad, 1);
-        code = -(a + 1);
-      } else {
-        if (k - ks >= kStageMaxGlobal) atomicAdd(bad, 1);
-        code = v;
-      }
-      const int dl = c - r;
-      const int dk = dl > NN / 2 ? 1 : (dl < -(NN / 2) ? -1 : 0);
-      const int rem = dl - dk * NN;
-      const int dj = rem > N / 2 ? 1 : (rem < -(N / 2) ? -1 : 0);
-      const int di = rem - dj * N;
-      if (di < -1 || di > 1) atomicAdd(bad, 1);
-      sa[k - ks] = code;
-      sx[k - ks] = (uint16_t)(up_chunks + ((dk + 1) * 3 + (dj + 1)) * L + lr + di + 1);
-    }
-    ib[rr] = r;
-    ib[RS + rr] = up_chunks + 4 * L + lr + 1;
-  } else {
+  if (r < 0) {
     ib[rr] = -1;
-    ib[RS + rr] = zc;
+    ib[RS + rr] = T == 1 ? rr : 0;
+    return;
   }
-  for (int k = n; k < 28; ++k) sa[k] = -(zc + 1);
-  for (int k = n; k < 32; ++k) sx[k] = (uint16_t)zc;
+  const int ks = row_map[r], ke = row_map[r + 1];
+  const int lr = r - d.R0;
+  if (ke - ks > kStageMaxRow || lr < 0 || lr >= RS || (T == 1 && lr != rr)) {
+    atomicAdd(bad, 1);
+    return;
+  }
+  const int NN = N * N;
+  int last = -1;
+  for (int k = ks; k < ke; ++k) {
+    const int c = col_entry[k], v = vpos[k];
+    const int dl = c - r;
+    const int dk = dl > NN / 2 ? 1 : (dl < -(NN / 2) ? -1 : 0);
+    const int rem = dl - dk * NN;
+    const int dj = rem > N / 2 ? 1 : (rem < -(N / 2) ? -1 : 0);
+    const int di = rem - dj * N;
+    const int slot = ((dk + 1) * 3 + (dj + 1)) * 3 + di + 1;
+    if (di < -1 || di > 1 || slot <= last) atomicAdd(bad, 1);  // 27-point, column order
+    last = slot;
+    int code;
+    if (c >= d.R0) {
+      const int a = v - d.slot0;
+      if (a < 0 || a >= up_chunks) atomicAdd(bad, 1);
+      code = -(a + 1);
+    } else {
+      if (slot >= kStageMaxGlobal) atomicAdd(bad, 1);
+      code = v;
+    }
+    if (slot >= 0 && slot < 27) sa[slot] = code;
+  }
+  ib[rr] = r;
+  ib[RS + rr] = lr;
 }
 
 template <int S>
@@ -366,6 +422,14 @@ static int stage_shape(int& T, int& L, int& RS, int& max_upper, int& idx_bytes, 
 }
 
 void set_pdl_enabled(int on) { pdl_enabled() = on; }
+
+bool staged_fuse_fin() {
+  static const int on = [] {
+    const char* e = getenv("ENPROP_STAGED_FUSE");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
 
 bool staged_supported(int s, int N) { return (s == 16 || s == 32) && N >= 8; }
 
@@ -474,7 +538,7 @@ void free_stage_map(StageMap& sm) {
 }
 
 template <int S>
-static cudaError_t cg_spmv_staged_s(bool tiles, const StageMap& sm, const double* values,
+static cudaError_t cg_spmv_staged_s(bool tiles, bool fuse_fin, const StageMap& sm, const double* values,
                                     const double* p, double* q, const FinArgs& f, cudaStream_t st) {
   using Sh = StagedShape<S>;
   // per device: SM count, published only after the shared-memory opt-in is
@@ -502,17 +566,18 @@ static cudaError_t cg_spmv_staged_s(bool tiles, const StageMap& sm, const double
   const int grid = sm.nstages < nsm ? sm.nstages : nsm;
   if (tiles)
     launch_kk(2, k_cg_spmv_staged<S, true>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
-                                                           values, p, q, f);
+                                                           values, p, q, f, fuse_fin ? 1 : 0);
   else
     launch_kk(2, k_cg_spmv_staged<S, false>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
-                                                            values, p, q, f);
+                                                            values, p, q, f, 0);
   return cudaGetLastError();
 }
 
-cudaError_t launch_cg_spmv_staged(int s, bool tiles, const StageMap& sm, const double* values,
-                                  const double* p, double* q, const FinArgs& f, cudaStream_t st) {
-  if (s == 32) return cg_spmv_staged_s<32>(tiles, sm, values, p, q, f, st);
-  if (s == 16) return cg_spmv_staged_s<16>(tiles, sm, values, p, q, f, st);
+cudaError_t launch_cg_spmv_staged(int s, bool tiles, bool fuse_fin, const StageMap& sm,
+                                  const double* values, const double* p, double* q, const FinArgs& f,
+                                  cudaStream_t st) {
+  if (s == 32) return cg_spmv_staged_s<32>(tiles, fuse_fin, sm, values, p, q, f, st);
+  if (s == 16) return cg_spmv_staged_s<16>(tiles, fuse_fin, sm, values, p, q, f, st);
   return cudaErrorInvalidValue;
 }
 
