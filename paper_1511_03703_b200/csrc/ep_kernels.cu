@@ -242,22 +242,22 @@ cudaError_t launch_axpby(int s, int64_t n, int /*per_lane*/, const double* alpha
 // =============================================================================
 // Block shape: NT threads, TPR threads per row, RPC row slots per pass, P
 // passes per block (a thread owns P rows; their loads are issued together).
-template <int S, int P = 1>
+template <int S, int P = 1, int NT_ = 256>
 struct TileShape {
   static constexpr int V = SpmvShape<S>::V;
   static constexpr int TPR = S / V;                // threads per row
-  static constexpr int NT = 256;                   // threads per block
+  static constexpr int NT = NT_;                   // threads per block
   static constexpr int RPC = NT / TPR;             // row slots per pass
   static constexpr int ROWS = RPC * P;             // row slots per block
   static constexpr int TPC = ROWS / kTileRows;     // tiles per block
-  static_assert(RPC % kTileRows == 0, "a pass must cover whole tiles");
+  static_assert(ROWS % kTileRows == 0, "a block must cover whole tiles");
 };
 
 
 // Row of block slot `slot` in canonical tiling (-1: none).
-template <int S, int P>
+template <int S, int P, int NT = 256>
 __device__ __forceinline__ int tile_row(const TileMap& tm, int slot) {
-  using Sh = TileShape<S, P>;
+  using Sh = TileShape<S, P, NT>;
   const int tile = blockIdx.x * Sh::TPC + slot / kTileRows;
   if (tile >= tm.num_tiles()) return -1;
   int r0, nr;
@@ -271,9 +271,9 @@ __device__ __forceinline__ int tile_row(const TileMap& tm, int slot) {
 // registers in the canonical order (v[i] += v[i+h], h = 8,4,2,1; rows past the
 // tile end hold +0.0) and writes the tile partial. The dot is closed by
 // k_fin_segments, so blocks retire right after this (no global round trip).
-template <int S, int P>
+template <int S, int P, int NT = 256>
 __device__ __forceinline__ void tiles_finish(const TileMap& tm, const double* sprod, const FinArgs& f) {
-  using Sh = TileShape<S, P>;
+  using Sh = TileShape<S, P, NT>;
   __syncthreads();
   for (int idx = threadIdx.x; idx < Sh::TPC * S; idx += Sh::NT) {
     const int lt = idx / S, e = idx - lt * S;
@@ -517,12 +517,12 @@ cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v,
 // k_fin_serial forms the dot.  All kernels early-exit once the solve is done,
 // so the host may enqueue ahead of its convergence check.
 // =============================================================================
-template <int S, int P, bool kTiles>
+template <int S, int P, bool kTiles, int NT = 256>
 __device__ __forceinline__ int cg_row(const TileMap& tm, int slot) {
   if constexpr (kTiles) {
-    return tile_row<S, P>(tm, slot);
+    return tile_row<S, P, NT>(tm, slot);
   } else {
-    const int row = blockIdx.x * TileShape<S, P>::ROWS + slot;
+    const int row = blockIdx.x * TileShape<S, P, NT>::ROWS + slot;
     return row < tm.rows ? row : -1;
   }
 }
@@ -608,6 +608,21 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
 static int g_spmv_variant = -1;  // ENPROP_OPT_SPMV_VARIANT (process-wide; -1 auto, see SpmvVariant)
 void set_spmv_variant(int v) { g_spmv_variant = (v >= 0 && v <= 6) ? v : -1; }
 int spmv_variant() { return g_spmv_variant; }
+
+// Vector kernels of the CG loop run 128-thread blocks capped at 48 registers
+// (kVecNT): small enough to be co-resident with a staged-SpMV CTA of another
+// sample group (which leaves ~6 K registers and ~17 KB of shared memory per
+// SM), so concurrent groups overlap their HBM-bound passes with the SpMV.
+constexpr int kVecNT = 128;
+
+// block size of the CG vector kernels (ENPROP_VEC_NT env: 128 default, or 256)
+int vec_nt() {
+  static const int nt = [] {
+    const char* e = getenv("ENPROP_VEC_NT");
+    return (e && atoi(e) == 256) ? 256 : kVecNT;
+  }();
+  return nt;
+}
 
 template <int S>
 struct WarpTile {
@@ -841,15 +856,15 @@ __global__ void __launch_bounds__(256, SpmvVariant<kVar>::kMinBlocks) k_cg_spmv_
 // where p_old is read anyway, which saves one vector pass per iteration.
 constexpr int kDirPasses = 2;
 
-template <int S>
-__global__ void __launch_bounds__(256) k_cg_direction(int rows, const double* __restrict__ r,
+template <int S, int NT>
+__global__ void __launch_bounds__(NT, 65536 / (NT * 48)) k_cg_direction(int rows, const double* __restrict__ r,
                                                       const double* __restrict__ p_old,
                                                       double* __restrict__ p_new,
                                                       double* __restrict__ x,
                                                       const CgState* __restrict__ cg) {
   EP_PDL_ENTRY();
   constexpr int P = kDirPasses;
-  using Sh = TileShape<S, P>;
+  using Sh = TileShape<S, P, NT>;
   constexpr int V = Sh::V;
   if (cg->done) return;
   const bool first = cg->it == 0;
@@ -926,9 +941,14 @@ cudaError_t launch_cg_flush(int s, int rows, double* x, double* const* p, const 
 template <int S>
 static cudaError_t cg_direction_s(int rows, const double* r, const double* p_old, double* p_new,
                                   double* x, const CgState* cg, cudaStream_t st) {
-  using Sd = TileShape<S, kDirPasses>;
   if (rows <= 0) return cudaSuccess;
-  launch_kk(1, k_cg_direction<S>, dim3((rows + Sd::ROWS - 1) / Sd::ROWS), dim3(256), 0, st, rows, r, p_old, p_new, x, cg);
+  if (vec_nt() == 128) {
+    using Sd = TileShape<S, kDirPasses, 128>;
+    launch_kk(1, k_cg_direction<S, 128>, dim3((rows + Sd::ROWS - 1) / Sd::ROWS), dim3(128), 0, st, rows, r, p_old, p_new, x, cg);
+  } else {
+    using Sd = TileShape<S, kDirPasses, 256>;
+    launch_kk(1, k_cg_direction<S, 256>, dim3((rows + Sd::ROWS - 1) / Sd::ROWS), dim3(256), 0, st, rows, r, p_old, p_new, x, cg);
+  }
   return cudaGetLastError();
 }
 
@@ -948,8 +968,8 @@ static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, bool run_direction, con
   const int blocks = tiles ? (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC : (tm.rows + Sh::ROWS - 1) / Sh::ROWS;
   if (blocks == 0) return cudaSuccess;
   if (!fused_dir && run_direction) {  // else the caller ran the direction pass (+ halo)
-    using Sd = TileShape<S, kDirPasses>;
-    launch_kk(1, k_cg_direction<S>, dim3((tm.rows + Sd::ROWS - 1) / Sd::ROWS), dim3(256), 0, st, tm.rows, r, p_old, p_new, x, f.cg);
+    using Sd = TileShape<S, kDirPasses, 256>;
+    launch_kk(1, k_cg_direction<S, 256>, dim3((tm.rows + Sd::ROWS - 1) / Sd::ROWS), dim3(256), 0, st, tm.rows, r, p_old, p_new, x, f.cg);
   }
 #define EP_CG_SPMV(T, D, Y)                                                                   \
   launch_kk(2, k_cg_spmv<S, T, D, Y>, dim3(blocks), dim3(256), 0, st, tm, row_map, col_entry, values, r, p_old, p_new, q, \
@@ -1015,12 +1035,12 @@ cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, bool run_direction
 // kernels.hpp:84: 1.0*y is exact); r.r for the next dot.  P rows per thread,
 // all loads issued before any arithmetic.  (x is updated one pass later, in
 // k_cg_direction / k_cg_flush.)
-template <int S, bool kTiles>
-__global__ void __launch_bounds__(256) k_cg_update(const TileMap tm, double* __restrict__ r,
+template <int S, bool kTiles, int NT>
+__global__ void __launch_bounds__(NT, 65536 / (NT * 48)) k_cg_update(const TileMap tm, double* __restrict__ r,
                                                    const double* __restrict__ q, const FinArgs f) {
   EP_PDL_ENTRY();
-  constexpr int P = kStreamPasses;
-  using Sh = TileShape<S, P>;
+  constexpr int P = NT == 128 ? 2 : kStreamPasses;  // 48-register cap at 128 threads
+  using Sh = TileShape<S, P, NT>;
   constexpr int V = Sh::V;
   const CgState* cg = f.cg;
   if (cg->done) return;
@@ -1037,7 +1057,7 @@ __global__ void __launch_bounds__(256) k_cg_update(const TileMap tm, double* __r
   VecD<V> rv[P], qv[P];
 #pragma unroll
   for (int ps = 0; ps < P; ++ps) {
-    row[ps] = cg_row<S, P, kTiles>(tm, ps * Sh::RPC + threadIdx.x / Sh::TPR);
+    row[ps] = cg_row<S, P, kTiles, NT>(tm, ps * Sh::RPC + threadIdx.x / Sh::TPR);
     if (row[ps] >= 0) {
       const size_t off = (size_t)row[ps] * S + lane0;
       rv[ps] = ld_vec<V>(r + off);
@@ -1064,18 +1084,25 @@ __global__ void __launch_bounds__(256) k_cg_update(const TileMap tm, double* __r
       for (int j = 0; j < V; ++j) sprod[slot * S + lane0 + j] = pr.v[j];
     }
   }
-  if constexpr (kTiles) tiles_finish<S, P>(tm, sprod, f);
+  if constexpr (kTiles) tiles_finish<S, P, NT>(tm, sprod, f);
+}
+
+template <int S, int NT>
+static cudaError_t cg_update_nt(bool tiles, const TileMap& tm, double* r, const double* q,
+                                const FinArgs& f, cudaStream_t st) {
+  using Sh = TileShape<S, NT == 128 ? 2 : kStreamPasses, NT>;
+  const int blocks = tiles ? (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC : (tm.rows + Sh::ROWS - 1) / Sh::ROWS;
+  if (blocks == 0) return cudaSuccess;
+  if (tiles) launch_kk(8, k_cg_update<S, true, NT>, dim3(blocks), dim3(NT), 0, st, tm, r, q, f);
+  else launch_kk(8, k_cg_update<S, false, NT>, dim3(blocks), dim3(NT), 0, st, tm, r, q, f);
+  return cudaGetLastError();
 }
 
 template <int S>
 static cudaError_t cg_update_s(bool tiles, const TileMap& tm, double* r, const double* q,
                                const FinArgs& f, cudaStream_t st) {
-  using Sh = TileShape<S, kStreamPasses>;
-  const int blocks = tiles ? (tm.num_tiles() + Sh::TPC - 1) / Sh::TPC : (tm.rows + Sh::ROWS - 1) / Sh::ROWS;
-  if (blocks == 0) return cudaSuccess;
-  if (tiles) launch_kk(8, k_cg_update<S, true>, dim3(blocks), dim3(256), 0, st, tm, r, q, f);
-  else launch_kk(8, k_cg_update<S, false>, dim3(blocks), dim3(256), 0, st, tm, r, q, f);
-  return cudaGetLastError();
+  if (vec_nt() == 128) return cg_update_nt<S, 128>(tiles, tm, r, q, f, st);
+  return cg_update_nt<S, 256>(tiles, tm, r, q, f, st);
 }
 
 cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* r, const double* q,
