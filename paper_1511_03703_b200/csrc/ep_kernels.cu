@@ -484,7 +484,12 @@ __global__ void __launch_bounds__(32 * SerialShape<S>::LG) k_fin_serial(
       for (int k = 0; k < K; ++k) cur[k] = EP_DMUL(ua[k], va[k]);
     }
   }
-  if (lane == 0) f.seg_sums[e] = acc;
+  if (lane == 0) {
+    f.seg_sums[e] = acc;
+    // every writing warp fences its own store: thread 0's release below only
+    // covers its own warp's stores, and the last block reads all of them
+    __threadfence();
+  }
   __syncthreads();
   if (threadIdx.x == 0) s_final = (atomic_add_acq_rel_gpu(f.seg_done, 1) == Sh::GROUPS - 1);
   __syncthreads();
