@@ -176,30 +176,15 @@ struct StagedCta {
     // and add +0.0 * x (the running sum starts at +0.0 and never becomes
     // -0.0, so adding a signed zero changes no bit).  x of slot (run, di) sits
     // at position lr + di + 1 of x run `run`.
-    //   s = 32: the two rows of a warp (half h, local rows lr0 + h) share two of
-    //   their three x positions per run: both halves load lr0+1 and lr0+2 from
-    //   the same addresses (one 256-byte wavefront pair), then lr0 resp. lr0+3.
     double s0 = 0.0, s1 = 0.0;
     double2 pown = make_double2(0.0, 0.0);
     const unsigned char* xb = sb + Sh::UP_CHUNKS * Sh::CH + lane0 * 8;
-    const int h = (S == 32) ? ((threadIdx.x >> 4) & 1) : 0;
-    const int lr0 = lr - h;
 #pragma unroll
     for (int run = 0; run < 9; ++run) {
       const unsigned char* xr = xb + run * Sh::L * Sh::CH;
-      double2 xm, x0, xp;
-      if constexpr (S == 32) {
-        const double2 A = *reinterpret_cast<const double2*>(xr + (lr0 + 1) * Sh::CH);
-        const double2 B = *reinterpret_cast<const double2*>(xr + (lr0 + 2) * Sh::CH);
-        const double2 C = *reinterpret_cast<const double2*>(xr + (h ? lr0 + 3 : lr0) * Sh::CH);
-        xm = h ? A : C;
-        x0 = h ? B : A;
-        xp = h ? C : B;
-      } else {
-        xm = *reinterpret_cast<const double2*>(xr + lr * Sh::CH);
-        x0 = *reinterpret_cast<const double2*>(xr + (lr + 1) * Sh::CH);
-        xp = *reinterpret_cast<const double2*>(xr + (lr + 2) * Sh::CH);
-      }
+      const double2 xm = *reinterpret_cast<const double2*>(xr + lr * Sh::CH);
+      const double2 x0 = *reinterpret_cast<const double2*>(xr + (lr + 1) * Sh::CH);
+      const double2 xp = *reinterpret_cast<const double2*>(xr + (lr + 2) * Sh::CH);
       if (run == 4) pown = x0;  // the row's own p
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
