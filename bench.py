@@ -272,8 +272,8 @@ def run_ours(args):
     achieved = byt / (avg_spmv_ms / 1e3) / 1e9
     it_ms = det["iteration"] / nit
     # the library's auto choice (ep_capi.cu enprop_problem_solve): the staged
-    # kernel for symmetric storage + canonical dots at s in {16, 32}
-    if nnz_st < nnz and args.dot == "canonical" and S in (16, 32):
+    # kernel for symmetric storage + canonical dots at s in {4, 16, 32}
+    if nnz_st < nnz and args.dot == "canonical" and S in (4, 16, 32):
         kname = f"k_cg_spmv_staged<{S},true>"
     else:
         kname = "k_cg_spmv_warp<32,true,true,2>" if nnz_st < nnz else "k_cg_spmv_warp<32,true,false,0>"

@@ -812,7 +812,7 @@ int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* i
   EP_CUDA(launch_negate(len, p->residual, p->rhs, p->ctx->stream));
   p->ctx->launches += 1;
   // stage-pipelined SpMV (ep_staged.cu): structured graph + symmetric storage,
-  // s in {16, 32}, canonical dots, automatic variant selection. (The serial
+  // s in {4, 16, 32}, canonical dots, automatic variant selection. (The serial
   // order keeps the warp kernel: its latency-bound dot chains need other
   // groups' kernels alongside, and the persistent staged kernel fills the SMs.)
   const StageMap* stage = nullptr;

@@ -51,10 +51,10 @@ struct StagedShape {
   static constexpr int UP_CHUNKS = RS * kStageMaxUpper;
   static constexpr int X_CHUNKS = 9 * L;
   static constexpr int ZC = UP_CHUNKS + X_CHUNKS;   // the zero chunk (padding entries)
-  static constexpr int BIG_BYTES = (ZC + 1) * CH;
+  static constexpr int BIG_BYTES = ((ZC + 1) * CH + 127) / 128 * 128;
   static constexpr int HDR = 2 * RS + 4;            // ints: srow[RS], slr[RS], stage id, pad
   static constexpr int IDX_BYTES = HDR * 4 + RS * ROWE * 4;
-  static constexpr int NIDX = 4;                    // index blocks in flight (ring depth)
+  static constexpr int NIDX = S >= 16 ? 4 : 2;      // index blocks in flight (ring depth; smem-limited at s < 16)
   static constexpr int RED_BYTES = RS * S * 8;
   static constexpr int SMEM = 2 * BIG_BYTES + NIDX * IDX_BYTES + 2 * RED_BYTES + 64;
   static_assert(RS * TPR == 256, "one thread per (row slot, sample pair)");
@@ -154,7 +154,7 @@ struct StagedCta {
     const bool prod = threadIdx.x == 0 && has(it + 2);
     if (prod) dn = desc[stage_of(it + 2)];
     if (has(it + 1)) {  // the next stage's transposed gathers fly during this stage
-      mbar_wait(&bar[2 + ((it + 1) & (Sh::NIDX - 1))], ((it + 1) >> 2) & 1);
+      mbar_wait(&bar[2 + ((it + 1) & (Sh::NIDX - 1))], ((it + 1) / Sh::NIDX) & 1);
       gather(it + 1, Gn);
     }
     const int* ib = idx(it);
@@ -416,7 +416,9 @@ bool staged_fuse_fin() {
   return on != 0;
 }
 
-bool staged_supported(int s, int N) { return (s == 16 || s == 32) && N >= 8; }
+// s = 8 measured slower than the warp-per-tile kernel (0.125 vs 0.096 ms at
+// 64^3), s = 4 faster (0.081 vs 0.087), s = 16 / 32 faster (tools/kernel_bench.py --ab)
+bool staged_supported(int s, int N) { return (s == 4 || s == 16 || s == 32) && N >= 8; }
 
 cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
                             const int* col_entry, const int* vpos, const int* up_start,
@@ -425,7 +427,8 @@ cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
   if (!staged_supported(s, N) || tm.rows != N * N * N) return cudaErrorInvalidValue;
   int T = 0, L = 0, RS = 0, max_upper = 0, idx_bytes = 0, zc = 0;
   if (s == 32) stage_shape<32>(T, L, RS, max_upper, idx_bytes, zc);
-  else stage_shape<16>(T, L, RS, max_upper, idx_bytes, zc);
+  else if (s == 16) stage_shape<16>(T, L, RS, max_upper, idx_bytes, zc);
+  else stage_shape<4>(T, L, RS, max_upper, idx_bytes, zc);
   const int rows = tm.rows;
   std::vector<int> hup(rows + 1);
   cudaError_t err = cudaMemcpyAsync(hup.data(), up_start, (rows + 1) * sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -563,6 +566,7 @@ cudaError_t launch_cg_spmv_staged(int s, bool tiles, bool fuse_fin, const StageM
                                   cudaStream_t st) {
   if (s == 32) return cg_spmv_staged_s<32>(tiles, fuse_fin, sm, values, p, q, f, st);
   if (s == 16) return cg_spmv_staged_s<16>(tiles, fuse_fin, sm, values, p, q, f, st);
+  if (s == 4) return cg_spmv_staged_s<4>(tiles, fuse_fin, sm, values, p, q, f, st);
   return cudaErrorInvalidValue;
 }
 

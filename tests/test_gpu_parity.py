@@ -473,7 +473,7 @@ def test_symmetric_storage_is_bitwise_neutral(ctx, R, mode, s):
 
 @pytest.mark.parametrize("mode", [DOT_SERIAL, DOT_CANONICAL])
 @pytest.mark.parametrize("s,n,seg", [(32, 7, 0), (32, 12, 0), (32, 23, 0), (16, 8, 0), (16, 19, 0),
-                                     (32, 12, 1000), (16, 12, 77)])
+                                     (32, 12, 1000), (16, 12, 77), (4, 17, 0), (4, 30, 0), (4, 9, 50)])
 def test_staged_spmv_is_bitwise_equal_to_warp_kernel(ctx, mode, s, n, seg):
     """The stage-pipelined CG SpMV (ep_staged.cu; auto-selected for structured
     problems with symmetric storage at s in {16, 32}) gives the same bits as the
