@@ -214,6 +214,8 @@ inline int pdl_mask() {
   return m;
 }
 
+constexpr int kLaunchCooperative = 64;  // launch_kk kind flag
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_kk(int kind, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                              cudaStream_t st, Args... args) {
@@ -222,11 +224,20 @@ inline cudaError_t launch_kk(int kind, void (*kernel)(KArgs...), dim3 grid, dim3
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (pdl_enabled() && (pdl_mask() & kind)) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (kind & kLaunchCooperative) {  // all CTAs co-resident (grid-wide barrier inside)
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n].val.cooperative = 1;
+    ++n;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = (pdl_enabled() && (pdl_mask() & kind)) ? 1 : 0;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 

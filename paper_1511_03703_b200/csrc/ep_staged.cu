@@ -553,7 +553,10 @@ static cudaError_t cg_spmv_staged_s(bool tiles, bool fuse_fin, const StageMap& s
   if (sm.nstages == 0) return cudaSuccess;
   const int grid = sm.nstages < nsm ? sm.nstages : nsm;
   if (tiles)
-    launch_kk(2, k_cg_spmv_staged<S, true>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
+    // the fused finalize's grid barrier needs every CTA resident: a
+    // cooperative launch guarantees it even with other streams' kernels
+    // (possibly persistent ones of concurrent sample groups) on the GPU
+    launch_kk(2 | (fuse_fin ? kLaunchCooperative : 0), k_cg_spmv_staged<S, true>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
                                                            values, p, q, f, fuse_fin ? 1 : 0);
   else
     launch_kk(2, k_cg_spmv_staged<S, false>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
