@@ -7,25 +7,29 @@
 // interchangeable.  What changes is how the bytes reach the SM.
 //
 // A stage is T = 32/S consecutive canonical tiles (16 T rows, a contiguous row
-// range [R0, R1)).  One persistent CTA per SM walks the stages round-robin
-// (CTA c takes stages c, c + grid, ...: the SMs sweep the matrix together, so a
-// plane's upper slots are still in L2 when the next plane re-reads them
-// transposed) through a two-deep ring of shared-memory stage buffers.  Thread 0
-// fills a buffer with cp.async.bulk (TMA engine) copies completing on an
-// mbarrier:
+// range [R0, R1)).  One persistent CTA per SM walks the stages in a band sweep
+// order (CTA c takes sweep positions c, c + grid, ...; a band of mesh lines is
+// swept through all planes before the next band, so the upper slots a row
+// reads transposed are still in L2) through a two-deep ring of shared-memory
+// stage buffers.  Thread 0 fills a buffer with cp.async.bulk (TMA engine)
+// copies completing on an mbarrier:
 //   * the stage's stored slots (diagonal + upper of its rows): one contiguous
 //     range of the symmetric value array, up to 16 T x 14 x 8S = 57 KB;
 //   * the direction vector around the stage: the 27-point neighbours of rows
 //     [R0, R1) lie in 9 contiguous row runs [R0-1 + dj N + dk N^2, R1+1 + ...),
 //     dj, dk in {-1,0,1} (x-fastest numbering, mesh.hpp:24-26), 9 x 18 x 8S
 //     bytes at S = 32 instead of 16 x 27 gathers;
-//   * a precomputed index block (k_stage_fill): per row the local entry start,
-//     per entry the smem row of its x operand and where its value lives.
+//   * a precomputed index block (k_stage_fill, its own ring): per row slot
+//     the row and local row, per stencil slot (27, column order) where the
+//     value lives; x of slot (run, di) is at position lr + di + 1 of x run
+//     `run` (computed).
 // Only the lower entries whose transposed slot belongs to an earlier stage
-// (<= 13 per row, all in the row's leading entries) are gathered from global
-// memory into registers, issued together as soon as the buffer is ready.
-// The register file therefore only holds the transposed gathers; the streamed
-// bytes are in flight in the TMA engine, a stage ahead of the compute.
+// (<= 13 per row, the leading stencil slots) are gathered from global memory
+// into registers, one stage ahead.  The register file therefore only holds
+// the transposed gathers; the streamed bytes are in flight in the TMA engine.
+// With tiles, the kernel also closes the p.q dot: after a grid barrier
+// (cooperative launch) the CTAs fold the canonical segments and the last one
+// runs the CG phase (ep_fin.cuh), replacing the separate finalize launch.
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
