@@ -148,6 +148,10 @@ struct StagedCta {
     }
   }
 
+  // in-stage value code: 0x80000000 | (byte offset >> 4); (code << 4) drops the flag
+  __device__ __forceinline__ double2 slot_val(const unsigned char* lb, int c) const {
+    return *reinterpret_cast<const double2*>(lb + ((uint32_t)c << 4));
+  }
   __device__ __forceinline__ double2 chunk(const unsigned char* sb, int c) const {
     return *reinterpret_cast<const double2*>(sb + c * Sh::CH + lane0 * 8);
   }
@@ -182,13 +186,14 @@ struct StagedCta {
     // at position lr + di + 1 of x run `run`.
     double s0 = 0.0, s1 = 0.0;
     double2 pown = make_double2(0.0, 0.0);
-    const unsigned char* xb = sb + Sh::UP_CHUNKS * Sh::CH + lane0 * 8;
+    const unsigned char* lb = sb + lane0 * 8;  // this thread's samples in chunk 0
+    const unsigned char* xb = lb + Sh::UP_CHUNKS * Sh::CH + lr * Sh::CH;
 #pragma unroll
     for (int run = 0; run < 9; ++run) {
       const unsigned char* xr = xb + run * Sh::L * Sh::CH;
-      const double2 xm = *reinterpret_cast<const double2*>(xr + lr * Sh::CH);
-      const double2 x0 = *reinterpret_cast<const double2*>(xr + (lr + 1) * Sh::CH);
-      const double2 xp = *reinterpret_cast<const double2*>(xr + (lr + 2) * Sh::CH);
+      const double2 xm = *reinterpret_cast<const double2*>(xr);
+      const double2 x0 = *reinterpret_cast<const double2*>(xr + Sh::CH);
+      const double2 xp = *reinterpret_cast<const double2*>(xr + 2 * Sh::CH);
       if (run == 4) pown = x0;  // the row's own p
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
@@ -197,9 +202,9 @@ struct StagedCta {
         double2 a;
         if (k < kStageMaxGlobal) {
           a = Gc.v[k];
-          if (c < 0) a = chunk(sb, -c - 1);
+          if (c < 0) a = slot_val(lb, c);
         } else {
-          a = chunk(sb, -c - 1);
+          a = slot_val(lb, c);
         }
         const double2 xv = d == 0 ? xm : (d == 1 ? x0 : xp);
         s0 = EP_DADD(s0, EP_DMUL(a.x, xv.x));
@@ -338,10 +343,10 @@ __global__ void __launch_bounds__(256, 1) k_cg_spmv_staged(
 //   int g, pad[3]      canonical stage id (tiles g*T + ti)
 //   int sa[RS][28]     value of stencil slot k = run*3 + di + 1, run =
 //                      (dk+1)*3 + dj+1 (column order): >= 0 global slot (the
-//                      transposed entry of an earlier stage's row), < 0:
-//                      -(chunk + 1) in the stage buffer; absent neighbours and
-//                      empty slots point at the zero chunk
-__global__ void k_stage_fill(const TileMap tm, int nstages, int T, int N, int L, int RS,
+//                      transposed entry of an earlier stage's row), else
+//                      0x80000000 | (byte offset in the stage buffer >> 4);
+//                      absent neighbours and empty slots point at the zero chunk
+__global__ void k_stage_fill(const TileMap tm, int nstages, int T, int N, int L, int RS, int ch,
                              int up_chunks, int zc, int idx_bytes,
                              const StageDesc* __restrict__ desc, const int* __restrict__ row_map,
                              const int* __restrict__ col_entry, const int* __restrict__ vpos,
@@ -355,7 +360,8 @@ __global__ void k_stage_fill(const TileMap tm, int nstages, int T, int N, int L,
   const int hdr = 2 * RS + 4;
   int* sa = ib + hdr + rr * 28;
   if (rr == 0) ib[2 * RS] = g;  // stage id for the tile trees
-  for (int k = 0; k < 28; ++k) sa[k] = -(zc + 1);
+  auto smem_code = [&](int chunk) { return (int)(0x80000000u | (uint32_t)(chunk * ch >> 4)); };
+  for (int k = 0; k < 28; ++k) sa[k] = smem_code(zc);
   const int b = g * T + rr / kTileRows, t = rr % kTileRows;
   int r0 = 0, nr = 0;
   if (b < tm.num_tiles()) tm.tile(b, r0, nr);
@@ -387,7 +393,7 @@ __global__ void k_stage_fill(const TileMap tm, int nstages, int T, int N, int L,
     if (c >= d.R0) {
       const int a = v - d.slot0;
       if (a < 0 || a >= up_chunks) atomicAdd(bad, 1);
-      code = -(a + 1);
+      code = smem_code(a);
     } else {
       if (slot >= kStageMaxGlobal) atomicAdd(bad, 1);
       code = v;
@@ -509,7 +515,7 @@ cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
     err = cudaMemcpyAsync(sm.desc, hd.data(), hd.size() * sizeof(StageDesc), cudaMemcpyHostToDevice, st);
   if (err == cudaSuccess) {
     const int work = sm.nstages * RS;
-    k_stage_fill<<<(work + 255) / 256, 256, 0, st>>>(tm, sm.nstages, T, N, L, RS, max_upper, zc,
+    k_stage_fill<<<(work + 255) / 256, 256, 0, st>>>(tm, sm.nstages, T, N, L, RS, 8 * s, max_upper, zc,
                                                      idx_bytes, sm.desc, row_map, col_entry, vpos,
                                                      sm.blk, bad);
     err = cudaGetLastError();
