@@ -25,7 +25,7 @@ namespace ep {
 // Dirichlet is +0.0 and only the Jacobian is formed.
 // =============================================================================
 template <int S, bool kNonlinear, bool kHasU>
-__global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
+__global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ AsmArgs a) {
   const int gt = blockIdx.x * blockDim.x + threadIdx.x;
   const int lrow = gt / S;  // local row
   const int row = a.row_begin + lrow;  // global node id
@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(256) k_assemble(const AsmArgs a) {
   if (lrow >= a.rows) return;
   const int n = a.n, N = n + 1, n2 = 2 * n;
   const int i = row % N, j = (row / N) % N, k = row / (N * N);
-  const AsmTables& T = *a.tab;
+  const AsmTables& T = a.T;  // kernel parameter: uniform constant-bank reads
   const double wd = T.wd;
 
   double acc[27];

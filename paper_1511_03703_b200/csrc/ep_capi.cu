@@ -492,6 +492,7 @@ int make_asm_setup(enprop_ctx* c, int n, const enprop_kl_params* kl,
   a.mean = f.mean;
   a.F = out.F;
   a.tab = out.tab;
+  a.T = T;
   a.nonlinear = (coeffs && (coeffs->alpha != 0.0 || coeffs->beta != 0.0)) ? 1 : 0;
   for (int i = 0; i < f.m; ++i) {
     for (int k = 0; k < 3; ++k) a.mode_axes[i][k] = f.mode_axes[i * 3 + k];

@@ -27,7 +27,8 @@ struct AsmArgs {
   int m;                 // KL terms
   double mean;           // kappa0
   const double* F;       // KL axis tables [m][2n]: f_t((c + off_b) * h)
-  const AsmTables* tab;  // device
+  const AsmTables* tab;  // device copy (kept for the dist path's uploads)
+  AsmTables T;           // the same tables by value: kernel-parameter (constant bank) reads
   const int* row_map;    // device
   const double* u;       // [rows][s] or nullptr (= 0)
   const double* y;       // [m][s]
