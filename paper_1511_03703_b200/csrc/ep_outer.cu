@@ -60,13 +60,47 @@ __global__ void __launch_bounds__(kOuterRows) k_spmv_outer(int rows, int cols, i
   }
 }
 
+// Asynchronous staging (cp.async, LDGSTS): n elements of T from src into shared
+// memory at sbase + phase, where phase = src's element offset inside its 16-byte
+// granule, so source and destination share the 16-byte phase and every whole
+// granule moves with one 16-byte copy; the (at most two) partial granules at the
+// ends move element by element. Nothing outside [src, src + n) is read. All of a
+// thread's copies are in flight together (no register round trip); the caller
+// waits with cp_async_wait_all() + __syncthreads(). Returns the phase.
+__device__ __forceinline__ void cp_async16(void* d, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(d)), "l"(g) : "memory");
+}
+template <int B>
+__device__ __forceinline__ void cp_async_small(void* d, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(d)), "l"(g), "n"(B) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <typename T>
+__device__ __forceinline__ int stage_async(T* sbase, const T* src, int n) {
+  constexpr int E = 16 / sizeof(T);
+  const int ph = (int)((reinterpret_cast<uintptr_t>(src) & 15) / sizeof(T));
+  const T* g0 = src - ph;  // 16-byte aligned; only elements >= ph are read
+  const int total = ph + n;
+  const int ng = (total + E - 1) / E;
+  for (int g = threadIdx.x; g < ng; g += blockDim.x) {
+    const int lo = g * E, hi = lo + E;
+    if (lo >= ph && hi <= total) {
+      cp_async16(sbase + lo, g0 + lo);
+    } else {
+      for (int i = max(lo, ph); i < min(hi, total); ++i) cp_async_small<sizeof(T)>(sbase + i, g0 + i);
+    }
+  }
+  return ph;
+}
+
 // Ensemble-layout SpMV for narrow ensembles (s <= 8): a row's s values are only
 // 8s <= 64 bytes, so one thread per (row, sample) walking its row would issue
 // strided, uncoalesced loads. Instead a CTA stages its row block's contiguous
-// column-index and value ranges in shared memory with coalesced loads, then
-// thread (row, sample e) sums its row in entry order from shared memory
-// (kernels.hpp:15-26, bitwise). Falls back to direct reads for blocks whose
-// entries exceed the staging capacity.
+// column-index and value ranges in shared memory with asynchronous 16-byte
+// copies (stage_async), then thread (row, sample e) sums its row in entry order
+// from shared memory (kernels.hpp:15-26, bitwise). Falls back to direct reads
+// for blocks whose entries exceed the staging capacity.
 template <int S>
 __global__ void __launch_bounds__(kOuterRows) k_spmv_small(int rows, const int* __restrict__ row_map,
                                                            const int* __restrict__ col_entry,
@@ -75,22 +109,30 @@ __global__ void __launch_bounds__(kOuterRows) k_spmv_small(int rows, const int* 
                                                            double* __restrict__ z) {
   constexpr int RB = kOuterRows / S;   // rows per CTA
   constexpr int CAP = RB * 28;         // staged entries
-  __shared__ int scol[CAP];
-  __shared__ double sval[CAP * S];
+  __shared__ __align__(16) int scol_raw[CAP + 4];
+  __shared__ __align__(16) double sval_raw[CAP * S + 2];
   const int r0 = blockIdx.x * RB;
   const int r1 = imin(r0 + RB, rows);
   const int row = r0 + threadIdx.x / S, e = threadIdx.x % S;
   const int k0 = __ldg(row_map + r0), k1 = __ldg(row_map + r1);
   const int n = k1 - k0;
   const bool staged = n <= CAP;
+  const int* scol = scol_raw;
+  const double* sval = sval_raw;
   if (staged) {
-    for (int i = threadIdx.x; i < n; i += kOuterRows) scol[i] = ld_stream_i32(col_entry + k0 + i);
-    const double* v0 = values + (size_t)k0 * S;
-    for (int i = threadIdx.x; i < n * S; i += kOuterRows) sval[i] = ld_stream<1>(v0 + i).v[0];
+    scol += stage_async(scol_raw, col_entry + k0, n);
+    sval += stage_async(sval_raw, values + (size_t)k0 * S, n * S);
+  }
+  int ks = 0, ke = 0;
+  if (row < rows) {
+    ks = __ldg(row_map + row) - k0;
+    ke = __ldg(row_map + row + 1) - k0;
+  }
+  if (staged) {
+    cp_async_wait_all();
     __syncthreads();
   }
   if (row >= rows) return;
-  const int ks = __ldg(row_map + row) - k0, ke = __ldg(row_map + row + 1) - k0;
   double sum = 0.0;
   if (staged) {
     for (int k = ks; k < ke; ++k) sum = EP_DADD(sum, EP_DMUL(sval[k * S + e], __ldg(x + (size_t)scol[k] * S + e)));
