@@ -101,14 +101,14 @@ __device__ __forceinline__ int stage_async(T* sbase, const T* src, int n) {
 // copies (stage_async), then thread (row, sample e) sums its row in entry order
 // from shared memory (kernels.hpp:15-26, bitwise). Falls back to direct reads
 // for blocks whose entries exceed the staging capacity.
-template <int S>
-__global__ void __launch_bounds__(kOuterRows) k_spmv_small(int rows, const int* __restrict__ row_map,
+template <int S, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_spmv_small(int rows, const int* __restrict__ row_map,
                                                            const int* __restrict__ col_entry,
                                                            const double* __restrict__ values,
                                                            const double* __restrict__ x,
                                                            double* __restrict__ z) {
-  constexpr int RB = kOuterRows / S;   // rows per CTA
-  constexpr int CAP = RB * 28;         // staged entries
+  constexpr int RB = NT / S;   // rows per CTA
+  constexpr int CAP = RB * 28;  // staged entries
   __shared__ __align__(16) int scol_raw[CAP + 4];
   __shared__ __align__(16) double sval_raw[CAP * S + 2];
   const int r0 = blockIdx.x * RB;
@@ -143,13 +143,49 @@ __global__ void __launch_bounds__(kOuterRows) k_spmv_small(int rows, const int* 
   z[(size_t)row * S + e] = sum;
 }
 
+// CTA size and register cap of the narrow-ensemble SpMV. Defaults (A/B at
+// 128^3, tools/small_ab.py): 64 threads for s = 1, 96 for s >= 2, capped at 64
+// registers (uncapped, ptxas takes 80-86 and s = 4/8 lose 25%). A/B switches:
+// ENPROP_SMALL_NT = 64 | 96 | 128, ENPROP_SMALL_REGS = 0 (uncapped) | 48 | 64.
+static int small_nt(int s) {
+  static const int nt = [] {
+    const char* e = getenv("ENPROP_SMALL_NT");
+    const int v = e ? atoi(e) : 0;
+    return (v == 64 || v == 96 || v == 128) ? v : 0;
+  }();
+  return nt ? nt : (s == 1 ? 64 : 96);
+}
+static int small_regs() {
+  static const int r = [] {
+    const char* e = getenv("ENPROP_SMALL_REGS");
+    const int v = e ? atoi(e) : 64;
+    return (v == 0 || v == 48) ? v : 64;
+  }();
+  return r;
+}
+
+template <int S, int NT>
+static cudaError_t spmv_small_nt(int rows, const int* row_map, const int* col_entry,
+                                 const double* values, const double* x, double* z, cudaStream_t st) {
+  constexpr int RB = NT / S;
+  if (rows <= 0) return cudaSuccess;
+  const int grid = (rows + RB - 1) / RB;
+  switch (small_regs()) {
+    case 0: k_spmv_small<S, NT, 1><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+    case 48: k_spmv_small<S, NT, 65536 / (NT * 48)><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+    default: k_spmv_small<S, NT, 65536 / (NT * 64)><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+  }
+  return cudaGetLastError();
+}
+
 template <int S>
 static cudaError_t spmv_small_s(int rows, const int* row_map, const int* col_entry,
                                 const double* values, const double* x, double* z, cudaStream_t st) {
-  constexpr int RB = kOuterRows / S;
-  if (rows <= 0) return cudaSuccess;
-  k_spmv_small<S><<<(rows + RB - 1) / RB, kOuterRows, 0, st>>>(rows, row_map, col_entry, values, x, z);
-  return cudaGetLastError();
+  switch (small_nt(S)) {
+    case 64: return spmv_small_nt<S, 64>(rows, row_map, col_entry, values, x, z, st);
+    case 128: return spmv_small_nt<S, 128>(rows, row_map, col_entry, values, x, z, st);
+    default: return spmv_small_nt<S, 96>(rows, row_map, col_entry, values, x, z, st);
+  }
 }
 
 cudaError_t launch_spmv_small(int s, int rows, const int* row_map, const int* col_entry,
