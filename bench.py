@@ -429,6 +429,22 @@ def bench_serial(torch, ep, workers, ys, args, cfg):
             "note": "DOT_SERIAL: the reference's reduction order, bitwise equal to its pcg_solve per sample"}
 
 
+def time_queued(torch, fn, reps, stream):
+    """Per-launch CUDA-event times of reps back-to-back launches of fn queued on
+    stream with no host synchronisation in between, so the host's launch
+    overhead overlaps the previous launch instead of being timed (a sync per
+    rep leaves the GPU idle while the next launch is issued: ~20 us, 10-15% of a
+    0.2 ms s = 1 SpMV). Returns the list of milliseconds."""
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        a.record(stream)
+        fn()
+        b.record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
 def bench_spmv(ctx, ep, torch, pack_group, O, hbm, peak_kind, reps=20):
     """cfg 3: enprop_spmv on the assembled + Dirichlet 128^3 matrix, s = 32, x
     uniform in [-1, 1); CUDA events on the context's (torch's current) stream."""
@@ -442,16 +458,8 @@ def bench_spmv(ctx, ep, torch, pack_group, O, hbm, peak_kind, reps=20):
     rm, ce, vals = p.row_map, p.col_entry, p.values
     for _ in range(3):
         ep.spmv(ctx, s, rm, ce, vals, x, z)
-    torch.cuda.synchronize()
-    times = []
     stream = torch.cuda.current_stream()
-    for _ in range(reps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        ep.spmv(ctx, s, rm, ce, vals, x, z)
-        b.record(stream)
-        torch.cuda.synchronize()
-        times.append(a.elapsed_time(b))
+    times = time_queued(torch, lambda: ep.spmv(ctx, s, rm, ce, vals, x, z), reps, stream)
     best = min(times)
     med = statistics.median(times)
     byt = spmv_bytes(p.nnz, p.rows, s)
@@ -485,19 +493,12 @@ def bench_spmv_widths(ctx, ep, torch, pack_group, O, hbm, n, gbs32, reps=10):
         z = torch.empty_like(x)
         for _ in range(3):
             ep.spmv(ctx, s, p.row_map, p.col_entry, vals, x, z)
-        ts = []
-        for _ in range(reps):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            ep.spmv(ctx, s, p.row_map, p.col_entry, vals, x, z)
-            b.record(stream)
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
+        ts = time_queued(torch, lambda: ep.spmv(ctx, s, p.row_map, p.col_entry, vals, x, z), reps, stream)
         med = statistics.median(ts)
         byt = spmv_bytes(p.nnz, p.rows, s)
         res[str(s)] = {"ms": round(med, 4), "gbs": round(byt / (med / 1e3) / 1e9, 1),
                        "frac": round(byt / (med / 1e3) / 1e9 / hbm, 4),
-                       "kernel": f"k_spmv_small<{s}>" if s <= 8 else f"k_spmv<{s}>"}
+                       "kernel": f"k_spmv_small<{s},{64 if s == 1 else 96}>" if s <= 8 else f"k_spmv<{s}>"}
         p.close()
         del vals, x, z
     res["32"] = {"gbs": gbs32, "frac": round(gbs32 / hbm, 4), "kernel": "k_spmv<32>"}
@@ -520,16 +521,7 @@ def bench_spmv_layouts(ctx, ep, torch, p, x, z, byt, commuted_ms, reps=5):
 
     def timed(fn):
         fn()
-        torch.cuda.synchronize()
-        ts = []
-        for _ in range(reps):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            fn()
-            b.record(stream)
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
-        return statistics.median(ts)
+        return statistics.median(time_queued(torch, fn, reps, stream))
 
     def scalar():
         for e in range(s):

@@ -1,6 +1,6 @@
 """Narrow-ensemble SpMV timing (s = 1, 4, 8) on the 128^3 matrix, for A/B runs of
 the k_spmv_small CTA size (ENPROP_SMALL_NT) in separate processes.  CUDA events
-on the current stream, median of --reps; the official numbers come from bench.py.
+on the current stream (launches queued back to back), median of --reps; the official numbers come from bench.py.
 
     ENPROP_SMALL_NT=64 python tools/small_ab.py [--n 128]
 """
@@ -18,6 +18,7 @@ import torch  # noqa: E402
 
 import paper_1511_03703_b200 as ep  # noqa: E402
 from oracles import Oracle, pack_group  # noqa: E402
+from bench import time_queued  # noqa: E402
 
 
 def main():
@@ -39,14 +40,7 @@ def main():
         z = torch.empty_like(x)
         for _ in range(3):
             ep.spmv(ctx, s, p.row_map, p.col_entry, vals, x, z)
-        ts = []
-        for _ in range(args.reps):
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(st)
-            ep.spmv(ctx, s, p.row_map, p.col_entry, vals, x, z)
-            b.record(st)
-            torch.cuda.synchronize()
-            ts.append(a.elapsed_time(b))
+        ts = time_queued(torch, lambda: ep.spmv(ctx, s, p.row_map, p.col_entry, vals, x, z), args.reps, st)
         med = statistics.median(ts)
         byt = p.nnz * (8 * s + 4) + 4 * (p.rows + 1) + 16 * s * p.rows
         out[str(s)] = {"ms": round(med, 4), "gbs": round(byt / (med / 1e3) / 1e9, 1)}
