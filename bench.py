@@ -498,7 +498,7 @@ def bench_spmv_widths(ctx, ep, torch, pack_group, O, hbm, n, gbs32, reps=10):
         byt = spmv_bytes(p.nnz, p.rows, s)
         res[str(s)] = {"ms": round(med, 4), "gbs": round(byt / (med / 1e3) / 1e9, 1),
                        "frac": round(byt / (med / 1e3) / 1e9 / hbm, 4),
-                       "kernel": f"k_spmv_small<{s},{64 if s == 1 else 96}>" if s <= 8 else f"k_spmv<{s}>"}
+                       "kernel": f"k_spmv_small<{s},64>" if s <= 8 else f"k_spmv<{s}>"}
         p.close()
         del vals, x, z
     res["32"] = {"gbs": gbs32, "frac": round(gbs32 / hbm, 4), "kernel": "k_spmv<32>"}

@@ -97,31 +97,39 @@ __device__ __forceinline__ int stage_async(T* sbase, const T* src, int n) {
 // Ensemble-layout SpMV for narrow ensembles (s <= 8): a row's s values are only
 // 8s <= 64 bytes, so one thread per (row, sample) walking its row would issue
 // strided, uncoalesced loads. Instead a CTA stages its row block's contiguous
-// column-index and value ranges in shared memory with asynchronous 16-byte
-// copies (stage_async), then thread (row, sample e) sums its row in entry order
-// from shared memory (kernels.hpp:15-26, bitwise). Falls back to direct reads
-// for blocks whose entries exceed the staging capacity.
-template <int S, int NT, int MINB>
+// column-index range in shared memory with asynchronous 16-byte copies
+// (stage_async), and thread (row, sample e) sums its row in entry order
+// (kernels.hpp:15-26, bitwise), reading x through the staged indices and its
+// values straight from global memory: a row block's values are one contiguous
+// range, so the CTA's value reads touch each 32-byte sector once between them
+// and L1 serves the rest; leaving them unstaged cuts the shared memory per CTA
+// (s = 1: 22.5 -> 8.2 KB) and raises the resident CTAs (MODE 1, the default;
+// A/B in profiles/round1/spmv_small_ab.jsonl). MODE 0 also stages the values,
+// MODE 2 only the values. Blocks whose entries exceed the staging capacity read
+// everything from global memory in the same order.
+template <int S, int NT, int MINB, int MODE>
 __global__ void __launch_bounds__(NT, MINB) k_spmv_small(int rows, const int* __restrict__ row_map,
                                                            const int* __restrict__ col_entry,
                                                            const double* __restrict__ values,
                                                            const double* __restrict__ x,
                                                            double* __restrict__ z) {
+  // MODE 0: stage indices and values; 1: indices only; 2: values only
+  constexpr bool kCols = MODE != 2, kVals = MODE != 1;
   constexpr int RB = NT / S;   // rows per CTA
   constexpr int CAP = RB * 28;  // staged entries
-  __shared__ __align__(16) int scol_raw[CAP + 4];
-  __shared__ __align__(16) double sval_raw[CAP * S + 2];
+  __shared__ __align__(16) int scol_raw[kCols ? CAP + 4 : 4];
+  __shared__ __align__(16) double sval_raw[kVals ? CAP * S + 2 : 2];
   const int r0 = blockIdx.x * RB;
   const int r1 = imin(r0 + RB, rows);
   const int row = r0 + threadIdx.x / S, e = threadIdx.x % S;
   const int k0 = __ldg(row_map + r0), k1 = __ldg(row_map + r1);
   const int n = k1 - k0;
   const bool staged = n <= CAP;
-  const int* scol = scol_raw;
-  const double* sval = sval_raw;
+  const int* scol = kCols ? scol_raw : col_entry + k0;
+  const double* sval = kVals ? sval_raw : values + (size_t)k0 * S;
   if (staged) {
-    scol += stage_async(scol_raw, col_entry + k0, n);
-    sval += stage_async(sval_raw, values + (size_t)k0 * S, n * S);
+    if constexpr (kCols) scol += stage_async(scol_raw, col_entry + k0, n);
+    if constexpr (kVals) sval += stage_async(sval_raw, values + (size_t)k0 * S, n * S);
   }
   int ks = 0, ke = 0;
   if (row < rows) {
@@ -135,7 +143,11 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv_small(int rows, const int* __
   if (row >= rows) return;
   double sum = 0.0;
   if (staged) {
-    for (int k = ks; k < ke; ++k) sum = EP_DADD(sum, EP_DMUL(sval[k * S + e], __ldg(x + (size_t)scol[k] * S + e)));
+    for (int k = ks; k < ke; ++k) {
+      const int c = kCols ? scol[k] : __ldg(scol + k);
+      const double a = kVals ? sval[k * S + e] : __ldg(sval + k * S + e);
+      sum = EP_DADD(sum, EP_DMUL(a, __ldg(x + (size_t)c * S + e)));
+    }
   } else {
     for (int k = k0 + ks; k < k0 + ke; ++k)
       sum = EP_DADD(sum, EP_DMUL(__ldg(values + (size_t)k * S + e), __ldg(x + (size_t)__ldg(col_entry + k) * S + e)));
@@ -143,17 +155,19 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv_small(int rows, const int* __
   z[(size_t)row * S + e] = sum;
 }
 
-// CTA size and register cap of the narrow-ensemble SpMV. Defaults (A/B at
-// 128^3, tools/small_ab.py): 64 threads for s = 1, 96 for s >= 2, capped at 64
-// registers (uncapped, ptxas takes 80-86 and s = 4/8 lose 25%). A/B switches:
-// ENPROP_SMALL_NT = 64 | 96 | 128, ENPROP_SMALL_REGS = 0 (uncapped) | 48 | 64.
-static int small_nt(int s) {
+// CTA size, register cap and staging mode of the narrow-ensemble SpMV.
+// Defaults (A/B at 128^3, tools/small_ab.py, profiles/round1/spmv_small_ab.jsonl):
+// 64 threads, capped at 64 registers (uncapped, ptxas takes 80-86 and s = 4/8
+// lose 25%), indices staged. A/B switches: ENPROP_SMALL_NT = 64 | 96 | 128,
+// ENPROP_SMALL_REGS = 0 (uncapped) | 48 | 64 (0 and 48 with ENPROP_SMALL_STAGE=0),
+// ENPROP_SMALL_STAGE = 0 | 1 | 2.
+static int small_nt(int) {
   static const int nt = [] {
     const char* e = getenv("ENPROP_SMALL_NT");
     const int v = e ? atoi(e) : 0;
-    return (v == 64 || v == 96 || v == 128) ? v : 0;
+    return (v == 96 || v == 128) ? v : 64;
   }();
-  return nt ? nt : (s == 1 ? 64 : 96);
+  return nt;
 }
 static int small_regs() {
   static const int r = [] {
@@ -170,10 +184,18 @@ static cudaError_t spmv_small_nt(int rows, const int* row_map, const int* col_en
   constexpr int RB = NT / S;
   if (rows <= 0) return cudaSuccess;
   const int grid = (rows + RB - 1) / RB;
-  switch (small_regs()) {
-    case 0: k_spmv_small<S, NT, 1><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
-    case 48: k_spmv_small<S, NT, 65536 / (NT * 48)><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
-    default: k_spmv_small<S, NT, 65536 / (NT * 64)><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+  static const int mode = [] {
+    const char* e = getenv("ENPROP_SMALL_STAGE");
+    const int v = e ? atoi(e) : 1;
+    return (v == 0 || v == 2) ? v : 1;
+  }();
+  constexpr int MB = 65536 / (NT * 64);
+  switch (small_regs() * 4 + mode) {
+    case 0: k_spmv_small<S, NT, 1, 0><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+    case 192: k_spmv_small<S, NT, 65536 / (NT * 48), 0><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+    case 256: k_spmv_small<S, NT, MB, 0><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+    case 258: k_spmv_small<S, NT, MB, 2><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+    default: k_spmv_small<S, NT, MB, 1><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
   }
   return cudaGetLastError();
 }
@@ -182,9 +204,9 @@ template <int S>
 static cudaError_t spmv_small_s(int rows, const int* row_map, const int* col_entry,
                                 const double* values, const double* x, double* z, cudaStream_t st) {
   switch (small_nt(S)) {
-    case 64: return spmv_small_nt<S, 64>(rows, row_map, col_entry, values, x, z, st);
+    case 96: return spmv_small_nt<S, 96>(rows, row_map, col_entry, values, x, z, st);
     case 128: return spmv_small_nt<S, 128>(rows, row_map, col_entry, values, x, z, st);
-    default: return spmv_small_nt<S, 96>(rows, row_map, col_entry, values, x, z, st);
+    default: return spmv_small_nt<S, 64>(rows, row_map, col_entry, values, x, z, st);
   }
 }
 
