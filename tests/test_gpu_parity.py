@@ -186,6 +186,35 @@ def test_spmv_mesh_matrix_bitwise(ctx, R, s):
     assert same(host(z), O.spmv(s, host(rm), host(ce), host(v), x))
 
 
+@pytest.mark.parametrize("s", WIDTHS)
+def test_spmv_dense_rows_bitwise(ctx, R, s):
+    """Row blocks whose entries exceed the kernels' shared-memory staging
+    capacity (100-entry rows) take the direct-read path: still bitwise."""
+    rng = np.random.default_rng(4242 + s)
+    rows, cols = 300, 100
+    rm, ce = random_crs(rng, rows, cols, 1.0)
+    vals = rng.uniform(-1, 1, (len(ce), s))
+    x = rng.uniform(-1, 1, (cols, s))
+    z = ep.spmv(ctx, s, dev(rm, torch.int32), dev(ce, torch.int32), dev(vals), dev(x), num_cols=cols)
+    assert same(host(z), R.spmv(s, rm, ce, vals, x, cols=cols))
+
+
+@pytest.mark.parametrize("mode", ["0", "2"])
+def test_spmv_small_staging_modes_bitwise(mode):
+    """The narrow-ensemble SpMV's A/B staging modes (ENPROP_SMALL_STAGE, read
+    once per process; default 1 is covered above) stay bitwise: the SpMV
+    parity cases rerun in a child process with the mode set."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, ENPROP_SMALL_STAGE=mode)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.join(here, "test_gpu_parity.py"),
+                        "-k", "spmv and bitwise and not staging_modes"],
+                       env=env, cwd=os.path.dirname(here), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
 def test_spmv_rejects_bad_length(ctx):
     rm = dev(np.array([0, 1, 2, 3], np.int32), torch.int32)
     ce = dev(np.array([0, 1, 2], np.int32), torch.int32)
