@@ -157,25 +157,29 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv_small(int rows, const int* __
 
 // CTA size, register cap and staging mode of the narrow-ensemble SpMV.
 // Defaults (A/B at 128^3, tools/small_ab.py, profiles/round1/spmv_small_ab.jsonl):
-// 64 threads, capped at 64 registers (uncapped, ptxas takes 80-86 and s = 4/8
-// lose 25%), indices staged. A/B switches: ENPROP_SMALL_NT = 64 | 96 | 128,
-// ENPROP_SMALL_REGS = 0 (uncapped) | 48 | 64 (0 and 48 with ENPROP_SMALL_STAGE=0),
+// 64 threads, indices staged, capped at 64 registers for s = 1 and 48 for s >= 2
+// (uncapped, ptxas takes 80-86). A/B switches: ENPROP_SMALL_NT = 64 | 96 | 128,
+// ENPROP_SMALL_REGS = 0 (uncapped) | 32 | 48 | 64 (0: mode 0 only; 32: mode 1 only),
 // ENPROP_SMALL_STAGE = 0 | 1 | 2.
 static int small_nt(int) {
   static const int nt = [] {
     const char* e = getenv("ENPROP_SMALL_NT");
-    const int v = e ? atoi(e) : 0;
+    const int v = (e && *e) ? atoi(e) : 0;
     return (v == 96 || v == 128) ? v : 64;
   }();
   return nt;
 }
-static int small_regs() {
+static int small_regs(int s) {
   static const int r = [] {
     const char* e = getenv("ENPROP_SMALL_REGS");
-    const int v = e ? atoi(e) : 64;
-    return (v == 0 || v == 48) ? v : 64;
+    const int v = (e && *e) ? atoi(e) : -1;
+    return (v == 0 || v == 32 || v == 48 || v == 64) ? v : -1;
   }();
-  return r;
+  // auto: 64 at s = 1 (more resident CTAs shrink L1 below the unstaged value
+  // reads' reuse distance: 48 registers cost 30%), 48 at s >= 2 (a row's s
+  // values share sectors across threads, so L1 reuse matters less and the
+  // extra residency wins: s = 4/8 at 96-98% of HBM vs 80% at 64)
+  return r >= 0 ? r : (s == 1 ? 64 : 48);
 }
 
 template <int S, int NT>
@@ -186,13 +190,15 @@ static cudaError_t spmv_small_nt(int rows, const int* row_map, const int* col_en
   const int grid = (rows + RB - 1) / RB;
   static const int mode = [] {
     const char* e = getenv("ENPROP_SMALL_STAGE");
-    const int v = e ? atoi(e) : 1;
+    const int v = (e && *e) ? atoi(e) : 1;
     return (v == 0 || v == 2) ? v : 1;
   }();
   constexpr int MB = 65536 / (NT * 64);
-  switch (small_regs() * 4 + mode) {
+  switch (small_regs(S) * 4 + mode) {
     case 0: k_spmv_small<S, NT, 1, 0><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
     case 192: k_spmv_small<S, NT, 65536 / (NT * 48), 0><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+    case 193: k_spmv_small<S, NT, 65536 / (NT * 48), 1><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+    case 129: k_spmv_small<S, NT, 65536 / (NT * 32), 1><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
     case 256: k_spmv_small<S, NT, MB, 0><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
     case 258: k_spmv_small<S, NT, MB, 2><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
     default: k_spmv_small<S, NT, MB, 1><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
