@@ -479,7 +479,7 @@ def bench_spmv(ctx, ep, torch, pack_group, O, hbm, peak_kind, reps=20):
 
 
 def bench_spmv_widths(ctx, ep, torch, pack_group, O, hbm, n, gbs32, reps=10):
-    """Ensemble SpMV GB/s at s = 1, 4, 8, 16 on the same 128^3 matrix family
+    """Ensemble SpMV GB/s at s = 1, 4, 8, 16 on the same 128^3 matrix family (s <= 16: k_spmv_small)
     (north_star: throughput at ensemble sizes 1/4/8/16/32); s = 32 is cfg 3."""
     res = {}
     stream = torch.cuda.current_stream()
@@ -498,7 +498,7 @@ def bench_spmv_widths(ctx, ep, torch, pack_group, O, hbm, n, gbs32, reps=10):
         byt = spmv_bytes(p.nnz, p.rows, s)
         res[str(s)] = {"ms": round(med, 4), "gbs": round(byt / (med / 1e3) / 1e9, 1),
                        "frac": round(byt / (med / 1e3) / 1e9 / hbm, 4),
-                       "kernel": f"k_spmv_small<{s},64>" if s <= 8 else f"k_spmv<{s}>"}
+                       "kernel": f"k_spmv_small<{s},64>" if s <= 16 else f"k_spmv<{s}>"}
         p.close()
         del vals, x, z
     res["32"] = {"gbs": gbs32, "frac": round(gbs32 / hbm, 4), "kernel": "k_spmv<32>"}
@@ -535,7 +535,7 @@ def bench_spmv_layouts(ctx, ep, torch, p, x, z, byt, commuted_ms, reps=5):
     gbs = lambda ms: round(byt / (ms / 1e3) / 1e9, 1)
     return {"commuted": {"ms": round(commuted_ms, 4), "gbs": gbs(commuted_ms), "kernel": "k_spmv<32>"},
             "outer": {"ms": round(outer_ms, 4), "gbs": gbs(outer_ms), "kernel": "k_spmv_outer"},
-            "scalar": {"ms": round(scalar_ms, 4), "gbs": gbs(scalar_ms), "kernel": "32 x k_spmv<1>"},
+            "scalar": {"ms": round(scalar_ms, 4), "gbs": gbs(scalar_ms), "kernel": "32 x k_spmv_small<1,64>"},
             "speedup_commuted_vs_scalar": round(scalar_ms / commuted_ms, 3),
             "speedup_commuted_vs_outer": round(outer_ms / commuted_ms, 3),
             "gate_bitwise": gate}

@@ -561,7 +561,7 @@ int enprop_spmv(enprop_ctx* c, int s, int rows, int cols, const int* row_map,
   if (rows < 0 || cols < 0) return fail(ENPROP_ERR_INVALID, "spmv: negative dimension");
   if (rows == 0) return ENPROP_OK;
   if (!row_map || !z || (cols > 0 && !x)) return fail(ENPROP_ERR_INVALID, "spmv: null argument");
-  if (s <= 8 && !c->spmv_pipeline)  // narrow rows: shared-memory staged blocks (ep_outer.cu)
+  if (s <= spmv_small_max() && !c->spmv_pipeline)  // narrow rows: shared-memory staged blocks (ep_outer.cu)
     EP_CUDA(launch_spmv_small(s, rows, row_map, col_entry, values, x, z, c->stream));
   else
     EP_CUDA(launch_spmv(s, rows, row_map, col_entry, values, x, z, c->spmv_pipeline != 0, c->stream));

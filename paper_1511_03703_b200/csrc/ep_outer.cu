@@ -216,6 +216,18 @@ static cudaError_t spmv_small_s(int rows, const int* row_map, const int* col_ent
   }
 }
 
+// widest ensemble enprop_spmv sends to k_spmv_small (ENPROP_SMALL_MAX: 8, 16
+// or 32; default 16: at 128^3, s = 16 runs at 97% of HBM here vs 90% in the
+// warp-per-row k_spmv<16>)
+int spmv_small_max() {
+  static const int m = [] {
+    const char* e = getenv("ENPROP_SMALL_MAX");
+    const int v = (e && *e) ? atoi(e) : 16;
+    return (v == 8 || v == 32) ? v : 16;
+  }();
+  return m;
+}
+
 cudaError_t launch_spmv_small(int s, int rows, const int* row_map, const int* col_entry,
                               const double* values, const double* x, double* z, cudaStream_t st) {
   switch (s) {
@@ -223,6 +235,8 @@ cudaError_t launch_spmv_small(int s, int rows, const int* row_map, const int* co
     case 2: return spmv_small_s<2>(rows, row_map, col_entry, values, x, z, st);
     case 4: return spmv_small_s<4>(rows, row_map, col_entry, values, x, z, st);
     case 8: return spmv_small_s<8>(rows, row_map, col_entry, values, x, z, st);
+    case 16: return spmv_small_s<16>(rows, row_map, col_entry, values, x, z, st);
+    case 32: return spmv_small_s<32>(rows, row_map, col_entry, values, x, z, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -30,7 +30,7 @@ def main():
     O = Oracle()
     out = {"nt": os.environ.get("ENPROP_SMALL_NT", "default"), "n": args.n}
     st = torch.cuda.current_stream()
-    for s in (1, 2, 4, 8):
+    for s in (1, 2, 4, 8, 16, 32):
         y = torch.as_tensor(pack_group(O.draw_samples(0, s, 3), s)).cuda()
         p = ep.Problem(ctx, args.n, s, ep.KlField(3, 1.0, 0.1, 1.0))
         p.assemble(y)
