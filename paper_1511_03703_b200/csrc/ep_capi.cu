@@ -44,7 +44,8 @@ struct CgWork {
   double* q = nullptr;
   double* partials = nullptr;  // canonical tile partials [tiles][s]
   double* seg_sums = nullptr;  // [segs][s]
-  int* counters = nullptr;     // [segs] arrival counters + [1] segment counter, self-resetting
+  int* counters = nullptr;     // kCounterInts counter words (ep_kernels.h)
+  double* prod = nullptr;      // serial order: p*q products [rows][s] (allocated on first use)
   double* hist = nullptr;
   CgState* state = nullptr;
   int rows = 0, s = 0, maxit = -1, tiles = 0, segs = 0;
@@ -52,27 +53,31 @@ struct CgWork {
 
 void free_work(CgWork& w) {
   for (void* p : {(void*)w.r, (void*)w.p[0], (void*)w.p[1], (void*)w.q, (void*)w.partials,
-                  (void*)w.seg_sums, (void*)w.counters, (void*)w.hist, (void*)w.state})
+                  (void*)w.seg_sums, (void*)w.counters, (void*)w.prod, (void*)w.hist,
+                  (void*)w.state})
     if (p) cudaFree(p);
   w = CgWork{};
 }
 
-int ensure_work(CgWork& w, int rows, int s, int maxit, const TileMap& tm) {
+int ensure_work(CgWork& w, int rows, int s, int maxit, const TileMap& tm, bool need_prod) {
   const int tiles = tm.num_tiles() > 0 ? tm.num_tiles() : 1;
   const int segs = tm.num_segs > 0 ? tm.num_segs : 1;
-  if (w.r && w.rows == rows && w.s == s && w.maxit >= maxit && w.tiles >= tiles && w.segs >= segs)
-    return ENPROP_OK;
-  free_work(w);
   const size_t vec = (size_t)rows * s * sizeof(double);
   const size_t vb = vec > 0 ? vec : 8;
+  if (w.r && w.rows == rows && w.s == s && w.maxit >= maxit && w.tiles >= tiles && w.segs >= segs) {
+    if (need_prod && !w.prod) EP_CUDA(cudaMalloc(&w.prod, vb));
+    return ENPROP_OK;
+  }
+  free_work(w);
+  if (need_prod) EP_CUDA(cudaMalloc(&w.prod, vb));
   EP_CUDA(cudaMalloc(&w.r, vb));
   EP_CUDA(cudaMalloc(&w.p[0], vb));
   EP_CUDA(cudaMalloc(&w.p[1], vb));
   EP_CUDA(cudaMalloc(&w.q, vb));
   EP_CUDA(cudaMalloc(&w.partials, (size_t)tiles * s * sizeof(double)));
   EP_CUDA(cudaMalloc(&w.seg_sums, (size_t)segs * s * sizeof(double)));
-  EP_CUDA(cudaMalloc(&w.counters, (size_t)(segs + 1) * sizeof(int)));
-  EP_CUDA(cudaMemset(w.counters, 0, (size_t)(segs + 1) * sizeof(int)));
+  EP_CUDA(cudaMalloc(&w.counters, kCounterInts * sizeof(int)));
+  EP_CUDA(cudaMemset(w.counters, 0, kCounterInts * sizeof(int)));
   EP_CUDA(cudaMalloc(&w.hist, (size_t)(maxit + 1) * s * sizeof(double)));
   EP_CUDA(cudaMalloc(&w.state, sizeof(CgState)));
   w.rows = rows;
@@ -83,12 +88,14 @@ int ensure_work(CgWork& w, int rows, int s, int maxit, const TileMap& tm) {
   return ENPROP_OK;
 }
 
-FinArgs fin_args(const CgWork& w, const TileMap& tm, int phase) {
+FinArgs fin_args(const CgWork& w, int phase) {
   FinArgs f;
   f.partials = w.partials;
   f.seg_sums = w.seg_sums;
-  f.seg_count = w.counters;
-  f.seg_done = w.counters + (tm.num_segs > 0 ? tm.num_segs : 1);
+  f.seg_done = w.counters;
+  f.bar = w.counters + 1;
+  f.ticket = w.counters + 3;
+  f.prod = w.prod;
   f.phase = phase;
   f.cg = w.state;
   f.hist = w.hist;
@@ -162,9 +169,10 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
            const int* vpos = nullptr, const StageMap* stage = nullptr) {
   const int seg = opt->seg_rows > 0 ? opt->seg_rows : 4096;
   const TileMap tm = make_tile_map(rows, seg);
-  int rc = ensure_work(w, rows, s, opt->max_iterations, tm);
-  if (rc) return rc;
   const bool canon = opt->dot_mode == ENPROP_DOT_CANONICAL;
+  // serial order: the SpMV writes the p*q products the chain kernel sums
+  int rc = ensure_work(w, rows, s, opt->max_iterations, tm, !canon);
+  if (rc) return rc;
   const int lanes = opt->flavour == ENPROP_CG_UNCOUPLED ? s : 1;
   const bool fused = ctx->fused_direction != 0 && vpos == nullptr;  // symmetric storage: split only
   cudaStream_t st = ctx->stream;
@@ -188,18 +196,18 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
     EP_CUDA(cudaMemsetAsync(x, 0, vec, st));
     EP_CUDA(cudaMemcpyAsync(w.r, b, vec, cudaMemcpyDeviceToDevice, st));
   }
-  const FinArgs f_init = fin_args(w, tm, kPhaseInit);
-  const FinArgs f_pq = fin_args(w, tm, kPhasePQ);
-  const FinArgs f_rr = fin_args(w, tm, kPhaseRR);
+  const FinArgs f_init = fin_args(w, kPhaseInit);
+  const FinArgs f_pq = fin_args(w, kPhasePQ);
+  const FinArgs f_rr = fin_args(w, kPhaseRR);
   const bool fin_kernel = canon;
-  // the staged SpMV finalizes p.q itself (grid barrier; needs >= 2 counters)
-  const bool fuse_pq = stage && canon && staged_fuse_fin() && tm.num_segs >= 2;
+  // the staged SpMV finalizes p.q itself (grid barrier)
+  const bool fuse_pq = stage && canon && staged_fuse_fin() && tm.num_segs >= 1;
   if (canon) {
     EP_CUDA(launch_dot_tiles(s, tm, w.r, w.r, f_init, st));
     if (fin_kernel) EP_CUDA(launch_fin_segments(s, tm, f_init, st));
     ctx->launches += fin_kernel ? 2 : 1;
-  } else {
-    EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, f_init, st));
+  } else {  // b_norm = norm2(b), rz = dot(r, z) (pcg.hpp:62-73): one chain over r = b
+    EP_CUDA(launch_chain(s, rows, w.r, nullptr, kChainSquare, f_init, st));
     ctx->launches += 1;
   }
 
@@ -224,12 +232,12 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
           EP_CUDA(launch_cg_spmv(s, canon, fused, false, tm, row_map, col_entry, values, w.r, p_old,
                                  p_new, w.q, x, p_new, vpos, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[2], st));
-        if (!canon) EP_CUDA(launch_fin_serial(s, rows, p_new, w.q, f_pq, st));
+        if (!canon) EP_CUDA(launch_chain(s, rows, w.prod, nullptr, kChainGiven, f_pq, st));
         if (fin_kernel && !fuse_pq) EP_CUDA(launch_fin_segments(s, tm, f_pq, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[3], st));
         EP_CUDA(launch_cg_update(s, canon, tm, w.r, w.q, f_rr, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[4], st));
-        if (!canon) EP_CUDA(launch_fin_serial(s, rows, w.r, w.r, f_rr, st));
+        if (!canon) EP_CUDA(launch_chain(s, rows, w.r, nullptr, kChainSquare, f_rr, st));
         if (fin_kernel) EP_CUDA(launch_fin_segments(s, tm, f_rr, st));
         if (ev) EP_CUDA(cudaEventRecord(ev[5], st));
         ctx->launches += (canon ? 2 : 4) + (fused ? 0 : 1) + (fin_kernel ? 2 : 0) - (fuse_pq ? 1 : 0);
@@ -596,15 +604,18 @@ int enprop_dot(enprop_ctx* c, int s, int64_t n, const double* u, const double* v
   const int segs = tm.num_segs > 0 ? tm.num_segs : 1;
   if (err == cudaSuccess) err = cudaMalloc(&w.partials, (size_t)tiles * s * sizeof(double));
   if (err == cudaSuccess) err = cudaMalloc(&w.seg_sums, (size_t)segs * s * sizeof(double));
-  if (err == cudaSuccess) err = cudaMalloc(&w.counters, (size_t)(segs + 1) * sizeof(int));
-  if (err == cudaSuccess) err = cudaMemsetAsync(w.counters, 0, (size_t)(segs + 1) * sizeof(int), c->stream);
-  FinArgs f = fin_args(w, tm, kPhaseNone);
+  if (err == cudaSuccess) err = cudaMalloc(&w.counters, kCounterInts * sizeof(int));
+  if (err == cudaSuccess) err = cudaMemsetAsync(w.counters, 0, kCounterInts * sizeof(int), c->stream);
+  FinArgs f = fin_args(w, kPhaseNone);
   f.lanes_out = out;
   if (err == cudaSuccess) {
     if (dot_mode == ENPROP_DOT_CANONICAL && rows > 0) {
       err = launch_dot_tiles(s, tm, u, v, f, c->stream);
       if (err == cudaSuccess) err = launch_fin_segments(s, tm, f, c->stream);
       c->launches += 2;
+    } else if (chain_aligned(u, v)) {
+      err = launch_chain(s, rows, u, v, u == v ? kChainSquare : kChainProduct, f, c->stream);
+      c->launches += 1;
     } else {
       err = launch_fin_serial(s, rows, u, v, f, c->stream);
       c->launches += 1;
@@ -813,13 +824,13 @@ int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* i
   EP_CUDA(launch_negate(len, p->residual, p->rhs, p->ctx->stream));
   p->ctx->launches += 1;
   // stage-pipelined SpMV (ep_staged.cu): structured graph + symmetric storage,
-  // s in {4, 16, 32}, canonical dots, automatic variant selection. (The serial
-  // order keeps the warp kernel: its latency-bound dot chains need other
-  // groups' kernels alongside, and the persistent staged kernel fills the SMs.)
+  // s in {4, 16, 32}, automatic variant selection; both dot orders (serial:
+  // the kernel writes the p*q products for the chain kernel; its stages are
+  // claimed dynamically, so SMs busy with other groups' chains do not stall it)
   const StageMap* stage = nullptr;
   const int N = p->desc.cells_per_axis + 1;
-  if (p->vpos && o.dot_mode == ENPROP_DOT_CANONICAL && spmv_variant() < 0 && staged_supported(s, N) &&
-      !p->stage_failed) {
+  if (p->vpos && spmv_variant() < 0 && staged_supported(s, N) && !p->stage_failed &&
+      (o.dot_mode == ENPROP_DOT_CANONICAL || staged_serial())) {
     if (!p->stage.desc || p->stage.tm.seg_rows != o.seg_rows) {
       const TileMap tm = make_tile_map(p->rows, o.seg_rows);
       const cudaError_t err = build_stage_map(s, tm, N, p->row_map, p->col_entry, p->vpos,

@@ -29,6 +29,14 @@
 
 namespace ep {
 
+// Tuning switches from the environment, read once per process by their call
+// sites: an unset OR empty variable means the default (so `VAR=` cannot flip
+// a switch silently).
+inline int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
 constexpr int kMaxS = 32;
 constexpr int kMaxTerms = 64;
 
@@ -207,10 +215,7 @@ inline int& pdl_enabled() {
 // ENPROP_PDL_MASK (env, tuning): kernel kinds launched with PDL (1 direction,
 // 2 SpMV, 4 finalize, 8 update, 16 other); default all
 inline int pdl_mask() {
-  static int m = [] {
-    const char* e = getenv("ENPROP_PDL_MASK");
-    return e ? atoi(e) : 31;
-  }();
+  static int m = env_int("ENPROP_PDL_MASK", 31);
   return m;
 }
 

@@ -167,8 +167,8 @@ int setup_rank(enprop_dist* D, DistRank& d, int r) {
   EP_CUDA(cudaMalloc(&d.seg_local, (size_t)D->maxplanes * s * sizeof(double)));
   EP_CUDA(cudaMemset(d.seg_local, 0, (size_t)D->maxplanes * s * sizeof(double)));
   EP_CUDA(cudaMalloc(&d.gathered, (size_t)P * D->maxplanes * s * sizeof(double)));
-  EP_CUDA(cudaMalloc(&d.counters, (size_t)(D->maxplanes + 1) * sizeof(int)));
-  EP_CUDA(cudaMemset(d.counters, 0, (size_t)(D->maxplanes + 1) * sizeof(int)));
+  EP_CUDA(cudaMalloc(&d.counters, kCounterInts * sizeof(int)));
+  EP_CUDA(cudaMemset(d.counters, 0, kCounterInts * sizeof(int)));
   EP_CUDA(cudaMalloc(&d.state, sizeof(CgState)));
   // global plane k lives at gathered[rank_of(k) * maxplanes + (k - k0(rank))]
   std::vector<int> pos(N);
@@ -182,22 +182,6 @@ int setup_rank(enprop_dist* D, DistRank& d, int r) {
   EP_CUDA(launch_build_graph_range(n, d.row_begin, d.rows, d.ext_begin, d.row_map, d.col_entry,
                                    D->ctx->stream));
   D->ctx->launches += 1;
-  if (getenv("EP_DIST_CHECK")) {  // debug: validate the graph slice on the host
-    EP_CUDA(cudaStreamSynchronize(D->ctx->stream));
-    std::vector<int> rm(d.rows + 1), ce(d.nnz);
-    EP_CUDA(cudaMemcpy(rm.data(), d.row_map, rm.size() * sizeof(int), cudaMemcpyDeviceToHost));
-    EP_CUDA(cudaMemcpy(ce.data(), d.col_entry, ce.size() * sizeof(int), cudaMemcpyDeviceToHost));
-    const int ext_rows = d.lo_rows + d.rows + d.hi_rows;
-    int bad = 0;
-    for (int i = 0; i < d.rows; ++i)
-      if (rm[i + 1] < rm[i]) ++bad;
-    if (rm[0] != 0 || rm[d.rows] != d.nnz) ++bad;
-    for (int64_t k = 0; k < d.nnz; ++k)
-      if (ce[k] < 0 || ce[k] >= ext_rows) ++bad;
-    fprintf(stderr, "rank %d: planes [%d,%d) row_begin %d rows %d lo %d hi %d ext_begin %d nnz %lld rm_end %d bad %d\n",
-            d.rank, d.k0, d.k1, d.row_begin, d.rows, d.lo_rows, d.hi_rows, d.ext_begin,
-            (long long)d.nnz, rm[d.rows], bad);
-  }
   return ENPROP_OK;
 }
 
@@ -205,8 +189,10 @@ FinArgs rank_fin(const DistRank& d, int phase) {
   FinArgs f;
   f.partials = d.partials;
   f.seg_sums = d.seg_local;
-  f.seg_count = d.counters;
-  f.seg_done = d.counters + (d.tm.num_segs > 0 ? d.tm.num_segs : 1);
+  f.seg_done = d.counters;
+  f.bar = d.counters + 1;
+  f.ticket = d.counters + 3;
+  f.prod = nullptr;
   f.phase = phase;
   f.cg = d.state;
   f.hist = d.hist;

@@ -583,6 +583,7 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
     st_vec<V>(q + (size_t)row * S + lane0, sum);
 #pragma unroll
     for (int j = 0; j < V; ++j) pr.v[j] = EP_DMUL(pn.v[j], sum.v[j]);
+    if (!kTiles && f.prod) st_vec<V>(f.prod + (size_t)row * S + lane0, pr);
   } else {
 #pragma unroll
     for (int j = 0; j < V; ++j) pr.v[j] = 0.0;
@@ -622,10 +623,7 @@ constexpr int kVecNT = 128;
 
 // block size of the CG vector kernels (ENPROP_VEC_NT env: 128 default, or 256)
 int vec_nt() {
-  static const int nt = [] {
-    const char* e = getenv("ENPROP_VEC_NT");
-    return (e && atoi(e) == 256) ? 256 : kVecNT;
-  }();
+  static const int nt = env_int("ENPROP_VEC_NT", kVecNT) == 256 ? 256 : kVecNT;
   return nt;
 }
 
@@ -821,6 +819,12 @@ __global__ void __launch_bounds__(256, SpmvVariant<kVar>::kMinBlocks) k_cg_spmv_
         const VecD<V> pn = ld_vec<V>(p_new + (size_t)row * S + lane0);
 #pragma unroll
         for (int j = 0; j < V; ++j) cur[j] = EP_DMUL(pn.v[j], sum.v[j]);
+      } else if (f.prod) {  // serial order: p*q for the chain kernel (kernels.hpp:67)
+        const VecD<V> pn = ld_vec<V>(p_new + (size_t)row * S + lane0);
+        VecD<V> pq;
+#pragma unroll
+        for (int j = 0; j < V; ++j) pq.v[j] = EP_DMUL(pn.v[j], sum.v[j]);
+        st_vec<V>(f.prod + (size_t)row * S + lane0, pq);
       }
     }
 #pragma unroll

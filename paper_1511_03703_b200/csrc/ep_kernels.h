@@ -60,11 +60,19 @@ enum Phase { kPhaseNone = 0, kPhaseInit = 1, kPhasePQ = 2, kPhaseRR = 3 };
 // Fused canonical finalize (ep_kernels.cu tiles_finish): where the tile
 // partials go, the self-resetting arrival counters, and what to do with the
 // lane totals (a CG scalar phase, or write them to lanes_out for kPhaseNone).
+// Counter words of one CG workspace (kCounterInts ints, zero at allocation;
+// each kernel that uses one leaves it as it found it, except the barrier's
+// monotonic generation): seg_done (finalize arrivals), the staged SpMV's grid
+// barrier (count, generation) and its stage ticket (dynamic stage claims).
+constexpr int kCounterInts = 4;
+
 struct FinArgs {
   double* partials;  // [num_tiles][s]
   double* seg_sums;  // [num_segs][s]
-  int* seg_count;    // [num_segs], zero between launches
-  int* seg_done;     // [1], zero between launches
+  int* seg_done;     // [1] finalize arrivals, zero between launches
+  int* bar;          // [2] grid barrier: arrivals (zero between launches), generation
+  int* ticket;       // [1] staged SpMV stage claims, zero between launches
+  double* prod;      // serial order: per-(row, sample) products p*q written by the SpMV
   int phase;
   CgState* cg;
   double* hist;
@@ -110,8 +118,19 @@ cudaError_t launch_dot_tiles(int s, const TileMap& tm, const double* u, const do
                              const FinArgs& f, cudaStream_t st);
 // serial (reference-order) dot straight from the vectors, then f.phase; uses
 // f.seg_sums[0..s) as the lane buffer and f.seg_done as its arrival counter
+// (any alignment; the chain kernel below is the fast path)
 cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v, const FinArgs& f,
                               cudaStream_t st);
+// serial (reference-order) dot by one chain CTA (ep_chain.cu): lane e of its
+// consumer warp runs sample e's chain acc = 0.0; acc += a_row (kernels.hpp:66-67)
+// over rows staged through shared memory by bulk copies, then f.phase.
+//   kChainGiven: a_row = u[row] (products already formed, v unused)
+//   kChainSquare: a_row = u[row]*u[row];  kChainProduct: a_row = u[row]*v[row]
+// u, v 16-byte aligned (chain_aligned); otherwise use launch_fin_serial.
+enum ChainKind { kChainGiven = 0, kChainSquare = 1, kChainProduct = 2 };
+bool chain_aligned(const void* u, const void* v);
+cudaError_t launch_chain(int s, int rows, const double* u, const double* v, int kind,
+                         const FinArgs& f, cudaStream_t st);
 // q = A p_new with p_new = (it==0 ? r : r + beta*p_old) formed on the fly; writes
 // p_new and q; with tiles, also the canonical p_new.q and its CG phase (f)
 // fused_dir = false: a separate k_cg_direction pass writes p_new first and the
@@ -172,12 +191,15 @@ void free_stage_map(StageMap& sm);
 // q = A p and (tiles) the canonical p.q tile partials; bitwise equal to the
 // warp-per-tile kernel
 // fuse_fin (tiles only): the kernel also runs the canonical finalize of p.q
-// (k_fin_segments' work and order) after a grid barrier, so no separate
-// finalize launch follows. Needs f.seg_count[0..1] zero between launches.
+// (k_fin_segments' work and order) after a grid barrier (f.bar), so no
+// separate finalize launch follows. Stages are claimed dynamically through
+// f.ticket (zero between launches). Without tiles, f.prod (if set) receives
+// the per-row products p*q for the serial-order chain.
 cudaError_t launch_cg_spmv_staged(int s, bool tiles, bool fuse_fin, const StageMap& sm,
                                   const double* values, const double* p, double* q, const FinArgs& f,
                                   cudaStream_t st);
 bool staged_fuse_fin();  // ENPROP_STAGED_FUSE (env, default 1)
+bool staged_serial();    // ENPROP_STAGED_SERIAL (env, default 1)
 int spmv_variant();  // ENPROP_OPT_SPMV_VARIANT (-1 = auto)
 void set_pdl_enabled(int on);  // ENPROP_OPT_PDL
 

@@ -159,20 +159,18 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv_small(int rows, const int* __
 // Defaults (A/B at 128^3, tools/small_ab.py, profiles/round1/spmv_small_ab.jsonl):
 // 64 threads, indices staged, capped at 64 registers for s = 1 and 48 for s >= 2
 // (uncapped, ptxas takes 80-86). A/B switches: ENPROP_SMALL_NT = 64 | 96 | 128,
-// ENPROP_SMALL_REGS = 0 (uncapped) | 32 | 48 | 64 (0: mode 0 only; 32: mode 1 only),
+// ENPROP_SMALL_REGS = 0 (uncapped; mode 0 only) | 32 | 48 | 64, every mode at each cap,
 // ENPROP_SMALL_STAGE = 0 | 1 | 2.
 static int small_nt(int) {
   static const int nt = [] {
-    const char* e = getenv("ENPROP_SMALL_NT");
-    const int v = (e && *e) ? atoi(e) : 0;
+    const int v = env_int("ENPROP_SMALL_NT", 0);
     return (v == 96 || v == 128) ? v : 64;
   }();
   return nt;
 }
 static int small_regs(int s) {
   static const int r = [] {
-    const char* e = getenv("ENPROP_SMALL_REGS");
-    const int v = (e && *e) ? atoi(e) : -1;
+    const int v = env_int("ENPROP_SMALL_REGS", -1);
     return (v == 0 || v == 32 || v == 48 || v == 64) ? v : -1;
   }();
   // auto: 64 at s = 1 (more resident CTAs shrink L1 below the unstaged value
@@ -189,8 +187,7 @@ static cudaError_t spmv_small_nt(int rows, const int* row_map, const int* col_en
   if (rows <= 0) return cudaSuccess;
   const int grid = (rows + RB - 1) / RB;
   static const int mode = [] {
-    const char* e = getenv("ENPROP_SMALL_STAGE");
-    const int v = (e && *e) ? atoi(e) : 1;
+    const int v = env_int("ENPROP_SMALL_STAGE", 1);
     return (v == 0 || v == 2) ? v : 1;
   }();
   constexpr int MB = 65536 / (NT * 64);
@@ -198,6 +195,9 @@ static cudaError_t spmv_small_nt(int rows, const int* row_map, const int* col_en
     case 0: k_spmv_small<S, NT, 1, 0><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
     case 192: k_spmv_small<S, NT, 65536 / (NT * 48), 0><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
     case 193: k_spmv_small<S, NT, 65536 / (NT * 48), 1><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+    case 194: k_spmv_small<S, NT, 65536 / (NT * 48), 2><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+    case 128: k_spmv_small<S, NT, 65536 / (NT * 32), 0><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+    case 130: k_spmv_small<S, NT, 65536 / (NT * 32), 2><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
     case 129: k_spmv_small<S, NT, 65536 / (NT * 32), 1><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
     case 256: k_spmv_small<S, NT, MB, 0><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
     case 258: k_spmv_small<S, NT, MB, 2><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
@@ -221,8 +221,7 @@ static cudaError_t spmv_small_s(int rows, const int* row_map, const int* col_ent
 // warp-per-row k_spmv<16>)
 int spmv_small_max() {
   static const int m = [] {
-    const char* e = getenv("ENPROP_SMALL_MAX");
-    const int v = (e && *e) ? atoi(e) : 16;
+    const int v = env_int("ENPROP_SMALL_MAX", 16);
     return (v == 8 || v == 32) ? v : 16;
   }();
   return m;

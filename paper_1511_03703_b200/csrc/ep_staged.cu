@@ -60,7 +60,8 @@ struct StagedShape {
   static constexpr int IDX_BYTES = HDR * 4 + RS * ROWE * 4;
   static constexpr int NIDX = S >= 16 ? 4 : 2;      // index blocks in flight (ring depth; smem-limited at s < 16)
   static constexpr int RED_BYTES = RS * S * 8;
-  static constexpr int SMEM = 2 * BIG_BYTES + NIDX * IDX_BYTES + 2 * RED_BYTES + 64;
+  static constexpr int CLAIM = NIDX > 3 ? NIDX : 3;  // stages claimed ahead of the current one
+  static constexpr int SMEM = 2 * BIG_BYTES + NIDX * IDX_BYTES + 2 * RED_BYTES + 64 + 32;
   static_assert(RS * TPR == 256, "one thread per (row slot, sample pair)");
   static_assert(BIG_BYTES % 128 == 0 && IDX_BYTES % 16 == 0, "alignment");
   static_assert(SMEM <= 232448, "stage ring exceeds shared memory");
@@ -88,14 +89,31 @@ struct StagedCta {
   unsigned char* smem;
   uint64_t* bar;  // [0,2): big buffers, [2,6): index ring
   double* red;
+  int* claims;    // [8] sweep positions of this CTA's stages it, it+1, ... (ring)
+  int* ticket;    // global claim counter (f.ticket)
   uint64_t pol;
   int rr, lane0;
 
-  // the it-th stage of this CTA: position blockIdx.x + it*grid of the sweep
-  // order (desc and index blocks are stored in sweep order; desc[pos].g is the
-  // stage's canonical id)
-  __device__ __forceinline__ int stage_of(int it) const { return (int)blockIdx.x + it * (int)gridDim.x; }
+  // The it-th stage of this CTA is the sweep position it claimed it-th (desc
+  // and index blocks are stored in sweep order; desc[pos].g is the stage's
+  // canonical id). Claims are dynamic: thread 0 draws tickets from a global
+  // counter CLAIM stages ahead, so the positions in flight across all CTAs
+  // stay a contiguous window of the sweep whatever the CTAs' start times (a
+  // CTA that starts late, e.g. behind another group's kernel on its SM, simply
+  // gets fewer stages). Every CTA draws exactly one ticket >= nstages; the
+  // CTA that draws the last of them (nstages + grid - 1) resets the counter.
+  __device__ __forceinline__ int stage_of(int it) const { return claims[it & 7]; }
   __device__ __forceinline__ bool has(int it) const { return stage_of(it) < nstages; }
+  // thread 0 only; claims must be made in order it = 0, 1, ...
+  __device__ __forceinline__ void claim(int it) const {
+    if (it > 0 && !has(it - 1)) {
+      claims[it & 7] = nstages;
+      return;
+    }
+    const int t = atomicAdd(ticket, 1);
+    if (t == nstages + (int)gridDim.x - 1) *ticket = 0;
+    claims[it & 7] = t < nstages ? t : nstages;
+  }
   __device__ __forceinline__ unsigned char* big(int it) const { return smem + (it & 1) * Sh::BIG_BYTES; }
   __device__ __forceinline__ const int* idx(int it) const {
     return reinterpret_cast<const int*>(smem + 2 * Sh::BIG_BYTES + (it & (Sh::NIDX - 1)) * Sh::IDX_BYTES);
@@ -212,6 +230,9 @@ struct StagedCta {
       }
     }
     if (row >= 0) *reinterpret_cast<double2*>(q + (size_t)row * S + lane0) = make_double2(s0, s1);
+    if (!kTiles && f.prod && row >= 0)  // serial order: p*q for the chain (kernels.hpp:67)
+      *reinterpret_cast<double2*>(f.prod + (size_t)row * S + lane0) =
+          make_double2(EP_DMUL(pown.x, s0), EP_DMUL(pown.y, s1));
     double* rb = red + (it & 1) * (Sh::RS * S);
     if constexpr (kTiles) {
       double c0 = 0.0, c1 = 0.0;
@@ -229,6 +250,7 @@ struct StagedCta {
     if (threadIdx.x == 0) {
       fence_proxy_async_smem();
       if (prod) issue_big(it + 2, dn);
+      claim(it + Sh::CLAIM);
       if (has(it + Sh::NIDX)) issue_idx(it + Sh::NIDX);
     }
     if constexpr (kTiles) {
@@ -254,6 +276,8 @@ struct StagedCta {
 // SM (at most), so all CTAs are resident or become resident as other streams'
 // kernels retire. Self-resetting counter + monotonic generation.
 __device__ __forceinline__ void grid_barrier(int* count, int* gen, int nblocks) {
+  // count returns to 0 at every release; gen only grows (its own word: no other
+  // counter of the workspace aliases it)
   __syncthreads();
   if (threadIdx.x == 0) {
     volatile int* vgen = gen;
@@ -281,13 +305,16 @@ __global__ void __launch_bounds__(256, 1) k_cg_spmv_staged(
   if (f.cg->done) return;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
+  unsigned char* tail = smem + 2 * Sh::BIG_BYTES + Sh::NIDX * Sh::IDX_BYTES + 2 * Sh::RED_BYTES;
   StagedCta<S> c{tm, N, nstages, desc, blk, values, p, q, f, smem,
-                 reinterpret_cast<uint64_t*>(smem + 2 * Sh::BIG_BYTES + Sh::NIDX * Sh::IDX_BYTES + 2 * Sh::RED_BYTES),
+                 reinterpret_cast<uint64_t*>(tail),
                  reinterpret_cast<double*>(smem + 2 * Sh::BIG_BYTES + Sh::NIDX * Sh::IDX_BYTES),
+                 reinterpret_cast<int*>(tail + 64), f.ticket,
                  l2_policy_evict_normal(), tid / Sh::TPR, (tid % Sh::TPR) * Sh::V};
   if (tid == 0) {
     for (int k = 0; k < 2 + Sh::NIDX; ++k) mbar_init(&c.bar[k], 1);
     fence_mbar_init();
+    for (int it = 0; it < Sh::CLAIM; ++it) c.claim(it);
   }
   // zero chunks (never written by the copies) and x-run areas: positions a
   // copy does not reach (clipped runs) are read for absent neighbours only,
@@ -304,15 +331,16 @@ __global__ void __launch_bounds__(256, 1) k_cg_spmv_staged(
     for (int it = 0; it < 2; ++it)
       if (c.has(it)) c.issue_big(it, desc[c.stage_of(it)]);
   }
-  if (!c.has(0)) return;
-  StageGather ga, gb;
-  mbar_wait(&c.bar[2], 0);
-  c.gather(0, ga);
-  for (int it = 0;;) {
-    c.template stage<kTiles>(it, ga, gb);
-    if (!c.has(++it)) break;
-    c.template stage<kTiles>(it, gb, ga);
-    if (!c.has(++it)) break;
+  if (c.has(0)) {  // (a CTA may draw no stage at all; it still joins the barrier)
+    StageGather ga, gb;
+    mbar_wait(&c.bar[2], 0);
+    c.gather(0, ga);
+    for (int it = 0;;) {
+      c.template stage<kTiles>(it, ga, gb);
+      if (!c.has(++it)) break;
+      c.template stage<kTiles>(it, gb, ga);
+      if (!c.has(++it)) break;
+    }
   }
   if constexpr (kTiles) {
     if (fuse_fin) {
@@ -320,7 +348,7 @@ __global__ void __launch_bounds__(256, 1) k_cg_spmv_staged(
       // every tile partial is written, CTA c folds segments c, c + grid, ...
       // and the last CTA to finish its folds forms the total and runs the CG
       // phase. The stage buffers are free now and serve as scratch.
-      grid_barrier(f.seg_count, f.seg_count + 1, gridDim.x);
+      grid_barrier(f.bar, f.bar + 1, gridDim.x);
       double* scratch = reinterpret_cast<double*>(smem);
       double* lanes = scratch + FinShape<S>::CHUNK * S + FinShape<S>::CHUNK2 * S;
       int* s_final = reinterpret_cast<int*>(lanes + S);
@@ -419,10 +447,14 @@ static int stage_shape(int& T, int& L, int& RS, int& max_upper, int& idx_bytes, 
 void set_pdl_enabled(int on) { pdl_enabled() = on; }
 
 bool staged_fuse_fin() {
-  static const int on = [] {
-    const char* e = getenv("ENPROP_STAGED_FUSE");
-    return e ? atoi(e) : 1;
-  }();
+  static const int on = env_int("ENPROP_STAGED_FUSE", 1);
+  return on != 0;
+}
+
+// ENPROP_STAGED_SERIAL (A/B, default 1): the staged kernel also serves the
+// serial dot order (writing the p*q products); 0 keeps the warp kernel there
+bool staged_serial() {
+  static const int on = env_int("ENPROP_STAGED_SERIAL", 1);
   return on != 0;
 }
 
@@ -488,8 +520,7 @@ cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
       key[g] = ((int64_t)(j / B) * N + k) * (int64_t)NN + (r - k * NN);
       ord[g] = (int)g;
     }
-    const char* env = getenv("ENPROP_STAGED_ORDER");  // "0": plain round-robin (A/B)
-    if (!env || atoi(env) != 0)
+    if (env_int("ENPROP_STAGED_ORDER", 1) != 0)  // 0: plain row order (A/B)
       std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return key[a] < key[b]; });
   }
   {  // store descriptors and index blocks in sweep order
