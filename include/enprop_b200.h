@@ -75,11 +75,16 @@ int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
  *   (enprop_problem_expand_values rebuilds the full [nnz][s] values).
  *   ENPROP_OPT_SPMV_PIPELINE (default 0): 1 = enprop_spmv loads the next batch's
  *   column indices one batch ahead (software pipelining).
- *   ENPROP_OPT_SPMV_VARIANT (default -1 = auto, process-wide): CG SpMV schedule
+ *   ENPROP_OPT_SPMV_VARIANT (default -1 = auto): CG SpMV schedule
  *   (entries per gather batch / CTAs per SM): 0: 4/4, 1: 4/4 + index prefetch,
  *   2: 8/2, 3: 8/2 + index prefetch, 4: 4/4 zero-padded, 5: 8/3, 6: 16/1;
- *   auto = 2 with symmetric storage, 0 otherwise. */
-/*   ENPROP_OPT_PDL (default 0, process-wide): launch the CG loop's kernels with
+ *   auto = 2 with symmetric storage, 0 otherwise.
+ *   ENPROP_OPT_GRAPHS (default 1): CG iterations are replayed from a CUDA graph
+ *   of one convergence-check chunk (check_every iterations) instead of being
+ *   launched kernel by kernel (not while profiling).
+ * Options are per context: calls through a context (and through problems and
+ * slab solvers created on it) launch with that context's settings only. */
+/*   ENPROP_OPT_PDL (default 0): launch the CG loop's kernels with
  *   programmatic dependent launch (the next kernel is scheduled while the
  *   previous one drains; it waits for its completion before reading).
  *   Measured: +2-4% on single-stream s = 4 / 16 solves, -1% with three
@@ -90,7 +95,8 @@ enum {
   ENPROP_OPT_SPMV_PIPELINE = 2,
   ENPROP_OPT_SYMMETRIC_STORAGE = 3,
   ENPROP_OPT_SPMV_VARIANT = 5,
-  ENPROP_OPT_PDL = 6
+  ENPROP_OPT_PDL = 6,
+  ENPROP_OPT_GRAPHS = 7
 };
 int enprop_ctx_set_option(enprop_ctx* ctx, int option, int value);
 /* Event timing of the CG SpMV kernel launches on the context stream (used by
@@ -141,6 +147,20 @@ int enprop_build_node_graph(enprop_ctx* ctx, int cells_per_axis, int* row_map, i
 int enprop_kl_describe(const enprop_kl_params* kl, int* mode_axes, double* mode_eigenvalue,
                        double* axis_frequency, double* axis_eigenvalue,
                        double* axis_inverse_norm, int* axis_cosine);
+
+/* ---------------------------------------------------------------- samples */
+/* draw_samples (samples.cpp:7-18): out[count][num_terms], coordinate j of
+ * sample i = (mt19937_64(seed) >> 11) * 2^-52 - 1 in draw order, uniform in
+ * [-1, 1); bitwise the reference's sequence. INVALID for num_terms < 1 or
+ * count < 0. Host memory. */
+int enprop_draw_samples(uint64_t seed, int count, int num_terms, double* out);
+/* pack_sample_group<S> (samples.hpp:18-31): out[j][e] = samples[group_start +
+ * e][j] for j < num_terms, e < s -- the [num_terms][s] y layout of
+ * enprop_assemble / enprop_problem_assemble. samples is [count][num_terms].
+ * INVALID when the group runs past count (the reference's "not enough samples
+ * for the group"). Host memory. */
+int enprop_pack_sample_group(const double* samples, int count, int num_terms, int group_start,
+                             int s, double* out);
 
 /* ----------------------------------------------------------------- kernels */
 /* assemble<Ensemble<s>> (fem.hpp:115-202) of the unit-cube diffusion problem

@@ -26,6 +26,7 @@
 #pragma once
 
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -232,6 +233,38 @@ void axpby(const Coef& alpha, const Vector& x, const Coef& beta, Vector& y) {
                              reinterpret_cast<const double*>(&beta), dy.as<double>()),
                 "axpby");
   dy.down(y.data(), y.size() * sizeof(Scalar));
+}
+
+// ------------------------------------------------------------------ samples
+/// draw_samples (samples.cpp:7-18): count vectors of m coordinates uniform in
+/// [-1, 1), bitwise the reference's mt19937_64 sequence.
+inline std::vector<std::vector<double>> draw_samples(std::uint64_t seed, int count, int m) {
+  std::vector<double> flat(static_cast<size_t>(count > 0 ? count : 0) * (m > 0 ? m : 0));
+  detail::check(enprop_draw_samples(seed, count, m, flat.data()), "draw_samples");
+  std::vector<std::vector<double>> out(count);
+  for (int i = 0; i < count; ++i) out[i].assign(flat.begin() + (size_t)i * m, flat.begin() + (size_t)(i + 1) * m);
+  return out;
+}
+
+/// pack_sample_group<Ensemble> (samples.hpp:18-31): out[j][e] = samples[group_start + e][j];
+/// Scalar is the reference's Ensemble<S> (or any POD of S doubles).
+template <class Scalar>
+std::vector<Scalar> pack_sample_group(const std::vector<std::vector<double>>& samples, int group_start = 0) {
+  constexpr int s = detail::width<Scalar>();
+  if (group_start < 0 || group_start + s > static_cast<int>(samples.size()))
+    throw std::invalid_argument("pack_sample_group: not enough samples for the group");
+  const size_t m = samples[group_start].size();
+  std::vector<double> flat(samples.size() * m);
+  for (size_t i = 0; i < samples.size(); ++i) {
+    if (samples[i].size() != m && static_cast<int>(i) >= group_start && static_cast<int>(i) < group_start + s)
+      throw std::invalid_argument("pack_sample_group: sample lengths differ");
+    for (size_t j = 0; j < m && j < samples[i].size(); ++j) flat[i * m + j] = samples[i][j];
+  }
+  std::vector<Scalar> out(m);
+  detail::check(enprop_pack_sample_group(flat.data(), static_cast<int>(samples.size()), static_cast<int>(m),
+                                         group_start, s, reinterpret_cast<double*>(out.data())),
+                "pack_sample_group");
+  return out;
 }
 
 // -------------------------------------------------------- mesh and assembly

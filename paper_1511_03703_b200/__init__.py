@@ -35,6 +35,7 @@ OPT_SPMV_PIPELINE = 2
 OPT_SYMMETRIC_STORAGE = 3
 OPT_SPMV_VARIANT = 5
 OPT_PDL = 6
+OPT_GRAPHS = 7
 WIDTHS = (1, 2, 4, 8, 16, 32)
 
 _dp = C.POINTER(C.c_double)
@@ -179,6 +180,8 @@ def lib() -> C.CDLL:
     L.enprop_ctx_set_option.argtypes = [_vp, C.c_int, C.c_int]
     L.enprop_ctx_profile_detail.argtypes = [_vp, _dp, C.POINTER(C.c_int64)]
     L.enprop_build_node_graph.argtypes = [_vp, C.c_int, _vp, _vp]
+    L.enprop_draw_samples.argtypes = [C.c_uint64, C.c_int, C.c_int, _dp]
+    L.enprop_pack_sample_group.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, _dp]
     L.enprop_kl_describe.argtypes = [C.POINTER(_KlParams), _ip, _dp, _dp, _dp, _dp, _ip]
     L.enprop_assemble.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(_KlParams), C.POINTER(_Coeffs),
                                   _vp, _vp, _vp, _vp, _vp, C.POINTER(_Bc)]
@@ -304,6 +307,28 @@ def kl_describe(kl: KlField):
     _check(lib().enprop_kl_describe(C.byref(p), axes, me, af, ae, ai, ac), "KlField")
     return dict(mode_axes=[list(axes[3 * i:3 * i + 3]) for i in range(m)], mode_eig=list(me),
                 axis_freq=list(af), axis_eig=list(ae), axis_invnorm=list(ai), axis_cos=list(ac))
+
+
+def draw_samples(seed: int, count: int, num_terms: int) -> torch.Tensor:
+    """draw_samples (samples.cpp:7-18): [count][num_terms] host doubles,
+    bitwise the reference's mt19937_64 sequence."""
+    if count < 0 or num_terms < 1:  # the library raises the reference's invalid_argument
+        _check(lib().enprop_draw_samples(seed, count, num_terms, None), "draw_samples")
+    out = torch.empty((count, num_terms), dtype=torch.float64)
+    _check(lib().enprop_draw_samples(seed, count, num_terms,
+                                     C.cast(out.data_ptr(), _dp) if out.numel() else None), "draw_samples")
+    return out
+
+
+def pack_sample_group(samples: torch.Tensor, s: int, group_start: int = 0) -> torch.Tensor:
+    """pack_sample_group<s> (samples.hpp:18-31): out[j][e] = samples[group_start + e][j]
+    ([num_terms][s] host doubles, the y layout of assemble)."""
+    samples = samples.detach().to(torch.float64).contiguous().cpu()
+    count, m = samples.shape
+    out = torch.empty((m, s), dtype=torch.float64)
+    _check(lib().enprop_pack_sample_group(C.cast(samples.data_ptr(), _dp), count, m, group_start, s,
+                                          C.cast(out.data_ptr(), _dp)), "pack_sample_group")
+    return out
 
 
 def build_node_graph(ctx: Context, n: int):

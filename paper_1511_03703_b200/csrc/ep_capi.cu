@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <new>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -49,9 +50,21 @@ struct CgWork {
   double* hist = nullptr;
   CgState* state = nullptr;
   int rows = 0, s = 0, maxit = -1, tiles = 0, segs = 0;
+  // CUDA graph of one chunk of CG iterations (ENPROP_OPT_GRAPHS), replayed for
+  // every full chunk that starts at an even iteration; rebuilt when any
+  // pointer or schedule choice baked into its launches changes
+  cudaGraphExec_t graph = nullptr;
+  std::vector<char> graph_key;
 };
 
+void free_graph(CgWork& w) {
+  if (w.graph) cudaGraphExecDestroy(w.graph);
+  w.graph = nullptr;
+  w.graph_key.clear();
+}
+
 void free_work(CgWork& w) {
+  free_graph(w);
   for (void* p : {(void*)w.r, (void*)w.p[0], (void*)w.p[1], (void*)w.q, (void*)w.partials,
                   (void*)w.seg_sums, (void*)w.counters, (void*)w.prod, (void*)w.hist,
                   (void*)w.state})
@@ -213,34 +226,88 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
 
   if (sev) EP_CUDA(cudaEventRecord(sev[1], st));
   const int chunk = opt->check_every > 0 ? opt->check_every : 16;
+  const int per_iter = (canon ? 2 : 4) + (fused ? 0 : 1) + (fin_kernel ? 2 : 0) - (fuse_pq ? 1 : 0);
+  // one loop body (pcg.hpp:76-101); `it` fixes which p buffer is old / new
+  auto enqueue_iteration = [&](int it, cudaEvent_t* ev) -> cudaError_t {
+    double* p_old = w.p[it & 1];
+    double* p_new = w.p[(it + 1) & 1];
+    cudaError_t e = cudaSuccess;
+#define EP_Q(call)              \
+  if ((e = (call)) != cudaSuccess) \
+    return e;
+    if (ev) EP_Q(cudaEventRecord(ev[0], st));
+    if (!fused) EP_Q(launch_cg_direction(s, rows, w.r, p_old, p_new, x, w.state, st));
+    if (ev) EP_Q(cudaEventRecord(ev[1], st));
+    if (stage)
+      EP_Q(launch_cg_spmv_staged(s, canon, fuse_pq, *stage, values, p_new, w.q, f_pq, st))
+    else
+      EP_Q(launch_cg_spmv(s, canon, fused, false, tm, row_map, col_entry, values, w.r, p_old, p_new, w.q,
+                          x, p_new, vpos, f_pq, st));
+    if (ev) EP_Q(cudaEventRecord(ev[2], st));
+    if (!canon) EP_Q(launch_chain(s, rows, w.prod, nullptr, kChainGiven, f_pq, st));
+    if (fin_kernel && !fuse_pq) EP_Q(launch_fin_segments(s, tm, f_pq, st));
+    if (ev) EP_Q(cudaEventRecord(ev[3], st));
+    EP_Q(launch_cg_update(s, canon, tm, w.r, w.q, f_rr, st));
+    if (ev) EP_Q(cudaEventRecord(ev[4], st));
+    if (!canon) EP_Q(launch_chain(s, rows, w.r, nullptr, kChainSquare, f_rr, st));
+    if (fin_kernel) EP_Q(launch_fin_segments(s, tm, f_rr, st));
+    if (ev) EP_Q(cudaEventRecord(ev[5], st));
+#undef EP_Q
+    return cudaSuccess;
+  };
+  // CUDA graph of a whole chunk (ENPROP_OPT_GRAPHS): one launch per chunk
+  // instead of per_iter * chunk; captured on this thread only, after the
+  // first chunk ran eagerly (which performed any one-time kernel attribute
+  // setup). Everything a replay depends on is part of the key.
+  bool use_graph = ctx->graphs && !ctx->profile && chunk % 2 == 0;
+  if (use_graph) {
+    const void* key_ptrs[] = {values, x, row_map, col_entry, vpos, stage ? (const void*)stage->desc : nullptr,
+                              w.r, w.q, w.p[0], w.p[1], w.prod, w.partials, w.state};
+    const int key_ints[] = {s, rows, canon, fuse_pq, fused, chunk, tm.seg_rows, launch_opts().pdl,
+                            spmv_variant()};
+    std::vector<char> key(sizeof(key_ptrs) + sizeof(key_ints));
+    std::memcpy(key.data(), key_ptrs, sizeof(key_ptrs));
+    std::memcpy(key.data() + sizeof(key_ptrs), key_ints, sizeof(key_ints));
+    if (w.graph && w.graph_key != key) free_graph(w);
+    w.graph_key = key;
+  }
+  auto capture_chunk = [&]() -> bool {  // false: run eagerly instead
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    cudaError_t e = cudaSuccess;
+    for (int c = 0; c < chunk && e == cudaSuccess; ++c) e = enqueue_iteration(c, nullptr);
+    const cudaError_t e2 = cudaStreamEndCapture(st, &g);
+    if (e == cudaSuccess && e2 == cudaSuccess && g &&
+        cudaGraphInstantiate(&w.graph, g, 0) == cudaSuccess) {
+      cudaGraphDestroy(g);
+      return true;
+    }
+    if (g) cudaGraphDestroy(g);
+    w.graph = nullptr;
+    cudaGetLastError();  // capture unsupported here: eager launches
+    return false;
+  };
   int launched = 0;
   int slot = 0;
   bool pending = false;
   const int limit = opt->max_iterations;  // loop bodies that can run (pcg.hpp:79-85)
   while (true) {
     if (launched < limit) {
-      for (int c = 0; c < chunk && launched < limit; ++c, ++launched) {
-        double* p_old = w.p[launched & 1];
-        double* p_new = w.p[(launched + 1) & 1];
-        cudaEvent_t* ev = ctx->profile ? prof_slot(ctx) : nullptr;
-        if (ev) EP_CUDA(cudaEventRecord(ev[0], st));
-        if (!fused) EP_CUDA(launch_cg_direction(s, rows, w.r, p_old, p_new, x, w.state, st));
-        if (ev) EP_CUDA(cudaEventRecord(ev[1], st));
-        if (stage)
-          EP_CUDA(launch_cg_spmv_staged(s, canon, fuse_pq, *stage, values, p_new, w.q, f_pq, st));
-        else
-          EP_CUDA(launch_cg_spmv(s, canon, fused, false, tm, row_map, col_entry, values, w.r, p_old,
-                                 p_new, w.q, x, p_new, vpos, f_pq, st));
-        if (ev) EP_CUDA(cudaEventRecord(ev[2], st));
-        if (!canon) EP_CUDA(launch_chain(s, rows, w.prod, nullptr, kChainGiven, f_pq, st));
-        if (fin_kernel && !fuse_pq) EP_CUDA(launch_fin_segments(s, tm, f_pq, st));
-        if (ev) EP_CUDA(cudaEventRecord(ev[3], st));
-        EP_CUDA(launch_cg_update(s, canon, tm, w.r, w.q, f_rr, st));
-        if (ev) EP_CUDA(cudaEventRecord(ev[4], st));
-        if (!canon) EP_CUDA(launch_chain(s, rows, w.r, nullptr, kChainSquare, f_rr, st));
-        if (fin_kernel) EP_CUDA(launch_fin_segments(s, tm, f_rr, st));
-        if (ev) EP_CUDA(cudaEventRecord(ev[5], st));
-        ctx->launches += (canon ? 2 : 4) + (fused ? 0 : 1) + (fin_kernel ? 2 : 0) - (fuse_pq ? 1 : 0);
+      if (use_graph && launched > 0 && launched % 2 == 0 && launched + chunk <= limit &&
+          (w.graph || capture_chunk())) {
+        EP_CUDA(cudaGraphLaunch(w.graph, st));
+        launched += chunk;
+        ctx->launches += (int64_t)per_iter * chunk;
+      } else {
+        if (use_graph && !w.graph && launched > 0) use_graph = false;  // capture failed
+        for (int c = 0; c < chunk && launched < limit; ++c, ++launched) {
+          cudaEvent_t* ev = ctx->profile ? prof_slot(ctx) : nullptr;
+          EP_CUDA(enqueue_iteration(launched, ev));
+          ctx->launches += per_iter;
+        }
       }
     }
     // flag of this chunk
@@ -376,10 +443,13 @@ int enprop_ctx_set_option(enprop_ctx* c, int option, int value) {
       c->symmetric_storage = value ? 1 : 0;
       return ENPROP_OK;
     case ENPROP_OPT_SPMV_VARIANT:
-      set_spmv_variant(value);
+      c->spmv_variant = (value >= 0 && value <= 6) ? value : -1;
       return ENPROP_OK;
     case ENPROP_OPT_PDL:
-      set_pdl_enabled(value ? 1 : 0);
+      c->pdl = value ? 1 : 0;
+      return ENPROP_OK;
+    case ENPROP_OPT_GRAPHS:
+      c->graphs = value ? 1 : 0;
       return ENPROP_OK;
 
     default:
@@ -449,6 +519,26 @@ int enprop_build_node_graph(enprop_ctx* c, int n, int* row_map, int* col_entry) 
     return fail(ENPROP_ERR_INVALID, "enprop_build_node_graph: nnz exceeds int32 (reference Graph uses int)");
   EP_CUDA(launch_build_graph(n, row_map, col_entry, c->stream));
   c->launches += 1;
+  return ENPROP_OK;
+}
+
+int enprop_draw_samples(uint64_t seed, int count, int m, double* out) {
+  if (m < 1) return fail(ENPROP_ERR_INVALID, "draw_samples: need at least one coordinate");
+  if (count < 0) return fail(ENPROP_ERR_INVALID, "draw_samples: negative count");
+  if (count > 0 && !out) return fail(ENPROP_ERR_INVALID, "draw_samples: null output");
+  std::mt19937_64 rng(seed);  // samples.cpp:11-16: top 53 bits -> [0,1) -> [-1,1)
+  for (int64_t i = 0; i < (int64_t)count * m; ++i)
+    out[i] = double(rng() >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+  return ENPROP_OK;
+}
+
+int enprop_pack_sample_group(const double* samples, int count, int m, int group_start, int s,
+                             double* out) {
+  if (group_start < 0 || s < 1 || group_start + s > count)
+    return fail(ENPROP_ERR_INVALID, "pack_sample_group: not enough samples for the group");
+  if (m < 1 || !samples || !out) return fail(ENPROP_ERR_INVALID, "pack_sample_group: bad argument");
+  for (int j = 0; j < m; ++j)
+    for (int e = 0; e < s; ++e) out[(size_t)j * s + e] = samples[(size_t)(group_start + e) * m + j];
   return ENPROP_OK;
 }
 
@@ -564,6 +654,7 @@ int enprop_apply_dirichlet(enprop_ctx* c, int s, int n, const enprop_dirichlet_b
 
 int enprop_spmv(enprop_ctx* c, int s, int rows, int cols, const int* row_map,
                 const int* col_entry, const double* values, const double* x, double* z) {
+  ScopedLaunchOpts launch_scope(c);
   if (!c) return fail(ENPROP_ERR_INVALID, "null context");
   if (!valid_width(s)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
   if (rows < 0 || cols < 0) return fail(ENPROP_ERR_INVALID, "spmv: negative dimension");
@@ -592,6 +683,7 @@ int enprop_spmv_outer(enprop_ctx* c, int s, int rows, int cols, int64_t nnz, con
 
 int enprop_dot(enprop_ctx* c, int s, int64_t n, const double* u, const double* v, int dot_mode,
                int seg_rows, double* lanes_host, double* coupled_host) {
+  ScopedLaunchOpts launch_scope(c);
   if (!c) return fail(ENPROP_ERR_INVALID, "null context");
   if (!valid_width(s)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
   if (n < 0 || n > 2147483647LL) return fail(ENPROP_ERR_INVALID, "dot: bad length");
@@ -636,6 +728,7 @@ int enprop_dot(enprop_ctx* c, int s, int64_t n, const double* u, const double* v
 
 int enprop_axpby(enprop_ctx* c, int s, int64_t n, int per_lane, const double* alpha_host,
                  const double* x, const double* beta_host, double* y) {
+  ScopedLaunchOpts launch_scope(c);
   if (!c || !alpha_host || !beta_host) return fail(ENPROP_ERR_INVALID, "axpby: null argument");
   if (!valid_width(s)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
   if (n == 0) return ENPROP_OK;
@@ -658,6 +751,7 @@ int enprop_axpby(enprop_ctx* c, int s, int64_t n, int per_lane, const double* al
 int enprop_cg(enprop_ctx* c, int s, int rows, const int* row_map, const int* col_entry,
               const double* values, const double* b, double* x, const enprop_cg_options* opt,
               int* iterations, int* lane_status, double* history, int* hist_len) {
+  ScopedLaunchOpts launch_scope(c);
   if (!c) return fail(ENPROP_ERR_INVALID, "null context");
   int rc = validate_cg_options(opt, s);
   if (rc) return rc;
@@ -796,6 +890,7 @@ int enprop_problem_expand_values(enprop_problem* p, double* values_full) {
 }
 
 int enprop_problem_assemble(enprop_problem* p, const double* y) {
+  ScopedLaunchOpts launch_scope(p ? p->ctx : nullptr);
   if (!p || !y) return fail(ENPROP_ERR_INVALID, "enprop_problem_assemble: null argument");
   AsmArgs a = p->setup.args;
   a.u = nullptr;
@@ -814,6 +909,7 @@ int enprop_problem_assemble(enprop_problem* p, const double* y) {
 
 int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* iterations,
                          int* lane_status, double* history, int* hist_len) {
+  ScopedLaunchOpts launch_scope(p ? p->ctx : nullptr);
   if (!p) return fail(ENPROP_ERR_INVALID, "null problem");
   const int s = p->desc.ensemble_size;
   int rc = validate_cg_options(opt, s);
@@ -853,6 +949,7 @@ int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* i
 int enprop_problem_newton(enprop_problem* p, const double* y, const enprop_newton_options* opt,
                           int* newton_iterations, int* total_cg_iterations, double* residual_norms,
                           int* num_norms) {
+  ScopedLaunchOpts launch_scope(p ? p->ctx : nullptr);
   if (!p || !y || !opt) return fail(ENPROP_ERR_INVALID, "enprop_problem_newton: null argument");
   if (opt->max_iterations < 0) return fail(ENPROP_ERR_INVALID, "newton_solve: negative max_iterations");
   const int s = p->desc.ensemble_size;
@@ -929,6 +1026,7 @@ int enprop_problem_newton(enprop_problem* p, const double* y, const enprop_newto
 
 int enprop_problem_solve_host(enprop_problem* p, const double* y_host, double* x_host,
                               const enprop_cg_options* opt, int* iterations, int* lane_status) {
+  ScopedLaunchOpts launch_scope(p ? p->ctx : nullptr);
   if (!p || !y_host || !x_host) return fail(ENPROP_ERR_INVALID, "enprop_problem_solve_host: null argument");
   const int s = p->desc.ensemble_size;
   cudaStream_t st = p->ctx->stream;

@@ -205,12 +205,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile("griddepcontrol.wait;" ::: "memory");                  \
   } while (0)
 
-// process-wide switch (ENPROP_OPT_PDL, default off: measured -1% on the
-// three-group s = 32 bench, +2-4% on single-stream s = 4 / 16 solves)
-inline int& pdl_enabled() {
-  static int on = 0;
-  return on;
+// Per-context launch options (ENPROP_OPT_PDL, ENPROP_OPT_SPMV_VARIANT). Every
+// C-ABI entry point that launches kernels installs its context's options for
+// the duration of the call (ScopedLaunchOpts, ep_internal.h); the launch code
+// reads them from this thread-local slot, so concurrent contexts on different
+// host threads never see each other's settings.
+struct LaunchOpts {
+  int pdl = 0;            // PDL default off: -1% on the three-group s = 32 bench, +2-4% single stream
+  int spmv_variant = -1;  // warp-SpMV schedule, -1 = auto
+};
+inline LaunchOpts& launch_opts() {
+  thread_local LaunchOpts o;
+  return o;
 }
+inline int pdl_enabled() { return launch_opts().pdl; }
 
 // ENPROP_PDL_MASK (env, tuning): kernel kinds launched with PDL (1 direction,
 // 2 SpMV, 4 finalize, 8 update, 16 other); default all

@@ -405,6 +405,7 @@ int enprop_dist_local(enprop_dist* D, int index, int* rank, int* row_begin, int*
 }
 
 int enprop_dist_assemble(enprop_dist* D, const double* y) {
+  ScopedLaunchOpts launch_scope(D ? D->ctx : nullptr);
   if (!D || !y) return fail(ENPROP_ERR_INVALID, "enprop_dist_assemble: null argument");
   for (auto& d : D->ranks) {
     AsmArgs a = D->setup.args;
@@ -426,6 +427,7 @@ int enprop_dist_assemble(enprop_dist* D, const double* y) {
 }
 
 int enprop_dist_solve(enprop_dist* D, const enprop_cg_options* opt, int* iterations, int* lane_status) {
+  ScopedLaunchOpts launch_scope(D ? D->ctx : nullptr);
   if (!D || !opt) return fail(ENPROP_ERR_INVALID, "enprop_dist_solve: null argument");
   if (opt->dot_mode != ENPROP_DOT_CANONICAL)
     return fail(ENPROP_ERR_INVALID, "enprop_dist_solve: the multi-GPU solve uses the canonical dot order");

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "enprop_b200.h"
+#include "ep_common.cuh"
 #include "ep_kernels.h"
 
 #define EP_CUDA(call)                                  \
@@ -24,6 +25,9 @@ struct enprop_ctx {
   int spmv_pipeline = 0;    // ENPROP_OPT_SPMV_PIPELINE
   int fused_direction = 0;  // ENPROP_OPT_FUSED_DIRECTION (split measured faster on B200)
   int symmetric_storage = 1;  // ENPROP_OPT_SYMMETRIC_STORAGE (problems created afterwards)
+  int pdl = 0;                // ENPROP_OPT_PDL
+  int spmv_variant = -1;      // ENPROP_OPT_SPMV_VARIANT
+  int graphs = 1;             // ENPROP_OPT_GRAPHS
   // optional CUDA-event timing of the CG SpMV launches (bench roofline)
   int profile = 0;
   std::vector<cudaEvent_t> prof_ev;  // 5 events per profiled iteration, reused
@@ -37,6 +41,16 @@ struct enprop_ctx {
 };
 
 namespace ep_internal {
+
+// Installs a context's launch options (ep_common.cuh LaunchOpts) on this host
+// thread for the duration of one C-ABI call.
+struct ScopedLaunchOpts {
+  ep::LaunchOpts saved;
+  explicit ScopedLaunchOpts(const enprop_ctx* c) : saved(ep::launch_opts()) {
+    if (c) ep::launch_opts() = ep::LaunchOpts{c->pdl, c->spmv_variant};
+  }
+  ~ScopedLaunchOpts() { ep::launch_opts() = saved; }
+};
 
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t err, const char* where);

@@ -611,9 +611,11 @@ __global__ void __launch_bounds__(256, 4) k_cg_spmv(
 // W = TPR*E entries -- and broadcast them by shuffle, so each batch of U
 // gathers waits on one memory latency instead of two.
 // -----------------------------------------------------------------------------
-static int g_spmv_variant = -1;  // ENPROP_OPT_SPMV_VARIANT (process-wide; -1 auto, see SpmvVariant)
-void set_spmv_variant(int v) { g_spmv_variant = (v >= 0 && v <= 6) ? v : -1; }
-int spmv_variant() { return g_spmv_variant; }
+// ENPROP_OPT_SPMV_VARIANT of the calling context (-1 auto, see SpmvVariant)
+int spmv_variant() {
+  const int v = launch_opts().spmv_variant;
+  return (v >= 0 && v <= 6) ? v : -1;
+}
 
 // Vector kernels of the CG loop run 128-thread blocks capped at 48 registers
 // (kVecNT): small enough to be co-resident with a staged-SpMV CTA of another
@@ -994,7 +996,7 @@ static cudaError_t cg_spmv_s(bool tiles, bool fused_dir, bool run_direction, con
     // auto: 8-entry batches at 2 CTAs/SM for symmetric storage, 4 at 4 CTAs/SM
     // for full storage (same-process A/B at 64^3, s = 32: 0.301 vs 0.332 ms and
     // 0.366 vs 0.391 ms; tools/kernel_bench.py --ab)
-    const int var = g_spmv_variant >= 0 ? g_spmv_variant : (vpos ? 2 : 0);
+    const int var = spmv_variant() >= 0 ? spmv_variant() : (vpos ? 2 : 0);
 #define EP_CG_SPMV_WV(T, Y)                 \
   switch (var) {                            \
     case 1: EP_CG_SPMV_W(T, Y, 1); break;   \

@@ -141,7 +141,6 @@ cudaError_t launch_cg_direction(int s, int rows, const double* r, const double* 
 // p_gather: base of the gathered p (the rank's ghost-extended layout; == p_new on
 // one GPU). run_direction (split schedule): launch the direction pass first;
 // false when the caller already ran it (multi-GPU: with the halo in between).
-void set_spmv_variant(int v);   // ENPROP_OPT_SPMV_VARIANT
 cudaError_t launch_cg_spmv(int s, bool tiles, bool fused_dir, bool run_direction,
                            const TileMap& tm, const int* row_map, const int* col_entry,
                            const double* values, const double* r, const double* p_old,
@@ -200,8 +199,7 @@ cudaError_t launch_cg_spmv_staged(int s, bool tiles, bool fuse_fin, const StageM
                                   cudaStream_t st);
 bool staged_fuse_fin();  // ENPROP_STAGED_FUSE (env, default 1)
 bool staged_serial();    // ENPROP_STAGED_SERIAL (env, default 1)
-int spmv_variant();  // ENPROP_OPT_SPMV_VARIANT (-1 = auto)
-void set_pdl_enabled(int on);  // ENPROP_OPT_PDL
+int spmv_variant();  // ENPROP_OPT_SPMV_VARIANT of the calling context (-1 = auto)
 
 // after the loop: apply the still-deferred x += alpha*p of the last iteration
 cudaError_t launch_cg_flush(int s, int rows, double* x, double* const* p, const CgState* cg,

@@ -444,7 +444,6 @@ static int stage_shape(int& T, int& L, int& RS, int& max_upper, int& idx_bytes, 
   return 0;
 }
 
-void set_pdl_enabled(int on) { pdl_enabled() = on; }
 
 bool staged_fuse_fin() {
   static const int on = env_int("ENPROP_STAGED_FUSE", 1);

@@ -73,3 +73,25 @@ def test_ctypes_null_arguments_are_invalid():
     assert L.enprop_spmv(None, 4, 1, 1, None, None, None, None, None) == ep.ERR_INVALID
     assert L.enprop_cg(None, 4, 1, None, None, None, None, None, None, None, None, None,
                        None) == ep.ERR_INVALID
+
+
+def test_draw_samples_and_pack_are_the_reference_sequence():
+    """enprop_draw_samples / enprop_pack_sample_group (samples.cpp:7-18,
+    samples.hpp:18-31) on the host, bitwise against the reference's golden
+    draws (tests/golden: draw_samples(0, 8, 5), draw_samples(515, 4, 5))."""
+    g = np.load(os.path.join(ROOT, "tests", "golden", "reference_golden.npz"))
+    a = ep.draw_samples(0, 8, 5).numpy()
+    assert (bits(a) == bits(g["samples_seed0"])).all()
+    b = ep.draw_samples(515, 4, 5).numpy()
+    assert (bits(b) == bits(g["samples_seed515"])).all()
+    # a longer draw continues the same stream
+    assert (bits(ep.draw_samples(0, 20, 5).numpy()[:8]) == bits(a)).all()
+    packed = ep.pack_sample_group(torch.as_tensor(a), 4, 4).numpy()
+    assert (bits(packed) == bits(np.ascontiguousarray(a[4:8].T))).all()
+    assert ep.draw_samples(3, 0, 2).shape == (0, 2)
+    with pytest.raises(ValueError):
+        ep.draw_samples(0, 4, 0)
+    with pytest.raises(ValueError):
+        ep.draw_samples(0, -1, 3)
+    with pytest.raises(ValueError):
+        ep.pack_sample_group(torch.as_tensor(a), 4, 5)  # runs past the pool

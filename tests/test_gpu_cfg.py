@@ -1,0 +1,178 @@
+"""GPU parity at the BASELINE configurations, in the modes bench.py measures.
+
+* cfg 2 (64^3, s = 32, KL m = 3, sigma = 0.1, seed 0, group 0, tol 1e-6):
+  - the benchmarked serial order (staged SpMV + chain kernel, uncoupled)
+    against the UNMODIFIED reference's s x pcg_solve<double> on the extracted
+    components (src/bench.cpp:340-349): identical per-sample iteration counts,
+    bitwise residual histories and bitwise solutions (SHA-256 of each sample's
+    solution) -- fixtures made by the reference itself
+    (tests/golden/make_cfg2.py -> cfg2_64_s32.npz);
+  - the canonical order against the C restatement (oracle/enprop_oracle.c,
+    DOT_CANONICAL, plane segments), same fixture.
+* cfg 3 (128^3, s = 32): enprop_spmv on the assembled + Dirichlet matrix
+  bitwise against the C restatement's spmv (oracle), all 57M entries.
+* Workspace reuse across solve shapes (the grid barrier's counter
+  words must not alias the finalize counter).
+"""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1511_03703_b200 as ep
+from oracles import CG_COUPLED, CG_UNCOUPLED, DOT_CANONICAL, DOT_SERIAL, Oracle, bits, pack_group
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+FIXTURE = os.path.join(HERE, "golden", "cfg2_64_s32.npz")
+O = Oracle()
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = ep.Context(0)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def fx():
+    return dict(np.load(FIXTURE))
+
+
+@pytest.fixture(scope="module")
+def cfg2(ctx):
+    n, s, m = 64, 32, 3
+    y = ep.pack_sample_group(ep.draw_samples(0, s, m), s, 0).cuda()
+    p = ep.Problem(ctx, n, s, ep.KlField(m, 1.0, 0.1, 1.0))
+    p.assemble(y)
+    yield p, y
+    p.close()
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def check_against(p, fx, key, it, hist):
+    x = p.solution.cpu().numpy()
+    s = x.shape[1]
+    assert list(it) == fx[f"{key}_iterations"].tolist()
+    for e in range(s):
+        h = np.array(hist[e])
+        ref = fx[f"{key}_history"][e]
+        ref = ref[~np.isnan(ref)]
+        assert (bits(h) == bits(ref)).all(), f"residual history of sample {e}"
+        assert sha(x[:, e]) == fx[f"{key}_x_sha"][e], f"solution of sample {e}"
+
+
+def test_cfg2_assembly_is_the_reference(cfg2, fx):
+    p, _ = cfg2
+    assert sha(p.values.cpu().numpy()) == fx["values_sha"][0]
+    assert sha(p.residual.cpu().numpy()) == fx["residual_sha"][0]
+
+
+def test_cfg2_serial_uncoupled_is_reference_bitwise(cfg2, fx):
+    """The headline mode: every sample's iterations, history and solution are
+    the reference's own s x pcg_solve<double>."""
+    p, y = cfg2
+    cfg = ep.SolverConfig(tol=1e-6, max_iterations=10000, flavour=CG_UNCOUPLED, dot_mode=DOT_SERIAL)
+    it, hist, st = p.solve(cfg)
+    torch.cuda.synchronize()
+    assert all(v == 0 for v in st)
+    check_against(p, fx, "ref", it, hist)
+
+
+def test_cfg2_serial_concurrent_groups_are_reference_bitwise(ctx, fx):
+    """Several groups solved concurrently on their own streams (as bench.py
+    runs them) give the same bits as the reference for the shared group."""
+    import threading
+    n, s, m = 64, 32, 3
+    pool = ep.draw_samples(0, 3 * s, m)
+    cfg = ep.SolverConfig(tol=1e-6, max_iterations=10000, flavour=CG_UNCOUPLED, dot_mode=DOT_SERIAL)
+    ws = []
+    for g in range(3):
+        st = torch.cuda.Stream()
+        c = ep.Context(0, use_torch_stream=False)
+        c.set_stream(st.cuda_stream)
+        p = ep.Problem(c, n, s, ep.KlField(m, 1.0, 0.1, 1.0))
+        p.assemble(ep.pack_sample_group(pool, s, s * g).cuda())
+        ws.append((c, p))
+    out = [None] * 3
+
+    def run(i):
+        out[i] = ws[i][1].solve(cfg)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(3)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    check_against(ws[0][1], fx, "ref", out[0][0], out[0][1])
+    for c, p in ws:
+        p.close()
+        c.close()
+
+
+def test_cfg2_canonical_uncoupled_is_restatement_bitwise(cfg2, fx):
+    p, y = cfg2
+    cfg = ep.SolverConfig(tol=1e-6, max_iterations=10000, flavour=CG_UNCOUPLED, dot_mode=DOT_CANONICAL)
+    it, hist, st = p.solve(cfg)
+    torch.cuda.synchronize()
+    check_against(p, fx, "canon", it, hist)
+
+
+def test_cfg2_canonical_deltas_against_reference(fx):
+    """What the canonical order costs in parity at cfg 2 (reported by bench.py as
+    canonical_vs_reference): per-sample iteration counts differ from the
+    reference's by up to 5 (fixture: 0..5, the tree sums converge slightly
+    sooner), so the canonical order does NOT meet north_star's identical
+    iteration counts; the serial order does (test above)."""
+    d = fx["canon_iterations"].astype(int) - fx["ref_iterations"].astype(int)
+    assert np.abs(d).max() <= 5
+    assert (d != 0).any()  # documents that the orders really differ
+
+
+def test_workspace_reuse_across_segmentations(ctx):
+    """a canonical solve with plane segments (fused staged finalize,
+    grid barrier) followed by one with a single segment on the same problem
+    must finish and equal the restatement (counter words are not shared)."""
+    n, s, m = 12, 32, 3
+    N = n + 1
+    y = pack_group(O.draw_samples(0, s, m), s)
+    p = ep.Problem(ctx, n, s, ep.KlField(m, 1.0, 0.1, 1.0))
+    p.assemble(torch.as_tensor(y).cuda())
+    f = O.kl(m, 1.0, 0.1, 1.0)
+    ov, orr = O.assemble(s, n, f, y, dirichlet=True)
+    rm, ce = O.graph(n)
+    for seg in (0, N ** 3, 0, N ** 3):
+        cfg = ep.SolverConfig(tol=1e-7, flavour=CG_COUPLED, dot_mode=DOT_CANONICAL, seg_rows=seg)
+        it, _, _ = p.solve(cfg)
+        o = O.pcg(s, rm, ce, ov, -orr, 1e-7, 1000, flavour=CG_COUPLED, mode=DOT_CANONICAL,
+                  seg=N * N if seg == 0 else seg)
+        assert it == o["iterations"][0]
+        assert (bits(p.solution.cpu().numpy()) == bits(o["x"])).all()
+    p.close()
+
+
+@pytest.mark.slow
+def test_cfg3_spmv_128_cubed_bitwise_against_oracle(ctx):
+    """cfg 3: the 128^3 matrix (assembled + Dirichlet, seed 0), s = 32, x uniform
+    in [-1, 1): enprop_spmv equals the C restatement's spmv bit for bit."""
+    n, s, m = 128, 32, 3
+    y = ep.pack_sample_group(ep.draw_samples(0, s, m), s, 0).cuda()
+    p = ep.Problem(ctx, n, s, ep.KlField(m, 1.0, 0.1, 1.0))
+    p.assemble(y)
+    vals = p.values
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.rand((p.rows, s), dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    z = ep.spmv(ctx, s, p.row_map, p.col_entry, vals, x)
+    torch.cuda.synchronize()
+    rm, ce = p.row_map.cpu().numpy(), p.col_entry.cpu().numpy()
+    vh = vals.cpu().numpy()
+    del vals
+    zo = O.spmv(s, rm, ce, vh, x.cpu().numpy())
+    assert (bits(z.cpu().numpy()) == bits(zo)).all()
+    p.close()
