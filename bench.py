@@ -178,13 +178,14 @@ def run_groups(torch, workers, jobs, cfg, host=False):
         for item in jobs[i]:
             if host:
                 y_host, x_host = item
-                it, st, rc = w.prob.solve_host(y_host, x_host, cfg)
+                it, st, rc = w.prob.solve_host(y_host, x_host, cfg)  # lists (one per lane)
             else:
                 w.prob.assemble(item)
                 it, _, st = w.prob.solve(cfg)
+            it = list(it) if isinstance(it, (list, tuple)) else [it]  # coupled: one count
             its.append(max(it))
             sts.extend(st)
-            lanes.append(list(it))
+            lanes.append(it)
         out[i] = (its, sts, lanes)
 
     th = [threading.Thread(target=run, args=(i,)) for i in range(len(workers))]
@@ -526,7 +527,7 @@ def bench_cfg5(ep, torch, device):
         cfg = solver_cfg(ep, "canonical", flavour=fl, maxit=20000)
         ms, res = timed_round(torch, [w], [[y]], cfg)
         it = res[0][2][0]
-        out[name] = {"iterations": it if fl == ep.CG_UNCOUPLED else it[0],
+        out[name] = {"iterations": it if fl == ep.CG_UNCOUPLED else it[0],  # per lane / coupled
                      "samples_per_s": round(S / (ms / 1e3), 3), "ms": round(ms, 1)}
     w.close()
     return out

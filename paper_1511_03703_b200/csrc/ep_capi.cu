@@ -232,17 +232,20 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
     double* p_old = w.p[it & 1];
     double* p_new = w.p[(it + 1) & 1];
     cudaError_t e = cudaSuccess;
-#define EP_Q(call)              \
-  if ((e = (call)) != cudaSuccess) \
-    return e;
+#define EP_Q(call)                 \
+  do {                             \
+    if ((e = (call)) != cudaSuccess) \
+      return e;                    \
+  } while (0)
     if (ev) EP_Q(cudaEventRecord(ev[0], st));
     if (!fused) EP_Q(launch_cg_direction(s, rows, w.r, p_old, p_new, x, w.state, st));
     if (ev) EP_Q(cudaEventRecord(ev[1], st));
-    if (stage)
-      EP_Q(launch_cg_spmv_staged(s, canon, fuse_pq, *stage, values, p_new, w.q, f_pq, st))
-    else
+    if (stage) {
+      EP_Q(launch_cg_spmv_staged(s, canon, fuse_pq, *stage, values, p_new, w.q, f_pq, st));
+    } else {
       EP_Q(launch_cg_spmv(s, canon, fused, false, tm, row_map, col_entry, values, w.r, p_old, p_new, w.q,
                           x, p_new, vpos, f_pq, st));
+    }
     if (ev) EP_Q(cudaEventRecord(ev[2], st));
     if (!canon) EP_Q(launch_chain(s, rows, w.prod, nullptr, kChainGiven, f_pq, st));
     if (fin_kernel && !fuse_pq) EP_Q(launch_fin_segments(s, tm, f_pq, st));
