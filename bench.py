@@ -314,6 +314,10 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.skip_configs:
         extra["cfg5"] = bench_cfg5(ep, torch, local)
         extra["cfg4_one_gpu"] = bench_cfg4_one_gpu(ep, torch, local)
+    if not args.skip_dd:  # every rank takes part (strong scaling of one 256^3 ensemble)
+        dd = bench_cfg4_dd(ep, torch, dist, local, rank, world, args.dd_mesh)
+        if rank == 0:
+            extra["cfg4_dd"] = dd
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:
         cpu = cpu_baseline_sample()
@@ -545,6 +549,52 @@ def bench_cfg4_one_gpu(ep, torch, device):
     return {"mesh": 256, "samples_per_s": round(S / (ms / 1e3), 3), "ms": round(ms, 1),
             "cg_iterations_max": res[0][0], "dot_order": "canonical",
             "note": "serial order at 256^3: a dot chain is 17M dependent DADDs (~72 ms); one group cannot hide it"}
+
+
+def bench_cfg4_dd(ep, torch, dist, local, rank, world, n, steps=1):
+    """cfg 4 (north_star: 1 -> 8 GPUs on 256^3): ONE s=32 ensemble on the n^3
+    mesh split into z-slabs over the `world` ranks of this job (partition.cpp
+    rule), halo of p and all-gathered per-plane dot sums over the CUDA-IPC
+    transport (NVLink P2P between GPUs; the in-process transport at 1 rank);
+    canonical order, so every rank count gives the one-GPU bits. Strong
+    scaling: samples/s of the whole job; device time, max over ranks."""
+    import uuid
+    job = None
+    if world > 1:
+        obj = [uuid.uuid4().hex[:16] if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        job = obj[0]
+    ctx = ep.Context(local)
+    kl = ep.KlField(M_TERMS, 1.0, SIGMA, 1.0)
+    d = ep.Dist(ctx, n, S, world, rank, kl=kl, ipc_job=job)
+    pool = ep.draw_samples(0, S * (steps + 1), M_TERMS)
+    cfg = solver_cfg(ep, "canonical", maxit=20000)
+    d.assemble(ep.pack_sample_group(pool, S, 0).cuda())  # warm-up solve
+    d.solve(cfg)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0.record(st)
+    iters = []
+    for k in range(steps):
+        d.assemble(ep.pack_sample_group(pool, S, S * (k + 1)).cuda())
+        it, status = d.solve(cfg)
+        iters.append(max(it))
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    d.close()
+    ctx.close()
+    return {"mesh": n, "ranks": world, "samples_per_s": round(steps * S / (ms / 1e3), 3), "ms": round(ms, 1),
+            "cg_iterations_max": iters, "dot_order": "canonical",
+            "transport": "CUDA IPC (NVLink P2P)" if world > 1 else "single rank",
+            "scaling": "strong (one ensemble per step split over the ranks)"}
 
 
 def time_queued(torch, fn, reps, stream):
@@ -821,6 +871,7 @@ def main():
     ap.add_argument("--skip-asm", action="store_true")
     ap.add_argument("--skip-widths", action="store_true")
     ap.add_argument("--skip-configs", action="store_true", help="skip cfg 4 (one GPU) and cfg 5")
+    ap.add_argument("--skip-dd", action="store_true", help="skip the cfg 4 slab solve over the job's ranks")
     ap.add_argument("--workload", choices=["groups", "dd"], default="groups",
                     help="groups: cfg 2 sample groups (default); dd: cfg 4 domain decomposition")
     ap.add_argument("--dd-mesh", type=int, default=256)

@@ -296,6 +296,15 @@ int enprop_nccl_unique_id(void* out, size_t bytes);
 typedef struct enprop_dist enprop_dist;
 int enprop_dist_create(enprop_ctx* ctx, const enprop_problem_desc* desc, int nranks, int rank,
                        const void* nccl_id, enprop_dist** out);
+/* The same over the CUDA-IPC transport: one process per rank on any GPUs of
+ * one node -- several ranks may share one GPU, which NCCL refuses. `job` names
+ * the host board (/dev/shm/enprop_b200_<job>) that every rank of the job opens;
+ * it must be unique per job (e.g. a random token from rank 0). Peers exchange
+ * through their exported buffers and interprocess events: stream waits and
+ * cudaMemcpyAsync (NVLink P2P between GPUs), never a kernel waiting on another
+ * rank. Blocks until all nranks have joined (ENPROP_ERR_CUDA after 120 s). */
+int enprop_dist_create_ipc(enprop_ctx* ctx, const enprop_problem_desc* desc, int nranks, int rank,
+                           const char* job, enprop_dist** out);
 int enprop_dist_destroy(enprop_dist* d);
 /* assemble + Dirichlet of every local rank's rows; y [num_terms][s] on the device */
 int enprop_dist_assemble(enprop_dist* d, const double* y);

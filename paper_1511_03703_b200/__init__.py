@@ -204,6 +204,7 @@ def lib() -> C.CDLL:
     L.enprop_problem_solve_host.argtypes = [_vp, _vp, _vp, C.POINTER(_CgOptions), _ip, _ip]
     L.enprop_nccl_unique_id.argtypes = [_vp, C.c_size_t]
     L.enprop_dist_create.argtypes = [_vp, C.POINTER(_ProblemDesc), C.c_int, C.c_int, _vp, C.POINTER(_vp)]
+    L.enprop_dist_create_ipc.argtypes = [_vp, C.POINTER(_ProblemDesc), C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]
     L.enprop_dist_destroy.argtypes = [_vp]
     L.enprop_dist_assemble.argtypes = [_vp, _vp]
     L.enprop_dist_solve.argtypes = [_vp, C.POINTER(_CgOptions), _ip, _ip]
@@ -643,21 +644,27 @@ def predicted_speedup(a: float, b: float, s: float) -> float:
 
 class Dist:
     """Ensemble problem domain-decomposed into z-slabs of node planes over
-    `nranks` (partition.cpp:31-72 rule).  nccl_id=None emulates all ranks in
-    this process on one GPU (stream-ordered copies as transport); with an id,
-    this process is `rank` of an NCCL job.  Canonical dot order only; results
+    `nranks` (partition.cpp:31-72 rule).  nccl_id=None and ipc_job=None
+    emulate all ranks in this process on one GPU (stream-ordered copies as
+    transport); with an NCCL id this process is `rank` of an NCCL job; with an
+    ipc_job name it is `rank` of a CUDA-IPC job (peers on any GPUs of the node,
+    several per GPU allowed).  Canonical dot order only; results
     are bitwise independent of nranks."""
 
     def __init__(self, ctx: Context, n: int, s: int, nranks: int, rank: int = 0,
                  nccl_id: Optional[bytes] = None, kl: KlField = None,
-                 coeffs: PdeCoefficients = None, bc: DirichletBc = None):
+                 coeffs: PdeCoefficients = None, bc: DirichletBc = None, ipc_job: Optional[str] = None):
         self.ctx, self.n, self.s, self.nranks = ctx, n, s, nranks
         self.kl = kl or KlField()
         d = _ProblemDesc(n, s, self.kl._c(), (coeffs or PdeCoefficients())._c(),
                          (bc or DirichletBc())._c())
         h = _vp()
-        idbuf = None if nccl_id is None else (C.c_char * 128).from_buffer_copy(nccl_id)
-        _check(lib().enprop_dist_create(ctx.h, C.byref(d), nranks, rank, idbuf, C.byref(h)), "Dist")
+        if ipc_job is not None:  # CUDA-IPC transport: this process is `rank` of an IPC job
+            _check(lib().enprop_dist_create_ipc(ctx.h, C.byref(d), nranks, rank, ipc_job.encode(), C.byref(h)),
+                   "Dist")
+        else:
+            idbuf = None if nccl_id is None else (C.c_char * 128).from_buffer_copy(nccl_id)
+            _check(lib().enprop_dist_create(ctx.h, C.byref(d), nranks, rank, idbuf, C.byref(h)), "Dist")
         self.h = h
 
     def assemble(self, y: torch.Tensor):

@@ -14,19 +14,43 @@
 // totals, hence alpha/beta/iterations/solutions, identical to the one-GPU
 // solve bit for bit, independent of the rank count.
 //
-// Transports: NCCL (one process per GPU; libnccl.so.2 loaded at run time, so
-// an already loaded copy — e.g. torch's — is shared), or an in-process
-// emulation of all ranks on one GPU where the halo and the all-gather are
-// stream-ordered device copies (no kernel waits on another rank).
+// Transports:
+//  * NCCL (one process per GPU; libnccl.so.2 loaded at run time, so an already
+//    loaded copy -- e.g. torch's -- is shared): ncclSend/ncclRecv for the halo,
+//    ncclAllGather for the per-plane sums;
+//  * CUDA IPC (one process per rank, any GPUs of one node, including several
+//    ranks on ONE GPU, which NCCL refuses): every rank exports its p buffers,
+//    its per-plane sum buffers and three interprocess events; a host board in
+//    /dev/shm carries the handles and, per rank and event kind, how many
+//    records have been issued. A consumer waits on the host until the
+//    producer's record for the needed step has been issued, then makes its
+//    stream wait on the producer's event (cudaStreamWaitEvent) and copies from
+//    the peer's memory with cudaMemcpyAsync (NVLink P2P between GPUs, a device
+//    copy on one GPU). No kernel ever waits on another rank: only stream-event
+//    waits, so co-located ranks cannot deadlock each other's SMs.
+//    Ordering: halo pulls and all-gathers happen every phase, so no rank can
+//    issue the next record of a kind before every peer has issued its wait on
+//    the current one (each record follows the rank's waits on all peers'
+//    previous phase); the per-plane sums are double buffered by phase (p.q /
+//    r.r) so a fast rank never overwrites sums a slow rank still copies;
+//  * an in-process emulation of all ranks on one GPU where the halo and the
+//    all-gather are stream-ordered device copies (testing).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <fcntl.h>
 #include <nccl.h>
+#include <sched.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <string>
 #include <vector>
 
 #include "enprop_b200.h"
@@ -103,7 +127,8 @@ struct DistRank {
   double *values = nullptr, *residual = nullptr, *x = nullptr, *r = nullptr, *q = nullptr;
   double* p[2] = {nullptr, nullptr};  // ext layout
   TileMap tm{};
-  double *partials = nullptr, *seg_local = nullptr, *gathered = nullptr, *hist = nullptr;
+  double *partials = nullptr, *gathered = nullptr, *hist = nullptr;
+  double* seg[2] = {nullptr, nullptr};  // per-plane sums of this rank: [0] p.q, [1] r.r (and init)
   int* counters = nullptr;
   int* plane_pos = nullptr;
   CgState* state = nullptr;
@@ -111,14 +136,42 @@ struct DistRank {
 
 }  // namespace
 
+namespace {
+enum Transport { kEmulated = 0, kNccl = 1, kIpc = 2 };
+enum EvKind { kEvP = 0, kEvPQ = 1, kEvRR = 2 };
+constexpr int kIpcMaxRanks = 64;
+
+// Host board of an IPC job (/dev/shm, one per job name, zero-filled on creation).
+struct IpcSlot {
+  cudaIpcMemHandle_t p[2], seg[2];
+  cudaIpcEventHandle_t ev[3];
+  int device;
+  std::atomic<int> published;
+  std::atomic<long long> seq[3];  // records issued per event kind
+};
+struct IpcBoard {
+  std::atomic<int> joined, opened, closed;
+  IpcSlot slot[kIpcMaxRanks];
+};
+}  // namespace
+
 struct enprop_dist {
   enprop_ctx* ctx = nullptr;
   enprop_problem_desc desc{};
   int nranks = 1, n = 0, N = 0, plane = 0, maxplanes = 0, maxit = -1;
+  int transport = kEmulated;
   bool emulated = true;
   ncclComm_t comm = nullptr;
   AsmSetup setup;
-  std::vector<DistRank> ranks;  // emulated: all ranks; NCCL: this process's rank
+  std::vector<DistRank> ranks;  // emulated: all ranks; NCCL / IPC: this process's rank
+  // IPC transport
+  std::string board_name;
+  IpcBoard* board = nullptr;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  long long seq[3] = {0, 0, 0};
+  std::vector<double*> peer_p[2], peer_seg[2];  // opened peer buffers (own ones for self)
+  std::vector<cudaEvent_t> peer_ev[3];
+  bool ipc_open = false;
 };
 
 namespace {
@@ -132,7 +185,7 @@ void plane_range(int N, int P, int r, int& k0, int& k1) {
 void free_rank(DistRank& d) {
   for (void* q : {(void*)d.row_map, (void*)d.col_entry, (void*)d.values, (void*)d.residual,
                   (void*)d.x, (void*)d.r, (void*)d.q, (void*)d.p[0], (void*)d.p[1],
-                  (void*)d.partials, (void*)d.seg_local, (void*)d.gathered, (void*)d.hist,
+                  (void*)d.partials, (void*)d.seg[0], (void*)d.seg[1], (void*)d.gathered, (void*)d.hist,
                   (void*)d.counters, (void*)d.plane_pos, (void*)d.state})
     if (q) cudaFree(q);
   d = DistRank{};
@@ -164,8 +217,10 @@ int setup_rank(enprop_dist* D, DistRank& d, int r) {
   EP_CUDA(cudaMemset(d.p[0], 0, ext));
   EP_CUDA(cudaMemset(d.p[1], 0, ext));
   EP_CUDA(cudaMalloc(&d.partials, (size_t)std::max(d.tm.num_tiles(), 1) * s * sizeof(double)));
-  EP_CUDA(cudaMalloc(&d.seg_local, (size_t)D->maxplanes * s * sizeof(double)));
-  EP_CUDA(cudaMemset(d.seg_local, 0, (size_t)D->maxplanes * s * sizeof(double)));
+  for (int k = 0; k < 2; ++k) {
+    EP_CUDA(cudaMalloc(&d.seg[k], (size_t)D->maxplanes * s * sizeof(double)));
+    EP_CUDA(cudaMemset(d.seg[k], 0, (size_t)D->maxplanes * s * sizeof(double)));
+  }
   EP_CUDA(cudaMalloc(&d.gathered, (size_t)P * D->maxplanes * s * sizeof(double)));
   EP_CUDA(cudaMalloc(&d.counters, kCounterInts * sizeof(int)));
   EP_CUDA(cudaMemset(d.counters, 0, kCounterInts * sizeof(int)));
@@ -188,7 +243,7 @@ int setup_rank(enprop_dist* D, DistRank& d, int r) {
 FinArgs rank_fin(const DistRank& d, int phase) {
   FinArgs f;
   f.partials = d.partials;
-  f.seg_sums = d.seg_local;
+  f.seg_sums = d.seg[phase == kPhasePQ ? 0 : 1];
   f.seg_done = d.counters;
   f.bar = d.counters + 1;
   f.ticket = d.counters + 3;
@@ -200,6 +255,142 @@ FinArgs rank_fin(const DistRank& d, int phase) {
   f.seg_only = 1;
   f.defer = 1;
   return f;
+}
+
+// owned-row layout of rank r: (ext_begin, lo ghost rows, owned rows)
+void rank_layout(const enprop_dist* D, int r, int& ext_begin, int& lo_rows, int& rows) {
+  int k0, k1;
+  plane_range(D->N, D->nranks, r, k0, k1);
+  lo_rows = k0 > 0 ? D->plane : 0;
+  rows = (k1 - k0) * D->plane;
+  ext_begin = k0 * D->plane - lo_rows;
+}
+
+constexpr double kIpcTimeoutS = 120.0;
+
+// host wait until rank q has issued `target` records of `kind` (or time out)
+int ipc_wait_seq(enprop_dist* D, int q, int kind, long long target) {
+  auto& cnt = D->board->slot[q].seq[kind];
+  if (cnt.load(std::memory_order_acquire) >= target) return ENPROP_OK;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned spin = 0; cnt.load(std::memory_order_acquire) < target; ++spin) {
+    if ((spin & 1023) == 1023) {
+      sched_yield();
+      if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > kIpcTimeoutS)
+        return fail(ENPROP_ERR_CUDA, "enprop_dist (ipc): timed out waiting for rank " + std::to_string(q));
+    }
+  }
+  return ENPROP_OK;
+}
+
+// record this rank's event of `kind` after the work already on the stream and
+// announce it on the board
+int ipc_publish(enprop_dist* D, int kind) {
+  EP_CUDA(cudaEventRecord(D->ev[kind], D->ctx->stream));
+  D->seq[kind] += 1;
+  D->board->slot[D->ranks[0].rank].seq[kind].store(D->seq[kind], std::memory_order_release);
+  return ENPROP_OK;
+}
+
+// make the stream wait for rank q's record of `kind` matching ours
+int ipc_wait(enprop_dist* D, int q, int kind) {
+  int rc = ipc_wait_seq(D, q, kind, D->seq[kind]);
+  if (rc) return rc;
+  EP_CUDA(cudaStreamWaitEvent(D->ctx->stream, D->peer_ev[kind][q], 0));
+  return ENPROP_OK;
+}
+
+// wait on the host until every rank has bumped `counter` to nranks
+int ipc_barrier(enprop_dist* D, std::atomic<int>& counter) {
+  counter.fetch_add(1, std::memory_order_acq_rel);
+  const auto t0 = std::chrono::steady_clock::now();
+  while (counter.load(std::memory_order_acquire) < D->nranks) {
+    sched_yield();
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > kIpcTimeoutS)
+      return fail(ENPROP_ERR_CUDA, "enprop_dist (ipc): timed out waiting for the other ranks to join");
+  }
+  return ENPROP_OK;
+}
+
+int ipc_setup(enprop_dist* D, const char* job) {
+  D->board_name = std::string("/enprop_b200_") + job;
+  const int fd = shm_open(D->board_name.c_str(), O_CREAT | O_RDWR, 0600);
+  if (fd < 0) return fail(ENPROP_ERR_CUDA, "enprop_dist (ipc): shm_open failed for " + D->board_name);
+  if (ftruncate(fd, sizeof(IpcBoard)) != 0) {
+    close(fd);
+    return fail(ENPROP_ERR_CUDA, "enprop_dist (ipc): ftruncate failed");
+  }
+  void* m = mmap(nullptr, sizeof(IpcBoard), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (m == MAP_FAILED) return fail(ENPROP_ERR_CUDA, "enprop_dist (ipc): mmap failed");
+  D->board = static_cast<IpcBoard*>(m);
+  DistRank& d = D->ranks[0];
+  IpcSlot& me = D->board->slot[d.rank];
+  for (int k = 0; k < 3; ++k) {
+    EP_CUDA(cudaEventCreateWithFlags(&D->ev[k], cudaEventDisableTiming | cudaEventInterprocess));
+    EP_CUDA(cudaIpcGetEventHandle(&me.ev[k], D->ev[k]));
+  }
+  for (int k = 0; k < 2; ++k) {
+    EP_CUDA(cudaIpcGetMemHandle(&me.p[k], d.p[k]));
+    EP_CUDA(cudaIpcGetMemHandle(&me.seg[k], d.seg[k]));
+  }
+  EP_CUDA(cudaGetDevice(&me.device));
+  me.published.store(1, std::memory_order_release);
+  int rc = ipc_barrier(D, D->board->joined);
+  if (rc) return rc;
+  for (int k = 0; k < 2; ++k) {
+    D->peer_p[k].assign(D->nranks, nullptr);
+    D->peer_seg[k].assign(D->nranks, nullptr);
+  }
+  for (int k = 0; k < 3; ++k) D->peer_ev[k].assign(D->nranks, nullptr);
+  D->ipc_open = true;
+  for (int q = 0; q < D->nranks; ++q) {
+    IpcSlot& sl = D->board->slot[q];
+    const bool self = q == d.rank;
+    const bool nb = q == d.rank - 1 || q == d.rank + 1;
+    for (int k = 0; k < 2; ++k) {
+      if (self) {
+        D->peer_p[k][q] = d.p[k];
+        D->peer_seg[k][q] = d.seg[k];
+        continue;
+      }
+      void* ptr = nullptr;
+      if (nb) {
+        EP_CUDA(cudaIpcOpenMemHandle(&ptr, sl.p[k], cudaIpcMemLazyEnablePeerAccess));
+        D->peer_p[k][q] = static_cast<double*>(ptr);
+      }
+      EP_CUDA(cudaIpcOpenMemHandle(&ptr, sl.seg[k], cudaIpcMemLazyEnablePeerAccess));
+      D->peer_seg[k][q] = static_cast<double*>(ptr);
+    }
+    for (int k = 0; k < 3; ++k) {
+      if (self) D->peer_ev[k][q] = D->ev[k];
+      else EP_CUDA(cudaIpcOpenEventHandle(&D->peer_ev[k][q], sl.ev[k]));
+    }
+  }
+  return ipc_barrier(D, D->board->opened);
+}
+
+void ipc_teardown(enprop_dist* D) {
+  if (!D->board) return;
+  const int me = D->ranks.empty() ? -1 : D->ranks[0].rank;
+  if (D->ipc_open) {
+    cudaStreamSynchronize(D->ctx->stream);
+    for (int q = 0; q < D->nranks; ++q) {
+      if (q == me) continue;
+      for (int k = 0; k < 2; ++k) {
+        if (D->peer_p[k][q]) cudaIpcCloseMemHandle(D->peer_p[k][q]);
+        if (D->peer_seg[k][q]) cudaIpcCloseMemHandle(D->peer_seg[k][q]);
+      }
+    }
+  }
+  // the last rank out removes the board; peers keep their exported buffers
+  // alive until everyone has closed its mappings
+  ipc_barrier(D, D->board->closed);
+  for (int k = 0; k < 3; ++k)
+    if (D->ev[k]) cudaEventDestroy(D->ev[k]);
+  if (me == 0) shm_unlink(D->board_name.c_str());
+  munmap(D->board, sizeof(IpcBoard));
+  D->board = nullptr;
 }
 
 // halo of the p buffer `which` (first owned plane -> rank-1's hi ghost, last
@@ -225,6 +416,25 @@ int halo(enprop_dist* D, int which) {
     return ENPROP_OK;
   }
   DistRank& d = D->ranks[0];
+  if (D->transport == kIpc) {  // publish p[which], pull the neighbours' boundary planes
+    int rc = ipc_publish(D, kEvP);
+    if (rc) return rc;
+    if (d.rank > 0) {
+      int lo, lr, rws;
+      rank_layout(D, d.rank - 1, lo, lr, rws);
+      if ((rc = ipc_wait(D, d.rank - 1, kEvP))) return rc;
+      EP_CUDA(cudaMemcpyAsync(d.p[which], D->peer_p[which][d.rank - 1] + (size_t)(lr + rws - D->plane) * s,
+                              pe * sizeof(double), cudaMemcpyDefault, st));
+    }
+    if (d.rank + 1 < D->nranks) {
+      int lo, lr, rws;
+      rank_layout(D, d.rank + 1, lo, lr, rws);
+      if ((rc = ipc_wait(D, d.rank + 1, kEvP))) return rc;
+      EP_CUDA(cudaMemcpyAsync(d.p[which] + (size_t)(d.lo_rows + d.rows) * s, D->peer_p[which][d.rank + 1] + (size_t)lr * s,
+                              pe * sizeof(double), cudaMemcpyDefault, st));
+    }
+    return ENPROP_OK;
+  }
   auto& api = nccl();
   EP_NCCL(api.GroupStart());
   if (d.rank > 0) {
@@ -239,17 +449,30 @@ int halo(enprop_dist* D, int which) {
   return ENPROP_OK;
 }
 
-int allgather(enprop_dist* D) {
+// all-gather of the per-plane sums of `phase` (seg[0] for p.q, seg[1] else)
+int allgather(enprop_dist* D, int phase) {
   const size_t cnt = (size_t)D->maxplanes * D->desc.ensemble_size;
+  const int b = phase == kPhasePQ ? 0 : 1;
   cudaStream_t st = D->ctx->stream;
   if (D->emulated) {
     for (auto& dst : D->ranks)
       for (size_t q = 0; q < D->ranks.size(); ++q)
-        EP_CUDA(cudaMemcpyAsync(dst.gathered + q * cnt, D->ranks[q].seg_local, cnt * sizeof(double),
+        EP_CUDA(cudaMemcpyAsync(dst.gathered + q * cnt, D->ranks[q].seg[b], cnt * sizeof(double),
                                 cudaMemcpyDeviceToDevice, st));
     return ENPROP_OK;
   }
-  EP_NCCL(nccl().AllGather(D->ranks[0].seg_local, D->ranks[0].gathered, cnt, ncclDouble, D->comm, st));
+  DistRank& d = D->ranks[0];
+  if (D->transport == kIpc) {
+    const int kind = phase == kPhasePQ ? kEvPQ : kEvRR;
+    int rc = ipc_publish(D, kind);
+    if (rc) return rc;
+    for (int q = 0; q < D->nranks; ++q) {
+      if (q != d.rank && (rc = ipc_wait(D, q, kind))) return rc;
+      EP_CUDA(cudaMemcpyAsync(d.gathered + q * cnt, D->peer_seg[b][q], cnt * sizeof(double), cudaMemcpyDefault, st));
+    }
+    return ENPROP_OK;
+  }
+  EP_NCCL(nccl().AllGather(d.seg[b], d.gathered, cnt, ncclDouble, D->comm, st));
   return ENPROP_OK;
 }
 
@@ -278,6 +501,7 @@ int enprop_nccl_unique_id(void* out, size_t bytes) {
 
 int enprop_dist_destroy(enprop_dist* D) {
   if (!D) return ENPROP_OK;
+  ipc_teardown(D);
   for (auto& d : D->ranks) free_rank(d);
   free_asm_setup(D->setup);
   if (D->comm) nccl().CommDestroy(D->comm);
@@ -285,8 +509,8 @@ int enprop_dist_destroy(enprop_dist* D) {
   return ENPROP_OK;
 }
 
-int enprop_dist_create(enprop_ctx* c, const enprop_problem_desc* desc, int nranks, int rank,
-                       const void* nccl_id, enprop_dist** out) {
+static int dist_create(enprop_ctx* c, const enprop_problem_desc* desc, int nranks, int rank,
+                       const void* nccl_id, const char* ipc_job, enprop_dist** out) {
   if (!c || !desc || !out) return fail(ENPROP_ERR_INVALID, "enprop_dist_create: null argument");
   if (!valid_width(desc->ensemble_size)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
   const int n = desc->cells_per_axis;
@@ -303,14 +527,15 @@ int enprop_dist_create(enprop_ctx* c, const enprop_problem_desc* desc, int nrank
   D->N = n + 1;
   D->plane = D->N * D->N;
   D->maxplanes = (D->N + nranks - 1) / nranks;
-  D->emulated = nccl_id == nullptr;
+  D->transport = nccl_id ? kNccl : (ipc_job ? kIpc : kEmulated);
+  D->emulated = D->transport == kEmulated;
   auto bail = [&](int rc) {
     enprop_dist_destroy(D);
     return rc;
   };
   int rc = make_asm_setup(c, n, &desc->kl, &desc->coeffs, D->setup);
   if (rc) return bail(rc);
-  if (!D->emulated) {
+  if (D->transport == kNccl) {
     if (!nccl().load()) return bail(fail(ENPROP_ERR_CUDA, "libnccl.so.2 could not be loaded"));
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
@@ -325,8 +550,25 @@ int enprop_dist_create(enprop_ctx* c, const enprop_problem_desc* desc, int nrank
   }
   cudaError_t err = cudaStreamSynchronize(c->stream);
   if (err != cudaSuccess) return bail(cuda_fail(err, "enprop_dist_create"));
+  if (D->transport == kIpc) {
+    if (nranks > kIpcMaxRanks) return bail(fail(ENPROP_ERR_INVALID, "enprop_dist (ipc): at most 64 ranks"));
+    rc = ipc_setup(D, ipc_job);
+    if (rc) return bail(rc);
+  }
   *out = D;
   return ENPROP_OK;
+}
+
+int enprop_dist_create(enprop_ctx* c, const enprop_problem_desc* desc, int nranks, int rank,
+                       const void* nccl_id, enprop_dist** out) {
+  return dist_create(c, desc, nranks, rank, nccl_id, nullptr, out);
+}
+
+int enprop_dist_create_ipc(enprop_ctx* c, const enprop_problem_desc* desc, int nranks, int rank,
+                           const char* job, enprop_dist** out) {
+  if (!job || !*job || std::strchr(job, '/'))
+    return fail(ENPROP_ERR_INVALID, "enprop_dist_create_ipc: job name must be non-empty, without '/'");
+  return dist_create(c, desc, nranks, rank, nullptr, job, out);
 }
 
 int enprop_dist_time_halo(enprop_dist* D, int reps, double* seconds) {
@@ -460,7 +702,7 @@ int enprop_dist_solve(enprop_dist* D, const enprop_cg_options* opt, int* iterati
     EP_CUDA(launch_fin_segments(s, d.tm, rank_fin(d, kPhaseInit), st));
     ctx->launches += 3;
   }
-  int rc = allgather(D);
+  int rc = allgather(D, kPhaseInit);
   if (rc) return rc;
   rc = fin_all(D, kPhaseInit);
   if (rc) return rc;
@@ -485,13 +727,13 @@ int enprop_dist_solve(enprop_dist* D, const enprop_cg_options* opt, int* iterati
         EP_CUDA(launch_fin_segments(s, d.tm, rank_fin(d, kPhasePQ), st));
         ctx->launches += 2;
       }
-      if ((rc = allgather(D)) || (rc = fin_all(D, kPhasePQ))) return rc;
+      if ((rc = allgather(D, kPhasePQ)) || (rc = fin_all(D, kPhasePQ))) return rc;
       for (auto& d : D->ranks) {
         EP_CUDA(launch_cg_update(s, true, d.tm, d.r, d.q, rank_fin(d, kPhaseRR), st));
         EP_CUDA(launch_fin_segments(s, d.tm, rank_fin(d, kPhaseRR), st));
         ctx->launches += 2;
       }
-      if ((rc = allgather(D)) || (rc = fin_all(D, kPhaseRR))) return rc;
+      if ((rc = allgather(D, kPhaseRR)) || (rc = fin_all(D, kPhaseRR))) return rc;
     }
     EP_CUDA(cudaMemcpyAsync(&ctx->pinned_flags[slot], &D->ranks[0].state->done, sizeof(int),
                             cudaMemcpyDeviceToHost, st));
