@@ -37,7 +37,56 @@
 
 #include "enprop_b200.h"
 
+// Result / system types: when the reference's headers are on the include path
+// the drop-in returns the reference's own types (enprop::SolveResult<S>,
+// enprop::AssembledSystem<S>, enprop::NewtonResult<S>), so call sites such as
+//     enprop::SolveResult<E> r = enprop_b200::pcg_solve(...);
+// compile unchanged; otherwise structurally identical local types are used.
+#if !defined(ENPROP_B200_STANDALONE_TYPES) && __has_include("enprop/pcg.hpp") && __has_include("enprop/fem.hpp")
+#include "enprop/fem.hpp"
+#include "enprop/pcg.hpp"
+#define ENPROP_B200_REFERENCE_TYPES 1
+#endif
+
 namespace enprop_b200 {
+
+#ifdef ENPROP_B200_REFERENCE_TYPES
+template <class Scalar>
+using SolveResult = ::enprop::SolveResult<Scalar>;
+template <class Scalar>
+using AssembledSystem = ::enprop::AssembledSystem<Scalar>;
+template <class Scalar>
+using NewtonResult = ::enprop::NewtonResult<Scalar>;
+#else
+/// Same fields as enprop::SolveResult<Scalar> (pcg.hpp:33-38).
+template <class Scalar>
+struct SolveResult {
+  std::vector<Scalar> solution;
+  int iterations = 0;
+  std::vector<double> residual_history;
+};
+/// Same fields as enprop::CrsMatrix<Scalar> (crs.hpp:19-69).
+template <class Scalar>
+struct CrsMatrix {
+  int num_rows = 0, num_cols = 0;
+  std::vector<int> row_map, col_entry;
+  std::vector<Scalar> values;
+};
+/// Same fields as enprop::AssembledSystem<Scalar> (fem.hpp:34-38).
+template <class Scalar>
+struct AssembledSystem {
+  CrsMatrix<Scalar> matrix;
+  std::vector<Scalar> residual;
+};
+/// Same fields as enprop::NewtonResult<Scalar> (fem.hpp:251-257).
+template <class Scalar>
+struct NewtonResult {
+  std::vector<Scalar> solution;
+  int iterations = 0;
+  int total_cg_iterations = 0;
+  std::vector<double> residual_norms;
+};
+#endif
 
 #ifndef ENPROP_B200_SOLVER_ERROR
 /// Thrown like enprop::SolverError (pcg.hpp:22-31). Define
@@ -299,10 +348,9 @@ enprop_pde_coeffs coeffs_of(const Coeffs& c) {
 /// assemble<Scalar> (fem.hpp:115-202). Ctx is enprop::AssemblyContext (or any
 /// type with mesh().cells_per_axis()), Field an enprop::KlField, Coeffs an
 /// enprop::PdeCoefficients, System an enprop::AssembledSystem<Scalar>.
-template <class Ctx, class Field, class Coeffs, class Vector, class Samples, class System>
-void assemble(const Ctx& actx, const Field& field, const Coeffs& coeffs, const Vector& u,
+template <class Scalar, class Ctx, class Field, class Coeffs, class Samples, class System>
+void assemble(const Ctx& actx, const Field& field, const Coeffs& coeffs, const std::vector<Scalar>& u,
               const Samples& samples, System& out) {
-  using Scalar = detail::scalar_of<Vector>;
   constexpr int s = detail::width<Scalar>();
   const int n = actx.mesh().cells_per_axis();
   const int64_t rows = static_cast<int64_t>(n + 1) * (n + 1) * (n + 1);
@@ -334,6 +382,15 @@ void assemble(const Ctx& actx, const Field& field, const Coeffs& coeffs, const V
   dr.down(out.residual.data(), rows * sizeof(Scalar));
 }
 
+/// assemble<Scalar> returning the system by value (fem.hpp:204-210).
+template <class Scalar, class Ctx, class Field, class Coeffs, class Samples>
+AssembledSystem<Scalar> assemble(const Ctx& actx, const Field& field, const Coeffs& coeffs,
+                                 const std::vector<Scalar>& u, const Samples& samples) {
+  AssembledSystem<Scalar> out;
+  assemble<Scalar>(actx, field, coeffs, u, samples, out);
+  return out;
+}
+
 /// apply_dirichlet (fem.hpp:218-243) on a system assembled on `mesh`.
 template <class System, class Mesh, class Bc, class Vector>
 void apply_dirichlet(System& system, const Mesh& mesh, const Bc& bc, const Vector& u) {
@@ -358,14 +415,6 @@ void apply_dirichlet(System& system, const Mesh& mesh, const Bc& bc, const Vecto
 }
 
 // ------------------------------------------------------------------------ CG
-/// Same fields as enprop::SolveResult<Scalar> (pcg.hpp:33-38).
-template <class Scalar>
-struct SolveResult {
-  std::vector<Scalar> solution;
-  int iterations = 0;
-  std::vector<double> residual_history;
-};
-
 /// pcg_solve (pcg.hpp:52-103) with the identity preconditioner (pcg.hpp:40-45):
 /// coupled ensemble CG = pcg_solve<Ensemble<S>>; at S = 1, pcg_solve<double>.
 /// Config is an enprop::SolverConfig (tol, max_iterations).
@@ -439,6 +488,61 @@ UncoupledResult<detail::scalar_of<Vector>> pcg_solve_uncoupled(const Matrix& a, 
   r.residual_history.resize(s);
   for (int e = 0; e < s; ++e)
     for (int it = 0; it < hlen[e]; ++it) r.residual_history[e].push_back(hist[static_cast<size_t>(it) * s + e]);
+  return r;
+}
+
+// ------------------------------------------------------------------ Newton
+/// newton_solve (fem.hpp:265-302) on the device-resident problem
+/// (enprop_problem_newton): from u = 0, assemble residual + Jacobian at u,
+/// impose Dirichlet, stop when the coupled residual norm falls below
+/// options.tol times the first, else solve J du = -f by CG (options.linear)
+/// and u = 1.0*du + 1.0*u. Mesh is an enprop::StructuredMesh, Options an
+/// enprop::NewtonOptions (tol, max_iterations, linear; its multigrid block is
+/// not used: the linear solves are identity-preconditioned, so
+/// total_cg_iterations differ from the reference's MG-preconditioned count,
+/// while the iterate, the step count and the norms follow the same recursion).
+/// The Jacobian solves run in the coupled ensemble CG of pcg_solve<Scalar>.
+/// Throws SolverError with the residual norms after max_iterations steps.
+template <class Scalar, class Mesh, class Field, class Coeffs, class Bc, class Options>
+NewtonResult<Scalar> newton_solve(const Mesh& mesh, const Field& field, const Coeffs& coeffs,
+                                  const std::vector<Scalar>& samples, const Bc& bc,
+                                  const Options& options) {
+  constexpr int s = detail::width<Scalar>();
+  if (static_cast<int>(samples.size()) != field.num_terms())
+    throw std::invalid_argument("newton_solve: sample vector length mismatch");
+  auto& rt = detail::Runtime::get();
+  enprop_problem_desc d{};
+  d.cells_per_axis = mesh.cells_per_axis();
+  d.ensemble_size = s;
+  d.kl = detail::kl_of(field);
+  d.coeffs = detail::coeffs_of(coeffs);
+  d.bc = enprop_dirichlet_bc{bc.x0_value, bc.x1_value};
+  enprop_problem* p = nullptr;
+  detail::check(enprop_problem_create(rt.ctx, &d, &p), "newton_solve");
+  std::unique_ptr<enprop_problem, int (*)(enprop_problem*)> guard(p, enprop_problem_destroy);
+  detail::Buf dy(samples.data(), samples.size() * sizeof(Scalar));
+  enprop_newton_options o{};
+  o.tol = options.tol;
+  o.max_iterations = options.max_iterations;
+  o.linear = enprop_cg_options{ENPROP_CG_COUPLED, static_cast<int>(dot_order()), 0, options.linear.tol,
+                               options.linear.max_iterations, 16};
+  int steps = 0, cg_total = 0, nn = 0;
+  std::vector<double> norms(static_cast<size_t>(options.max_iterations > 0 ? options.max_iterations : 0) + 1);
+  const int rc = enprop_problem_newton(p, dy.as<double>(), &o, &steps, &cg_total, norms.data(), &nn);
+  norms.resize(nn);
+  if (rc == ENPROP_ERR_NO_CONVERGENCE || rc == ENPROP_ERR_INDEFINITE)
+    throw ENPROP_B200_SOLVER_ERROR(enprop_last_error(), std::move(norms));
+  detail::check(rc, "newton_solve");
+  NewtonResult<Scalar> r;
+  int rows = 0;
+  double* x = nullptr;
+  detail::check(enprop_problem_views(p, &rows, nullptr, nullptr, nullptr, nullptr, nullptr, &x), "newton_solve");
+  r.solution.resize(rows);
+  detail::check(enprop_memcpy_d2h(rt.ctx, r.solution.data(), x, static_cast<size_t>(rows) * sizeof(Scalar)),
+                "newton_solve");
+  r.iterations = steps;
+  r.total_cg_iterations = cg_total;
+  r.residual_norms = std::move(norms);
   return r;
 }
 

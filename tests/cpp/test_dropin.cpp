@@ -169,6 +169,87 @@ static void uncoupled_is_per_sample_scalar(int n) {
   }
 }
 
+// value-returning assemble (fem.hpp:204-210), the reference's result types
+// through the drop-in, and draw_samples / pack_sample_group (samples.cpp:7-18)
+template <int S>
+static void value_forms_and_samples(int n) {
+  StructuredMesh mesh(n);
+  AssemblyContext ctx(mesh);
+  KlField field(3, 1.0, 0.1, 1.0);
+  const auto pool = draw_samples(0, 3 * S, 3);
+  const auto pool2 = enprop_b200::draw_samples(0, 3 * S, 3);
+  CHECK(pool == pool2);
+  const auto y = pack_sample_group<S>(pool, S);
+  const auto y2 = enprop_b200::pack_sample_group<Ensemble<S>>(pool2, S);
+  CHECK(same_bits(y, y2));
+  DenseVector<Ensemble<S>> u0(mesh.num_nodes(), Ensemble<S>(0.0));
+  AssembledSystem<Ensemble<S>> a =
+      enprop::assemble<Ensemble<S>>(ctx, field, PdeCoefficients{}, u0, std::span<const Ensemble<S>>(y));
+  AssembledSystem<Ensemble<S>> b =
+      enprop_b200::assemble<Ensemble<S>>(ctx, field, PdeCoefficients{}, u0, std::span<const Ensemble<S>>(y2));
+  CHECK(same_bits(a.matrix.values, b.matrix.values) && same_bits(a.residual, b.residual));
+  enprop::apply_dirichlet(a, mesh, DirichletBc{}, u0);
+  DenseVector<Ensemble<S>> rhs(a.residual.size());
+  for (size_t i = 0; i < rhs.size(); ++i) rhs[i] = -a.residual[i];
+  SolverConfig cfg;
+  cfg.tol = 1e-7;
+  enprop::SolveResult<Ensemble<S>> r1 = enprop::pcg_solve(a.matrix, rhs, IdentityPreconditioner{}, cfg);
+  enprop::SolveResult<Ensemble<S>> r2 = enprop_b200::pcg_solve(a.matrix, rhs, IdentityPreconditioner{}, cfg);
+  CHECK(r1.iterations == r2.iterations && same_bits(r1.solution, r2.solution));
+  bool inval = false;
+  try {
+    enprop_b200::pack_sample_group<Ensemble<S>>(pool2, 3 * S);
+  } catch (const std::invalid_argument&) {
+    inval = true;
+  }
+  CHECK(inval);
+}
+
+// newton_solve (fem.hpp:265-302) through the drop-in against the same loop
+// composed from the reference's own pieces with IdentityPreconditioner (the
+// drop-in's linear solves are identity-preconditioned)
+template <int S>
+static void newton(int n, double beta) {
+  StructuredMesh mesh(n);
+  AssemblyContext ctx(mesh);
+  KlField field(3, 1.0, 0.1, 1.0);
+  const PdeCoefficients coeffs{0.0, beta, {1.0, 0.0, 0.0}};
+  const auto y = pack_sample_group<S>(draw_samples(7, S, 3), 0);
+  NewtonOptions opt;
+  opt.tol = 1e-8;
+  opt.linear.tol = 1e-10;
+  // reference pieces, identity-preconditioned (fem.hpp:273-301 otherwise)
+  DenseVector<Ensemble<S>> u(mesh.num_nodes(), Ensemble<S>(0.0));
+  std::vector<double> norms;
+  int steps = 0, cg_total = 0;
+  double initial = 0.0;
+  AssembledSystem<Ensemble<S>> sys;
+  for (int step = 0;; ++step) {
+    enprop::assemble<Ensemble<S>>(ctx, field, coeffs, u, std::span<const Ensemble<S>>(y), sys);
+    enprop::apply_dirichlet(sys, mesh, DirichletBc{}, u);
+    const double norm = enprop::norm2(sys.residual);
+    norms.push_back(norm);
+    if (step == 0) {
+      initial = norm;
+      if (initial == 0.0) break;
+    } else if (norm < opt.tol * initial) {
+      steps = step;
+      break;
+    }
+    DenseVector<Ensemble<S>> rhs(sys.residual.size());
+    for (size_t i = 0; i < rhs.size(); ++i) rhs[i] = -sys.residual[i];
+    auto lin = enprop::pcg_solve(sys.matrix, rhs, IdentityPreconditioner{}, opt.linear);
+    cg_total += lin.iterations;
+    enprop::axpby(1.0, lin.solution, 1.0, u);
+  }
+  enprop::NewtonResult<Ensemble<S>> r =
+      enprop_b200::newton_solve(mesh, field, coeffs, y, DirichletBc{}, opt);
+  CHECK(r.iterations == steps);
+  CHECK(r.total_cg_iterations == cg_total);
+  CHECK(r.residual_norms == norms);
+  CHECK(same_bits(r.solution, u));
+}
+
 int main() {
   spmv_dot_axpby<1>();
   spmv_dot_axpby<2>();
@@ -189,6 +270,11 @@ int main() {
   assembly_and_cg<Ensemble<4>>(6);
   assembly_and_cg<Ensemble<32>>(5);
   uncoupled_is_per_sample_scalar<8>(7);
+  value_forms_and_samples<4>(5);
+  value_forms_and_samples<32>(4);
+  newton<4>(5, 0.0);
+  newton<4>(5, 0.7);
+  newton<1>(6, 0.7);
 
   // iteration exhaustion throws the reference's SolverError with the history
   // (test_pcg.cpp:164-179)
