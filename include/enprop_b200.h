@@ -281,6 +281,39 @@ int enprop_problem_newton(enprop_problem* p, const double* y, const enprop_newto
                           int* newton_iterations, int* total_cg_iterations,
                           double* residual_norms, int* num_norms);
 
+/* ------------------------------------------- multigrid preconditioner (f4) */
+/* MgOptions (multigrid.hpp:14-20); NULL options select the defaults
+ * {500, 2, 30.0, 1.1, 40}. */
+typedef struct {
+  int coarse_row_threshold;
+  int chebyshev_degree;
+  double eigenvalue_ratio;
+  double eigenvalue_boost;
+  int power_iterations;
+} enprop_mg_options;
+
+typedef struct enprop_mg enprop_mg;
+/* build_hierarchy (multigrid.hpp:362-396) of the ensemble operator values
+ * [nnz][s] (device CRS, full storage): aggregation, Galerkin products and
+ * power-iteration eigenvalue estimates on the host in the reference's order,
+ * the coarsest level's dense LU per component on the device (bitwise the
+ * reference's factors). The hierarchy owns copies of every level. */
+int enprop_mg_build(enprop_ctx* ctx, int s, int num_rows, const int* row_map, const int* col_entry,
+                    const double* values, const enprop_mg_options* opt, enprop_mg** out);
+int enprop_mg_destroy(enprop_mg* h);
+/* levels, rows per level (<= max_levels entries) and the smoothed levels'
+ * lambda_max estimates [num_levels-1][s] (each may be NULL) */
+int enprop_mg_describe(enprop_mg* h, int* num_levels, int* rows, int max_levels, double* lambda_max);
+/* one V-cycle (multigrid.hpp:402-425) on the finest level: x updated in place
+ * toward A x = b (device [rows][s]); MgPreconditioner = one V-cycle from x = 0 */
+int enprop_mg_vcycle(enprop_mg* h, const double* b, double* x);
+/* pcg_solve(A, b, MgPreconditioner(h), cfg) (pcg.hpp:52-103) from x0 = 0, in
+ * the reference's serial dot order: COUPLED = pcg_solve<Ensemble<s>>,
+ * UNCOUPLED = s x pcg_solve<double> (per-lane scalars; converged lanes frozen).
+ * Outputs as enprop_cg. */
+int enprop_mg_pcg(enprop_mg* h, const double* b, double* x, const enprop_cg_options* opt,
+                  int* iterations, int* lane_status, double* history, int* hist_len);
+
 /* ------------------------------------ multi-GPU: slab domain decomposition */
 /* The node planes z = k of the mesh are split over nranks like the
  * reference's partition (partition.cpp:31-72; lower ranks take the extra

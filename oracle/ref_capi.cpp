@@ -38,6 +38,7 @@
 #include "enprop/samples.hpp"
 #include "enprop/partition.hpp"
 #include "enprop/halo.hpp"
+#include "enprop/multigrid.hpp"
 
 using namespace enprop;
 
@@ -515,6 +516,96 @@ int ref_time_group(int s, int coupled, int n, int m, double mean, double sigma, 
       times[0] = std::chrono::duration<double>(t1 - t0).count();
       times[1] = std::chrono::duration<double>(t2 - t1).count();
       times[2] = ran;
+    });
+  });
+}
+
+// ---- multigrid (multigrid.hpp): the reference's own hierarchy, V-cycle and
+// MG-preconditioned pcg_solve, for the f4 parity tests. `scalar` with s == 1
+// uses the plain-double hierarchy (the per-sample path of bench.cpp:322-330).
+}  // extern "C"
+
+static MgOptions mg_options(int thr, int deg, double ratio, double boost, int pits) {
+  MgOptions o;
+  o.coarse_row_threshold = thr;
+  o.chebyshev_degree = deg;
+  o.eigenvalue_ratio = ratio;
+  o.eigenvalue_boost = boost;
+  o.power_iterations = pits;
+  return o;
+}
+
+template <typename F>
+static void with_scalar(int s, int scalar, F&& f) {
+  if (scalar && s == 1) f(double{});
+  else with_width(s, [&](auto w) { f(E<decltype(w)::value>{}); });
+}
+
+extern "C" {
+
+// levels, rows per level, lambda_max [levels-1][s]
+int ref_mg_describe(int s, int scalar, int rows, const int* row_map, const int* col_entry, const double* values,
+                    int thr, int deg, double ratio, double boost, int pits, int* num_levels, int* level_rows,
+                    int max_levels, double* lambda_max) {
+  return guarded([&] {
+    with_scalar(s, scalar, [&](auto tag) {
+      using T = decltype(tag);
+      auto a = make_matrix<T>(rows, rows, row_map, col_entry, values);
+      MgHierarchy<T> h = build_hierarchy(a, mg_options(thr, deg, ratio, boost, pits));
+      *num_levels = h.num_levels();
+      for (int k = 0; k < h.num_levels() && k < max_levels; ++k) {
+        level_rows[k] = h.levels[k].a.num_rows;
+        if (k + 1 < h.num_levels()) {
+          const T lm = h.levels[k].smoother.lambda_max;
+          std::memcpy(lambda_max + (size_t)k * s, &lm, sizeof(T));
+        }
+      }
+    });
+  });
+}
+
+// one V-cycle on level 0: x updated in place
+int ref_mg_vcycle(int s, int scalar, int rows, const int* row_map, const int* col_entry, const double* values,
+                  int thr, int deg, double ratio, double boost, int pits, const double* b, double* x) {
+  return guarded([&] {
+    with_scalar(s, scalar, [&](auto tag) {
+      using T = decltype(tag);
+      auto a = make_matrix<T>(rows, rows, row_map, col_entry, values);
+      MgHierarchy<T> h = build_hierarchy(a, mg_options(thr, deg, ratio, boost, pits));
+      auto bb = from_raw<T>(b, rows);
+      auto xx = from_raw<T>(x, rows);
+      vcycle(h, bb, xx);
+      to_raw(xx, x);
+    });
+  });
+}
+
+// pcg_solve(a, b, MgPreconditioner(h), cfg); history must hold maxit+1 doubles
+int ref_mg_pcg(int s, int scalar, int rows, const int* row_map, const int* col_entry, const double* values,
+               int thr, int deg, double ratio, double boost, int pits, const double* b, double tol, int maxit,
+               double* x, int* iterations, double* history, int* hist_len) {
+  *hist_len = 0;
+  *iterations = -1;
+  return guarded([&] {
+    with_scalar(s, scalar, [&](auto tag) {
+      using T = decltype(tag);
+      auto a = make_matrix<T>(rows, rows, row_map, col_entry, values);
+      MgHierarchy<T> h = build_hierarchy(a, mg_options(thr, deg, ratio, boost, pits));
+      auto bb = from_raw<T>(b, rows);
+      SolverConfig cfg;
+      cfg.tol = tol;
+      cfg.max_iterations = maxit;
+      try {
+        auto res = pcg_solve(a, bb, MgPreconditioner<T>(h), cfg);
+        to_raw(res.solution, x);
+        *iterations = res.iterations;
+        for (std::size_t i = 0; i < res.residual_history.size(); ++i) history[i] = res.residual_history[i];
+        *hist_len = (int)res.residual_history.size();
+      } catch (const SolverError& err) {
+        for (std::size_t i = 0; i < err.history().size(); ++i) history[i] = err.history()[i];
+        *hist_len = (int)err.history().size();
+        throw;
+      }
     });
   });
 }

@@ -82,6 +82,12 @@ class _NewtonOptions(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iterations", C.c_int), ("linear", _CgOptions)]
 
 
+class _MgOptions(C.Structure):
+    _fields_ = [("coarse_row_threshold", C.c_int), ("chebyshev_degree", C.c_int),
+                ("eigenvalue_ratio", C.c_double), ("eigenvalue_boost", C.c_double),
+                ("power_iterations", C.c_int)]
+
+
 class _ProblemDesc(C.Structure):
     _fields_ = [("cells_per_axis", C.c_int), ("ensemble_size", C.c_int), ("kl", _KlParams),
                 ("coeffs", _Coeffs), ("bc", _Bc)]
@@ -131,6 +137,20 @@ class SolverConfig:
     def _c(self):
         return _CgOptions(self.flavour, self.dot_mode, self.seg_rows, self.tol,
                           self.max_iterations, self.check_every)
+
+
+@dataclass
+class MgOptions:
+    """MgOptions (multigrid.hpp:14-20)."""
+    coarse_row_threshold: int = 500
+    chebyshev_degree: int = 2
+    eigenvalue_ratio: float = 30.0
+    eigenvalue_boost: float = 1.1
+    power_iterations: int = 40
+
+    def _c(self):
+        return _MgOptions(self.coarse_row_threshold, self.chebyshev_degree, self.eigenvalue_ratio,
+                          self.eigenvalue_boost, self.power_iterations)
 
 
 @dataclass
@@ -204,6 +224,11 @@ def lib() -> C.CDLL:
     L.enprop_problem_solve_host.argtypes = [_vp, _vp, _vp, C.POINTER(_CgOptions), _ip, _ip]
     L.enprop_nccl_unique_id.argtypes = [_vp, C.c_size_t]
     L.enprop_dist_create.argtypes = [_vp, C.POINTER(_ProblemDesc), C.c_int, C.c_int, _vp, C.POINTER(_vp)]
+    L.enprop_mg_build.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp, _vp, C.POINTER(_MgOptions), C.POINTER(_vp)]
+    L.enprop_mg_destroy.argtypes = [_vp]
+    L.enprop_mg_describe.argtypes = [_vp, _ip, _ip, C.c_int, _dp]
+    L.enprop_mg_vcycle.argtypes = [_vp, _vp, _vp]
+    L.enprop_mg_pcg.argtypes = [_vp, _vp, _vp, C.POINTER(_CgOptions), _ip, _ip, _dp, _ip]
     L.enprop_dist_create_ipc.argtypes = [_vp, C.POINTER(_ProblemDesc), C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]
     L.enprop_dist_destroy.argtypes = [_vp]
     L.enprop_dist_assemble.argtypes = [_vp, _vp]
@@ -483,6 +508,65 @@ def pcg_solve(ctx: Context, s: int, row_map, col_entry, values, b, config: Solve
     else:
         _check(rc, "pcg_solve")
     return SolveResult(x, iters, history, lstat)
+
+
+class MgHierarchy:
+    """build_hierarchy (multigrid.hpp:362-396) of an ensemble operator (device
+    CRS, full storage, values [nnz][s]); vcycle() is one V-cycle
+    (multigrid.hpp:402-425), pcg() is pcg_solve with MgPreconditioner in the
+    reference's serial dot order (coupled, or uncoupled per-lane)."""
+
+    def __init__(self, ctx: Context, s: int, row_map, col_entry, values, options: MgOptions = None):
+        self.ctx, self.s = ctx, s
+        self.rows = row_map.numel() - 1
+        opt = (options or MgOptions())._c()
+        h = _vp()
+        _check(lib().enprop_mg_build(ctx.h, s, self.rows, _ptr(row_map), _ptr(col_entry), _ptr(values),
+                                     C.byref(opt), C.byref(h)), "build_hierarchy")
+        self.h = h
+
+    def describe(self):
+        """(rows per level, lambda_max per smoothed level [levels-1][s])"""
+        nl = C.c_int()
+        rows = (C.c_int * 64)()
+        lm = (C.c_double * (64 * self.s))()
+        _check(lib().enprop_mg_describe(self.h, C.byref(nl), rows, 64, lm))
+        L = nl.value
+        return [rows[k] for k in range(L)], [[lm[k * self.s + e] for e in range(self.s)] for k in range(L - 1)]
+
+    def vcycle(self, b, x):
+        _need_cuda(b, torch.float64, "b")
+        _need_cuda(x, torch.float64, "x")
+        _check(lib().enprop_mg_vcycle(self.h, _ptr(b), _ptr(x)), "vcycle")
+        return x
+
+    def pcg(self, b, config: SolverConfig = None, raise_on_failure: bool = True) -> SolveResult:
+        cfg = config or SolverConfig()
+        _need_cuda(b, torch.float64, "b")
+        x = torch.empty((self.rows, self.s), dtype=torch.float64, device=b.device)
+        lanes = self.s if cfg.flavour == CG_UNCOUPLED else 1
+        it, ls, hl = ((C.c_int * lanes)() for _ in range(3))
+        hist = (C.c_double * ((cfg.max_iterations + 1) * lanes))()
+        opt = cfg._c()
+        rc = lib().enprop_mg_pcg(self.h, _ptr(b), _ptr(x), C.byref(opt), it, ls, hist, hl)
+        iters, history, lstat = _collect(cfg, self.s, it, ls, hist, hl)
+        if rc in (ERR_NO_CONVERGENCE, ERR_INDEFINITE):
+            if raise_on_failure:
+                raise SolverError(_err(), history, rc, iters)
+        else:
+            _check(rc, "pcg_solve")
+        return SolveResult(x, iters, history, lstat)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().enprop_mg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Problem:

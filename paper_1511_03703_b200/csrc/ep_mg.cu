@@ -1,0 +1,885 @@
+// Multigrid preconditioner: the reference's aggregation AMG
+// (proj/include/enprop/multigrid.hpp, src/multigrid.cpp) with its V-cycle and
+// Chebyshev smoother on the device, bitwise in the reference's operation order.
+//
+//  * Setup (build_hierarchy, multigrid.hpp:362-396) runs on the host, as in
+//    the reference: connection graph (:38-76), greedy root aggregation
+//    (multigrid.cpp:5-43), piecewise-constant P and R = P^T (:79-107),
+//    Galerkin coarse operator in the reference's accumulation order
+//    (:114-160), diagonal and power-iteration lambda_max per component
+//    (:170-206). This file is compiled with -ffp-contract=off on the host.
+//  * The coarsest operator is factored by dense LU with partial pivoting per
+//    component ON THE DEVICE (DenseLuSolver::factor, :297-317): one CTA per
+//    component, the reference's right-looking order (pivot = first maximum,
+//    full-row swaps, multiplier then trailing update), so the factors are the
+//    reference's bits. The reference's own host LU makes >= 64^3 infeasible
+//    (the Dirichlet rows stay singleton aggregates: >= 2(n+1)^2 coarse rows).
+//  * V-cycle (:402-425) on the device: Chebyshev (:232-260) with per-lane
+//    recurrence coefficients precomputed on the host in the reference's order,
+//    residual, restriction as an SpMV with R (bitwise launch_spmv), zero coarse
+//    guess, recursion, prolongation x += 1.0 * z[aggregate], post-smoothing.
+//    Coarse solve (:269-290): pivot swaps, forward substitution as a column
+//    sweep (each row still subtracts its terms in increasing column order),
+//    back substitution as one chain per component (its row order leaves no
+//    parallelism: row r's first term needs y[r+1]).
+//  * pcg_solve with MgPreconditioner (pcg.hpp:52-103): host-driven loop, the
+//    reference's serial dot order through the chain kernel (ep_chain.cu);
+//    coupled (one decision) or uncoupled (per-lane scalars, converged lanes
+//    frozen), matching s x pcg_solve<double> on extracted components.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "enprop_b200.h"
+#include "ep_common.cuh"
+#include "ep_internal.h"
+#include "ep_kernels.h"
+
+using namespace ep;
+using namespace ep_internal;
+
+namespace {
+
+// ============================================================== device kernels
+// Chebyshev first step (multigrid.hpp:244-246): r = b - tmp; p = (r / diag) / theta; x += p
+template <int S>
+__global__ void k_cheb_first(int64_t n, const double* __restrict__ b, const double* __restrict__ tmp,
+                             const double* __restrict__ diag, const double* __restrict__ theta,
+                             double* __restrict__ r, double* __restrict__ p, double* __restrict__ x) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n * S) return;
+  const int e = (int)(g % S);
+  const double rv = EP_DSUB(b[g], tmp[g]);
+  const double pv = __ddiv_rn(__ddiv_rn(rv, diag[g]), theta[e]);
+  r[g] = rv;
+  p[g] = pv;
+  x[g] = EP_DADD(x[g], pv);
+}
+
+// Chebyshev step k (:248-257): r -= tmp; p = pc*p + zc*(r / diag); x += p
+template <int S>
+__global__ void k_cheb_next(int64_t n, const double* __restrict__ tmp, const double* __restrict__ diag,
+                            const double* __restrict__ pc, const double* __restrict__ zc,
+                            double* __restrict__ r, double* __restrict__ p, double* __restrict__ x) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n * S) return;
+  const int e = (int)(g % S);
+  const double rv = EP_DSUB(r[g], tmp[g]);
+  const double pv = EP_DADD(EP_DMUL(pc[e], p[g]), EP_DMUL(zc[e], __ddiv_rn(rv, diag[g])));
+  r[g] = rv;
+  p[g] = pv;
+  x[g] = EP_DADD(x[g], pv);
+}
+
+// V-cycle residual (:411-412): tmp = b - tmp
+template <int S>
+__global__ void k_sub_from(int64_t n, const double* __restrict__ b, double* __restrict__ tmp) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < n * S) tmp[g] = EP_DSUB(b[g], tmp[g]);
+}
+
+// prolongation (:418-420): x[row] += P.values[k] * z[P.col[k]] with one entry 1.0 per row
+template <int S>
+__global__ void k_prolong(int64_t n, const int* __restrict__ agg, const double* __restrict__ z,
+                          double* __restrict__ x) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n * S) return;
+  const int64_t row = g / S;
+  const int e = (int)(g - row * S);
+  x[g] = EP_DADD(x[g], EP_DMUL(1.0, z[(int64_t)agg[row] * S + e]));
+}
+
+// masked axpby for the MG-PCG loop: y = a*x + 1.0*y on active lanes (pcg.hpp:94-95)
+template <int S>
+__global__ void k_axpy_masked(int64_t n, const double* __restrict__ a, const int* __restrict__ act,
+                              const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n * S) return;
+  const int e = (int)(g % S);
+  if (act[e]) y[g] = EP_DADD(EP_DMUL(a[e], x[g]), EP_DMUL(1.0, y[g]));
+}
+
+// p = 1.0*z + beta*p on active lanes (pcg.hpp:101)
+template <int S>
+__global__ void k_direction_masked(int64_t n, const double* __restrict__ beta, const int* __restrict__ act,
+                                   const double* __restrict__ z, double* __restrict__ p) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n * S) return;
+  const int e = (int)(g % S);
+  if (act[e]) p[g] = EP_DADD(EP_DMUL(1.0, z[g]), EP_DMUL(beta[e], p[g]));
+}
+
+// Dense LU with partial pivoting of one component per CTA (DenseLuSolver::factor,
+// multigrid.hpp:297-317): lu is [s][n][n] row-major, piv [s][n]. Pivot row = the
+// first row with the largest |lu[row][k]| (strict '>' in row order).
+constexpr int kLuThreads = 1024;
+
+__global__ void __launch_bounds__(kLuThreads) k_lu_factor(int n, double* __restrict__ lu_all,
+                                                           int* __restrict__ piv_all, int* __restrict__ singular) {
+  double* lu = lu_all + (size_t)blockIdx.x * n * n;
+  int* piv = piv_all + (size_t)blockIdx.x * n;
+  __shared__ double s_best[kLuThreads / 32];
+  __shared__ int s_row[kLuThreads / 32];
+  __shared__ int s_pivot;
+  __shared__ double s_inv;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int k = 0; k < n; ++k) {
+    // argmax over rows >= k, first index on ties
+    double best = -1.0;
+    int brow = n;
+    for (int row = k + tid; row < n; row += kLuThreads) {
+      const double c = fabs(lu[(size_t)row * n + k]);
+      if (c > best) {
+        best = c;
+        brow = row;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const double ob = __shfl_down_sync(0xffffffffu, best, o);
+      const int orow = __shfl_down_sync(0xffffffffu, brow, o);
+      if (ob > best || (ob == best && orow < brow)) {
+        best = ob;
+        brow = orow;
+      }
+    }
+    if (lane == 0) {
+      s_best[warp] = best;
+      s_row[warp] = brow;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double b = s_best[0];
+      int r = s_row[0];
+      for (int w = 1; w < kLuThreads / 32; ++w)
+        if (s_best[w] > b || (s_best[w] == b && s_row[w] < r)) {
+          b = s_best[w];
+          r = s_row[w];
+        }
+      if (b == 0.0) atomicExch(singular, 1);
+      s_pivot = r < n ? r : k;
+      piv[k] = s_pivot;
+    }
+    __syncthreads();
+    const int pr = s_pivot;
+    if (pr != k)
+      for (int col = tid; col < n; col += kLuThreads) {
+        const double t = lu[(size_t)k * n + col];
+        lu[(size_t)k * n + col] = lu[(size_t)pr * n + col];
+        lu[(size_t)pr * n + col] = t;
+      }
+    __syncthreads();
+    if (tid == 0) s_inv = __ddiv_rn(1.0, lu[(size_t)k * n + k]);
+    __syncthreads();
+    const double inv = s_inv;
+    // multipliers, then the trailing update row by row (each element's
+    // operations are the reference's: lu[row][col] -= mult * lu[k][col])
+    const int rows = n - k - 1;
+    for (int i = tid; i < rows; i += kLuThreads) {
+      const int row = k + 1 + i;
+      lu[(size_t)row * n + k] = EP_DMUL(lu[(size_t)row * n + k], inv);
+    }
+    __syncthreads();
+    const int cols = n - k - 1;
+    const int64_t work = (int64_t)rows * cols;
+    for (int64_t t = tid; t < work; t += kLuThreads) {
+      const int row = k + 1 + (int)(t / cols), col = k + 1 + (int)(t % cols);
+      const double mult = lu[(size_t)row * n + k];
+      lu[(size_t)row * n + col] = EP_DSUB(lu[(size_t)row * n + col], EP_DMUL(mult, lu[(size_t)k * n + col]));
+    }
+    __syncthreads();
+  }
+}
+
+// DenseLuSolver::solve (multigrid.hpp:269-290) of one component per CTA:
+// x[row][e] from b[row][e] (ensemble layout), lu [s][n][n], luT [s][n][n]
+// (column-major copy for the forward sweep), piv [s][n]; y in shared memory.
+template <int S>
+__global__ void __launch_bounds__(kLuThreads) k_lu_solve(int n, const double* __restrict__ lu_all,
+                                                         const double* __restrict__ luT_all,
+                                                         const int* __restrict__ piv_all,
+                                                         const double* __restrict__ b, double* __restrict__ x) {
+  extern __shared__ double y[];
+  const int e = blockIdx.x;
+  const double* lu = lu_all + (size_t)e * n * n;
+  const double* luT = luT_all + (size_t)e * n * n;
+  const int* piv = piv_all + (size_t)e * n;
+  const int tid = threadIdx.x;
+  for (int row = tid; row < n; row += kLuThreads) y[row] = b[(size_t)row * S + e];
+  __syncthreads();
+  if (tid == 0)  // row swaps in order k = 0..n-1 (:276-277)
+    for (int k = 0; k < n; ++k)
+      if (piv[k] != k) {
+        const double t = y[k];
+        y[k] = y[piv[k]];
+        y[piv[k]] = t;
+      }
+  __syncthreads();
+  // forward (:278-282): acc = y[row]; acc -= lu[row][col]*y[col], col ascending;
+  // as a column sweep every row still applies its columns in ascending order
+  for (int col = 0; col + 1 < n; ++col) {
+    const double yc = y[col];
+    for (int row = col + 1 + tid; row < n; row += kLuThreads)
+      y[row] = EP_DSUB(y[row], EP_DMUL(luT[(size_t)col * n + row], yc));
+    __syncthreads();
+  }
+  // backward (:283-287): acc = y[row]; acc -= lu[row][col]*y[col] for col =
+  // row+1..n-1; y[row] = acc / lu[row][row]. Row r's first term needs y[r+1],
+  // so the rows run one after another: warp 0 forms 32 products at a time
+  // into shared memory and lane 0 subtracts them in column order.
+  __shared__ double pbuf[32];
+  if (tid < 32) {
+    const int lane = tid;
+    for (int row = n - 1; row >= 0; --row) {
+      const double* lr = lu + (size_t)row * n;
+      double acc = y[row];
+      for (int col = row + 1; col < n; col += 32) {
+        const int c = col + lane;
+        pbuf[lane] = c < n ? EP_DMUL(lr[c], y[c]) : 0.0;
+        __syncwarp();
+        if (lane == 0) {
+          if (n - col >= 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc = EP_DSUB(acc, pbuf[j]);
+          } else {
+            for (int j = 0; j < n - col; ++j) acc = EP_DSUB(acc, pbuf[j]);
+          }
+        }
+        __syncwarp();
+      }
+      if (lane == 0) y[row] = __ddiv_rn(acc, lr[row]);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int row = tid; row < n; row += kLuThreads) x[(size_t)row * S + e] = y[row];
+}
+
+__global__ void k_transpose_sq(int n, const double* __restrict__ a, double* __restrict__ t) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nn = (int64_t)n * n;
+  if (g >= nn * gridDim.y) return;
+  const int64_t c = blockIdx.y;
+  const int64_t i = g / n, j = g % n;
+  if (g < nn) t[c * nn + j * n + i] = a[c * nn + i * n + j];
+}
+
+inline int blocks_for(int64_t work) { return (int)((work + 255) / 256); }
+
+#define EP_MG_DISPATCH(s, KER, grid, block, smem, st, ...) \
+  switch (s) {                                               \
+    case 1: KER<1><<<grid, block, smem, st>>>(__VA_ARGS__); break;   \
+    case 2: KER<2><<<grid, block, smem, st>>>(__VA_ARGS__); break;   \
+    case 4: KER<4><<<grid, block, smem, st>>>(__VA_ARGS__); break;   \
+    case 8: KER<8><<<grid, block, smem, st>>>(__VA_ARGS__); break;   \
+    case 16: KER<16><<<grid, block, smem, st>>>(__VA_ARGS__); break; \
+    case 32: KER<32><<<grid, block, smem, st>>>(__VA_ARGS__); break; \
+    default: break;                                          \
+  }
+
+// ================================================================= host setup
+struct HostCrs {
+  int rows = 0, cols = 0;
+  std::vector<int> rm, ce;
+  std::vector<double> v;  // [nnz][s]
+};
+
+int find_entry(const HostCrs& a, int row, int col) {
+  const auto b = a.ce.begin() + a.rm[row], e = a.ce.begin() + a.rm[row + 1];
+  const auto it = std::lower_bound(b, e, col);
+  return (it == e || *it != col) ? -1 : (int)(it - a.ce.begin());
+}
+
+// connection_graph (multigrid.hpp:38-76)
+void connection_graph(const HostCrs& a, int s, std::vector<int>& grm, std::vector<int>& gce) {
+  std::vector<char> keep(a.ce.size(), 0);
+  for (int row = 0; row < a.rows; ++row)
+    for (int k = a.rm[row]; k < a.rm[row + 1]; ++k) {
+      if (keep[k]) continue;
+      bool nonzero = false;
+      for (int e = 0; e < s && !nonzero; ++e) nonzero = a.v[(size_t)k * s + e] != 0.0;
+      if (!nonzero) continue;
+      keep[k] = 1;
+      const int col = a.ce[k];
+      if (col == row || col >= a.rows) continue;
+      const int t = find_entry(a, col, row);
+      if (t >= 0) keep[t] = 1;
+    }
+  grm.assign(a.rows + 1, 0);
+  for (int row = 0; row < a.rows; ++row) {
+    int c = 0;
+    for (int k = a.rm[row]; k < a.rm[row + 1]; ++k) c += keep[k];
+    grm[row + 1] = grm[row] + c;
+  }
+  gce.clear();
+  gce.reserve(grm.back());
+  for (int row = 0; row < a.rows; ++row)
+    for (int k = a.rm[row]; k < a.rm[row + 1]; ++k)
+      if (keep[k]) gce.push_back(a.ce[k]);
+}
+
+// aggregate_graph (src/multigrid.cpp:5-43)
+int aggregate_graph(int rows, const std::vector<int>& grm, const std::vector<int>& gce, std::vector<int>& agg) {
+  agg.assign(rows, -1);
+  int next_id = 0;
+  for (int row = 0; row < rows; ++row) {
+    if (agg[row] != -1) continue;
+    bool absorbed_any = false;
+    int smallest = -1;
+    for (int k = grm[row]; k < grm[row + 1]; ++k) {
+      const int col = gce[k];
+      if (col == row) continue;
+      if (agg[col] == -1) {
+        if (!absorbed_any) {
+          absorbed_any = true;
+          agg[row] = next_id;
+        }
+        agg[col] = next_id;
+      } else if (smallest == -1 || agg[col] < smallest) {
+        smallest = agg[col];
+      }
+    }
+    if (absorbed_any) ++next_id;
+    else if (smallest != -1) agg[row] = smallest;
+    else agg[row] = next_id++;
+  }
+  return next_id;
+}
+
+// galerkin_coarse (multigrid.hpp:114-160), per component in the reference's order
+HostCrs galerkin_coarse(const HostCrs& a, int s, const std::vector<int>& agg, int nc) {
+  std::vector<int> gmap(nc + 1, 0), grows(a.rows);
+  for (int i = 0; i < a.rows; ++i) ++gmap[agg[i] + 1];
+  for (int g = 0; g < nc; ++g) gmap[g + 1] += gmap[g];
+  {
+    std::vector<int> at(gmap.begin(), gmap.end() - 1);
+    for (int i = 0; i < a.rows; ++i) grows[at[agg[i]]++] = i;
+  }
+  HostCrs c;
+  c.rows = c.cols = nc;
+  c.rm.assign(nc + 1, 0);
+  std::vector<double> accum((size_t)nc * s, 0.0);
+  std::vector<int> touched;
+  std::vector<char> seen(nc, 0);
+  for (int big = 0; big < nc; ++big) {
+    touched.clear();
+    for (int idx = gmap[big]; idx < gmap[big + 1]; ++idx) {
+      const int i = grows[idx];
+      for (int k = a.rm[i]; k < a.rm[i + 1]; ++k) {
+        const int cj = agg[a.ce[k]];
+        double* acc = &accum[(size_t)cj * s];
+        const double* v = &a.v[(size_t)k * s];
+        if (!seen[cj]) {
+          seen[cj] = 1;
+          touched.push_back(cj);
+          for (int e = 0; e < s; ++e) acc[e] = v[e];
+        } else {
+          for (int e = 0; e < s; ++e) acc[e] += v[e];
+        }
+      }
+    }
+    std::sort(touched.begin(), touched.end());
+    for (int cj : touched) {
+      c.ce.push_back(cj);
+      for (int e = 0; e < s; ++e) c.v.push_back(accum[(size_t)cj * s + e]);
+      seen[cj] = 0;
+    }
+    c.rm[big + 1] = (int)c.ce.size();
+  }
+  return c;
+}
+
+// diagonal_of (crs.hpp:124-132)
+std::vector<double> diagonal_of(const HostCrs& a, int s) {
+  std::vector<double> d((size_t)a.rows * s, 0.0);
+  for (int row = 0; row < a.rows; ++row) {
+    const int k = find_entry(a, row, row);
+    if (k >= 0)
+      for (int e = 0; e < s; ++e) d[(size_t)row * s + e] = a.v[(size_t)k * s + e];
+  }
+  return d;
+}
+
+// spmv (kernels.hpp:15-26) on the host: sum = 0; sum += a_k * x_col in entry order
+void host_spmv(const HostCrs& a, int s, const std::vector<double>& x, std::vector<double>& z) {
+  z.assign((size_t)a.rows * s, 0.0);
+  for (int row = 0; row < a.rows; ++row)
+    for (int e = 0; e < s; ++e) {
+      double sum = 0.0;
+      for (int k = a.rm[row]; k < a.rm[row + 1]; ++k) sum += a.v[(size_t)k * s + e] * x[(size_t)a.ce[k] * s + e];
+      z[(size_t)row * s + e] = sum;
+    }
+}
+
+// power_lambda_max (multigrid.hpp:170-206), per component; status 1 zero
+// diagonal, 2 collapsed iteration (the reference's domain_error)
+int power_lambda_max(const HostCrs& a, int s, const std::vector<double>& diag, int iterations,
+                     std::vector<double>& lmax) {
+  lmax.assign(s, 1.0);
+  for (double d : diag)
+    if (d == 0.0) return 1;
+  std::vector<double> v((size_t)a.rows * s, 1.0), w;
+  for (int it = 0; it < iterations; ++it) {
+    host_spmv(a, s, v, w);
+    for (size_t i = 0; i < w.size(); ++i) w[i] /= diag[i];
+    if (it + 1 == iterations) {
+      for (int e = 0; e < s; ++e) {
+        double num = 0.0, den = 0.0;
+        for (int row = 0; row < a.rows; ++row) {
+          num += v[(size_t)row * s + e] * w[(size_t)row * s + e];
+          den += v[(size_t)row * s + e] * v[(size_t)row * s + e];
+        }
+        lmax[e] = num / den;
+      }
+      return 0;
+    }
+    std::vector<double> scale(s, 0.0);
+    for (int row = 0; row < a.rows; ++row)
+      for (int e = 0; e < s; ++e) {
+        const double aw = std::fabs(w[(size_t)row * s + e]);
+        scale[e] = scale[e] > aw ? scale[e] : aw;  // Ensemble max (ensemble.hpp:221-226)
+      }
+    for (int e = 0; e < s; ++e)
+      if (scale[e] == 0.0) return 2;
+    for (int row = 0; row < a.rows; ++row)
+      for (int e = 0; e < s; ++e) v[(size_t)row * s + e] = w[(size_t)row * s + e] / scale[e];
+  }
+  return 0;
+}
+
+struct LevelDev {
+  int rows = 0, coarse_rows = 0;
+  int64_t nnz = 0, rnnz = 0;
+  int *rm = nullptr, *ce = nullptr, *rrm = nullptr, *rce = nullptr, *agg = nullptr;
+  double *vals = nullptr, *rvals = nullptr, *diag = nullptr;
+  double* cheb = nullptr;  // [theta | pc_2 | zc_2 | pc_3 | zc_3 ...] x s
+  double *b = nullptr, *x = nullptr, *r = nullptr, *p = nullptr, *tmp = nullptr;
+  std::vector<double> lmax;
+};
+
+}  // namespace
+
+struct enprop_mg {
+  enprop_ctx* ctx = nullptr;
+  int s = 0;
+  enprop_mg_options opt{};
+  std::vector<LevelDev> lv;  // lv.back() is the coarsest (dense LU)
+  int coarse_n = 0;
+  double *lu = nullptr, *luT = nullptr;
+  int* piv = nullptr;
+  // PCG workspace (level-0 sized)
+  double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr, *coef = nullptr, *lanes = nullptr;
+  int* act = nullptr;
+  CgState* fin_state = nullptr;
+};
+
+namespace {
+
+void free_level(LevelDev& l) {
+  for (void* q : {(void*)l.rm, (void*)l.ce, (void*)l.rrm, (void*)l.rce, (void*)l.agg, (void*)l.vals,
+                  (void*)l.rvals, (void*)l.diag, (void*)l.cheb, (void*)l.b, (void*)l.x, (void*)l.r,
+                  (void*)l.p, (void*)l.tmp})
+    if (q) cudaFree(q);
+  l = LevelDev{};
+}
+
+template <class T>
+int upload(T** dst, const std::vector<T>& src) {
+  EP_CUDA(cudaMalloc(dst, std::max<size_t>(src.size(), 1) * sizeof(T)));
+  if (!src.empty()) EP_CUDA(cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return ENPROP_OK;
+}
+
+// Chebyshev recurrence scalars per lane (multigrid.hpp:236-256), in the
+// reference's Ensemble operation order
+std::vector<double> cheb_coeffs(const std::vector<double>& lmax, int s, const enprop_mg_options& o) {
+  const int deg = o.chebyshev_degree;
+  std::vector<double> out((size_t)(1 + 2 * std::max(deg - 1, 0)) * s);
+  for (int e = 0; e < s; ++e) {
+    const double top = lmax[e] * o.eigenvalue_boost;
+    const double bottom = lmax[e] / o.eigenvalue_ratio;
+    const double theta = (top + bottom) * 0.5;
+    const double delta = (top - bottom) * 0.5;
+    const double sigma = theta / delta;
+    double rho = 1.0 / sigma;
+    out[e] = theta;
+    for (int k = 2; k <= deg; ++k) {
+      const double rho_next = 1.0 / (2.0 * sigma - rho);
+      out[(size_t)(1 + 2 * (k - 2)) * s + e] = rho_next * rho;
+      out[(size_t)(2 + 2 * (k - 2)) * s + e] = 2.0 * rho_next / delta;
+      rho = rho_next;
+    }
+  }
+  return out;
+}
+
+cudaError_t spmv_level(enprop_mg* h, int s, int rows, int cols, const int* rm, const int* ce,
+                       const double* v, const double* x, double* z) {
+  h->ctx->launches += 1;
+  if (s <= spmv_small_max()) return launch_spmv_small(s, rows, rm, ce, v, x, z, h->ctx->stream);
+  return launch_spmv(s, rows, rm, ce, v, x, z, false, h->ctx->stream);
+}
+
+int chebyshev(enprop_mg* h, LevelDev& l, const double* b, double* x) {
+  const int s = h->s;
+  cudaStream_t st = h->ctx->stream;
+  const int64_t n = l.rows;
+  EP_CUDA(spmv_level(h, s, l.rows, l.rows, l.rm, l.ce, l.vals, x, l.tmp));
+  EP_MG_DISPATCH(s, k_cheb_first, blocks_for(n * s), 256, 0, st, n, b, l.tmp, l.diag, l.cheb, l.r, l.p, x);
+  h->ctx->launches += 1;
+  for (int k = 2; k <= h->opt.chebyshev_degree; ++k) {
+    EP_CUDA(spmv_level(h, s, l.rows, l.rows, l.rm, l.ce, l.vals, l.p, l.tmp));
+    const double* pc = l.cheb + (size_t)(1 + 2 * (k - 2)) * s;
+    const double* zc = l.cheb + (size_t)(2 + 2 * (k - 2)) * s;
+    EP_MG_DISPATCH(s, k_cheb_next, blocks_for(n * s), 256, 0, st, n, l.tmp, l.diag, pc, zc, l.r, l.p, x);
+    h->ctx->launches += 1;
+  }
+  return cudaGetLastError() == cudaSuccess ? ENPROP_OK : cuda_fail(cudaGetLastError(), "chebyshev");
+}
+
+int coarse_solve(enprop_mg* h, const double* b, double* x) {
+  const int n = h->coarse_n, s = h->s;
+  const size_t smem = (size_t)n * sizeof(double);
+  EP_MG_DISPATCH(s, k_lu_solve, s, kLuThreads, smem, h->ctx->stream, n, h->lu, h->luT, h->piv, b, x);
+  h->ctx->launches += 1;
+  EP_CUDA(cudaGetLastError());
+  return ENPROP_OK;
+}
+
+// vcycle (multigrid.hpp:402-425) on level k: b, x device vectors of that level
+int vcycle(enprop_mg* h, int k, const double* b, double* x) {
+  if (k + 1 == (int)h->lv.size()) return coarse_solve(h, b, x);
+  LevelDev& l = h->lv[k];
+  LevelDev& c = h->lv[k + 1];
+  const int s = h->s;
+  cudaStream_t st = h->ctx->stream;
+  int rc = chebyshev(h, l, b, x);
+  if (rc) return rc;
+  EP_CUDA(spmv_level(h, s, l.rows, l.rows, l.rm, l.ce, l.vals, x, l.tmp));
+  EP_MG_DISPATCH(s, k_sub_from, blocks_for((int64_t)l.rows * s), 256, 0, st, (int64_t)l.rows, b, l.tmp);
+  EP_CUDA(spmv_level(h, s, l.coarse_rows, l.rows, l.rrm, l.rce, l.rvals, l.tmp, c.b));  // rc = R tmp
+  EP_CUDA(cudaMemsetAsync(c.x, 0, (size_t)c.rows * s * sizeof(double), st));        // z = 0
+  h->ctx->launches += 1;
+  if ((rc = vcycle(h, k + 1, c.b, c.x))) return rc;
+  EP_MG_DISPATCH(s, k_prolong, blocks_for((int64_t)l.rows * s), 256, 0, st, (int64_t)l.rows, l.agg, c.x, x);
+  h->ctx->launches += 1;
+  EP_CUDA(cudaGetLastError());
+  return chebyshev(h, l, b, x);
+}
+
+}  // namespace
+
+extern "C" {
+
+int enprop_mg_destroy(enprop_mg* h) {
+  if (!h) return ENPROP_OK;
+  if (h->ctx) cudaStreamSynchronize(h->ctx->stream);
+  for (auto& l : h->lv) free_level(l);
+  for (void* q : {(void*)h->lu, (void*)h->luT, (void*)h->piv, (void*)h->r, (void*)h->z, (void*)h->p,
+                  (void*)h->q, (void*)h->coef, (void*)h->lanes, (void*)h->act, (void*)h->fin_state})
+    if (q) cudaFree(q);
+  delete h;
+  return ENPROP_OK;
+}
+
+int enprop_mg_build(enprop_ctx* c, int s, int rows, const int* row_map, const int* col_entry,
+                    const double* values, const enprop_mg_options* opt, enprop_mg** out) {
+  ScopedLaunchOpts launch_scope(c);
+  if (!c || !out || !row_map || !col_entry || !values) return fail(ENPROP_ERR_INVALID, "build_hierarchy: null argument");
+  if (!valid_width(s)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
+  if (rows <= 0) return fail(ENPROP_ERR_INVALID, "build_hierarchy: empty matrix");
+  enprop_mg_options o{500, 2, 30.0, 1.1, 40};  // MgOptions defaults (multigrid.hpp:14-20)
+  if (opt) o = *opt;
+  if (o.chebyshev_degree < 1 || o.power_iterations < 0)
+    return fail(ENPROP_ERR_INVALID, "build_hierarchy: bad multigrid options");
+  auto* h = new (std::nothrow) enprop_mg();
+  if (!h) return fail(ENPROP_ERR_OOM, "out of host memory");
+  h->ctx = c;
+  h->s = s;
+  h->opt = o;
+  auto bail = [&](int rc) {
+    enprop_mg_destroy(h);
+    return rc;
+  };
+  // the fine operator to the host (setup is host-sequential, as in the reference)
+  HostCrs a;
+  a.rows = a.cols = rows;
+  a.rm.resize(rows + 1);
+  cudaStream_t st = c->stream;
+  if (cudaMemcpyAsync(a.rm.data(), row_map, (rows + 1) * sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return bail(cuda_fail(cudaGetLastError(), "build_hierarchy"));
+  const int64_t nnz = a.rm[rows];
+  a.ce.resize(nnz);
+  a.v.resize((size_t)nnz * s);
+  if (cudaMemcpyAsync(a.ce.data(), col_entry, nnz * sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(a.v.data(), values, (size_t)nnz * s * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return bail(cuda_fail(cudaGetLastError(), "build_hierarchy"));
+  int rc = ENPROP_OK;
+  // levels (multigrid.hpp:370-389)
+  while (a.rows >= o.coarse_row_threshold) {
+    std::vector<int> grm, gce, agg;
+    connection_graph(a, s, grm, gce);
+    const int nc = aggregate_graph(a.rows, grm, gce, agg);
+    if (nc >= a.rows) break;
+    LevelDev l;
+    l.rows = a.rows;
+    l.coarse_rows = nc;
+    l.nnz = (int64_t)a.ce.size();
+    const std::vector<double> diag = diagonal_of(a, s);
+    const int pst = power_lambda_max(a, s, diag, o.power_iterations, l.lmax);
+    if (pst == 1) return bail(fail(ENPROP_ERR_INVALID, "power_lambda_max: zero diagonal entry"));
+    if (pst == 2) return bail(fail(ENPROP_ERR_INVALID, "power_lambda_max: iteration collapsed to zero"));
+    for (double v : l.lmax)
+      if (v <= 0.0) return bail(fail(ENPROP_ERR_INVALID, "build_hierarchy: non-positive eigenvalue estimate"));
+    // R = P^T (transpose of the one-entry-per-row prolongator, :96-107): row
+    // I lists its fine rows ascending, values 1.0
+    std::vector<int> rrm(nc + 1, 0), rce(a.rows);
+    for (int i = 0; i < a.rows; ++i) ++rrm[agg[i] + 1];
+    for (int g = 0; g < nc; ++g) rrm[g + 1] += rrm[g];
+    {
+      std::vector<int> at(rrm.begin(), rrm.end() - 1);
+      for (int i = 0; i < a.rows; ++i) rce[at[agg[i]]++] = i;
+    }
+    std::vector<double> ones((size_t)a.rows * s, 1.0);
+    HostCrs coarse = galerkin_coarse(a, s, agg, nc);
+    const size_t vec = (size_t)a.rows * s * sizeof(double);
+    if ((rc = upload(&l.rm, a.rm)) || (rc = upload(&l.ce, a.ce)) || (rc = upload(&l.vals, a.v)) ||
+        (rc = upload(&l.rrm, rrm)) || (rc = upload(&l.rce, rce)) || (rc = upload(&l.rvals, ones)) ||
+        (rc = upload(&l.agg, agg)) || (rc = upload(&l.diag, diag)) ||
+        (rc = upload(&l.cheb, cheb_coeffs(l.lmax, s, o))))
+      return bail(rc);
+    for (double** vp : {&l.b, &l.x, &l.r, &l.p, &l.tmp})
+      if (cudaMalloc(vp, vec) != cudaSuccess) return bail(cuda_fail(cudaErrorMemoryAllocation, "build_hierarchy"));
+    h->lv.push_back(l);
+    a = std::move(coarse);
+  }
+  {  // the coarsest level: dense LU per component on the device (:387-389)
+    LevelDev l;
+    l.rows = a.rows;
+    l.nnz = (int64_t)a.ce.size();
+    const size_t vec = (size_t)a.rows * s * sizeof(double);
+    if ((rc = upload(&l.rm, a.rm)) || (rc = upload(&l.ce, a.ce)) || (rc = upload(&l.vals, a.v))) return bail(rc);
+    for (double** vp : {&l.b, &l.x})
+      if (cudaMalloc(vp, vec) != cudaSuccess) return bail(cuda_fail(cudaErrorMemoryAllocation, "build_hierarchy"));
+    h->lv.push_back(l);
+    const int n = a.rows;
+    h->coarse_n = n;
+    if ((size_t)n * sizeof(double) > 200 * 1024)
+      return bail(fail(ENPROP_ERR_INVALID, "build_hierarchy: coarse level too large for the device LU solve"));
+    std::vector<double> dense((size_t)s * n * n, 0.0);
+    for (int row = 0; row < n; ++row)
+      for (int k = a.rm[row]; k < a.rm[row + 1]; ++k)
+        for (int e = 0; e < s; ++e) dense[(size_t)e * n * n + (size_t)row * n + a.ce[k]] = a.v[(size_t)k * s + e];
+    int* singular = nullptr;
+    if ((rc = upload(&h->lu, dense))) return bail(rc);
+    if (cudaMalloc(&h->luT, dense.size() * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&h->piv, (size_t)s * n * sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&singular, sizeof(int)) != cudaSuccess)
+      return bail(cuda_fail(cudaErrorMemoryAllocation, "build_hierarchy"));
+    cudaMemsetAsync(singular, 0, sizeof(int), st);
+    k_lu_factor<<<s, kLuThreads, 0, st>>>(n, h->lu, h->piv, singular);
+    k_transpose_sq<<<dim3(blocks_for((int64_t)n * n), s), 256, 0, st>>>(n, h->lu, h->luT);
+    c->launches += 2;
+    int hs = 0;
+    cudaError_t err = cudaGetLastError();
+    if (err == cudaSuccess) err = cudaMemcpyAsync(&hs, singular, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    cudaFree(singular);
+    if (err != cudaSuccess) return bail(cuda_fail(err, "build_hierarchy: coarse LU"));
+    if (hs) return bail(fail(ENPROP_ERR_INVALID, "DenseLuSolver: singular matrix"));
+  }
+  const int n0 = h->lv[0].rows;
+  const size_t vec = (size_t)n0 * s * sizeof(double);
+  for (double** vp : {&h->r, &h->z, &h->p, &h->q})
+    if (cudaMalloc(vp, vec) != cudaSuccess) return bail(cuda_fail(cudaErrorMemoryAllocation, "build_hierarchy"));
+  if (cudaMalloc(&h->coef, 2 * kMaxS * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&h->lanes, (kMaxS + 1) * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&h->act, kMaxS * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&h->fin_state, sizeof(CgState)) != cudaSuccess)
+    return bail(cuda_fail(cudaErrorMemoryAllocation, "build_hierarchy"));
+  *out = h;
+  return ENPROP_OK;
+}
+
+int enprop_mg_describe(enprop_mg* h, int* num_levels, int* rows, int max_levels, double* lambda_max) {
+  if (!h) return fail(ENPROP_ERR_INVALID, "null hierarchy");
+  const int L = (int)h->lv.size();
+  if (num_levels) *num_levels = L;
+  for (int k = 0; k < L && k < max_levels; ++k) {
+    if (rows) rows[k] = h->lv[k].rows;
+    if (lambda_max && k + 1 < L)
+      for (int e = 0; e < h->s; ++e) lambda_max[(size_t)k * h->s + e] = h->lv[k].lmax[e];
+  }
+  return ENPROP_OK;
+}
+
+int enprop_mg_vcycle(enprop_mg* h, const double* b, double* x) {
+  if (!h || !b || !x) return fail(ENPROP_ERR_INVALID, "vcycle: null argument");
+  ScopedLaunchOpts launch_scope(h->ctx);
+  return vcycle(h, 0, b, x);
+}
+
+}  // extern "C"
+
+namespace {
+
+// serial-order dot (kernels.hpp:62-69) into host lanes[s] (+ coupled sum)
+int mg_dot(enprop_mg* h, const double* u, const double* v, std::vector<double>& lanes, double& coupled) {
+  const int s = h->s, rows = h->lv[0].rows;
+  if (!chain_aligned(u, v)) return fail(ENPROP_ERR_INVALID, "pcg_solve (multigrid): vectors must be 16-byte aligned");
+  FinArgs f{};
+  f.phase = kPhaseNone;
+  f.cg = h->fin_state;
+  f.lanes_out = h->lanes;
+  EP_CUDA(launch_chain(s, rows, u, v, u == v ? kChainSquare : kChainProduct, f, h->ctx->stream));
+  h->ctx->launches += 1;
+  std::vector<double> hbuf(s + 1);
+  EP_CUDA(cudaMemcpyAsync(hbuf.data(), h->lanes, (s + 1) * sizeof(double), cudaMemcpyDeviceToHost, h->ctx->stream));
+  EP_CUDA(cudaStreamSynchronize(h->ctx->stream));
+  lanes.assign(hbuf.begin(), hbuf.begin() + s);
+  coupled = hbuf[s];
+  return ENPROP_OK;
+}
+
+int precondition(enprop_mg* h, const double* r, double* z) {
+  EP_CUDA(cudaMemsetAsync(z, 0, (size_t)h->lv[0].rows * h->s * sizeof(double), h->ctx->stream));
+  return vcycle(h, 0, r, z);  // MgPreconditioner (multigrid.hpp:430-440)
+}
+
+}  // namespace
+
+extern "C" {
+
+int enprop_mg_pcg(enprop_mg* h, const double* b, double* x, const enprop_cg_options* opt, int* iterations,
+                  int* lane_status, double* history, int* hist_len) {
+  if (!h || !b || !x || !opt) return fail(ENPROP_ERR_INVALID, "pcg_solve: null argument");
+  ScopedLaunchOpts launch_scope(h->ctx);
+  if (opt->dot_mode != ENPROP_DOT_SERIAL)
+    return fail(ENPROP_ERR_INVALID, "pcg_solve (multigrid): the reference's serial dot order only");
+  const int s = h->s, rows = h->lv[0].rows;
+  const bool unc = opt->flavour == ENPROP_CG_UNCOUPLED;
+  const int lanes = unc ? s : 1;
+  const int maxit = opt->max_iterations;
+  cudaStream_t st = h->ctx->stream;
+  const size_t vec = (size_t)rows * s * sizeof(double);
+  const int64_t n = rows;
+  std::vector<std::vector<double>> hist(lanes);
+  std::vector<int> its(lanes, 0), status(lanes, 0), active(lanes, 1);
+  auto finish = [&](int rc) {
+    for (int l = 0; l < lanes; ++l) {
+      if (iterations) iterations[l] = its[l];
+      if (lane_status) lane_status[l] = status[l];
+      if (hist_len) hist_len[l] = (int)hist[l].size();
+      if (history)
+        for (int it = 0; it <= maxit; ++it)
+          history[(size_t)it * lanes + l] = it < (int)hist[l].size() ? hist[l][it] : NAN;
+    }
+    return rc;
+  };
+  EP_CUDA(cudaMemsetAsync(x, 0, vec, st));
+  std::vector<double> ln;
+  double cp = 0.0;
+  int rc = mg_dot(h, b, b, ln, cp);  // b_norm = norm2(b)
+  if (rc) return rc;
+  std::vector<double> bnorm(lanes);
+  for (int l = 0; l < lanes; ++l) bnorm[l] = std::sqrt(unc ? ln[l] : cp);
+  bool any = false;
+  for (int l = 0; l < lanes; ++l) {
+    if (bnorm[l] == 0.0) {
+      hist[l].push_back(0.0);
+      active[l] = 0;
+    } else {
+      any = true;
+    }
+  }
+  if (!any) return finish(ENPROP_OK);
+  EP_CUDA(cudaMemcpyAsync(h->r, b, vec, cudaMemcpyDeviceToDevice, st));
+  if ((rc = precondition(h, h->r, h->z))) return rc;
+  EP_CUDA(cudaMemcpyAsync(h->p, h->z, vec, cudaMemcpyDeviceToDevice, st));
+  if ((rc = mg_dot(h, h->r, h->z, ln, cp))) return rc;
+  std::vector<double> rz(lanes);
+  for (int l = 0; l < lanes; ++l) rz[l] = unc ? ln[l] : cp;
+  std::vector<double> coef(2 * kMaxS, 0.0);
+  std::vector<int> act(kMaxS, 0);
+  auto upload_coef = [&](const std::vector<double>& a, const std::vector<int>& on) -> int {
+    for (int e = 0; e < s; ++e) {
+      coef[e] = a[unc ? e : 0];
+      act[e] = on[unc ? e : 0];
+    }
+    EP_CUDA(cudaMemcpyAsync(h->coef, coef.data(), s * sizeof(double), cudaMemcpyHostToDevice, st));
+    EP_CUDA(cudaMemcpyAsync(h->act, act.data(), s * sizeof(int), cudaMemcpyHostToDevice, st));
+    EP_CUDA(cudaStreamSynchronize(st));  // host buffers are reused next
+    return ENPROP_OK;
+  };
+  int worst = ENPROP_OK;
+  for (int it = 0;; ++it) {
+    if ((rc = mg_dot(h, h->r, h->r, ln, cp))) return rc;  // norm2(r)
+    bool live = false;
+    for (int l = 0; l < lanes; ++l) {
+      if (!active[l]) continue;
+      const double rel = std::sqrt(unc ? ln[l] : cp) / bnorm[l];
+      hist[l].push_back(rel);
+      if (rel < opt->tol) {
+        its[l] = it;
+        active[l] = 0;
+      } else if (it >= maxit) {
+        its[l] = it;
+        status[l] = ENPROP_ERR_NO_CONVERGENCE;
+        active[l] = 0;
+      } else {
+        live = true;
+      }
+    }
+    if (!live) break;
+    EP_CUDA(spmv_level(h, s, rows, rows, h->lv[0].rm, h->lv[0].ce, h->lv[0].vals, h->p, h->q));
+    if ((rc = mg_dot(h, h->p, h->q, ln, cp))) return rc;
+    std::vector<double> alpha(lanes, 0.0), malpha(lanes, 0.0);
+    for (int l = 0; l < lanes; ++l) {
+      if (!active[l]) continue;
+      const double pq = unc ? ln[l] : cp;
+      if (pq <= 0.0) {
+        status[l] = ENPROP_ERR_INDEFINITE;
+        its[l] = it;
+        active[l] = 0;
+        continue;
+      }
+      alpha[l] = rz[l] / pq;
+      malpha[l] = -alpha[l];
+    }
+    if ((rc = upload_coef(alpha, active))) return rc;  // x = alpha*p + 1.0*x
+    EP_MG_DISPATCH(s, k_axpy_masked, blocks_for(n * s), 256, 0, st, n, h->coef, h->act, h->p, x);
+    if ((rc = upload_coef(malpha, active))) return rc;  // r = -alpha*q + 1.0*r
+    EP_MG_DISPATCH(s, k_axpy_masked, blocks_for(n * s), 256, 0, st, n, h->coef, h->act, h->q, h->r);
+    h->ctx->launches += 2;
+    if ((rc = precondition(h, h->r, h->z))) return rc;
+    if ((rc = mg_dot(h, h->r, h->z, ln, cp))) return rc;
+    std::vector<double> beta(lanes, 0.0);
+    for (int l = 0; l < lanes; ++l) {
+      if (!active[l]) continue;
+      const double rz_next = unc ? ln[l] : cp;
+      beta[l] = rz_next / rz[l];
+      rz[l] = rz_next;
+    }
+    if ((rc = upload_coef(beta, active))) return rc;  // p = 1.0*z + beta*p
+    EP_MG_DISPATCH(s, k_direction_masked, blocks_for(n * s), 256, 0, st, n, h->coef, h->act, h->z, h->p);
+    h->ctx->launches += 1;
+    EP_CUDA(cudaGetLastError());
+  }
+  EP_CUDA(cudaStreamSynchronize(st));
+  for (int l = 0; l < lanes; ++l) worst = std::max(worst, status[l]);
+  finish(ENPROP_OK);
+  if (worst == ENPROP_ERR_NO_CONVERGENCE)
+    return fail(ENPROP_ERR_NO_CONVERGENCE, "pcg_solve: no convergence within " + std::to_string(maxit) + " iterations");
+  if (worst == ENPROP_ERR_INDEFINITE)
+    return fail(ENPROP_ERR_INDEFINITE, "pcg_solve: operator not positive definite (p'Ap <= 0)");
+  return ENPROP_OK;
+}
+
+}  // extern "C"

@@ -177,6 +177,10 @@ class RefLib:
         L.ref_distributed_spmv.argtypes = [C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, _ip]
         L.ref_time_group.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                      C.c_double, C.c_uint64, C.c_int, C.c_double, C.c_int, _dp, _ip]
+        _mg = [C.c_int, C.c_int, C.c_int, _ip, _ip, _dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int]
+        L.ref_mg_describe.argtypes = _mg + [_ip, _ip, C.c_int, _dp]
+        L.ref_mg_vcycle.argtypes = _mg + [_dp, _dp]
+        L.ref_mg_pcg.argtypes = _mg + [_dp, C.c_double, C.c_int, _dp, _ip, _dp, _ip]
         L.ref_time_spmv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                     C.c_uint64, C.c_int, _dp]
 
@@ -304,6 +308,36 @@ class RefLib:
         out = np.empty((count, m))
         self._check(self.lib.ref_draw_samples(seed, count, m, dptr(out)))
         return out
+
+    # ---- multigrid.hpp (f4): MgOptions = (threshold, degree, ratio, boost, power iterations)
+    def mg_describe(self, s, row_map, col_entry, values, opts=(500, 2, 30.0, 1.1, 40), scalar=False):
+        rows = len(row_map) - 1
+        nl = C.c_int()
+        lr = np.zeros(64, np.int32)
+        lm = np.zeros((64, s))
+        self._check(self.lib.ref_mg_describe(s, int(scalar), rows, iptr(row_map), iptr(col_entry),
+                                             dptr(np.ascontiguousarray(values)), *opts, C.byref(nl), iptr(lr),
+                                             64, dptr(lm)))
+        return lr[:nl.value].copy(), lm[:max(nl.value - 1, 0)].copy()
+
+    def mg_vcycle(self, s, row_map, col_entry, values, b, x, opts=(500, 2, 30.0, 1.1, 40), scalar=False):
+        rows = len(row_map) - 1
+        x = np.ascontiguousarray(x, dtype=np.float64).copy()
+        self._check(self.lib.ref_mg_vcycle(s, int(scalar), rows, iptr(row_map), iptr(col_entry),
+                                           dptr(np.ascontiguousarray(values)), *opts,
+                                           dptr(np.ascontiguousarray(b)), dptr(x)))
+        return x
+
+    def mg_pcg(self, s, row_map, col_entry, values, b, tol, maxit, opts=(500, 2, 30.0, 1.1, 40), scalar=False):
+        rows = len(row_map) - 1
+        x = np.zeros((rows, s))
+        it = C.c_int()
+        hl = C.c_int()
+        hist = np.empty(maxit + 2)
+        st = self.lib.ref_mg_pcg(s, int(scalar), rows, iptr(row_map), iptr(col_entry),
+                                 dptr(np.ascontiguousarray(values)), *opts, dptr(np.ascontiguousarray(b)), tol,
+                                 maxit, dptr(x), C.byref(it), dptr(hist), C.byref(hl))
+        return dict(status=st, x=x, iterations=it.value, history=hist[: hl.value].copy())
 
     def partition(self, n, p):
         out = np.empty((p, 2), np.int32)
