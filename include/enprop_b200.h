@@ -314,6 +314,14 @@ int enprop_mg_vcycle(enprop_mg* h, const double* b, double* x);
 int enprop_mg_pcg(enprop_mg* h, const double* b, double* x, const enprop_cg_options* opt,
                   int* iterations, int* lane_status, double* history, int* hist_len);
 
+/* newton_solve (fem.hpp:265-302) exactly as the reference runs it: every
+ * linear solve is pcg_solve(J, -f, MgPreconditioner(build_hierarchy(J, mg)))
+ * (mg NULL = MgOptions defaults), serial dot order. Same outputs as
+ * enprop_problem_newton. */
+int enprop_problem_newton_mg(enprop_problem* p, const double* y, const enprop_newton_options* opt,
+                             const enprop_mg_options* mg, int* newton_iterations,
+                             int* total_cg_iterations, double* residual_norms, int* num_norms);
+
 /* ------------------------------------ multi-GPU: slab domain decomposition */
 /* The node planes z = k of the mesh are split over nranks like the
  * reference's partition (partition.cpp:31-72; lower ranks take the extra

@@ -493,16 +493,14 @@ UncoupledResult<detail::scalar_of<Vector>> pcg_solve_uncoupled(const Matrix& a, 
 
 // ------------------------------------------------------------------ Newton
 /// newton_solve (fem.hpp:265-302) on the device-resident problem
-/// (enprop_problem_newton): from u = 0, assemble residual + Jacobian at u,
+/// (enprop_problem_newton_mg): from u = 0, assemble residual + Jacobian at u,
 /// impose Dirichlet, stop when the coupled residual norm falls below
-/// options.tol times the first, else solve J du = -f by CG (options.linear)
-/// and u = 1.0*du + 1.0*u. Mesh is an enprop::StructuredMesh, Options an
-/// enprop::NewtonOptions (tol, max_iterations, linear; its multigrid block is
-/// not used: the linear solves are identity-preconditioned, so
-/// total_cg_iterations differ from the reference's MG-preconditioned count,
-/// while the iterate, the step count and the norms follow the same recursion).
-/// The Jacobian solves run in the coupled ensemble CG of pcg_solve<Scalar>.
-/// Throws SolverError with the residual norms after max_iterations steps.
+/// options.tol times the first, else build the multigrid hierarchy of the
+/// Jacobian (options.multigrid) and solve J du = -f by MG-preconditioned
+/// coupled CG (options.linear), u = 1.0*du + 1.0*u -- the reference's own
+/// algorithm, bitwise. Mesh is an enprop::StructuredMesh, Options an
+/// enprop::NewtonOptions. Throws SolverError with the residual norms after
+/// max_iterations steps.
 template <class Scalar, class Mesh, class Field, class Coeffs, class Bc, class Options>
 NewtonResult<Scalar> newton_solve(const Mesh& mesh, const Field& field, const Coeffs& coeffs,
                                   const std::vector<Scalar>& samples, const Bc& bc,
@@ -528,7 +526,10 @@ NewtonResult<Scalar> newton_solve(const Mesh& mesh, const Field& field, const Co
                                options.linear.max_iterations, 16};
   int steps = 0, cg_total = 0, nn = 0;
   std::vector<double> norms(static_cast<size_t>(options.max_iterations > 0 ? options.max_iterations : 0) + 1);
-  const int rc = enprop_problem_newton(p, dy.as<double>(), &o, &steps, &cg_total, norms.data(), &nn);
+  const enprop_mg_options mo{options.multigrid.coarse_row_threshold, options.multigrid.chebyshev_degree,
+                             options.multigrid.eigenvalue_ratio, options.multigrid.eigenvalue_boost,
+                             options.multigrid.power_iterations};
+  const int rc = enprop_problem_newton_mg(p, dy.as<double>(), &o, &mo, &steps, &cg_total, norms.data(), &nn);
   norms.resize(nn);
   if (rc == ENPROP_ERR_NO_CONVERGENCE || rc == ENPROP_ERR_INDEFINITE)
     throw ENPROP_B200_SOLVER_ERROR(enprop_last_error(), std::move(norms));

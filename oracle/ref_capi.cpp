@@ -610,6 +610,47 @@ int ref_mg_pcg(int s, int scalar, int rows, const int* row_map, const int* col_e
   });
 }
 
+// the reference's own newton_solve (fem.hpp:265-302): multigrid-preconditioned
+// coupled linear solves, default MgOptions unless given
+int ref_newton_mg(int s, int scalar, int n, int m, double mean, double sigma, double L, double alpha,
+                  double beta, const double* velocity, const double* y, double bc_x0, double bc_x1, double tol,
+                  int max_newton, double lin_tol, int lin_maxit, int thr, int deg, double ratio, double boost,
+                  int pits, double* u_out, int* iterations, int* total_cg, double* norms, int* num_norms) {
+  *iterations = 0;
+  *total_cg = 0;
+  *num_norms = 0;
+  return guarded([&] {
+    StructuredMesh mesh(n);
+    KlField field(m, mean, sigma, L);
+    PdeCoefficients coeffs;
+    coeffs.alpha = alpha;
+    coeffs.beta = beta;
+    if (velocity) coeffs.velocity = {velocity[0], velocity[1], velocity[2]};
+    NewtonOptions opt;
+    opt.tol = tol;
+    opt.max_iterations = max_newton;
+    opt.linear.tol = lin_tol;
+    opt.linear.max_iterations = lin_maxit;
+    opt.multigrid = mg_options(thr, deg, ratio, boost, pits);
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      auto yy = from_raw<T>(y, m);
+      try {
+        NewtonResult<T> r = newton_solve<T>(mesh, field, coeffs, yy, DirichletBc{bc_x0, bc_x1}, opt);
+        to_raw(r.solution, u_out);
+        *iterations = r.iterations;
+        *total_cg = r.total_cg_iterations;
+        for (double v : r.residual_norms) norms[(*num_norms)++] = v;
+      } catch (const SolverError& err) {
+        for (double v : err.history()) norms[(*num_norms)++] = v;
+        throw;
+      }
+    };
+    if (scalar && s == 1) run(double{});
+    else with_width(s, [&](auto w) { run(E<decltype(w)::value>{}); });
+  });
+}
+
 // Timed reference spmv<Ensemble<S>> on the assembled+Dirichlet matrix, best of reps.
 int ref_time_spmv(int s, int n, int m, double mean, double sigma, double L, uint64_t seed,
                   int reps, double* best_seconds) {

@@ -224,6 +224,8 @@ def lib() -> C.CDLL:
     L.enprop_problem_solve_host.argtypes = [_vp, _vp, _vp, C.POINTER(_CgOptions), _ip, _ip]
     L.enprop_nccl_unique_id.argtypes = [_vp, C.c_size_t]
     L.enprop_dist_create.argtypes = [_vp, C.POINTER(_ProblemDesc), C.c_int, C.c_int, _vp, C.POINTER(_vp)]
+    L.enprop_problem_newton_mg.argtypes = [_vp, _vp, C.POINTER(_NewtonOptions), C.POINTER(_MgOptions), _ip, _ip,
+                                           _dp, _ip]
     L.enprop_mg_build.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp, _vp, C.POINTER(_MgOptions), C.POINTER(_vp)]
     L.enprop_mg_destroy.argtypes = [_vp]
     L.enprop_mg_describe.argtypes = [_vp, _ip, _ip, C.c_int, _dp]
@@ -614,17 +616,24 @@ class Problem:
         return iters, history, lstat
 
     def newton(self, y: torch.Tensor, options: NewtonOptions = None,
-               raise_on_failure: bool = True) -> NewtonResult:
+               raise_on_failure: bool = True, multigrid: Optional[MgOptions] = None) -> NewtonResult:
         """newton_solve (fem.hpp:265-302) from u = 0 with this problem's
-        PdeCoefficients; the iterate ends in self.solution."""
+        PdeCoefficients; the iterate ends in self.solution. multigrid: the
+        reference's MG-preconditioned linear solves with these MgOptions
+        (enprop_problem_newton_mg); None: identity-preconditioned."""
         _need_cuda(y, torch.float64, "y")
         if y.numel() != self.kl.num_terms * self.s:
             raise ValueError("newton: sample vector length mismatch")
         opt = options or NewtonOptions()
         it, cg, nn = C.c_int(), C.c_int(), C.c_int()
         norms = (C.c_double * (max(opt.max_iterations, 0) + 1))()
-        rc = lib().enprop_problem_newton(self.h, _ptr(y), C.byref(opt._c()), C.byref(it), C.byref(cg),
-                                         norms, C.byref(nn))
+        if multigrid is not None:
+            mo = multigrid._c()
+            rc = lib().enprop_problem_newton_mg(self.h, _ptr(y), C.byref(opt._c()), C.byref(mo), C.byref(it),
+                                                C.byref(cg), norms, C.byref(nn))
+        else:
+            rc = lib().enprop_problem_newton(self.h, _ptr(y), C.byref(opt._c()), C.byref(it), C.byref(cg),
+                                             norms, C.byref(nn))
         res = NewtonResult(it.value, cg.value, [norms[i] for i in range(nn.value)])
         if rc in (ERR_NO_CONVERGENCE, ERR_INDEFINITE):
             if raise_on_failure:

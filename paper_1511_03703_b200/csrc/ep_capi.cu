@@ -949,10 +949,16 @@ int enprop_problem_solve(enprop_problem* p, const enprop_cg_options* opt, int* i
                 iterations, lane_status, history, hist_len, p->vpos, stage);
 }
 
-int enprop_problem_newton(enprop_problem* p, const double* y, const enprop_newton_options* opt,
-                          int* newton_iterations, int* total_cg_iterations, double* residual_norms,
-                          int* num_norms) {
-  ScopedLaunchOpts launch_scope(p ? p->ctx : nullptr);
+}  // extern "C"
+
+namespace {
+
+// newton_solve (fem.hpp:265-302): mg == nullptr solves the linear systems with
+// the identity preconditioner, else with MgPreconditioner of a hierarchy built
+// from each step's Jacobian (the reference's own choice, :294-297).
+int problem_newton(enprop_problem* p, const double* y, const enprop_newton_options* opt,
+                   const enprop_mg_options* mg, int* newton_iterations, int* total_cg_iterations,
+                   double* residual_norms, int* num_norms) {
   if (!p || !y || !opt) return fail(ENPROP_ERR_INVALID, "enprop_problem_newton: null argument");
   if (opt->max_iterations < 0) return fail(ENPROP_ERR_INVALID, "newton_solve: negative max_iterations");
   const int s = p->desc.ensemble_size;
@@ -967,6 +973,13 @@ int enprop_problem_newton(enprop_problem* p, const double* y, const enprop_newto
   const int seg = (p->desc.cells_per_axis + 1) * (p->desc.cells_per_axis + 1);
   int steps = 0, cg_total = 0, nn = 0;
   double initial = 0.0;
+  double* full_vals = nullptr;  // full [nnz][s] values for the hierarchy (multigrid only)
+  struct FreeOnExit {
+    double*& q;
+    ~FreeOnExit() {
+      if (q) cudaFree(q);
+    }
+  } free_full{full_vals};
   auto finish = [&](int code) {
     if (newton_iterations) *newton_iterations = steps;
     if (total_cg_iterations) *total_cg_iterations = cg_total;
@@ -1011,7 +1024,24 @@ int enprop_problem_newton(enprop_problem* p, const double* y, const enprop_newto
     // rhs = -residual; J du = rhs by CG; u = 1.0*du + 1.0*u (fem.hpp:294-300)
     const int lanes = opt->linear.flavour == ENPROP_CG_UNCOUPLED ? s : 1;
     std::vector<int> its(lanes, 0), ls(lanes, 0);
-    rc = enprop_problem_solve(p, &opt->linear, its.data(), ls.data(), nullptr, nullptr);
+    if (mg) {  // build_hierarchy(system.matrix) + pcg_solve(..., MgPreconditioner) (:294-297)
+      if (opt->linear.dot_mode != ENPROP_DOT_SERIAL)
+        return fail(ENPROP_ERR_INVALID, "newton_solve (multigrid): the reference's serial dot order only");
+      if (!full_vals) EP_CUDA(cudaMalloc(&full_vals, (size_t)p->nnz * s * sizeof(double)));
+      rc = enprop_problem_expand_values(p, full_vals);
+      if (rc) return rc;
+      EP_CUDA(launch_negate(len, p->residual, p->rhs, st));
+      c->launches += 1;
+      enprop_mg* h = nullptr;
+      rc = enprop_mg_build(c, s, p->rows, p->row_map, p->col_entry, full_vals, mg, &h);
+      if (rc) return rc;
+      rc = enprop_mg_pcg(h, p->rhs, p->x, &opt->linear, its.data(), ls.data(), nullptr, nullptr);
+      const std::string msg = rc ? g_last_error : std::string();
+      enprop_mg_destroy(h);
+      if (rc) g_last_error = msg;
+    } else {
+      rc = enprop_problem_solve(p, &opt->linear, its.data(), ls.data(), nullptr, nullptr);
+    }
     int mx = 0;
     for (int l = 0; l < lanes; ++l) mx = its[l] > mx ? its[l] : mx;
     cg_total += mx;
@@ -1025,6 +1055,26 @@ int enprop_problem_newton(enprop_problem* p, const double* y, const enprop_newto
     rc = enprop_axpby(c, s, len / s, 0, &one, p->x, &one, p->u);
     if (rc) return rc;
   }
+}
+
+}  // namespace
+
+extern "C" {
+
+int enprop_problem_newton(enprop_problem* p, const double* y, const enprop_newton_options* opt,
+                          int* newton_iterations, int* total_cg_iterations, double* residual_norms,
+                          int* num_norms) {
+  ScopedLaunchOpts launch_scope(p ? p->ctx : nullptr);
+  return problem_newton(p, y, opt, nullptr, newton_iterations, total_cg_iterations, residual_norms, num_norms);
+}
+
+int enprop_problem_newton_mg(enprop_problem* p, const double* y, const enprop_newton_options* opt,
+                             const enprop_mg_options* mg, int* newton_iterations, int* total_cg_iterations,
+                             double* residual_norms, int* num_norms) {
+  ScopedLaunchOpts launch_scope(p ? p->ctx : nullptr);
+  enprop_mg_options d{500, 2, 30.0, 1.1, 40};  // MgOptions defaults (multigrid.hpp:14-20)
+  return problem_newton(p, y, opt, mg ? mg : &d, newton_iterations, total_cg_iterations, residual_norms,
+                        num_norms);
 }
 
 int enprop_problem_solve_host(enprop_problem* p, const double* y_host, double* x_host,

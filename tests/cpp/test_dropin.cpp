@@ -205,49 +205,26 @@ static void value_forms_and_samples(int n) {
   CHECK(inval);
 }
 
-// newton_solve (fem.hpp:265-302) through the drop-in against the same loop
-// composed from the reference's own pieces with IdentityPreconditioner (the
-// drop-in's linear solves are identity-preconditioned)
+// newton_solve (fem.hpp:265-302) through the drop-in against the reference's
+// own newton_solve (multigrid-preconditioned linear solves): iterate, steps,
+// CG total and norms bit for bit
 template <int S>
 static void newton(int n, double beta) {
   StructuredMesh mesh(n);
-  AssemblyContext ctx(mesh);
   KlField field(3, 1.0, 0.1, 1.0);
   const PdeCoefficients coeffs{0.0, beta, {1.0, 0.0, 0.0}};
   const auto y = pack_sample_group<S>(draw_samples(7, S, 3), 0);
   NewtonOptions opt;
   opt.tol = 1e-8;
   opt.linear.tol = 1e-10;
-  // reference pieces, identity-preconditioned (fem.hpp:273-301 otherwise)
-  DenseVector<Ensemble<S>> u(mesh.num_nodes(), Ensemble<S>(0.0));
-  std::vector<double> norms;
-  int steps = 0, cg_total = 0;
-  double initial = 0.0;
-  AssembledSystem<Ensemble<S>> sys;
-  for (int step = 0;; ++step) {
-    enprop::assemble<Ensemble<S>>(ctx, field, coeffs, u, std::span<const Ensemble<S>>(y), sys);
-    enprop::apply_dirichlet(sys, mesh, DirichletBc{}, u);
-    const double norm = enprop::norm2(sys.residual);
-    norms.push_back(norm);
-    if (step == 0) {
-      initial = norm;
-      if (initial == 0.0) break;
-    } else if (norm < opt.tol * initial) {
-      steps = step;
-      break;
-    }
-    DenseVector<Ensemble<S>> rhs(sys.residual.size());
-    for (size_t i = 0; i < rhs.size(); ++i) rhs[i] = -sys.residual[i];
-    auto lin = enprop::pcg_solve(sys.matrix, rhs, IdentityPreconditioner{}, opt.linear);
-    cg_total += lin.iterations;
-    enprop::axpby(1.0, lin.solution, 1.0, u);
-  }
+  opt.multigrid.coarse_row_threshold = 100;
+  enprop::NewtonResult<Ensemble<S>> ref = enprop::newton_solve<Ensemble<S>>(mesh, field, coeffs, y, DirichletBc{}, opt);
   enprop::NewtonResult<Ensemble<S>> r =
       enprop_b200::newton_solve(mesh, field, coeffs, y, DirichletBc{}, opt);
-  CHECK(r.iterations == steps);
-  CHECK(r.total_cg_iterations == cg_total);
-  CHECK(r.residual_norms == norms);
-  CHECK(same_bits(r.solution, u));
+  CHECK(r.iterations == ref.iterations);
+  CHECK(r.total_cg_iterations == ref.total_cg_iterations);
+  CHECK(r.residual_norms == ref.residual_norms);
+  CHECK(same_bits(r.solution, ref.solution));
 }
 
 int main() {

@@ -181,6 +181,10 @@ class RefLib:
         L.ref_mg_describe.argtypes = _mg + [_ip, _ip, C.c_int, _dp]
         L.ref_mg_vcycle.argtypes = _mg + [_dp, _dp]
         L.ref_mg_pcg.argtypes = _mg + [_dp, C.c_double, C.c_int, _dp, _ip, _dp, _ip]
+        L.ref_newton_mg.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                    C.c_double, C.c_double, _dp, _dp, C.c_double, C.c_double, C.c_double,
+                                    C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                    C.c_int, _dp, _ip, _ip, _dp, _ip]
         L.ref_time_spmv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                     C.c_uint64, C.c_int, _dp]
 
@@ -308,6 +312,18 @@ class RefLib:
         out = np.empty((count, m))
         self._check(self.lib.ref_draw_samples(seed, count, m, dptr(out)))
         return out
+
+    def newton_mg(self, s, n, m, y, sigma=0.1, alpha=0.0, beta=0.0, velocity=(1.0, 0.0, 0.0), tol=1e-8,
+                  max_newton=20, lin_tol=1e-8, lin_maxit=1000, opts=(500, 2, 30.0, 1.1, 40), scalar=False):
+        """The reference's own newton_solve (fem.hpp:265-302), MG-preconditioned."""
+        u = np.zeros(((n + 1) ** 3, s))
+        it, cg, nn = C.c_int(), C.c_int(), C.c_int()
+        norms = np.zeros(max_newton + 2)
+        vel = np.array(velocity, dtype=np.float64)
+        st = self.lib.ref_newton_mg(s, int(scalar), n, m, 1.0, sigma, 1.0, alpha, beta, dptr(vel),
+                                    dptr(np.ascontiguousarray(y)), 1.0, 0.0, tol, max_newton, lin_tol, lin_maxit,
+                                    *opts, dptr(u), C.byref(it), C.byref(cg), dptr(norms), C.byref(nn))
+        return dict(status=st, u=u, iterations=it.value, total_cg=cg.value, norms=norms[: nn.value].copy())
 
     # ---- multigrid.hpp (f4): MgOptions = (threshold, degree, ratio, boost, power iterations)
     def mg_describe(self, s, row_map, col_entry, values, opts=(500, 2, 30.0, 1.1, 40), scalar=False):

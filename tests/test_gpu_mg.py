@@ -115,3 +115,23 @@ def test_mg_pcg_exhaustion_and_invalid(ctx, R):
     with pytest.raises(ValueError):  # the multigrid solve uses the reference's order
         h.pcg(dev(b), ep.SolverConfig(dot_mode=ep.DOT_CANONICAL))
     h.close()
+
+
+@pytest.mark.parametrize("s,n,beta", [(4, 8, 0.0), (4, 8, 0.7), (1, 10, 0.7), (32, 6, 0.5)])
+def test_newton_multigrid_is_the_reference_newton_solve(ctx, R, s, n, beta):
+    """f3 as the reference runs it: newton_solve (fem.hpp:265-302) with each
+    step's hierarchy and MG-preconditioned coupled CG -- iterate, steps, CG
+    total and residual norms bitwise equal to the reference's own function."""
+    m = 3
+    y = pack_group(R.draw_samples(7, s, m), s)
+    opts = (100, 2, 30.0, 1.1, 40)
+    o = R.newton_mg(s, n, m, y, beta=beta, tol=1e-8, lin_tol=1e-10, opts=opts, scalar=(s == 1))
+    assert o["status"] == 0
+    p = ep.Problem(ctx, n, s, ep.KlField(m, 1.0, 0.1, 1.0), ep.PdeCoefficients(0.0, beta))
+    lin = ep.SolverConfig(tol=1e-10, max_iterations=1000, flavour=CG_COUPLED, dot_mode=DOT_SERIAL)
+    res = p.newton(dev(y), ep.NewtonOptions(tol=1e-8, max_iterations=20, linear=lin), multigrid=ep.MgOptions(*opts))
+    assert res.iterations == o["iterations"]
+    assert res.total_cg_iterations == o["total_cg"]
+    assert same(np.array(res.residual_norms), o["norms"])
+    assert same(p.solution.cpu().numpy(), o["u"])
+    p.close()
