@@ -72,7 +72,9 @@ int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
  *   ENPROP_OPT_SYMMETRIC_STORAGE (default 1): problems created afterwards store
  *   only the diagonal + upper triangle of the (exactly symmetric) assembled
  *   operator and read each lower entry from its transposed slot
- *   (enprop_problem_expand_values rebuilds the full [nnz][s] values).
+ *   (enprop_problem_expand_values rebuilds the full [nnz][s] values):
+ *   1 = from s = 4 up (at s = 1, 2 the slot map costs what it saves), 2 = at
+ *   every width, 0 = never (advection, alpha != 0, always stores all).
  *   ENPROP_OPT_SPMV_PIPELINE (default 0): 1 = enprop_spmv loads the next batch's
  *   column indices one batch ahead (software pipelining).
  *   ENPROP_OPT_SPMV_VARIANT (default -1 = auto): CG SpMV schedule

@@ -184,6 +184,7 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
   const TileMap tm = make_tile_map(rows, seg);
   const bool canon = opt->dot_mode == ENPROP_DOT_CANONICAL;
   // serial order: the SpMV writes the p*q products the chain kernel sums
+  // (except on the plain path, where the chain forms them from p and q)
   int rc = ensure_work(w, rows, s, opt->max_iterations, tm, !canon);
   if (rc) return rc;
   const int lanes = opt->flavour == ENPROP_CG_UNCOUPLED ? s : 1;
@@ -226,7 +227,15 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
 
   if (sev) EP_CUDA(cudaEventRecord(sev[1], st));
   const int chunk = opt->check_every > 0 ? opt->check_every : 16;
-  const int per_iter = (canon ? 2 : 4) + (fused ? 0 : 1) + (fin_kernel ? 2 : 0) - (fuse_pq ? 1 : 0);
+  // Full storage without the staged kernel: q = A p by the public SpMV kernels
+  // (k_spmv_small for s <= 16: one CTA stages its block's column indices;
+  // k_spmv at s = 32), then p.q as its own pass -- canonical tile partials
+  // (k_dot_tiles) or the serial chain over p and q. The warp-per-tile CG
+  // kernel (SpMV + tile trees in one pass) stays for symmetric storage and the
+  // fused-direction schedule. (64^3, s = 1: 0.077 -> ~0.03 ms per SpMV.)
+  const bool plain = !stage && !vpos && !fused && plain_cg_spmv();
+  const int per_iter = (canon ? 2 : 4) + (fused ? 0 : 1) + (fin_kernel ? 2 : 0) - (fuse_pq ? 1 : 0) +
+                       (plain && canon ? 1 : 0);
   // one loop body (pcg.hpp:76-101); `it` fixes which p buffer is old / new
   auto enqueue_iteration = [&](int it, cudaEvent_t* ev) -> cudaError_t {
     double* p_old = w.p[it & 1];
@@ -242,12 +251,21 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
     if (ev) EP_Q(cudaEventRecord(ev[1], st));
     if (stage) {
       EP_Q(launch_cg_spmv_staged(s, canon, fuse_pq, *stage, values, p_new, w.q, f_pq, st));
+    } else if (plain) {
+      if (s <= spmv_small_max())
+        EP_Q(launch_spmv_small(s, rows, row_map, col_entry, values, p_new, w.q, st));
+      else
+        EP_Q(launch_spmv(s, rows, row_map, col_entry, values, p_new, w.q, false, st));
+      if (canon) EP_Q(launch_dot_tiles(s, tm, p_new, w.q, f_pq, st));
     } else {
       EP_Q(launch_cg_spmv(s, canon, fused, false, tm, row_map, col_entry, values, w.r, p_old, p_new, w.q,
                           x, p_new, vpos, f_pq, st));
     }
     if (ev) EP_Q(cudaEventRecord(ev[2], st));
-    if (!canon) EP_Q(launch_chain(s, rows, w.prod, nullptr, kChainGiven, f_pq, st));
+    if (!canon) {
+      if (plain) EP_Q(launch_chain(s, rows, p_new, w.q, kChainProduct, f_pq, st));
+      else EP_Q(launch_chain(s, rows, w.prod, nullptr, kChainGiven, f_pq, st));
+    }
     if (fin_kernel && !fuse_pq) EP_Q(launch_fin_segments(s, tm, f_pq, st));
     if (ev) EP_Q(cudaEventRecord(ev[3], st));
     EP_Q(launch_cg_update(s, canon, tm, w.r, w.q, f_rr, st));
@@ -267,7 +285,7 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
     const void* key_ptrs[] = {values, x, row_map, col_entry, vpos, stage ? (const void*)stage->desc : nullptr,
                               w.r, w.q, w.p[0], w.p[1], w.prod, w.partials, w.state};
     const int key_ints[] = {s, rows, canon, fuse_pq, fused, chunk, tm.seg_rows, launch_opts().pdl,
-                            spmv_variant()};
+                            spmv_variant(), plain};
     std::vector<char> key(sizeof(key_ptrs) + sizeof(key_ints));
     std::memcpy(key.data(), key_ptrs, sizeof(key_ptrs));
     std::memcpy(key.data() + sizeof(key_ptrs), key_ints, sizeof(key_ints));
@@ -443,7 +461,7 @@ int enprop_ctx_set_option(enprop_ctx* c, int option, int value) {
       c->spmv_pipeline = value ? 1 : 0;
       return ENPROP_OK;
     case ENPROP_OPT_SYMMETRIC_STORAGE:
-      c->symmetric_storage = value ? 1 : 0;
+      c->symmetric_storage = value < 0 ? 0 : (value > 2 ? 2 : value);
       return ENPROP_OK;
     case ENPROP_OPT_SPMV_VARIANT:
       c->spmv_variant = (value >= 0 && value <= 6) ? value : -1;
@@ -830,7 +848,12 @@ int enprop_problem_create(enprop_ctx* c, const enprop_problem_desc* d, enprop_pr
   p->nnz_stored = p->nnz;
   // the assembled operator is exactly symmetric unless the
   // advection term (alpha != 0, fem.hpp:167-191) is on
-  if (c->symmetric_storage && d->coeffs.alpha == 0.0) {
+  // symmetric storage from s = 4 up (auto): at s = 1 and 2 the slot map costs
+  // about what it saves (s = 1: 28.8 MB of slots saved, 28.8 MB of slot map
+  // added at 64^3) and the full-storage narrow SpMV (k_spmv_small) is faster
+  // than gathering through it (64^3, s = 1: 0.077 -> 0.027 ms); at s = 8 the
+  // halved value bytes win (warp kernel 0.098 ms vs 0.108 for full storage)
+  if (d->coeffs.alpha == 0.0 && (c->symmetric_storage == 2 || (c->symmetric_storage == 1 && s >= 4))) {
     if ((err = cudaMalloc(&p->vpos, p->nnz * sizeof(int))) != cudaSuccess ||
         (err = cudaMalloc(&p->up_start, (p->rows + 1) * sizeof(int))) != cudaSuccess ||
         (err = build_sym(p->rows, p->row_map, p->col_entry, p->vpos, &p->nnz_stored, c->stream,

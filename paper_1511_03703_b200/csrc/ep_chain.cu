@@ -44,12 +44,20 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 constexpr int kChainChunkBytes = 16384;  // per operand vector per stage
 constexpr int kChainBlock = 64;          // rows per unrolled consumer block
 
-template <int NV>
+template <int NV, int D_ = (NV == 1 ? 8 : 6)>
 struct ChainRing {
   static constexpr int STAGE = kChainChunkBytes * NV;
-  static constexpr int D = NV == 1 ? 8 : 6;  // stages in the ring (128 / 192 KB)
+  static constexpr int D = D_;  // stages in the ring (default 128 / 192 KB)
   static constexpr int SMEM = D * STAGE + 2 * D * 8;
 };
+
+// ENPROP_CHAIN_STAGES (A/B): ring depth of the one-operand chains, 4 or 8
+// (default); 4 stages (64 KB) let a chain CTA share an SM with a staged-SpMV
+// CTA of the two-per-SM layout
+int chain_stages() {
+  static const int v = env_int("ENPROP_CHAIN_STAGES", 8) == 4 ? 4 : 8;
+  return v;
+}
 
 template <int S, int KIND>
 __device__ __forceinline__ double chain_term(const double* a, const double* b, int i) {
@@ -59,13 +67,13 @@ __device__ __forceinline__ double chain_term(const double* a, const double* b, i
   else return EP_DMUL(x, b[i * S]);
 }
 
-template <int S, int KIND>
+template <int S, int KIND, int DEPTH>
 __global__ void __launch_bounds__(64, 1) k_chain(int rows, const double* __restrict__ u,
                                                  const double* __restrict__ v, const FinArgs f) {
   EP_PDL_ENTRY();
   if ((f.phase == kPhasePQ || f.phase == kPhaseRR) && f.cg->done) return;
   constexpr int NV = KIND == kChainProduct ? 2 : 1;
-  using Ring = ChainRing<NV>;
+  using Ring = ChainRing<NV, DEPTH>;
   constexpr int D = Ring::D;
   constexpr int R = kChainChunkBytes / (8 * S);  // rows per stage
   constexpr int BLK = R < kChainBlock ? R : kChainBlock;
@@ -242,10 +250,10 @@ bool chain_aligned(const void* u, const void* v) {
   return ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
 }
 
-template <int S, int KIND>
-static cudaError_t chain_sk(int rows, const double* u, const double* v, const FinArgs& f, cudaStream_t st) {
+template <int S, int KIND, int DEPTH>
+static cudaError_t chain_skd(int rows, const double* u, const double* v, const FinArgs& f, cudaStream_t st) {
   constexpr int NV = KIND == kChainProduct ? 2 : 1;
-  constexpr int SMEM = ChainRing<NV>::SMEM;
+  constexpr int SMEM = ChainRing<NV, DEPTH>::SMEM;
   // shared-memory opt-in once per device (solves on several host threads)
   static std::atomic<int> ready[64];
   static std::mutex mu;
@@ -256,14 +264,20 @@ static cudaError_t chain_sk(int rows, const double* u, const double* v, const Fi
   if (!ready[dev].load(std::memory_order_acquire)) {
     std::lock_guard<std::mutex> lock(mu);
     if (!ready[dev].load(std::memory_order_relaxed)) {
-      err = cudaFuncSetAttribute(k_chain<S, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+      err = cudaFuncSetAttribute(k_chain<S, KIND, DEPTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
       if (err != cudaSuccess) return err;
       ready[dev].store(1, std::memory_order_release);
     }
   }
   if (chain_mode() == 1) launch_kk(4, k_chain_small<S, KIND>, dim3(1), dim3(32), 0, st, rows, u, v, f);
-  else launch_kk(4, k_chain<S, KIND>, dim3(1), dim3(64), SMEM, st, rows, u, v, f);
+  else launch_kk(4, k_chain<S, KIND, DEPTH>, dim3(1), dim3(64), SMEM, st, rows, u, v, f);
   return cudaGetLastError();
+}
+
+template <int S, int KIND>
+static cudaError_t chain_sk(int rows, const double* u, const double* v, const FinArgs& f, cudaStream_t st) {
+  if (KIND != kChainProduct && chain_stages() == 4) return chain_skd<S, KIND, 4>(rows, u, v, f, st);
+  return chain_skd<S, KIND, KIND == kChainProduct ? 6 : 8>(rows, u, v, f, st);
 }
 
 template <int S>

@@ -43,7 +43,11 @@
 
 namespace ep {
 
-template <int S>
+// NB = stage buffers per CTA: 2 (one persistent CTA per SM, the next stage's
+// buffer and transposed gathers in flight during the current one) or 1 (two
+// CTAs per SM at <= 128 registers: each CTA loads one stage while the other
+// computes; ENPROP_STAGED_CTAS=2).
+template <int S, int NB = 2>
 struct StagedShape {
   static constexpr int V = 2;
   static constexpr int TPR = S / V;                 // threads per row
@@ -58,13 +62,13 @@ struct StagedShape {
   static constexpr int BIG_BYTES = ((ZC + 1) * CH + 127) / 128 * 128;
   static constexpr int HDR = 2 * RS + 4;            // ints: srow[RS], slr[RS], stage id, pad
   static constexpr int IDX_BYTES = HDR * 4 + RS * ROWE * 4;
-  static constexpr int NIDX = S >= 16 ? 4 : 2;      // index blocks in flight (ring depth; smem-limited at s < 16)
+  static constexpr int NIDX = (S >= 16 && NB == 2) ? 4 : 2;  // index blocks in flight (ring depth; smem-limited)
   static constexpr int RED_BYTES = RS * S * 8;
   static constexpr int CLAIM = NIDX > 3 ? NIDX : 3;  // stages claimed ahead of the current one
-  static constexpr int SMEM = 2 * BIG_BYTES + NIDX * IDX_BYTES + 2 * RED_BYTES + 64 + 32;
+  static constexpr int SMEM = NB * BIG_BYTES + NIDX * IDX_BYTES + 2 * RED_BYTES + 64 + 32;
   static_assert(RS * TPR == 256, "one thread per (row slot, sample pair)");
   static_assert(BIG_BYTES % 128 == 0 && IDX_BYTES % 16 == 0, "alignment");
-  static_assert(SMEM <= 232448, "stage ring exceeds shared memory");
+  static_assert(SMEM <= (NB == 2 ? 232448 : 115712), "stage ring exceeds shared memory");
   static_assert(ZC < 65536, "chunk indices are 16-bit");
 };
 
@@ -75,9 +79,9 @@ struct StageGather {
   double2 v[kStageMaxGlobal];
 };
 
-template <int S>
+template <int S, int NB = 2>
 struct StagedCta {
-  using Sh = StagedShape<S>;
+  using Sh = StagedShape<S, NB>;
   const TileMap& tm;
   int N, nstages;
   const StageDesc* __restrict__ desc;
@@ -87,7 +91,7 @@ struct StagedCta {
   double* __restrict__ q;
   const FinArgs& f;
   unsigned char* smem;
-  uint64_t* bar;  // [0,2): big buffers, [2,6): index ring
+  uint64_t* bar;  // [0,NB): big buffers, [NB,NB+NIDX): index ring
   double* red;
   int* claims;    // [8] sweep positions of this CTA's stages it, it+1, ... (ring)
   int* ticket;    // global claim counter (f.ticket)
@@ -114,15 +118,18 @@ struct StagedCta {
     if (t == nstages + (int)gridDim.x - 1) *ticket = 0;
     claims[it & 7] = t < nstages ? t : nstages;
   }
-  __device__ __forceinline__ unsigned char* big(int it) const { return smem + (it & 1) * Sh::BIG_BYTES; }
+  __device__ __forceinline__ unsigned char* big(int it) const { return smem + (it & (NB - 1)) * Sh::BIG_BYTES; }
+  __device__ __forceinline__ uint64_t* big_bar(int it) const { return &bar[it & (NB - 1)]; }
+  __device__ __forceinline__ uint32_t big_parity(int it) const { return (it / NB) & 1; }
+  __device__ __forceinline__ uint64_t* idx_bar(int it) const { return &bar[NB + (it & (Sh::NIDX - 1))]; }
   __device__ __forceinline__ const int* idx(int it) const {
-    return reinterpret_cast<const int*>(smem + 2 * Sh::BIG_BYTES + (it & (Sh::NIDX - 1)) * Sh::IDX_BYTES);
+    return reinterpret_cast<const int*>(smem + NB * Sh::BIG_BYTES + (it & (Sh::NIDX - 1)) * Sh::IDX_BYTES);
   }
 
   // producer (thread 0)
   __device__ __forceinline__ void issue_big(int it, const StageDesc& d) const {
     unsigned char* sb = big(it);
-    uint64_t* b = &bar[it & 1];
+    uint64_t* b = big_bar(it);
     const int rows = tm.rows, NN = N * N;
     const int L = d.R1 - d.R0 + 2;
     const uint32_t upb = (uint32_t)(d.slot1 - d.slot0) * Sh::CH;
@@ -145,7 +152,7 @@ struct StagedCta {
     }
   }
   __device__ __forceinline__ void issue_idx(int it) const {
-    uint64_t* b = &bar[2 + (it & (Sh::NIDX - 1))];
+    uint64_t* b = idx_bar(it);
     mbar_arrive_expect_tx(b, Sh::IDX_BYTES);
     bulk_g2s((void*)idx(it), blk + (size_t)stage_of(it) * Sh::IDX_BYTES, Sh::IDX_BYTES, b);
   }
@@ -174,14 +181,21 @@ struct StagedCta {
     return *reinterpret_cast<const double2*>(sb + c * Sh::CH + lane0 * 8);
   }
 
+  // NB = 2: Gc holds this stage's gathers (issued one stage ahead), Gn
+  // receives the next stage's; NB = 1: Gc is gathered here (Gn unused)
   template <bool kTiles>
   __device__ __forceinline__ void stage(int it, StageGather& Gc, StageGather& Gn) const {
-    StageDesc dn;  // producer: descriptor of stage it + 2, loaded early
-    const bool prod = threadIdx.x == 0 && has(it + 2);
-    if (prod) dn = desc[stage_of(it + 2)];
-    if (has(it + 1)) {  // the next stage's transposed gathers fly during this stage
-      mbar_wait(&bar[2 + ((it + 1) & (Sh::NIDX - 1))], ((it + 1) / Sh::NIDX) & 1);
-      gather(it + 1, Gn);
+    StageDesc dn;  // producer: descriptor of stage it + NB, loaded early
+    const bool prod = threadIdx.x == 0 && has(it + NB);
+    if (prod) dn = desc[stage_of(it + NB)];
+    if constexpr (NB == 2) {
+      if (has(it + 1)) {  // the next stage's transposed gathers fly during this stage
+        mbar_wait(idx_bar(it + 1), ((it + 1) / Sh::NIDX) & 1);
+        gather(it + 1, Gn);
+      }
+    } else {
+      mbar_wait(idx_bar(it), (it / Sh::NIDX) & 1);
+      gather(it, Gc);
     }
     const int* ib = idx(it);
     const int row = ib[rr];
@@ -195,7 +209,7 @@ struct StagedCta {
         ca[4 * v] = w.x, ca[4 * v + 1] = w.y, ca[4 * v + 2] = w.z, ca[4 * v + 3] = w.w;
       }
     }
-    mbar_wait(&bar[it & 1], (it >> 1) & 1);
+    mbar_wait(big_bar(it), big_parity(it));
     const unsigned char* sb = big(it);
     // Stencil slots k = run*3 + di + 1 in column order, run = (dk+1)*3 + dj+1;
     // absent neighbours (and empty row slots) point the value at the zero chunk
@@ -249,7 +263,7 @@ struct StagedCta {
     __syncthreads();  // big buffer and index slot of stage it consumed, products in rb
     if (threadIdx.x == 0) {
       fence_proxy_async_smem();
-      if (prod) issue_big(it + 2, dn);
+      if (prod) issue_big(it + NB, dn);
       claim(it + Sh::CLAIM);
       if (has(it + Sh::NIDX)) issue_idx(it + Sh::NIDX);
     }
@@ -295,31 +309,31 @@ __device__ __forceinline__ void grid_barrier(int* count, int* gen, int nblocks) 
   __syncthreads();
 }
 
-template <int S, bool kTiles>
-__global__ void __launch_bounds__(256, 1) k_cg_spmv_staged(
+template <int S, bool kTiles, int NB>
+__global__ void __launch_bounds__(256, NB == 2 ? 1 : 2) k_cg_spmv_staged(
     const TileMap tm, int N, int nstages, const StageDesc* __restrict__ desc,
     const unsigned char* __restrict__ blk, const double* __restrict__ values,
     const double* __restrict__ p, double* __restrict__ q, const FinArgs f, int fuse_fin) {
-  using Sh = StagedShape<S>;
+  using Sh = StagedShape<S, NB>;
   EP_PDL_ENTRY();
   if (f.cg->done) return;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
-  unsigned char* tail = smem + 2 * Sh::BIG_BYTES + Sh::NIDX * Sh::IDX_BYTES + 2 * Sh::RED_BYTES;
-  StagedCta<S> c{tm, N, nstages, desc, blk, values, p, q, f, smem,
+  unsigned char* tail = smem + NB * Sh::BIG_BYTES + Sh::NIDX * Sh::IDX_BYTES + 2 * Sh::RED_BYTES;
+  StagedCta<S, NB> c{tm, N, nstages, desc, blk, values, p, q, f, smem,
                  reinterpret_cast<uint64_t*>(tail),
-                 reinterpret_cast<double*>(smem + 2 * Sh::BIG_BYTES + Sh::NIDX * Sh::IDX_BYTES),
+                 reinterpret_cast<double*>(smem + NB * Sh::BIG_BYTES + Sh::NIDX * Sh::IDX_BYTES),
                  reinterpret_cast<int*>(tail + 64), f.ticket,
                  l2_policy_evict_normal(), tid / Sh::TPR, (tid % Sh::TPR) * Sh::V};
   if (tid == 0) {
-    for (int k = 0; k < 2 + Sh::NIDX; ++k) mbar_init(&c.bar[k], 1);
+    for (int k = 0; k < NB + Sh::NIDX; ++k) mbar_init(&c.bar[k], 1);
     fence_mbar_init();
     for (int it = 0; it < Sh::CLAIM; ++it) c.claim(it);
   }
   // zero chunks (never written by the copies) and x-run areas: positions a
   // copy does not reach (clipped runs) are read for absent neighbours only,
   // times a zero value, so they must hold finite numbers
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < NB; ++b) {
     double2* z = reinterpret_cast<double2*>(smem + b * Sh::BIG_BYTES + Sh::UP_CHUNKS * Sh::CH);
     for (int i = tid; i < (Sh::X_CHUNKS + 1) * Sh::CH / 16; i += blockDim.x) z[i] = make_double2(0.0, 0.0);
   }
@@ -328,18 +342,23 @@ __global__ void __launch_bounds__(256, 1) k_cg_spmv_staged(
     fence_proxy_async_smem();  // the zero-filled x areas are rewritten by the copies
     for (int it = 0; it < Sh::NIDX; ++it)
       if (c.has(it)) c.issue_idx(it);
-    for (int it = 0; it < 2; ++it)
+    for (int it = 0; it < NB; ++it)
       if (c.has(it)) c.issue_big(it, desc[c.stage_of(it)]);
   }
   if (c.has(0)) {  // (a CTA may draw no stage at all; it still joins the barrier)
-    StageGather ga, gb;
-    mbar_wait(&c.bar[2], 0);
-    c.gather(0, ga);
-    for (int it = 0;;) {
-      c.template stage<kTiles>(it, ga, gb);
-      if (!c.has(++it)) break;
-      c.template stage<kTiles>(it, gb, ga);
-      if (!c.has(++it)) break;
+    if constexpr (NB == 2) {
+      StageGather ga, gb;
+      mbar_wait(c.idx_bar(0), 0);
+      c.gather(0, ga);
+      for (int it = 0;;) {
+        c.template stage<kTiles>(it, ga, gb);
+        if (!c.has(++it)) break;
+        c.template stage<kTiles>(it, gb, ga);
+        if (!c.has(++it)) break;
+      }
+    } else {
+      StageGather g;
+      for (int it = 0; c.has(it); ++it) c.template stage<kTiles>(it, g, g);
     }
   }
   if constexpr (kTiles) {
@@ -447,6 +466,11 @@ static int stage_shape(int& T, int& L, int& RS, int& max_upper, int& idx_bytes, 
 
 bool staged_fuse_fin() {
   static const int on = env_int("ENPROP_STAGED_FUSE", 1);
+  return on != 0;
+}
+
+bool plain_cg_spmv() {
+  static const int on = env_int("ENPROP_PLAIN_CG_SPMV", 1);
   return on != 0;
 }
 
@@ -565,10 +589,19 @@ void free_stage_map(StageMap& sm) {
   sm = StageMap{};
 }
 
-template <int S>
-static cudaError_t cg_spmv_staged_s(bool tiles, bool fuse_fin, const StageMap& sm, const double* values,
-                                    const double* p, double* q, const FinArgs& f, cudaStream_t st) {
-  using Sh = StagedShape<S>;
+// ENPROP_STAGED_CTAS (A/B): 2 = two CTAs per SM with one stage buffer each
+// (default at s >= 16: 64^3/s=32 canonical SpMV + fused finalize 0.272 ->
+// 0.236 ms, 24-group serial bench 536 -> 545 samples/s), 1 = one CTA per SM
+// with two buffers (s = 4 always: its index blocks do not fit twice)
+int staged_ctas() {
+  static const int v = env_int("ENPROP_STAGED_CTAS", 2) == 1 ? 1 : 2;
+  return v;
+}
+
+template <int S, int NB>
+static cudaError_t cg_spmv_staged_nb(bool tiles, bool fuse_fin, const StageMap& sm, const double* values,
+                                     const double* p, double* q, const FinArgs& f, cudaStream_t st) {
+  using Sh = StagedShape<S, NB>;
   // per device: SM count, published only after the shared-memory opt-in is
   // done (solves on several host threads launch concurrently)
   static std::atomic<int> sms[64];
@@ -582,26 +615,34 @@ static cudaError_t cg_spmv_staged_s(bool tiles, bool fuse_fin, const StageMap& s
       int count = 0;
       cudaError_t err = cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev);
       if (err == cudaSuccess)
-        err = cudaFuncSetAttribute(k_cg_spmv_staged<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM);
+        err = cudaFuncSetAttribute(k_cg_spmv_staged<S, true, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM);
       if (err == cudaSuccess)
-        err = cudaFuncSetAttribute(k_cg_spmv_staged<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM);
+        err = cudaFuncSetAttribute(k_cg_spmv_staged<S, false, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM);
       if (err != cudaSuccess) return err;
       sms[dev].store(count, std::memory_order_release);
     }
   }
-  const int nsm = sms[dev].load(std::memory_order_acquire);
+  const int slots = sms[dev].load(std::memory_order_acquire) * (NB == 2 ? 1 : 2);  // resident CTAs
   if (sm.nstages == 0) return cudaSuccess;
-  const int grid = sm.nstages < nsm ? sm.nstages : nsm;
+  const int grid = sm.nstages < slots ? sm.nstages : slots;
   if (tiles)
     // the fused finalize's grid barrier needs every CTA resident: a
     // cooperative launch guarantees it even with other streams' kernels
     // (possibly persistent ones of concurrent sample groups) on the GPU
-    launch_kk(2 | (fuse_fin ? kLaunchCooperative : 0), k_cg_spmv_staged<S, true>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
+    launch_kk(2 | (fuse_fin ? kLaunchCooperative : 0), k_cg_spmv_staged<S, true, NB>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
                                                            values, p, q, f, fuse_fin ? 1 : 0);
   else
-    launch_kk(2, k_cg_spmv_staged<S, false>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
+    launch_kk(2, k_cg_spmv_staged<S, false, NB>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
                                                             values, p, q, f, 0);
   return cudaGetLastError();
+}
+
+template <int S>
+static cudaError_t cg_spmv_staged_s(bool tiles, bool fuse_fin, const StageMap& sm, const double* values,
+                                    const double* p, double* q, const FinArgs& f, cudaStream_t st) {
+  if constexpr (S >= 16)  // s = 4's index blocks do not fit two CTAs per SM
+    if (staged_ctas() == 2) return cg_spmv_staged_nb<S, 1>(tiles, fuse_fin, sm, values, p, q, f, st);
+  return cg_spmv_staged_nb<S, 2>(tiles, fuse_fin, sm, values, p, q, f, st);
 }
 
 cudaError_t launch_cg_spmv_staged(int s, bool tiles, bool fuse_fin, const StageMap& sm,

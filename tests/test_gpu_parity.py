@@ -479,7 +479,11 @@ def test_symmetric_storage_is_bitwise_neutral(ctx, R, mode, s):
     y = dev(pack_group(R.draw_samples(3, s, m), s))
     kl = ep.KlField(m, 1.0, 0.2, 1.0)
     cfg = ep.SolverConfig(tol=1e-8, flavour=ep.CG_UNCOUPLED, dot_mode=mode)
-    ps = ep.Problem(ctx, n, s, kl)  # default: symmetric storage
+    ctx.set_option(ep.OPT_SYMMETRIC_STORAGE, 2)  # every width (default: s >= 4)
+    try:
+        ps = ep.Problem(ctx, n, s, kl)
+    finally:
+        ctx.set_option(ep.OPT_SYMMETRIC_STORAGE, 1)
     ctx.set_option(ep.OPT_SYMMETRIC_STORAGE, 0)
     try:
         pf = ep.Problem(ctx, n, s, kl)
