@@ -132,6 +132,17 @@ struct DistRank {
   int* counters = nullptr;
   int* plane_pos = nullptr;
   CgState* state = nullptr;
+  // staged mode (s in {4, 16, 32}, alpha = 0): symmetric storage of the store
+  // rows = lo ghost plane + owned rows (the ghost plane's upper slots are
+  // assembled here, no communication) and the stage-pipelined SpMV in owned
+  // coordinates (columns of the store graph are owned-row coordinates; the x
+  // runs reach the ghost planes of the ext p buffer)
+  bool staged = false;
+  int store_rows = 0;
+  int* vpos = nullptr;
+  int* up_start = nullptr;
+  int64_t nnz_stored = 0;
+  StageMap stage;
 };
 
 }  // namespace
@@ -186,8 +197,9 @@ void free_rank(DistRank& d) {
   for (void* q : {(void*)d.row_map, (void*)d.col_entry, (void*)d.values, (void*)d.residual,
                   (void*)d.x, (void*)d.r, (void*)d.q, (void*)d.p[0], (void*)d.p[1],
                   (void*)d.partials, (void*)d.seg[0], (void*)d.seg[1], (void*)d.gathered, (void*)d.hist,
-                  (void*)d.counters, (void*)d.plane_pos, (void*)d.state})
+                  (void*)d.counters, (void*)d.plane_pos, (void*)d.state, (void*)d.vpos, (void*)d.up_start})
     if (q) cudaFree(q);
+  free_stage_map(d.stage);
   d = DistRank{};
 }
 
@@ -201,14 +213,16 @@ int setup_rank(enprop_dist* D, DistRank& d, int r) {
   d.lo_rows = d.k0 > 0 ? plane : 0;
   d.hi_rows = d.k1 < N ? plane : 0;
   d.ext_begin = d.row_begin - d.lo_rows;
-  d.nnz = graph_start(n, d.row_begin + d.rows) - graph_start(n, d.row_begin);
+  d.staged = staged_supported(s, N) && D->desc.coeffs.alpha == 0.0 && D->ctx->symmetric_storage != 0;
+  d.store_rows = d.staged ? d.lo_rows + d.rows : d.rows;
+  const int store_begin = d.row_begin + d.rows - d.store_rows;  // ext_begin when staged
+  d.nnz = graph_start(n, d.row_begin + d.rows) - graph_start(n, store_begin);
   const size_t vec = (size_t)d.rows * s * sizeof(double);
   const size_t ext = (size_t)(d.lo_rows + d.rows + d.hi_rows) * s * sizeof(double);
   d.tm = make_tile_map(d.rows, plane);
-  EP_CUDA(cudaMalloc(&d.row_map, (d.rows + 1) * sizeof(int)));
+  EP_CUDA(cudaMalloc(&d.row_map, (d.store_rows + 1) * sizeof(int)));
   EP_CUDA(cudaMalloc(&d.col_entry, d.nnz * sizeof(int)));
-  EP_CUDA(cudaMalloc(&d.values, (size_t)d.nnz * s * sizeof(double)));
-  EP_CUDA(cudaMalloc(&d.residual, vec));
+  EP_CUDA(cudaMalloc(&d.residual, (size_t)d.store_rows * s * sizeof(double)));
   EP_CUDA(cudaMalloc(&d.x, vec));
   EP_CUDA(cudaMalloc(&d.r, vec));
   EP_CUDA(cudaMalloc(&d.q, vec));
@@ -234,9 +248,23 @@ int setup_rank(enprop_dist* D, DistRank& d, int r) {
   }
   EP_CUDA(cudaMalloc(&d.plane_pos, N * sizeof(int)));
   EP_CUDA(cudaMemcpy(d.plane_pos, pos.data(), N * sizeof(int), cudaMemcpyHostToDevice));
-  EP_CUDA(launch_build_graph_range(n, d.row_begin, d.rows, d.ext_begin, d.row_map, d.col_entry,
-                                   D->ctx->stream));
-  D->ctx->launches += 1;
+  cudaStream_t st = D->ctx->stream;
+  if (!d.staged) {  // full storage, columns in ext-buffer coordinates (the warp SpMV reads p from 0)
+    EP_CUDA(launch_build_graph_range(n, d.row_begin, d.rows, d.ext_begin, d.row_map, d.col_entry, st));
+    EP_CUDA(cudaMalloc(&d.values, (size_t)d.nnz * s * sizeof(double)));
+    d.nnz_stored = d.nnz;
+    D->ctx->launches += 1;
+    return ENPROP_OK;
+  }
+  // store rows [ext_begin, row_begin + rows), columns in owned coordinates
+  EP_CUDA(launch_build_graph_range(n, store_begin, d.store_rows, d.row_begin, d.row_map, d.col_entry, st));
+  EP_CUDA(cudaMalloc(&d.vpos, d.nnz * sizeof(int)));
+  EP_CUDA(cudaMalloc(&d.up_start, (d.store_rows + 1) * sizeof(int)));
+  EP_CUDA(build_sym(d.store_rows, d.row_map, d.col_entry, d.vpos, &d.nnz_stored, st, d.up_start, d.lo_rows));
+  EP_CUDA(cudaMalloc(&d.values, (size_t)d.nnz_stored * s * sizeof(double)));
+  EP_CUDA(build_stage_map(s, d.tm, N, d.row_map + d.lo_rows, d.col_entry, d.vpos, d.up_start + d.lo_rows,
+                          d.stage, st, -d.lo_rows, d.rows + d.hi_rows));
+  D->ctx->launches += 4;
   return ENPROP_OK;
 }
 
@@ -651,14 +679,14 @@ int enprop_dist_assemble(enprop_dist* D, const double* y) {
   if (!D || !y) return fail(ENPROP_ERR_INVALID, "enprop_dist_assemble: null argument");
   for (auto& d : D->ranks) {
     AsmArgs a = D->setup.args;
-    a.rows = d.rows;
-    a.row_begin = d.row_begin;
+    a.rows = d.store_rows;  // staged: the lo ghost plane's upper slots too (no communication)
+    a.row_begin = d.row_begin + d.rows - d.store_rows;
     a.u = nullptr;
     a.y = y;
     a.row_map = d.row_map;
     a.values = d.values;
     a.residual = d.residual;
-    a.vpos = nullptr;  // slabs keep the full CRS (lower entries of boundary rows live on the neighbour)
+    a.vpos = d.vpos;  // full storage (unstaged): nullptr
     a.dirichlet = 1;
     a.bc0 = D->desc.bc.x0_value;
     a.bc1 = D->desc.bc.x1_value;
@@ -697,7 +725,8 @@ int enprop_dist_solve(enprop_dist* D, const enprop_cg_options* opt, int* iterati
     const size_t vec = (size_t)d.rows * s * sizeof(double);
     EP_CUDA(cudaMemcpyAsync(d.state, &init, sizeof(init), cudaMemcpyHostToDevice, st));
     EP_CUDA(cudaMemsetAsync(d.x, 0, vec, st));
-    EP_CUDA(launch_negate((int64_t)d.rows * s, d.residual, d.r, st));  // b = -residual; r = b
+    EP_CUDA(launch_negate((int64_t)d.rows * s, d.residual + (size_t)(d.store_rows - d.rows) * s, d.r,
+                          st));  // b = -residual (owned rows); r = b
     EP_CUDA(launch_dot_tiles(s, d.tm, d.r, d.r, rank_fin(d, kPhaseInit), st));
     EP_CUDA(launch_fin_segments(s, d.tm, rank_fin(d, kPhaseInit), st));
     ctx->launches += 3;
@@ -721,9 +750,13 @@ int enprop_dist_solve(enprop_dist* D, const enprop_cg_options* opt, int* iterati
       }
       if ((rc = halo(D, pn))) return rc;
       for (auto& d : D->ranks) {
-        EP_CUDA(launch_cg_spmv(s, true, false, false, d.tm, d.row_map, d.col_entry, d.values, d.r,
-                               d.p[po] + (size_t)d.lo_rows * s, d.p[pn] + (size_t)d.lo_rows * s, d.q,
-                               d.x, d.p[pn], nullptr, rank_fin(d, kPhasePQ), st));
+        if (d.staged)
+          EP_CUDA(launch_cg_spmv_staged(s, true, false, d.stage, d.values, d.p[pn] + (size_t)d.lo_rows * s, d.q,
+                                        rank_fin(d, kPhasePQ), st));
+        else
+          EP_CUDA(launch_cg_spmv(s, true, false, false, d.tm, d.row_map, d.col_entry, d.values, d.r,
+                                 d.p[po] + (size_t)d.lo_rows * s, d.p[pn] + (size_t)d.lo_rows * s, d.q,
+                                 d.x, d.p[pn], nullptr, rank_fin(d, kPhasePQ), st));
         EP_CUDA(launch_fin_segments(s, d.tm, rank_fin(d, kPhasePQ), st));
         ctx->launches += 2;
       }

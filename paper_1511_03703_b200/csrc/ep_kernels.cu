@@ -1128,12 +1128,14 @@ cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* r, co
 // included, in column order): nnz_up = (nnz + rows)/2 for a structurally
 // symmetric graph. vpos[k] maps every entry of the full CRS to its slot.
 // =============================================================================
-__global__ void k_sym_count(int rows, const int* __restrict__ row_map,
+// Graph row r has coordinate r - base (a slab's store rows: `base` ghost rows
+// before the owned ones; columns are in owned coordinates); base = 0 on one GPU.
+__global__ void k_sym_count(int rows, int base, const int* __restrict__ row_map,
                             const int* __restrict__ col_entry, int* __restrict__ cnt) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
   int c = 0;
-  for (int k = row_map[r]; k < row_map[r + 1]; ++k) c += col_entry[k] >= r;
+  for (int k = row_map[r]; k < row_map[r + 1]; ++k) c += col_entry[k] >= r - base;
   cnt[r] = c;
 }
 
@@ -1147,26 +1149,33 @@ __device__ __forceinline__ int lower_bound_i(const int* a, int lo, int hi, int v
   return lo;
 }
 
-__global__ void k_sym_vpos(int rows, const int* __restrict__ row_map,
+__global__ void k_sym_vpos(int rows, int base, const int* __restrict__ row_map,
                            const int* __restrict__ col_entry, const int* __restrict__ up_start,
                            int* __restrict__ vpos, int* __restrict__ bad) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= rows) return;
+  const int rc = r - base;  // this row's coordinate
   const int rs = row_map[r], re = row_map[r + 1];
-  const int first_up = lower_bound_i(col_entry, rs, re, r);
+  const int first_up = lower_bound_i(col_entry, rs, re, rc);
   for (int k = rs; k < re; ++k) {
     const int c = col_entry[k];
-    if (c >= r) {
+    if (c >= rc) {
       vpos[k] = up_start[r] + (k - first_up);
     } else {  // transposed entry (c, r) in row c's upper part
-      const int cs = row_map[c], ce = row_map[c + 1];
+      const int cr = c + base;  // graph row of column c
+      if (cr < 0) {             // a ghost row's lower entry: never read
+        if (r >= base) atomicAdd(bad, 1);
+        vpos[k] = -1;
+        continue;
+      }
+      const int cs = row_map[cr], ce = row_map[cr + 1];
       const int fu = lower_bound_i(col_entry, cs, ce, c);
-      const int t = lower_bound_i(col_entry, fu, ce, r);
-      if (t >= ce || col_entry[t] != r) {
+      const int t = lower_bound_i(col_entry, fu, ce, rc);
+      if (t >= ce || col_entry[t] != rc) {
         atomicAdd(bad, 1);  // pattern not symmetric
         vpos[k] = 0;
       } else {
-        vpos[k] = up_start[c] + (t - fu);
+        vpos[k] = up_start[cr] + (t - fu);
       }
     }
   }
@@ -1203,7 +1212,7 @@ cudaError_t launch_sym_expand(int s, int64_t nnz, const int* vpos, const double*
 namespace ep {
 
 cudaError_t build_sym(int rows, const int* row_map, const int* col_entry, int* vpos,
-                      int64_t* nnz_up, cudaStream_t st, int* up_start) {
+                      int64_t* nnz_up, cudaStream_t st, int* up_start, int base) {
   int *cnt = nullptr, *start = nullptr, *bad = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
@@ -1213,14 +1222,14 @@ cudaError_t build_sym(int rows, const int* row_map, const int* col_entry, int* v
   if (err == cudaSuccess) err = cudaMemsetAsync(bad, 0, sizeof(int), st);
   if (err == cudaSuccess) err = cudaMemsetAsync(cnt + rows, 0, sizeof(int), st);
   if (err == cudaSuccess && rows > 0) {
-    k_sym_count<<<(rows + 255) / 256, 256, 0, st>>>(rows, row_map, col_entry, cnt);
+    k_sym_count<<<(rows + 255) / 256, 256, 0, st>>>(rows, base, row_map, col_entry, cnt);
     err = cudaGetLastError();
   }
   if (err == cudaSuccess) err = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, start, rows + 1, st);
   if (err == cudaSuccess) err = cudaMalloc(&tmp, tmp_bytes ? tmp_bytes : 8);
   if (err == cudaSuccess) err = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, start, rows + 1, st);
   if (err == cudaSuccess && rows > 0) {
-    k_sym_vpos<<<(rows + 255) / 256, 256, 0, st>>>(rows, row_map, col_entry, start, vpos, bad);
+    k_sym_vpos<<<(rows + 255) / 256, 256, 0, st>>>(rows, base, row_map, col_entry, start, vpos, bad);
     err = cudaGetLastError();
   }
   if (err == cudaSuccess && up_start)

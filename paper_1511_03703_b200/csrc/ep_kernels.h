@@ -153,8 +153,11 @@ cudaError_t launch_cg_update(int s, bool tiles, const TileMap& tm, double* r, co
 // to its stored slot; nnz_up = stored entries. Fails (InvalidValue) if the
 // pattern is not structurally symmetric.
 // up_start (optional, rows + 1 ints): first stored slot of each row.
+// base: graph row r has coordinate r - base and columns are coordinates (a
+// slab's store rows = `base` ghost rows + owned rows); ghost rows' lower
+// entries get vpos = -1 (never read).
 cudaError_t build_sym(int rows, const int* row_map, const int* col_entry, int* vpos,
-                      int64_t* nnz_up, cudaStream_t st, int* up_start = nullptr);
+                      int64_t* nnz_up, cudaStream_t st, int* up_start = nullptr, int base = 0);
 // full[k] = up[vpos[k]] (views / checks)
 cudaError_t launch_sym_expand(int s, int64_t nnz, const int* vpos, const double* up, double* full,
                               cudaStream_t st);
@@ -173,6 +176,7 @@ struct StageDesc {
 
 struct StageMap {
   int nstages = 0, s = 0, N = 0;
+  int xlo = 0, xhi = 0;  // rows of p the x runs may read: [xlo, xhi) (slab: ghost planes included)
   TileMap tm{};
   StageDesc* desc = nullptr;
   unsigned char* blk = nullptr;
@@ -183,9 +187,11 @@ bool staged_supported(int s, int N);
 // N = mesh nodes per axis (rows == N^3, the k_build_graph numbering); up_start =
 // first stored slot of each row (rows + 1). Fails (InvalidValue) for graphs
 // that are not the structured 27-point pattern.
+// Slabs: tm.rows is a multiple of N^2 (owned planes), columns and the x runs
+// may reach [xlo, xhi) (defaults: [0, tm.rows)).
 cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
                             const int* col_entry, const int* vpos, const int* up_start,
-                            StageMap& sm, cudaStream_t st);
+                            StageMap& sm, cudaStream_t st, int xlo = 0, int xhi = -1);
 void free_stage_map(StageMap& sm);
 // q = A p and (tiles) the canonical p.q tile partials; bitwise equal to the
 // warp-per-tile kernel

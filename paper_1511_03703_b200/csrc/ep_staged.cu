@@ -83,7 +83,7 @@ template <int S, int NB = 2>
 struct StagedCta {
   using Sh = StagedShape<S, NB>;
   const TileMap& tm;
-  int N, nstages;
+  int N, nstages, xlo, xhi;
   const StageDesc* __restrict__ desc;
   const unsigned char* __restrict__ blk;
   const double* __restrict__ values;
@@ -130,14 +130,14 @@ struct StagedCta {
   __device__ __forceinline__ void issue_big(int it, const StageDesc& d) const {
     unsigned char* sb = big(it);
     uint64_t* b = big_bar(it);
-    const int rows = tm.rows, NN = N * N;
+    const int NN = N * N;
     const int L = d.R1 - d.R0 + 2;
     const uint32_t upb = (uint32_t)(d.slot1 - d.slot0) * Sh::CH;
     uint32_t total = upb;
 #pragma unroll
     for (int run = 0; run < 9; ++run) {
       const int a = d.R0 - 1 + (run % 3 - 1) * N + (run / 3 - 1) * NN;
-      const int lo = a > 0 ? a : 0, hi = a + L < rows ? a + L : rows;
+      const int lo = a > xlo ? a : xlo, hi = a + L < xhi ? a + L : xhi;
       if (hi > lo) total += (uint32_t)(hi - lo) * Sh::CH;
     }
     mbar_arrive_expect_tx(b, total);
@@ -145,9 +145,9 @@ struct StagedCta {
 #pragma unroll
     for (int run = 0; run < 9; ++run) {
       const int a = d.R0 - 1 + (run % 3 - 1) * N + (run / 3 - 1) * NN;
-      const int lo = a > 0 ? a : 0, hi = a + L < rows ? a + L : rows;
+      const int lo = a > xlo ? a : xlo, hi = a + L < xhi ? a + L : xhi;
       if (hi > lo)
-        bulk_g2s(sb + (size_t)(Sh::UP_CHUNKS + run * Sh::L + (lo - a)) * Sh::CH, p + (size_t)lo * S,
+        bulk_g2s(sb + (size_t)(Sh::UP_CHUNKS + run * Sh::L + (lo - a)) * Sh::CH, p + (ptrdiff_t)lo * S,
                  (uint32_t)(hi - lo) * Sh::CH, b);
     }
   }
@@ -311,7 +311,7 @@ __device__ __forceinline__ void grid_barrier(int* count, int* gen, int nblocks) 
 
 template <int S, bool kTiles, int NB>
 __global__ void __launch_bounds__(256, NB == 2 ? 1 : 2) k_cg_spmv_staged(
-    const TileMap tm, int N, int nstages, const StageDesc* __restrict__ desc,
+    const TileMap tm, int N, int nstages, int xlo, int xhi, const StageDesc* __restrict__ desc,
     const unsigned char* __restrict__ blk, const double* __restrict__ values,
     const double* __restrict__ p, double* __restrict__ q, const FinArgs f, int fuse_fin) {
   using Sh = StagedShape<S, NB>;
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(256, NB == 2 ? 1 : 2) k_cg_spmv_staged(
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   unsigned char* tail = smem + NB * Sh::BIG_BYTES + Sh::NIDX * Sh::IDX_BYTES + 2 * Sh::RED_BYTES;
-  StagedCta<S, NB> c{tm, N, nstages, desc, blk, values, p, q, f, smem,
+  StagedCta<S, NB> c{tm, N, nstages, xlo, xhi, desc, blk, values, p, q, f, smem,
                  reinterpret_cast<uint64_t*>(tail),
                  reinterpret_cast<double*>(smem + NB * Sh::BIG_BYTES + Sh::NIDX * Sh::IDX_BYTES),
                  reinterpret_cast<int*>(tail + 64), f.ticket,
@@ -487,9 +487,9 @@ bool staged_supported(int s, int N) { return (s == 4 || s == 16 || s == 32) && N
 
 cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
                             const int* col_entry, const int* vpos, const int* up_start,
-                            StageMap& sm, cudaStream_t st) {
+                            StageMap& sm, cudaStream_t st, int xlo, int xhi) {
   free_stage_map(sm);
-  if (!staged_supported(s, N) || tm.rows != N * N * N) return cudaErrorInvalidValue;
+  if (!staged_supported(s, N) || tm.rows <= 0 || tm.rows % (N * N) != 0) return cudaErrorInvalidValue;
   int T = 0, L = 0, RS = 0, max_upper = 0, idx_bytes = 0, zc = 0;
   if (s == 32) stage_shape<32>(T, L, RS, max_upper, idx_bytes, zc);
   else if (s == 16) stage_shape<16>(T, L, RS, max_upper, idx_bytes, zc);
@@ -558,6 +558,8 @@ cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
   sm.s = s;
   sm.N = N;
   sm.tm = tm;
+  sm.xlo = xlo;
+  sm.xhi = xhi < 0 ? tm.rows : xhi;
   sm.blk_bytes = off;
   int* bad = nullptr;
   err = cudaMalloc(&sm.desc, hd.size() * sizeof(StageDesc) + 16);
@@ -629,10 +631,10 @@ static cudaError_t cg_spmv_staged_nb(bool tiles, bool fuse_fin, const StageMap& 
     // the fused finalize's grid barrier needs every CTA resident: a
     // cooperative launch guarantees it even with other streams' kernels
     // (possibly persistent ones of concurrent sample groups) on the GPU
-    launch_kk(2 | (fuse_fin ? kLaunchCooperative : 0), k_cg_spmv_staged<S, true, NB>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
+    launch_kk(2 | (fuse_fin ? kLaunchCooperative : 0), k_cg_spmv_staged<S, true, NB>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.xlo, sm.xhi, sm.desc, sm.blk,
                                                            values, p, q, f, fuse_fin ? 1 : 0);
   else
-    launch_kk(2, k_cg_spmv_staged<S, false, NB>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.desc, sm.blk,
+    launch_kk(2, k_cg_spmv_staged<S, false, NB>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.xlo, sm.xhi, sm.desc, sm.blk,
                                                             values, p, q, f, 0);
   return cudaGetLastError();
 }

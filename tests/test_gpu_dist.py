@@ -25,7 +25,7 @@ def same(a, b):
     return a.shape == b.shape and (bits(a) == bits(b)).all()
 
 
-@pytest.mark.parametrize("s", [1, 8, 32])
+@pytest.mark.parametrize("s", [1, 4, 8, 16, 32])  # 4, 16, 32: symmetric storage + the staged SpMV per slab
 @pytest.mark.parametrize("flavour", [CG_COUPLED, CG_UNCOUPLED])
 @pytest.mark.parametrize("nranks", [1, 2, 3, 5, 11])
 def test_emulated_ranks_equal_one_gpu_bitwise(ctx, s, flavour, nranks):
