@@ -55,7 +55,10 @@ struct ChainRing {
 // (default); 4 stages (64 KB) let a chain CTA share an SM with a staged-SpMV
 // CTA of the two-per-SM layout
 int chain_stages() {
-  static const int v = env_int("ENPROP_CHAIN_STAGES", 8) == 4 ? 4 : 8;
+  static const int v = [] {
+    const int e = env_int("ENPROP_CHAIN_STAGES", 8);
+    return e == 4 || e == 6 || e == 10 || e == 12 ? e : 8;
+  }();
   return v;
 }
 
@@ -277,6 +280,9 @@ static cudaError_t chain_skd(int rows, const double* u, const double* v, const F
 template <int S, int KIND>
 static cudaError_t chain_sk(int rows, const double* u, const double* v, const FinArgs& f, cudaStream_t st) {
   if (KIND != kChainProduct && chain_stages() == 4) return chain_skd<S, KIND, 4>(rows, u, v, f, st);
+  if (KIND != kChainProduct && chain_stages() == 6) return chain_skd<S, KIND, 6>(rows, u, v, f, st);
+  if (KIND != kChainProduct && chain_stages() == 10) return chain_skd<S, KIND, 10>(rows, u, v, f, st);
+  if (KIND != kChainProduct && chain_stages() == 12) return chain_skd<S, KIND, 12>(rows, u, v, f, st);
   return chain_skd<S, KIND, KIND == kChainProduct ? 6 : 8>(rows, u, v, f, st);
 }
 
