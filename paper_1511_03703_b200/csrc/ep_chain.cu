@@ -11,8 +11,9 @@
 //  * one CTA per dot; warp 0 consumes: lane e < S runs sample e's chain, so a
 //    row's S values are one contiguous 8S-byte read from shared memory and the
 //    chain never hands off between lanes;
-//  * warp 1 lane 0 produces: rows arrive as 16 KB stages (per operand) via
-//    cp.async.bulk into a ring of kChainStages, completing on mbarriers; the
+//  * warp 1 lane 0 produces: rows arrive as 32 KB stages (per operand) via
+//    cp.async.bulk into a 4-stage ring (3 for two operands), completing on
+//    mbarriers; the
 //    producer alone waits on `empty` barriers, so copy issue stays off the
 //    chain;
 //  * the consumer walks a stage in fully unrolled 64-row blocks (the compiler
@@ -44,9 +45,9 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 constexpr int kChainChunkBytes = 16384;  // per operand vector per stage
 constexpr int kChainBlock = 64;          // rows per unrolled consumer block
 
-template <int NV, int D_ = (NV == 1 ? 8 : 6)>
+template <int NV, int D_ = (NV == 1 ? 8 : 6), int CB = kChainChunkBytes>
 struct ChainRing {
-  static constexpr int STAGE = kChainChunkBytes * NV;
+  static constexpr int STAGE = CB * NV;
   static constexpr int D = D_;  // stages in the ring (default 128 / 192 KB)
   static constexpr int SMEM = D * STAGE + 2 * D * 8;
 };
@@ -70,15 +71,15 @@ __device__ __forceinline__ double chain_term(const double* a, const double* b, i
   else return EP_DMUL(x, b[i * S]);
 }
 
-template <int S, int KIND, int DEPTH>
+template <int S, int KIND, int DEPTH, int CB>
 __global__ void __launch_bounds__(64, 1) k_chain(int rows, const double* __restrict__ u,
                                                  const double* __restrict__ v, const FinArgs f) {
   EP_PDL_ENTRY();
   if ((f.phase == kPhasePQ || f.phase == kPhaseRR) && f.cg->done) return;
   constexpr int NV = KIND == kChainProduct ? 2 : 1;
-  using Ring = ChainRing<NV, DEPTH>;
+  using Ring = ChainRing<NV, DEPTH, CB>;
   constexpr int D = Ring::D;
-  constexpr int R = kChainChunkBytes / (8 * S);  // rows per stage
+  constexpr int R = CB / (8 * S);  // rows per stage
   constexpr int BLK = R < kChainBlock ? R : kChainBlock;
   static_assert(R % BLK == 0, "stage must hold whole blocks");
   extern __shared__ __align__(128) unsigned char smem[];
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(64, 1) k_chain(int rows, const double* __restr
       if (bytes) {
         bulk_g2s(smem + slot * Ring::STAGE, u + (size_t)r0 * S, bytes, &full[slot]);
         if constexpr (NV == 2)
-          bulk_g2s(smem + slot * Ring::STAGE + kChainChunkBytes, v + (size_t)r0 * S, bytes, &full[slot]);
+          bulk_g2s(smem + slot * Ring::STAGE + CB, v + (size_t)r0 * S, bytes, &full[slot]);
       }
     }
     return;
@@ -121,13 +122,18 @@ __global__ void __launch_bounds__(64, 1) k_chain(int rows, const double* __restr
     const int slot = c % D;
     mbar_wait(&full[slot], (c / D) & 1);
     const double* a = reinterpret_cast<const double*>(smem + slot * Ring::STAGE) + el;
-    const double* b = a + kChainChunkBytes / 8;
+    const double* b = a + CB / 8;
     const int nr = imin(R, rows - c * R);
     if (nr == R) {
+      // a block's terms (loads and, for squares / products, the DMULs) are
+      // formed before its add chain, so only the DADDs are dependent
 #pragma unroll 1
       for (int r0 = 0; r0 < R; r0 += BLK) {
+        double t[BLK];
 #pragma unroll
-        for (int i = 0; i < BLK; ++i) acc = EP_DADD(acc, (chain_term<S, KIND>(a, b, r0 + i)));
+        for (int i = 0; i < BLK; ++i) t[i] = chain_term<S, KIND>(a, b, r0 + i);
+#pragma unroll
+        for (int i = 0; i < BLK; ++i) acc = EP_DADD(acc, t[i]);
       }
     } else {  // last, partial stage
       const int nb = S == 1 ? (nr & ~1) : nr;
@@ -253,10 +259,10 @@ bool chain_aligned(const void* u, const void* v) {
   return ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
 }
 
-template <int S, int KIND, int DEPTH>
+template <int S, int KIND, int DEPTH, int CB = kChainChunkBytes>
 static cudaError_t chain_skd(int rows, const double* u, const double* v, const FinArgs& f, cudaStream_t st) {
   constexpr int NV = KIND == kChainProduct ? 2 : 1;
-  constexpr int SMEM = ChainRing<NV, DEPTH>::SMEM;
+  constexpr int SMEM = ChainRing<NV, DEPTH, CB>::SMEM;
   // shared-memory opt-in once per device (solves on several host threads)
   static std::atomic<int> ready[64];
   static std::mutex mu;
@@ -267,18 +273,29 @@ static cudaError_t chain_skd(int rows, const double* u, const double* v, const F
   if (!ready[dev].load(std::memory_order_acquire)) {
     std::lock_guard<std::mutex> lock(mu);
     if (!ready[dev].load(std::memory_order_relaxed)) {
-      err = cudaFuncSetAttribute(k_chain<S, KIND, DEPTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+      err = cudaFuncSetAttribute(k_chain<S, KIND, DEPTH, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
       if (err != cudaSuccess) return err;
       ready[dev].store(1, std::memory_order_release);
     }
   }
   if (chain_mode() == 1) launch_kk(4, k_chain_small<S, KIND>, dim3(1), dim3(32), 0, st, rows, u, v, f);
-  else launch_kk(4, k_chain<S, KIND, DEPTH>, dim3(1), dim3(64), SMEM, st, rows, u, v, f);
+  else launch_kk(4, k_chain<S, KIND, DEPTH, CB>, dim3(1), dim3(64), SMEM, st, rows, u, v, f);
   return cudaGetLastError();
+}
+
+// ENPROP_CHAIN_CHUNK (A/B): bytes per operand per stage, 32768 (default: 4
+// stages, 128 KB) or 16384 (8 stages, the same ring bytes). The larger stage
+// halves the per-stage barrier waits: 64^3, s = 32, p.q 1.57 -> 1.41 ms,
+// r.r 1.85 -> 1.66 ms per dot (tools/serial_ab.py)
+int chain_chunk() {
+  static const int v = env_int("ENPROP_CHAIN_CHUNK", 32768) == 16384 ? 16384 : 32768;
+  return v;
 }
 
 template <int S, int KIND>
 static cudaError_t chain_sk(int rows, const double* u, const double* v, const FinArgs& f, cudaStream_t st) {
+  if (chain_chunk() == 32768 && chain_stages() == 8)
+    return chain_skd<S, KIND, KIND == kChainProduct ? 3 : 4, 32768>(rows, u, v, f, st);
   if (KIND != kChainProduct && chain_stages() == 4) return chain_skd<S, KIND, 4>(rows, u, v, f, st);
   if (KIND != kChainProduct && chain_stages() == 6) return chain_skd<S, KIND, 6>(rows, u, v, f, st);
   if (KIND != kChainProduct && chain_stages() == 10) return chain_skd<S, KIND, 10>(rows, u, v, f, st);
