@@ -363,7 +363,28 @@ int enprop_dist_local(enprop_dist* d, int index, int* rank, int* row_begin, int*
  * seconds per exchange over `reps`, CUDA events on the context's stream. */
 int enprop_dist_time_halo(enprop_dist* d, int reps, double* seconds);
 
+/* One message of a halo exchange (ExchangeRecord, halo.hpp:86-91): here `time`
+ * is MEASURED -- the sender's cumulative seconds of its messages in this
+ * exchange (CUDA events around each copy / NCCL send-receive), where the
+ * reference accumulates a virtual clock. */
+typedef struct {
+  int rank, neighbor;
+  int64_t bytes;
+  double time;
+} enprop_exchange_record;
+/* One measured halo exchange of the solver's p buffer (one plane of s values
+ * to each neighbour), records in the reference's order (sender rank, then its
+ * lower link before its upper link: partition.cpp:59-72). Emulated: every
+ * rank's messages; NCCL / IPC: the messages this process takes part in (IPC
+ * pulls: sender = the neighbour). elapsed = max cumulative time over senders. */
+int enprop_dist_exchange_trace(enprop_dist* d, enprop_exchange_record* out, int max_records,
+                               int* count, double* elapsed_seconds);
+
 /* ------------------------------------------------ halo timing model (host) */
+/* write_exchange_trace_csv (halo.cpp:192-202): header
+ * "rank,neighbor,bytes,virtual_time", one "%d,%d,%lld,%.17g" line per record;
+ * INVALID when the file cannot be written. */
+int enprop_write_exchange_trace_csv(const char* path, const enprop_exchange_record* recs, int count);
 /* fit_halo_model (halo.cpp:156-181): least-squares T(s) = a + b*s through
  * (s[i], t[i]), i < n; INVALID for n < 2 or all s equal (singular). */
 int enprop_fit_halo_model(int n, const double* s, const double* t, double* a, double* b,

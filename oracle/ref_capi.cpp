@@ -386,6 +386,16 @@ int ref_newton_identity(int s, int scalar, int n, int m, double mean, double sig
   });
 }
 
+// write_exchange_trace_csv (halo.cpp:192-202) on given records
+int ref_write_trace_csv(const char* path, int n, const int* rank, const int* nb, const int64_t* bytes,
+                        const double* t) {
+  return guarded([&] {
+    std::vector<ExchangeRecord> tr(n);
+    for (int i = 0; i < n; ++i) tr[i] = ExchangeRecord{rank[i], nb[i], bytes[i], t[i]};
+    write_exchange_trace_csv(path, tr);
+  });
+}
+
 // fit_halo_model / predicted_speedup (halo.cpp:156-188).
 int ref_fit_halo_model(int n, const double* s, const double* t, double* a, double* b, double* rss) {
   return guarded([&] {

@@ -88,6 +88,10 @@ class _MgOptions(C.Structure):
                 ("power_iterations", C.c_int)]
 
 
+class _ExchangeRecord(C.Structure):
+    _fields_ = [("rank", C.c_int), ("neighbor", C.c_int), ("bytes", C.c_int64), ("time", C.c_double)]
+
+
 class _ProblemDesc(C.Structure):
     _fields_ = [("cells_per_axis", C.c_int), ("ensemble_size", C.c_int), ("kl", _KlParams),
                 ("coeffs", _Coeffs), ("bc", _Bc)]
@@ -233,6 +237,8 @@ def lib() -> C.CDLL:
     L.enprop_mg_pcg.argtypes = [_vp, _vp, _vp, C.POINTER(_CgOptions), _ip, _ip, _dp, _ip]
     L.enprop_dist_create_ipc.argtypes = [_vp, C.POINTER(_ProblemDesc), C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]
     L.enprop_dist_destroy.argtypes = [_vp]
+    L.enprop_dist_exchange_trace.argtypes = [_vp, C.POINTER(_ExchangeRecord), C.c_int, _ip, _dp]
+    L.enprop_write_exchange_trace_csv.argtypes = [C.c_char_p, C.POINTER(_ExchangeRecord), C.c_int]
     L.enprop_dist_assemble.argtypes = [_vp, _vp]
     L.enprop_dist_solve.argtypes = [_vp, C.POINTER(_CgOptions), _ip, _ip]
     L.enprop_dist_local_count.argtypes = [_vp]
@@ -727,6 +733,15 @@ def fit_halo_model(samples):
     return a.value, b.value, r.value
 
 
+def write_exchange_trace_csv(path: str, records) -> None:
+    """write_exchange_trace_csv (halo.cpp:192-202): records of (rank, neighbor,
+    bytes, time) -- e.g. Dist.exchange_trace()[0]."""
+    arr = (_ExchangeRecord * max(len(records), 1))()
+    for i, (rk, nb, by, t) in enumerate(records):
+        arr[i] = _ExchangeRecord(rk, nb, by, t)
+    _check(lib().enprop_write_exchange_trace_csv(path.encode(), arr, len(records)), "write_exchange_trace_csv")
+
+
 def predicted_speedup(a: float, b: float, s: float) -> float:
     """predicted_speedup (halo.cpp:183-188): s*(a + b)/(a + b*s)."""
     out = C.c_double()
@@ -785,6 +800,15 @@ class Dist:
         sec = C.c_double()
         _check(lib().enprop_dist_time_halo(self.h, reps, C.byref(sec)), "time_halo")
         return sec.value
+
+    def exchange_trace(self, max_records: int = 4096):
+        """One measured halo exchange: ([(rank, neighbor, bytes, cumulative seconds)], elapsed
+        seconds) in the reference's record order (halo.cpp:140-150)."""
+        recs = (_ExchangeRecord * max_records)()
+        n, el = C.c_int(), C.c_double()
+        _check(lib().enprop_dist_exchange_trace(self.h, recs, max_records, C.byref(n), C.byref(el)),
+               "exchange_trace")
+        return [(recs[i].rank, recs[i].neighbor, recs[i].bytes, recs[i].time) for i in range(n.value)], el.value
 
     def local(self):
         """[(rank, row_begin, rows, x view [rows][s])] of the ranks in this process."""

@@ -622,6 +622,118 @@ int enprop_dist_time_halo(enprop_dist* D, int reps, double* seconds) {
   return ENPROP_OK;
 }
 
+int enprop_write_exchange_trace_csv(const char* path, const enprop_exchange_record* recs, int count) {
+  // halo.cpp:192-202, same format
+  if (!path || count < 0 || (count > 0 && !recs))
+    return fail(ENPROP_ERR_INVALID, "write_exchange_trace_csv: bad argument");
+  std::FILE* f = std::fopen(path, "w");
+  if (f == nullptr) return fail(ENPROP_ERR_INVALID, std::string("write_exchange_trace_csv: cannot open ") + path);
+  std::fputs("rank,neighbor,bytes,virtual_time\n", f);
+  for (int i = 0; i < count; ++i)
+    std::fprintf(f, "%d,%d,%lld,%.17g\n", recs[i].rank, recs[i].neighbor, static_cast<long long>(recs[i].bytes),
+                 recs[i].time);
+  if (std::fclose(f) != 0)
+    return fail(ENPROP_ERR_INVALID, std::string("write_exchange_trace_csv: failed writing ") + path);
+  return ENPROP_OK;
+}
+
+int enprop_dist_exchange_trace(enprop_dist* D, enprop_exchange_record* out, int max_records, int* count,
+                               double* elapsed_seconds) {
+  if (!D || !count) return fail(ENPROP_ERR_INVALID, "enprop_dist_exchange_trace: null argument");
+  const int s = D->desc.ensemble_size;
+  const size_t pe = (size_t)D->plane * s;
+  const int64_t bytes = (int64_t)pe * sizeof(double);
+  cudaStream_t st = D->ctx->stream;
+  struct Msg {
+    int from, to;
+    cudaEvent_t a, b;
+  };
+  std::vector<Msg> msgs;
+  auto timed = [&](int from, int to, auto&& issue) -> int {
+    Msg m{from, to, nullptr, nullptr};
+    EP_CUDA(cudaEventCreate(&m.a));
+    EP_CUDA(cudaEventCreate(&m.b));
+    msgs.push_back(m);
+    EP_CUDA(cudaEventRecord(m.a, st));
+    int rc = issue();
+    if (rc) return rc;
+    EP_CUDA(cudaEventRecord(m.b, st));
+    return ENPROP_OK;
+  };
+  int rc = halo(D, 0);  // warm-up (connection setup)
+  if (rc) return rc;
+  if (D->emulated) {
+    for (size_t i = 0; i < D->ranks.size() && !rc; ++i) {
+      DistRank& d = D->ranks[i];
+      if (i > 0) {
+        DistRank& lo = D->ranks[i - 1];
+        rc = timed((int)i, (int)i - 1, [&]() -> int {
+          EP_CUDA(cudaMemcpyAsync(lo.p[0] + (size_t)(lo.lo_rows + lo.rows) * s, d.p[0] + (size_t)d.lo_rows * s,
+                                  pe * sizeof(double), cudaMemcpyDeviceToDevice, st));
+          return ENPROP_OK;
+        });
+      }
+      if (!rc && i + 1 < D->ranks.size()) {
+        DistRank& hi = D->ranks[i + 1];
+        rc = timed((int)i, (int)i + 1, [&]() -> int {
+          EP_CUDA(cudaMemcpyAsync(hi.p[0], d.p[0] + (size_t)(d.lo_rows + d.rows - D->plane) * s,
+                                  pe * sizeof(double), cudaMemcpyDeviceToDevice, st));
+          return ENPROP_OK;
+        });
+      }
+    }
+  } else if (D->transport == kIpc) {
+    DistRank& d = D->ranks[0];
+    rc = ipc_publish(D, kEvP);
+    for (int nb : {d.rank - 1, d.rank + 1}) {
+      if (rc || nb < 0 || nb >= D->nranks) continue;
+      int lo, lr, rws;
+      rank_layout(D, nb, lo, lr, rws);
+      if ((rc = ipc_wait(D, nb, kEvP))) break;
+      rc = timed(nb, d.rank, [&]() -> int {
+        double* dst = nb < d.rank ? d.p[0] : d.p[0] + (size_t)(d.lo_rows + d.rows) * s;
+        const double* src = D->peer_p[0][nb] + (size_t)(nb < d.rank ? lr + rws - D->plane : lr) * s;
+        EP_CUDA(cudaMemcpyAsync(dst, src, pe * sizeof(double), cudaMemcpyDefault, st));
+        return ENPROP_OK;
+      });
+    }
+  } else {  // NCCL: each link's send/receive pair as its own group
+    DistRank& d = D->ranks[0];
+    auto& api = nccl();
+    for (int nb : {d.rank - 1, d.rank + 1}) {
+      if (rc || nb < 0 || nb >= D->nranks) continue;
+      rc = timed(d.rank, nb, [&]() -> int {
+        const bool down = nb < d.rank;
+        EP_NCCL(api.GroupStart());
+        EP_NCCL(api.Send(d.p[0] + (size_t)(down ? d.lo_rows : d.lo_rows + d.rows - D->plane) * s, pe, ncclDouble, nb,
+                         D->comm, st));
+        EP_NCCL(api.Recv(down ? d.p[0] : d.p[0] + (size_t)(d.lo_rows + d.rows) * s, pe, ncclDouble, nb, D->comm, st));
+        EP_NCCL(api.GroupEnd());
+        return ENPROP_OK;
+      });
+    }
+  }
+  cudaError_t err = cudaStreamSynchronize(st);
+  std::vector<double> clock(D->nranks, 0.0);
+  double elapsed = 0.0;
+  int n = 0;
+  for (const Msg& m : msgs) {
+    float ms = 0.0f;
+    if (err == cudaSuccess) err = cudaEventElapsedTime(&ms, m.a, m.b);
+    clock[m.from] += ms * 1e-3;
+    elapsed = std::max(elapsed, clock[m.from]);
+    if (out && n < max_records) out[n] = enprop_exchange_record{m.from, m.to, bytes, clock[m.from]};
+    ++n;
+    cudaEventDestroy(m.a);
+    cudaEventDestroy(m.b);
+  }
+  if (rc) return rc;
+  if (err != cudaSuccess) return cuda_fail(err, "enprop_dist_exchange_trace");
+  *count = n;
+  if (elapsed_seconds) *elapsed_seconds = elapsed;
+  return ENPROP_OK;
+}
+
 int enprop_fit_halo_model(int n, const double* s, const double* t, double* a, double* b,
                           double* rss) {
   // halo.cpp:156-181, same operations in the same order

@@ -185,6 +185,7 @@ class RefLib:
                                     C.c_double, C.c_double, _dp, _dp, C.c_double, C.c_double, C.c_double,
                                     C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                     C.c_int, _dp, _ip, _ip, _dp, _ip]
+        L.ref_write_trace_csv.argtypes = [C.c_char_p, C.c_int, _ip, _ip, C.POINTER(C.c_int64), _dp]
         L.ref_time_spmv.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                     C.c_uint64, C.c_int, _dp]
 
@@ -312,6 +313,16 @@ class RefLib:
         out = np.empty((count, m))
         self._check(self.lib.ref_draw_samples(seed, count, m, dptr(out)))
         return out
+
+    def write_trace_csv(self, path, records):
+        """write_exchange_trace_csv (halo.cpp:192-202); records: (rank, neighbor, bytes, time)"""
+        n = len(records)
+        rk = np.array([r[0] for r in records], np.int32)
+        nb = np.array([r[1] for r in records], np.int32)
+        by = np.array([r[2] for r in records], np.int64)
+        t = np.array([r[3] for r in records], np.float64)
+        return self.lib.ref_write_trace_csv(path.encode(), n, iptr(rk), iptr(nb),
+                                            by.ctypes.data_as(C.POINTER(C.c_int64)), dptr(t))
 
     def newton_mg(self, s, n, m, y, sigma=0.1, alpha=0.0, beta=0.0, velocity=(1.0, 0.0, 0.0), tol=1e-8,
                   max_newton=20, lin_tol=1e-8, lin_maxit=1000, opts=(500, 2, 30.0, 1.1, 40), scalar=False):

@@ -80,3 +80,23 @@ def test_time_halo_measures_the_exchange(ctx):
     a, b, rss = ep.fit_halo_model([(1, times[1]), (32, times[32])])
     assert rss == 0.0 or rss < 1e-18  # two points: an exact line
     assert a + b * 32 == pytest.approx(times[32], rel=1e-9, abs=1e-15)
+
+
+def test_exchange_trace_records_the_measured_exchange(ctx, tmp_path):
+    """Dist.exchange_trace (f2): one record per message in the reference's order
+    (sender rank, lower link before upper: partition.cpp:59-72), one plane of s
+    values each, the sender's cumulative measured time; exported as the
+    reference's CSV."""
+    n, s = 10, 4
+    d = ep.Dist(ctx, n, s, nranks=3, kl=ep.KlField(3, 1.0, 0.1, 1.0))
+    recs, elapsed = d.exchange_trace()
+    assert [(r[0], r[1]) for r in recs] == [(0, 1), (1, 0), (1, 2), (2, 1)]
+    assert all(r[2] == (n + 1) ** 2 * s * 8 for r in recs)
+    assert all(r[3] > 0 for r in recs)
+    assert recs[2][3] > recs[1][3]  # rank 1's clock accumulates over its two messages
+    assert elapsed == max(r[3] for r in recs)
+    path = tmp_path / "trace.csv"
+    ep.write_exchange_trace_csv(str(path), recs)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "rank,neighbor,bytes,virtual_time" and len(lines) == 5
+    d.close()

@@ -47,3 +47,20 @@ def test_fit_halo_model_known_line_and_errors():
         ep.predicted_speedup(1.0, 1.0, 0.5)
     with pytest.raises(ValueError):
         ep.predicted_speedup(0.0, 0.0, 2.0)
+
+
+def test_exchange_trace_csv_is_the_reference_format(tmp_path):
+    """enprop_write_exchange_trace_csv writes the same bytes as the reference's
+    write_exchange_trace_csv (halo.cpp:192-202), and fails on an unwritable path
+    (the reference throws runtime_error there)."""
+    from oracles import RefLib
+    R = RefLib()
+    recs = [(0, 1, 81 * 2 * 8, 1.25e-6), (1, 0, 1296, 2.5000000000000004e-06), (1, 2, 1296, 3.1e-06),
+            (2, 1, 1296, 1.0 / 3.0)]
+    a, b = tmp_path / "ours.csv", tmp_path / "ref.csv"
+    ep.write_exchange_trace_csv(str(a), recs)
+    assert R.write_trace_csv(str(b), recs) == 0
+    assert a.read_bytes() == b.read_bytes()
+    assert a.read_text().splitlines()[0] == "rank,neighbor,bytes,virtual_time"
+    with pytest.raises(ValueError):
+        ep.write_exchange_trace_csv("/nonexistent-dir/trace.csv", recs)
