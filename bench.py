@@ -727,7 +727,13 @@ def bench_halo_model(ep, torch, n=128, nranks=2, reps=50):
         del d
         torch.cuda.synchronize()
     a, b, rss = ep.fit_halo_model(samples)
+    d = ep.Dist(ctx, n, 32, nranks=3, kl=ep.KlField(M_TERMS, 1.0, SIGMA, 1.0))
+    trace, elapsed = d.exchange_trace()  # halo.cpp:140-150 record order, measured times
+    d.close()
     return {"transport": f"emulated ({nranks} ranks on one GPU: device-to-device copies)",
+            "trace_s32_3ranks": {"records": [{"rank": r[0], "neighbor": r[1], "bytes": r[2],
+                                              "time_us": round(r[3] * 1e6, 3)} for r in trace],
+                                 "elapsed_us": round(elapsed * 1e6, 3)},
             "mesh": n, "plane_bytes_per_component": (n + 1) ** 2 * 8,
             "measured_us": {str(s): round(t * 1e6, 3) for s, t in samples},
             "fit": {"a_us": round(a * 1e6, 4), "b_us_per_component": round(b * 1e6, 5),

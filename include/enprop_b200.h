@@ -194,6 +194,12 @@ int enprop_spmv_outer(enprop_ctx* ctx, int ensemble_size, int num_rows, int num_
                       const int* row_map, const int* col_entry, const double* values,
                       const double* x, double* z);
 
+/* Diagnostics: the narrow-ensemble SpMV configuration enprop_spmv launches
+ * for width s (CTA threads, register cap -- 0 = uncapped -- and staging mode;
+ * set by the ENPROP_SMALL_* environment switches), and whether s is routed to
+ * it at all (s <= ENPROP_SMALL_MAX). */
+int enprop_spmv_small_config(int s, int* routed, int* threads, int* reg_cap, int* stage_mode);
+
 /* dot (kernels.hpp:62-69): per-lane sums lanes_host[s] (may be NULL) and the
  * coupled reduce_sum coupled_host (may be NULL) in the given order.
  * seg_rows is the canonical segment length (ignored for SERIAL). */

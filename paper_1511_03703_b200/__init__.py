@@ -212,6 +212,7 @@ def lib() -> C.CDLL:
     L.enprop_apply_dirichlet.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(_Bc), _vp, _vp, _vp,
                                          _vp, _vp]
     L.enprop_spmv.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp]
+    L.enprop_spmv_small_config.argtypes = [C.c_int, _ip, _ip, _ip, _ip]
     L.enprop_dot.argtypes = [_vp, C.c_int, C.c_int64, _vp, _vp, C.c_int, C.c_int, _dp, _dp]
     L.enprop_axpby.argtypes = [_vp, C.c_int, C.c_int64, C.c_int, _dp, _vp, _dp, _vp]
     L.enprop_cg.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp,
@@ -423,6 +424,13 @@ def spmv(ctx: Context, s: int, row_map, col_entry, values, x, z=None, num_cols=N
     _check(lib().enprop_spmv(ctx.h, s, rows, cols, _ptr(row_map), _ptr(col_entry), _ptr(values),
                              _ptr(x), _ptr(z)), "spmv")
     return z
+
+
+def spmv_small_config(s: int) -> dict:
+    """Diagnostics: the narrow-ensemble SpMV configuration enprop_spmv launches at width s."""
+    r, nt, rc, md = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    _check(lib().enprop_spmv_small_config(s, C.byref(r), C.byref(nt), C.byref(rc), C.byref(md)))
+    return dict(routed=bool(r.value), threads=nt.value, reg_cap=rc.value, stage_mode=md.value)
 
 
 def spmv_outer(ctx: Context, ensemble_size: int, row_map, col_entry, values, x, z=None, num_cols=None):

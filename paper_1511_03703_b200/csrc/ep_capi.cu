@@ -689,6 +689,13 @@ int enprop_spmv(enprop_ctx* c, int s, int rows, int cols, const int* row_map,
   return ENPROP_OK;
 }
 
+int enprop_spmv_small_config(int s, int* routed, int* threads, int* reg_cap, int* stage_mode) {
+  if (!valid_width(s)) return fail(ENPROP_ERR_INVALID, "ensemble width outside {1,2,4,8,16,32}");
+  if (routed) *routed = s <= spmv_small_max();
+  spmv_small_config(s, threads, reg_cap, stage_mode);
+  return ENPROP_OK;
+}
+
 int enprop_spmv_outer(enprop_ctx* c, int s, int rows, int cols, int64_t nnz, const int* row_map,
                       const int* col_entry, const double* values, const double* x, double* z) {
   if (!c) return fail(ENPROP_ERR_INVALID, "null context");

@@ -105,6 +105,7 @@ cudaError_t launch_spmv(int s, int rows, const int* row_map, const int* col_entr
                         cudaStream_t st);
 // narrow ensembles (s <= 16): row blocks staged in shared memory (ep_outer.cu)
 int spmv_small_max();  // widest s routed to launch_spmv_small (16; 8 or 32 by env)
+void spmv_small_config(int s, int* threads, int* reg_cap, int* stage_mode);
 cudaError_t launch_spmv_small(int s, int rows, const int* row_map, const int* col_entry,
                               const double* values, const double* x, double* z, cudaStream_t st);
 // spmv_outer (kernels.hpp:38-56): sample-major values[e*nnz + k], x[e*cols + c], z[e*rows + row]

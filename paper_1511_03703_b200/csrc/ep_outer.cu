@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(NT, MINB) k_spmv_small(int rows, const int* __
 // Defaults (A/B at 128^3, tools/small_ab.py, profiles/round1/spmv_small_ab.jsonl):
 // 64 threads, indices staged, capped at 64 registers for s = 1 and 48 for s >= 2
 // (uncapped, ptxas takes 80-86). A/B switches: ENPROP_SMALL_NT = 64 | 96 | 128,
-// ENPROP_SMALL_REGS = 0 (uncapped; mode 0 only) | 32 | 48 | 64, every mode at each cap,
+// ENPROP_SMALL_REGS = 0 (uncapped) | 32 | 48 | 64, every mode at each cap,
 // ENPROP_SMALL_STAGE = 0 | 1 | 2.
 static int small_nt(int) {
   static const int nt = [] {
@@ -180,19 +180,26 @@ static int small_regs(int s) {
   return r >= 0 ? r : (s == 1 ? 64 : 48);
 }
 
+static int small_mode() {
+  static const int mode = [] {
+    const int v = env_int("ENPROP_SMALL_STAGE", 1);
+    return (v == 0 || v == 2) ? v : 1;
+  }();
+  return mode;
+}
+
 template <int S, int NT>
 static cudaError_t spmv_small_nt(int rows, const int* row_map, const int* col_entry,
                                  const double* values, const double* x, double* z, cudaStream_t st) {
   constexpr int RB = NT / S;
   if (rows <= 0) return cudaSuccess;
   const int grid = (rows + RB - 1) / RB;
-  static const int mode = [] {
-    const int v = env_int("ENPROP_SMALL_STAGE", 1);
-    return (v == 0 || v == 2) ? v : 1;
-  }();
+  const int mode = small_mode();
   constexpr int MB = 65536 / (NT * 64);
   switch (small_regs(S) * 4 + mode) {
     case 0: k_spmv_small<S, NT, 1, 0><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+    case 1: k_spmv_small<S, NT, 1, 1><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
+    case 2: k_spmv_small<S, NT, 1, 2><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
     case 192: k_spmv_small<S, NT, 65536 / (NT * 48), 0><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
     case 193: k_spmv_small<S, NT, 65536 / (NT * 48), 1><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
     case 194: k_spmv_small<S, NT, 65536 / (NT * 48), 2><<<grid, NT, 0, st>>>(rows, row_map, col_entry, values, x, z); break;
@@ -219,6 +226,14 @@ static cudaError_t spmv_small_s(int rows, const int* row_map, const int* col_ent
 // widest ensemble enprop_spmv sends to k_spmv_small (ENPROP_SMALL_MAX: 8, 16
 // or 32; default 16: at 128^3, s = 16 runs at 97% of HBM here vs 90% in the
 // warp-per-row k_spmv<16>)
+// the configuration launch_spmv_small launches for width s (every (register
+// cap, staging mode) pair has its own instantiation: nothing falls back)
+void spmv_small_config(int s, int* threads, int* reg_cap, int* stage_mode) {
+  if (threads) *threads = small_nt(s);
+  if (reg_cap) *reg_cap = small_regs(s);
+  if (stage_mode) *stage_mode = small_mode();
+}
+
 int spmv_small_max() {
   static const int m = [] {
     const int v = env_int("ENPROP_SMALL_MAX", 16);

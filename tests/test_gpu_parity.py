@@ -213,6 +213,17 @@ def test_spmv_small_staging_modes_bitwise(mode):
                         "-k", "spmv and bitwise and not staging_modes"],
                        env=env, cwd=os.path.dirname(here), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    # the mode under test is the one that launches, at every width
+    # and register cap it is routed with (no silent fallback to mode 1)
+    probe = ("import paper_1511_03703_b200 as ep, json; "
+             "print(json.dumps([ep.spmv_small_config(s) for s in (1, 2, 4, 8, 16)]))")
+    for regs in ("", "0", "32", "48", "64"):
+        env2 = dict(env, ENPROP_SMALL_REGS=regs)
+        out = subprocess.run([sys.executable, "-c", probe], env=env2, cwd=os.path.dirname(here),
+                             capture_output=True, text=True, timeout=120)
+        import json
+        cfgs = json.loads(out.stdout.strip().splitlines()[-1])
+        assert all(c["stage_mode"] == int(mode) for c in cfgs), (regs, cfgs)
 
 
 def test_spmv_rejects_bad_length(ctx):
