@@ -184,8 +184,14 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
   const TileMap tm = make_tile_map(rows, seg);
   const bool canon = opt->dot_mode == ENPROP_DOT_CANONICAL;
   // serial order: the SpMV writes the p*q products the chain kernel sums
-  // (except on the plain path, where the chain forms them from p and q)
-  int rc = ensure_work(w, rows, s, opt->max_iterations, tm, !canon);
+  // (except on the plain path, or with ENPROP_CHAIN_PQ=1, where the chain
+  // forms them from p and q)
+  int rc = ensure_work(w, rows, s, opt->max_iterations, tm, !canon && !chain_forms_pq());
+  if (!rc && chain_forms_pq() && w.prod) {
+    cudaFree(w.prod);
+    w.prod = nullptr;
+    free_graph(w);
+  }
   if (rc) return rc;
   const int lanes = opt->flavour == ENPROP_CG_UNCOUPLED ? s : 1;
   const bool fused = ctx->fused_direction != 0 && vpos == nullptr;  // symmetric storage: split only
@@ -263,7 +269,7 @@ int run_cg(enprop_ctx* ctx, int s, int rows, const int* row_map, const int* col_
     }
     if (ev) EP_Q(cudaEventRecord(ev[2], st));
     if (!canon) {
-      if (plain) EP_Q(launch_chain(s, rows, p_new, w.q, kChainProduct, f_pq, st));
+      if (plain || !w.prod) EP_Q(launch_chain(s, rows, p_new, w.q, kChainProduct, f_pq, st));
       else EP_Q(launch_chain(s, rows, w.prod, nullptr, kChainGiven, f_pq, st));
     }
     if (fin_kernel && !fuse_pq) EP_Q(launch_fin_segments(s, tm, f_pq, st));
