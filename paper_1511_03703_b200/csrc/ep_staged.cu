@@ -64,7 +64,8 @@ struct StagedShape {
   static constexpr int IDX_BYTES = HDR * 4 + RS * ROWE * 4;
   static constexpr int NIDX = (S >= 16 && NB == 2) ? 4 : 2;  // index blocks in flight (ring depth; smem-limited)
   static constexpr int RED_BYTES = RS * S * 8;
-  static constexpr int CLAIM = NIDX > 3 ? NIDX : 3;  // stages claimed ahead of the current one
+  static constexpr int PFMAX = 3;                    // L2 prefetch distance beyond the stage buffers (max)
+  static constexpr int CLAIM = NB + PFMAX + 1 > NIDX ? NB + PFMAX + 1 : NIDX;  // stages claimed ahead
   static constexpr int SMEM = NB * BIG_BYTES + NIDX * IDX_BYTES + 2 * RED_BYTES + 64 + 32;
   static_assert(RS * TPR == 256, "one thread per (row slot, sample pair)");
   static_assert(BIG_BYTES % 128 == 0 && IDX_BYTES % 16 == 0, "alignment");
@@ -98,6 +99,7 @@ struct StagedCta {
   uint64_t pol;
   int rr, lane0;
   int l2_hints;                // ENPROP_STAGED_L2HINT (A/B)
+  int pf;                      // ENPROP_STAGED_PF: L2 prefetch distance in stages beyond the buffers
   uint64_t pol_last, pol_first;
 
   // The it-th stage of this CTA is the sweep position it claimed it-th (desc
@@ -157,6 +159,19 @@ struct StagedCta {
                  (uint32_t)(hi - lo) * Sh::CH, b);
     }
   }
+  // L2 prefetch of a later stage's HBM-fresh bytes: its stored slots and the
+  // x runs of the plane ahead (dk = +1; the other runs were read by earlier stages)
+  __device__ __forceinline__ void prefetch_stage(const StageDesc& d) const {
+    const uint32_t upb = (uint32_t)(d.slot1 - d.slot0) * Sh::CH;
+    if (upb) prefetch_l2_bulk(values + (size_t)d.slot0 * S, upb);
+    const int NN = N * N, L = d.R1 - d.R0 + 2;
+#pragma unroll
+    for (int run = 6; run < 9; ++run) {
+      const int a = d.R0 - 1 + (run % 3 - 1) * N + NN;
+      const int lo = a > xlo ? a : xlo, hi = a + L < xhi ? a + L : xhi;
+      if (hi > lo) prefetch_l2_bulk(p + (ptrdiff_t)lo * S, (uint32_t)(hi - lo) * Sh::CH);
+    }
+  }
   __device__ __forceinline__ void issue_idx(int it) const {
     uint64_t* b = idx_bar(it);
     mbar_arrive_expect_tx(b, Sh::IDX_BYTES);
@@ -192,9 +207,11 @@ struct StagedCta {
   // receives the next stage's; NB = 1: Gc is gathered here (Gn unused)
   template <bool kTiles>
   __device__ __forceinline__ void stage(int it, StageGather& Gc, StageGather& Gn) const {
-    StageDesc dn;  // producer: descriptor of stage it + NB, loaded early
+    StageDesc dn, dp;  // producer: descriptors of stage it + NB (and it + NB + pf), loaded early
     const bool prod = threadIdx.x == 0 && has(it + NB);
     if (prod) dn = desc[stage_of(it + NB)];
+    const bool pfetch = threadIdx.x == 0 && pf > 0 && has(it + NB + pf);
+    if (pfetch) dp = desc[stage_of(it + NB + pf)];
     if constexpr (NB == 2) {
       if (has(it + 1)) {  // the next stage's transposed gathers fly during this stage
         mbar_wait(idx_bar(it + 1), ((it + 1) / Sh::NIDX) & 1);
@@ -271,6 +288,7 @@ struct StagedCta {
     if (threadIdx.x == 0) {
       fence_proxy_async_smem();
       if (prod) issue_big(it + NB, dn);
+      if (pfetch) prefetch_stage(dp);
       claim(it + Sh::CLAIM);
       if (has(it + Sh::NIDX)) issue_idx(it + Sh::NIDX);
     }
@@ -320,7 +338,7 @@ template <int S, bool kTiles, int NB>
 __global__ void __launch_bounds__(256, NB == 2 ? 1 : 2) k_cg_spmv_staged(
     const TileMap tm, int N, int nstages, int xlo, int xhi, const StageDesc* __restrict__ desc,
     const unsigned char* __restrict__ blk, const double* __restrict__ values,
-    const double* __restrict__ p, double* __restrict__ q, const FinArgs f, int fuse_fin, int l2_hints) {
+    const double* __restrict__ p, double* __restrict__ q, const FinArgs f, int fuse_fin, int l2_hints, int pf) {
   using Sh = StagedShape<S, NB>;
   EP_PDL_ENTRY();
   if (f.cg->done) return;
@@ -331,7 +349,7 @@ __global__ void __launch_bounds__(256, NB == 2 ? 1 : 2) k_cg_spmv_staged(
                  reinterpret_cast<uint64_t*>(tail),
                  reinterpret_cast<double*>(smem + NB * Sh::BIG_BYTES + Sh::NIDX * Sh::IDX_BYTES),
                  reinterpret_cast<int*>(tail + 64), f.ticket,
-                 l2_policy_evict_normal(), tid / Sh::TPR, (tid % Sh::TPR) * Sh::V, l2_hints,
+                 l2_policy_evict_normal(), tid / Sh::TPR, (tid % Sh::TPR) * Sh::V, l2_hints, pf,
                  l2_policy_evict_last(), l2_policy_evict_first()};
   if (tid == 0) {
     for (int k = 0; k < NB + Sh::NIDX; ++k) mbar_init(&c.bar[k], 1);
@@ -352,6 +370,8 @@ __global__ void __launch_bounds__(256, NB == 2 ? 1 : 2) k_cg_spmv_staged(
       if (c.has(it)) c.issue_idx(it);
     for (int it = 0; it < NB; ++it)
       if (c.has(it)) c.issue_big(it, desc[c.stage_of(it)]);
+    for (int it = NB; it < NB + pf; ++it)
+      if (c.has(it)) c.prefetch_stage(desc[c.stage_of(it)]);
   }
   if (c.has(0)) {  // (a CTA may draw no stage at all; it still joins the barrier)
     if constexpr (NB == 2) {
@@ -482,6 +502,21 @@ bool staged_fuse_fin() {
 int staged_l2hint() {
   static const int on = env_int("ENPROP_STAGED_L2HINT", 0);
   return on != 0;
+}
+
+// ENPROP_STAGED_PF (A/B): L2 prefetch distance in stages beyond the stage
+// buffers, 0-3; default 1. The kernel is latency-bound on its stage stream
+// (ncu: L1/shared data path 52% busy, issue 7%, stalls on long scoreboard and
+// barriers), and a TMA L2 prefetch of the next-but-one stage's HBM-fresh bytes
+// (stored slots + the x runs of the plane ahead) makes its shared-memory fill
+// an L2 hit: 64^3 s=32 serial-order SpMV 0.249 -> 0.220 ms, 24-group bench
+// +4%; 2 stages 0.233, 3 stages 0.316 ms (L2 thrash)
+int staged_pf() {
+  static const int v = [] {
+    const int e = env_int("ENPROP_STAGED_PF", 1);
+    return e < 0 ? 0 : (e > 3 ? 3 : e);
+  }();
+  return v;
 }
 
 bool chain_forms_pq() {
@@ -652,10 +687,10 @@ static cudaError_t cg_spmv_staged_nb(bool tiles, bool fuse_fin, const StageMap& 
     // cooperative launch guarantees it even with other streams' kernels
     // (possibly persistent ones of concurrent sample groups) on the GPU
     launch_kk(2 | (fuse_fin ? kLaunchCooperative : 0), k_cg_spmv_staged<S, true, NB>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.xlo, sm.xhi, sm.desc, sm.blk,
-                                                           values, p, q, f, fuse_fin ? 1 : 0, staged_l2hint());
+                                                           values, p, q, f, fuse_fin ? 1 : 0, staged_l2hint(), staged_pf());
   else
     launch_kk(2, k_cg_spmv_staged<S, false, NB>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.xlo, sm.xhi, sm.desc, sm.blk,
-                                                            values, p, q, f, 0, staged_l2hint());
+                                                            values, p, q, f, 0, staged_l2hint(), staged_pf());
   return cudaGetLastError();
 }
 
