@@ -282,7 +282,12 @@ struct StagedCta {
     }
     // tile existence (first row slot of each tile), read before the barrier:
     // thread 0 refills this index slot right after it
-    const bool tile_exists = threadIdx.x < 32 && ib[(threadIdx.x / S) * kTileRows] >= 0;
+    // the stage's tile trees run in one warp, rotating over the CTA's warps
+    // stage by stage so no warp is late to every barrier
+    const int tree_warp = it & 7;
+    const int tl = threadIdx.x & 31;
+    const bool tree = (threadIdx.x >> 5) == tree_warp;
+    const bool tile_exists = tree && ib[(tl / S) * kTileRows] >= 0;
     const int gid = ib[2 * Sh::RS];  // canonical stage id (tile trees)
     __syncthreads();  // big buffer and index slot of stage it consumed, products in rb
     if (threadIdx.x == 0) {
@@ -293,8 +298,8 @@ struct StagedCta {
       if (has(it + Sh::NIDX)) issue_idx(it + Sh::NIDX);
     }
     if constexpr (kTiles) {
-      if (threadIdx.x < 32) {  // tile trees: lane -> (tile, sample); v[i] += v[i+h], h = 8,4,2,1
-        const int tt = threadIdx.x / S, e = threadIdx.x % S;
+      if (tree) {  // tile trees: lane -> (tile, sample); v[i] += v[i+h], h = 8,4,2,1
+        const int tt = tl / S, e = tl % S;
         const int b2 = gid * Sh::T + tt;
         if (tile_exists) {
           double v[kTileRows];
