@@ -98,9 +98,7 @@ struct StagedCta {
   int* ticket;    // global claim counter (f.ticket)
   uint64_t pol;
   int rr, lane0;
-  int l2_hints;                // ENPROP_STAGED_L2HINT (A/B)
   int pf;                      // ENPROP_STAGED_PF: L2 prefetch distance in stages beyond the buffers
-  uint64_t pol_last, pol_first;
 
   // The it-th stage of this CTA is the sweep position it claimed it-th (desc
   // and index blocks are stored in sweep order; desc[pos].g is the stage's
@@ -145,11 +143,7 @@ struct StagedCta {
       if (hi > lo) total += (uint32_t)(hi - lo) * Sh::CH;
     }
     mbar_arrive_expect_tx(b, total);
-    if (l2_hints) {  // the upper slots are re-read transposed by the next plane's rows: keep them
-      bulk_g2s_hint(sb, values + (size_t)d.slot0 * S, upb, b, pol_last);
-    } else {
-      bulk_g2s(sb, values + (size_t)d.slot0 * S, upb, b);
-    }
+    bulk_g2s(sb, values + (size_t)d.slot0 * S, upb, b);
 #pragma unroll
     for (int run = 0; run < 9; ++run) {
       const int a = d.R0 - 1 + (run % 3 - 1) * N + (run / 3 - 1) * NN;
@@ -175,8 +169,7 @@ struct StagedCta {
   __device__ __forceinline__ void issue_idx(int it) const {
     uint64_t* b = idx_bar(it);
     mbar_arrive_expect_tx(b, Sh::IDX_BYTES);
-    if (l2_hints) bulk_g2s_hint((void*)idx(it), blk + (size_t)stage_of(it) * Sh::IDX_BYTES, Sh::IDX_BYTES, b, pol_first);
-    else bulk_g2s((void*)idx(it), blk + (size_t)stage_of(it) * Sh::IDX_BYTES, Sh::IDX_BYTES, b);
+    bulk_g2s((void*)idx(it), blk + (size_t)stage_of(it) * Sh::IDX_BYTES, Sh::IDX_BYTES, b);
   }
 
   __device__ __forceinline__ void gather(int it, StageGather& G) const {
@@ -343,7 +336,7 @@ template <int S, bool kTiles, int NB>
 __global__ void __launch_bounds__(256, NB == 2 ? 1 : 2) k_cg_spmv_staged(
     const TileMap tm, int N, int nstages, int xlo, int xhi, const StageDesc* __restrict__ desc,
     const unsigned char* __restrict__ blk, const double* __restrict__ values,
-    const double* __restrict__ p, double* __restrict__ q, const FinArgs f, int fuse_fin, int l2_hints, int pf) {
+    const double* __restrict__ p, double* __restrict__ q, const FinArgs f, int fuse_fin, int pf) {
   using Sh = StagedShape<S, NB>;
   EP_PDL_ENTRY();
   if (f.cg->done) return;
@@ -354,8 +347,7 @@ __global__ void __launch_bounds__(256, NB == 2 ? 1 : 2) k_cg_spmv_staged(
                  reinterpret_cast<uint64_t*>(tail),
                  reinterpret_cast<double*>(smem + NB * Sh::BIG_BYTES + Sh::NIDX * Sh::IDX_BYTES),
                  reinterpret_cast<int*>(tail + 64), f.ticket,
-                 l2_policy_evict_normal(), tid / Sh::TPR, (tid % Sh::TPR) * Sh::V, l2_hints, pf,
-                 l2_policy_evict_last(), l2_policy_evict_first()};
+                 l2_policy_evict_normal(), tid / Sh::TPR, (tid % Sh::TPR) * Sh::V, pf};
   if (tid == 0) {
     for (int k = 0; k < NB + Sh::NIDX; ++k) mbar_init(&c.bar[k], 1);
     fence_mbar_init();
@@ -499,13 +491,6 @@ static int stage_shape(int& T, int& L, int& RS, int& max_upper, int& idx_bytes, 
 
 bool staged_fuse_fin() {
   static const int on = env_int("ENPROP_STAGED_FUSE", 1);
-  return on != 0;
-}
-
-// ENPROP_STAGED_L2HINT (A/B, default 0): L2 evict_last on the staged SpMV's
-// upper-slot copies, evict_first on its index blocks
-int staged_l2hint() {
-  static const int on = env_int("ENPROP_STAGED_L2HINT", 0);
   return on != 0;
 }
 
@@ -692,10 +677,10 @@ static cudaError_t cg_spmv_staged_nb(bool tiles, bool fuse_fin, const StageMap& 
     // cooperative launch guarantees it even with other streams' kernels
     // (possibly persistent ones of concurrent sample groups) on the GPU
     launch_kk(2 | (fuse_fin ? kLaunchCooperative : 0), k_cg_spmv_staged<S, true, NB>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.xlo, sm.xhi, sm.desc, sm.blk,
-                                                           values, p, q, f, fuse_fin ? 1 : 0, staged_l2hint(), staged_pf());
+                                                           values, p, q, f, fuse_fin ? 1 : 0, staged_pf());
   else
     launch_kk(2, k_cg_spmv_staged<S, false, NB>, dim3(grid), dim3(256), Sh::SMEM, st, sm.tm, sm.N, sm.nstages, sm.xlo, sm.xhi, sm.desc, sm.blk,
-                                                            values, p, q, f, 0, staged_l2hint(), staged_pf());
+                                                            values, p, q, f, 0, staged_pf());
   return cudaGetLastError();
 }
 

@@ -70,25 +70,22 @@ def main():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--skip-chain", action="store_true")
     ap.add_argument("--staged", default="0,1", help="ENPROP_STAGED_SERIAL values to compare")
-    ap.add_argument("--chain", default="0", help="ENPROP_CHAIN values to compare")
     a = ap.parse_args()
     if not a.skip_chain:
         print(json.dumps({"chain_ms_incl_host_alloc": chain_times()}), flush=True)
         for s in (1, 32):
             print(json.dumps(phase_times(s)), flush=True)
         print(json.dumps(phase_times(32, dot="canonical")), flush=True)
-    for g, st, ch in [(g, st, ch) for ch in a.chain.split(",") for st in a.staged.split(",")
-                      for g in a.groups.split(",")]:
+    for g, st in [(g, st) for st in a.staged.split(",") for g in a.groups.split(",")]:
         cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--dot", "serial", "--groups", g,
                "--steps", str(a.steps), "--warmup", "1", "--skip-spmv", "--skip-cpu", "--profile-only"]
-        r = subprocess.run(cmd, capture_output=True, text=True, env=dict(os.environ, ENPROP_STAGED_SERIAL=st, ENPROP_CHAIN=ch))
+        r = subprocess.run(cmd, capture_output=True, text=True, env=dict(os.environ, ENPROP_STAGED_SERIAL=st))
         line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-2000:]
         try:
             d = json.loads(line)
             d["samples_per_s"] = round(int(g) * 32 * a.steps / (d["ms"] / 1e3), 2)
             d["groups"] = int(g)
             d["staged_serial"] = st
-            d["chain"] = ch
             d.pop("iters", None)
             print(json.dumps(d), flush=True)
         except ValueError:
