@@ -360,6 +360,17 @@ int enprop_dist_assemble(enprop_dist* d, const double* y);
 /* CG on A x = -residual, canonical dot order (DOT_SERIAL is INVALID here) */
 int enprop_dist_solve(enprop_dist* d, const enprop_cg_options* opt, int* iterations,
                       int* lane_status);
+/* newton_solve (fem.hpp:265-302) over the slabs, with Alg. 2's halo step: from
+ * u = 0, every step imports the neighbours' boundary planes of u, assembles
+ * the local rows at u, forms the coupled residual norm in the canonical order,
+ * and solves J du = -f by enprop_dist_solve (identity preconditioner). Every
+ * rank takes the same decisions; norms, steps, CG iterations and u are bitwise
+ * those of enprop_problem_newton on one GPU with DOT_CANONICAL. The iterate
+ * ends in each local rank's x (enprop_dist_local). Outputs and errors as
+ * enprop_problem_newton; linear.dot_mode must be DOT_CANONICAL. */
+int enprop_dist_newton(enprop_dist* d, const double* y, const enprop_newton_options* opt,
+                       int* newton_iterations, int* total_cg_iterations, double* residual_norms,
+                       int* num_norms);
 /* local ranks (1 with NCCL, nranks when emulated) and their owned rows / solution */
 int enprop_dist_local_count(enprop_dist* d);
 int enprop_dist_local(enprop_dist* d, int index, int* rank, int* row_begin, int* rows,

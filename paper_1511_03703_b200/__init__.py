@@ -242,6 +242,7 @@ def lib() -> C.CDLL:
     L.enprop_write_exchange_trace_csv.argtypes = [C.c_char_p, C.POINTER(_ExchangeRecord), C.c_int]
     L.enprop_dist_assemble.argtypes = [_vp, _vp]
     L.enprop_dist_solve.argtypes = [_vp, C.POINTER(_CgOptions), _ip, _ip]
+    L.enprop_dist_newton.argtypes = [_vp, _vp, C.POINTER(_NewtonOptions), _ip, _ip, _dp, _ip]
     L.enprop_dist_local_count.argtypes = [_vp]
     L.enprop_dist_local.argtypes = [_vp, C.c_int, _ip, _ip, _ip, C.POINTER(_vp)]
     _lib = L
@@ -801,6 +802,27 @@ class Dist:
         else:
             _check(rc, "solve")
         return (list(it) if cfg.flavour == CG_UNCOUPLED else it[0]), list(ls)
+
+    def newton(self, y: torch.Tensor, options: NewtonOptions = None,
+               raise_on_failure: bool = True) -> NewtonResult:
+        """newton_solve (fem.hpp:265-302) over the slabs with Alg. 2's u halo
+        (identity-preconditioned canonical CG); bitwise Problem.newton on one
+        GPU with DOT_CANONICAL. The iterate ends in the ranks' x (local())."""
+        _need_cuda(y, torch.float64, "y")
+        if y.numel() != self.kl.num_terms * self.s:
+            raise ValueError("newton: sample vector length mismatch")
+        opt = options or NewtonOptions(linear=SolverConfig(dot_mode=DOT_CANONICAL))
+        it, cg, nn = C.c_int(), C.c_int(), C.c_int()
+        norms = (C.c_double * (max(opt.max_iterations, 0) + 1))()
+        rc = lib().enprop_dist_newton(self.h, _ptr(y), C.byref(opt._c()), C.byref(it), C.byref(cg), norms,
+                                      C.byref(nn))
+        res = NewtonResult(it.value, cg.value, [norms[i] for i in range(nn.value)])
+        if rc in (ERR_NO_CONVERGENCE, ERR_INDEFINITE):
+            if raise_on_failure:
+                raise SolverError(_err(), res.residual_norms, rc, res.iterations)
+        else:
+            _check(rc, "newton")
+        return res
 
     def time_halo(self, reps: int = 20) -> float:
         """Mean seconds of one halo exchange of the solver's p buffer (one plane

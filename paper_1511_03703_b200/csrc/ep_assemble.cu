@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ AsmArg
 #pragma unroll
       for (int di = -1; di <= 0; ++di) {
         const int ci = i + di, cj = j + dj, ck = k + dk;
-        if (ci < 0 || ci >= n || cj < 0 || cj >= n || ck < 0 || ck >= n) continue;
+        if (ci < 0 || ci >= n || cj < 0 || cj >= n || ck < a.kc_lo || ck >= n) continue;
         const int iloc = (-di) | ((-dj) << 1) | ((-dk) << 2);  // row P's corner in the cell
 
         // kappa at the 8 Gauss points (kl.hpp:67-81): kappa = mean, then for each
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(256) k_assemble(const __grid_constant__ AsmArg
       for (int t = 0; t < 27; ++t) {
         const int ox = t % 3 - 1, oy = (t / 3) % 3 - 1, oz = t / 9 - 1;
         const int ii = i + ox, jj = j + oy, kk = k + oz;
-        if (jj < 0 || jj >= N || kk < 0 || kk >= N) continue;
+        if (jj < 0 || jj >= N || kk < a.kc_lo || kk >= N) continue;
         if (ii == 0 || ii == n) {
           const double g = ii == 0 ? a.bc0 : a.bc1;
           const double uc = kHasU ? a.u[(size_t)(ii + N * (jj + N * kk) - a.u_shift) * S + e] : 0.0;

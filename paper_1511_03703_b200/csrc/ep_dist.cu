@@ -128,10 +128,13 @@ struct DistRank {
   double* p[2] = {nullptr, nullptr};  // ext layout
   TileMap tm{};
   double *partials = nullptr, *gathered = nullptr, *hist = nullptr;
-  double* seg[2] = {nullptr, nullptr};  // per-plane sums of this rank: [0] p.q, [1] r.r (and init)
+  // per-plane sums of this rank: [0] init r.r and p.q, [1] r.r and Newton's
+  // residual norm; see seg_buffer for why the phases alternate this way
+  double* seg[2] = {nullptr, nullptr};
   int* counters = nullptr;
   int* plane_pos = nullptr;
   CgState* state = nullptr;
+  double* u = nullptr;  // Newton iterate, owned rows (enprop_dist_newton)
   // staged mode (s in {4, 16, 32}, alpha = 0): symmetric storage of the store
   // rows = lo ghost plane + owned rows (the ghost plane's upper slots are
   // assembled here, no communication) and the stage-pipelined SpMV in owned
@@ -149,16 +152,16 @@ struct DistRank {
 
 namespace {
 enum Transport { kEmulated = 0, kNccl = 1, kIpc = 2 };
-enum EvKind { kEvP = 0, kEvPQ = 1, kEvRR = 2 };
+enum EvKind { kEvP = 0, kEvPQ = 1, kEvRR = 2, kEvSync = 3, kEvKinds = 4 };
 constexpr int kIpcMaxRanks = 64;
 
 // Host board of an IPC job (/dev/shm, one per job name, zero-filled on creation).
 struct IpcSlot {
   cudaIpcMemHandle_t p[2], seg[2];
-  cudaIpcEventHandle_t ev[3];
+  cudaIpcEventHandle_t ev[kEvKinds];
   int device;
   std::atomic<int> published;
-  std::atomic<long long> seq[3];  // records issued per event kind
+  std::atomic<long long> seq[kEvKinds];  // records issued per event kind
 };
 struct IpcBoard {
   std::atomic<int> joined, opened, closed;
@@ -178,10 +181,10 @@ struct enprop_dist {
   // IPC transport
   std::string board_name;
   IpcBoard* board = nullptr;
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
-  long long seq[3] = {0, 0, 0};
+  cudaEvent_t ev[kEvKinds] = {};
+  long long seq[kEvKinds] = {};
   std::vector<double*> peer_p[2], peer_seg[2];  // opened peer buffers (own ones for self)
-  std::vector<cudaEvent_t> peer_ev[3];
+  std::vector<cudaEvent_t> peer_ev[kEvKinds];
   bool ipc_open = false;
 };
 
@@ -197,7 +200,7 @@ void free_rank(DistRank& d) {
   for (void* q : {(void*)d.row_map, (void*)d.col_entry, (void*)d.values, (void*)d.residual,
                   (void*)d.x, (void*)d.r, (void*)d.q, (void*)d.p[0], (void*)d.p[1],
                   (void*)d.partials, (void*)d.seg[0], (void*)d.seg[1], (void*)d.gathered, (void*)d.hist,
-                  (void*)d.counters, (void*)d.plane_pos, (void*)d.state, (void*)d.vpos, (void*)d.up_start})
+                  (void*)d.counters, (void*)d.plane_pos, (void*)d.state, (void*)d.vpos, (void*)d.up_start, (void*)d.u})
     if (q) cudaFree(q);
   free_stage_map(d.stage);
   d = DistRank{};
@@ -268,10 +271,20 @@ int setup_rank(enprop_dist* D, DistRank& d, int r) {
   return ENPROP_OK;
 }
 
+// Which per-plane sum buffer a phase writes. Over IPC a peer pulls this
+// rank's buffer on its own stream after this rank publishes it. The pull is
+// known complete only once that peer publishes again and this rank's stream
+// waits on it. The all-gathers wait on every rank, so alternating buffers
+// orders the CG loop: init (1), PQ (0), RR (1), PQ (0), ... Newton's norm (0)
+// follows a solve's last RR, which waited on every rank's publish after its
+// last PQ pull. A solve's init follows the last RR of the previous solve on the
+// same buffer, and ipc_quiesce orders that (halos order only the neighbours).
+int seg_buffer(int phase) { return phase == kPhasePQ || phase == kPhaseNone ? 0 : 1; }
+
 FinArgs rank_fin(const DistRank& d, int phase) {
   FinArgs f;
   f.partials = d.partials;
-  f.seg_sums = d.seg[phase == kPhasePQ ? 0 : 1];
+  f.seg_sums = d.seg[seg_buffer(phase)];
   f.seg_done = d.counters;
   f.bar = d.counters + 1;
   f.ticket = d.counters + 3;
@@ -328,6 +341,15 @@ int ipc_wait(enprop_dist* D, int q, int kind) {
   return ENPROP_OK;
 }
 
+// device-side all-rank fence: this stream continues once every rank's stream
+// has reached its own ipc_quiesce (and so finished its earlier pulls)
+int ipc_quiesce(enprop_dist* D) {
+  int rc = ipc_publish(D, kEvSync);
+  for (int q = 0; q < D->nranks && !rc; ++q)
+    if (q != D->ranks[0].rank) rc = ipc_wait(D, q, kEvSync);
+  return rc;
+}
+
 // wait on the host until every rank has bumped `counter` to nranks
 int ipc_barrier(enprop_dist* D, std::atomic<int>& counter) {
   counter.fetch_add(1, std::memory_order_acq_rel);
@@ -354,7 +376,7 @@ int ipc_setup(enprop_dist* D, const char* job) {
   D->board = static_cast<IpcBoard*>(m);
   DistRank& d = D->ranks[0];
   IpcSlot& me = D->board->slot[d.rank];
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < kEvKinds; ++k) {
     EP_CUDA(cudaEventCreateWithFlags(&D->ev[k], cudaEventDisableTiming | cudaEventInterprocess));
     EP_CUDA(cudaIpcGetEventHandle(&me.ev[k], D->ev[k]));
   }
@@ -370,7 +392,7 @@ int ipc_setup(enprop_dist* D, const char* job) {
     D->peer_p[k].assign(D->nranks, nullptr);
     D->peer_seg[k].assign(D->nranks, nullptr);
   }
-  for (int k = 0; k < 3; ++k) D->peer_ev[k].assign(D->nranks, nullptr);
+  for (int k = 0; k < kEvKinds; ++k) D->peer_ev[k].assign(D->nranks, nullptr);
   D->ipc_open = true;
   for (int q = 0; q < D->nranks; ++q) {
     IpcSlot& sl = D->board->slot[q];
@@ -390,7 +412,7 @@ int ipc_setup(enprop_dist* D, const char* job) {
       EP_CUDA(cudaIpcOpenMemHandle(&ptr, sl.seg[k], cudaIpcMemLazyEnablePeerAccess));
       D->peer_seg[k][q] = static_cast<double*>(ptr);
     }
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < kEvKinds; ++k) {
       if (self) D->peer_ev[k][q] = D->ev[k];
       else EP_CUDA(cudaIpcOpenEventHandle(&D->peer_ev[k][q], sl.ev[k]));
     }
@@ -414,7 +436,7 @@ void ipc_teardown(enprop_dist* D) {
   // the last rank out removes the board; peers keep their exported buffers
   // alive until everyone has closed its mappings
   ipc_barrier(D, D->board->closed);
-  for (int k = 0; k < 3; ++k)
+  for (int k = 0; k < kEvKinds; ++k)
     if (D->ev[k]) cudaEventDestroy(D->ev[k]);
   if (me == 0) shm_unlink(D->board_name.c_str());
   munmap(D->board, sizeof(IpcBoard));
@@ -477,10 +499,10 @@ int halo(enprop_dist* D, int which) {
   return ENPROP_OK;
 }
 
-// all-gather of the per-plane sums of `phase` (seg[0] for p.q, seg[1] else)
+// all-gather of the per-plane sums of `phase` (buffer seg_buffer(phase))
 int allgather(enprop_dist* D, int phase) {
   const size_t cnt = (size_t)D->maxplanes * D->desc.ensemble_size;
-  const int b = phase == kPhasePQ ? 0 : 1;
+  const int b = seg_buffer(phase);
   cudaStream_t st = D->ctx->stream;
   if (D->emulated) {
     for (auto& dst : D->ranks)
@@ -504,10 +526,10 @@ int allgather(enprop_dist* D, int phase) {
   return ENPROP_OK;
 }
 
-int fin_all(enprop_dist* D, int phase) {
+int fin_all(enprop_dist* D, int phase, double* lanes_out = nullptr) {
   const int s = D->desc.ensemble_size;
   for (auto& d : D->ranks) {
-    EP_CUDA(launch_fin_gathered(s, D->N, d.gathered, d.plane_pos, phase, d.state, d.hist, nullptr,
+    EP_CUDA(launch_fin_gathered(s, D->N, d.gathered, d.plane_pos, phase, d.state, d.hist, lanes_out,
                                 D->ctx->stream));
     D->ctx->launches += 1;
   }
@@ -786,14 +808,21 @@ int enprop_dist_local(enprop_dist* D, int index, int* rank, int* row_begin, int*
   return ENPROP_OK;
 }
 
-int enprop_dist_assemble(enprop_dist* D, const double* y) {
-  ScopedLaunchOpts launch_scope(D ? D->ctx : nullptr);
-  if (!D || !y) return fail(ENPROP_ERR_INVALID, "enprop_dist_assemble: null argument");
+}  // extern "C"
+
+namespace {
+
+// assemble + Dirichlet of the local ranks' store rows at u (nullptr = 0). With
+// u, the caller has put each rank's iterate with its ghost planes into the
+// ext-layout p[0] (the u halo, Alg. 2's first step).
+int dist_assemble(enprop_dist* D, const double* y, bool with_u) {
   for (auto& d : D->ranks) {
     AsmArgs a = D->setup.args;
     a.rows = d.store_rows;  // staged: the lo ghost plane's upper slots too (no communication)
     a.row_begin = d.row_begin + d.rows - d.store_rows;
-    a.u = nullptr;
+    a.kc_lo = d.store_rows > d.rows ? d.k0 - 1 : 0;  // ghost rows: cells toward the owned planes only
+    a.u = with_u ? d.p[0] : nullptr;
+    a.u_shift = d.ext_begin;
     a.y = y;
     a.row_map = d.row_map;
     a.values = d.values;
@@ -806,6 +835,16 @@ int enprop_dist_assemble(enprop_dist* D, const double* y) {
     D->ctx->launches += 1;
   }
   return ENPROP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int enprop_dist_assemble(enprop_dist* D, const double* y) {
+  ScopedLaunchOpts launch_scope(D ? D->ctx : nullptr);
+  if (!D || !y) return fail(ENPROP_ERR_INVALID, "enprop_dist_assemble: null argument");
+  return dist_assemble(D, y, false);
 }
 
 int enprop_dist_solve(enprop_dist* D, const enprop_cg_options* opt, int* iterations, int* lane_status) {
@@ -826,6 +865,10 @@ int enprop_dist_solve(enprop_dist* D, const enprop_cg_options* opt, int* iterati
       EP_CUDA(cudaMalloc(&d.hist, (size_t)(opt->max_iterations + 1) * s * sizeof(double)));
     }
     D->maxit = opt->max_iterations;
+  }
+  if (D->transport == kIpc) {  // the init sums reuse the previous solve's RR buffer
+    int rc = ipc_quiesce(D);
+    if (rc) return rc;
   }
   CgState init;
   std::memset(&init, 0, sizeof(init));
@@ -913,6 +956,106 @@ int enprop_dist_solve(enprop_dist* D, const enprop_cg_options* opt, int* iterati
   if (fin.status == ENPROP_ERR_INDEFINITE)
     return fail(ENPROP_ERR_INDEFINITE, "pcg_solve: operator not positive definite (p'Ap <= 0)");
   return ENPROP_OK;
+}
+
+// newton_solve (fem.hpp:265-302) over the slabs, with Alg. 2's first step:
+// every step imports the neighbours' boundary planes of u (the iterate is
+// staged in the ext-layout p[0] and exchanged by the solver's own halo), then
+// assembles the local rows at u. The coupled residual norm is the canonical
+// dot (per-plane sums all-gathered, summed in global plane order, then over
+// the lanes). J du = -f is solved by enprop_dist_solve, and u = 1.0*du + 1.0*u.
+// Every rank sees the same norms and takes the same decisions. The result is
+// bitwise enprop_problem_newton on one GPU with the canonical dot order.
+int enprop_dist_newton(enprop_dist* D, const double* y, const enprop_newton_options* opt,
+                       int* newton_iterations, int* total_cg_iterations, double* residual_norms,
+                       int* num_norms) {
+  ScopedLaunchOpts launch_scope(D ? D->ctx : nullptr);
+  if (!D || !y || !opt) return fail(ENPROP_ERR_INVALID, "enprop_dist_newton: null argument");
+  if (opt->max_iterations < 0) return fail(ENPROP_ERR_INVALID, "newton_solve: negative max_iterations");
+  if (opt->linear.dot_mode != ENPROP_DOT_CANONICAL)
+    return fail(ENPROP_ERR_INVALID, "enprop_dist_newton: the multi-GPU solve uses the canonical dot order");
+  const int s = D->desc.ensemble_size;
+  cudaStream_t st = D->ctx->stream;
+  double* scratch = nullptr;  // [0, 2s): the axpby coefficients (1.0); [2s, 3s + 1): the norm's lanes
+  EP_CUDA(cudaMalloc(&scratch, (3 * s + 1) * sizeof(double)));
+  struct FreeOnExit {
+    double* q;
+    ~FreeOnExit() { cudaFree(q); }
+  } free_scratch{scratch};
+  std::vector<double> ones(2 * s, 1.0);
+  EP_CUDA(cudaMemcpyAsync(scratch, ones.data(), 2 * s * sizeof(double), cudaMemcpyHostToDevice, st));
+  for (auto& d : D->ranks) {
+    const size_t vec = (size_t)d.rows * s * sizeof(double);
+    if (!d.u) EP_CUDA(cudaMalloc(&d.u, vec));
+    EP_CUDA(cudaMemsetAsync(d.u, 0, vec, st));  // result.solution = 0 (fem.hpp:271)
+  }
+  int steps = 0, cg_total = 0, nn = 0;
+  double initial = 0.0;
+  auto finish = [&](int code) {
+    if (newton_iterations) *newton_iterations = steps;
+    if (total_cg_iterations) *total_cg_iterations = cg_total;
+    if (num_norms) *num_norms = nn;
+    for (auto& d : D->ranks) {  // the iterate is reported in each rank's x
+      cudaError_t err = cudaMemcpyAsync(d.x, d.u, (size_t)d.rows * s * sizeof(double), cudaMemcpyDeviceToDevice, st);
+      if (err != cudaSuccess) return cuda_fail(err, "enprop_dist_newton");
+    }
+    cudaError_t err = cudaStreamSynchronize(st);
+    if (err != cudaSuccess) return cuda_fail(err, "enprop_dist_newton");
+    return code;
+  };
+  for (int step = 0;; ++step) {
+    // u halo (Alg. 2: import the off-rank entries of u), then assemble at u
+    for (auto& d : D->ranks)
+      EP_CUDA(cudaMemcpyAsync(d.p[0] + (size_t)d.lo_rows * s, d.u, (size_t)d.rows * s * sizeof(double),
+                              cudaMemcpyDeviceToDevice, st));
+    int rc = halo(D, 0);
+    if (rc) return rc;
+    if ((rc = dist_assemble(D, y, true))) return rc;
+    // norm2(system.residual) (fem.hpp:277): coupled, canonical order
+    for (auto& d : D->ranks) {
+      const double* res = d.residual + (size_t)(d.store_rows - d.rows) * s;
+      EP_CUDA(launch_dot_tiles(s, d.tm, res, res, rank_fin(d, kPhaseNone), st));
+      EP_CUDA(launch_fin_segments(s, d.tm, rank_fin(d, kPhaseNone), st));
+      D->ctx->launches += 2;
+    }
+    if ((rc = allgather(D, kPhaseNone))) return rc;
+    if ((rc = fin_all(D, kPhaseNone, scratch + 2 * s))) return rc;
+    double dot = 0.0;
+    EP_CUDA(cudaMemcpyAsync(&dot, scratch + 3 * s, sizeof(double), cudaMemcpyDeviceToHost, st));
+    EP_CUDA(cudaStreamSynchronize(st));
+    const double norm = std::sqrt(dot);
+    if (residual_norms && nn <= opt->max_iterations) residual_norms[nn] = norm;
+    ++nn;
+    if (step == 0) {
+      initial = norm;
+      if (initial == 0.0) return finish(ENPROP_OK);
+    } else if (norm < opt->tol * initial) {
+      steps = step;
+      return finish(ENPROP_OK);
+    }
+    if (step >= opt->max_iterations) {
+      steps = step;
+      finish(ENPROP_OK);
+      return fail(ENPROP_ERR_NO_CONVERGENCE, "newton_solve: no convergence within " +
+                                                 std::to_string(opt->max_iterations) + " iterations");
+    }
+    const int lanes = opt->linear.flavour == ENPROP_CG_UNCOUPLED ? s : 1;
+    std::vector<int> its(lanes, 0), ls(lanes, 0);
+    rc = enprop_dist_solve(D, &opt->linear, its.data(), ls.data());
+    int mx = 0;
+    for (int l = 0; l < lanes; ++l) mx = its[l] > mx ? its[l] : mx;
+    cg_total += mx;
+    if (rc) {
+      steps = step;
+      const std::string msg = enprop_last_error();
+      finish(ENPROP_OK);
+      return fail(rc, msg);
+    }
+    for (auto& d : D->ranks) {  // axpby(1.0, du, 1.0, u) (fem.hpp:300)
+      EP_CUDA(launch_axpby(s, d.rows, 0, scratch, scratch + s, d.x, d.u, st));
+      D->ctx->launches += 1;
+    }
+  }
 }
 
 }  // extern "C"

@@ -24,6 +24,9 @@ struct AsmArgs {
   int rows;              // rows assembled by this launch ((n+1)^3 on one GPU)
   int row_begin;         // global node id of local row 0 (a rank's slab; 0 on one GPU)
   int u_shift;           // u is indexed by (global node - u_shift)
+  int kc_lo;             // lowest cell plane read: a slab's lo ghost rows (only their
+                         // upper slots toward the owned plane are used) skip the
+                         // cells below, so u is read only inside the rank's halo
   int m;                 // KL terms
   double mean;           // kappa0
   const double* F;       // KL axis tables [m][2n]: f_t((c + off_b) * h)

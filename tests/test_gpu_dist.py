@@ -48,6 +48,42 @@ def test_emulated_ranks_equal_one_gpu_bitwise(ctx, s, flavour, nranks):
     d.close()
 
 
+@pytest.mark.parametrize("s", [1, 4, 32])
+@pytest.mark.parametrize("alpha,beta", [(0.0, 1.0), (0.4, 1.0)])  # staged slabs at s = 4, 32 / full storage
+@pytest.mark.parametrize("nranks", [2, 3, 5])
+def test_dist_newton_equals_one_gpu_bitwise(ctx, s, alpha, beta, nranks):
+    """Newton over the slabs (f3 with Alg. 2's u halo): every step imports the
+    neighbours' boundary planes of u before assembling, so residual norms,
+    steps, CG iterations and the iterate equal the one-GPU Newton (canonical
+    order) bit for bit."""
+    n, m = 9, 3
+    y = torch.as_tensor(pack_group(O.draw_samples(5, s, m), s)).cuda()
+    kl = ep.KlField(m, 1.0, 0.2, 1.0)
+    coeffs = ep.PdeCoefficients(alpha, beta)
+    opt = ep.NewtonOptions(tol=1e-9, max_iterations=20,
+                           linear=ep.SolverConfig(tol=1e-10, max_iterations=2000, dot_mode=ep.DOT_CANONICAL))
+    p = ep.Problem(ctx, n, s, kl, coeffs=coeffs)
+    r1 = p.newton(y, opt)
+    u1 = p.solution.cpu().numpy()
+    d = ep.Dist(ctx, n, s, nranks, kl=kl, coeffs=coeffs)
+    r2 = d.newton(y, opt)
+    u2 = d.solution().cpu().numpy()
+    assert r1.iterations >= 2  # the nonlinear term is live: more than one step
+    assert (r1.iterations, r1.total_cg_iterations) == (r2.iterations, r2.total_cg_iterations)
+    assert same(np.array(r1.residual_norms), np.array(r2.residual_norms))
+    assert same(u1, u2)
+    p.close()
+    d.close()
+
+
+def test_dist_newton_rejects_serial_order(ctx):
+    d = ep.Dist(ctx, 3, 4, 2, kl=ep.KlField(3, 1.0, 0.1, 1.0), coeffs=ep.PdeCoefficients(0.0, 1.0))
+    with pytest.raises(ValueError):
+        d.newton(torch.zeros((3, 4), dtype=torch.float64, device="cuda"),
+                 ep.NewtonOptions(linear=ep.SolverConfig(dot_mode=ep.DOT_SERIAL)))
+    d.close()
+
+
 def test_partition_matches_reference_rule(ctx):
     R = RefLib()
     n = 10
