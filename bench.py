@@ -502,12 +502,16 @@ def bench_assembly(ep, torch, w, y, hbm, peak_kind, reps=5):
                      "frac": round(tf / (dgemm / 2), 4)}}
 
 
-def bench_widths(ep, torch, device, pool, kl, groups=16):
+WIDTH_GROUPS = {1: 32, 4: 32, 8: 32, 16: 24}  # one stream each, <= the 32 hardware queues
+
+
+def bench_widths(ep, torch, device, pool, kl):
     """cfg 2 at s = 1, 4, 8, 16 (north_star: throughput at ensemble sizes
-    1/4/8/16/32): `groups` concurrent groups per width, one round, both dot
-    orders (the serial order is bitwise the reference at every width)."""
+    1/4/8/16/32): WIDTH_GROUPS[s] concurrent groups per width (narrow groups
+    are latency-bound, so more of them fit), one round, both dot orders (the
+    serial order is bitwise the reference at every width)."""
     out = {}
-    for s in (1, 4, 8, 16):
+    for s, groups in WIDTH_GROUPS.items():
         ws = [GroupWorker(ep, torch, device, kl, s=s) for _ in range(groups)]
         ys = [ep.pack_sample_group(pool, s, s * i).cuda() for i in range(groups)]
         res = {}

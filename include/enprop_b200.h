@@ -371,6 +371,11 @@ int enprop_dist_solve(enprop_dist* d, const enprop_cg_options* opt, int* iterati
 int enprop_dist_newton(enprop_dist* d, const double* y, const enprop_newton_options* opt,
                        int* newton_iterations, int* total_cg_iterations, double* residual_norms,
                        int* num_norms);
+/* Staged slabs (s in {4, 16, 32}): the local rank's SpMV stages and how many
+ * of them are interior (rows at least one plane from every ghost plane). Each
+ * CG iteration runs the interior stages while the halo is in flight and the
+ * rest after it. Unstaged slabs report 0 / 0. */
+int enprop_dist_stages(enprop_dist* d, int index, int* interior, int* total);
 /* local ranks (1 with NCCL, nranks when emulated) and their owned rows / solution */
 int enprop_dist_local_count(enprop_dist* d);
 int enprop_dist_local(enprop_dist* d, int index, int* rank, int* row_begin, int* rows,

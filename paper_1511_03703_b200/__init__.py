@@ -244,6 +244,7 @@ def lib() -> C.CDLL:
     L.enprop_dist_solve.argtypes = [_vp, C.POINTER(_CgOptions), _ip, _ip]
     L.enprop_dist_newton.argtypes = [_vp, _vp, C.POINTER(_NewtonOptions), _ip, _ip, _dp, _ip]
     L.enprop_dist_local_count.argtypes = [_vp]
+    L.enprop_dist_stages.argtypes = [_vp, C.c_int, _ip, _ip]
     L.enprop_dist_local.argtypes = [_vp, C.c_int, _ip, _ip, _ip, C.POINTER(_vp)]
     _lib = L
     return L
@@ -848,6 +849,16 @@ class Dist:
             _check(lib().enprop_dist_local(self.h, i, C.byref(rk), C.byref(rb), C.byref(rows), C.byref(xp)))
             x = _wrap_device_ptr(xp.value, rows.value * self.s, torch.float64, self.ctx.device)
             out.append((rk.value, rb.value, rows.value, x.view(rows.value, self.s)))
+        return out
+
+    def stages(self):
+        """[(interior, total)] SpMV stages of the local ranks: the interior ones
+        run while the halo is in flight (0, 0 for unstaged slabs)."""
+        out = []
+        for i in range(lib().enprop_dist_local_count(self.h)):
+            a, b = C.c_int(), C.c_int()
+            _check(lib().enprop_dist_stages(self.h, i, C.byref(a), C.byref(b)), "stages")
+            out.append((a.value, b.value))
         return out
 
     def solution(self) -> torch.Tensor:

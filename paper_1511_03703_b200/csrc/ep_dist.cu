@@ -178,6 +178,9 @@ struct enprop_dist {
   ncclComm_t comm = nullptr;
   AsmSetup setup;
   std::vector<DistRank> ranks;  // emulated: all ranks; NCCL / IPC: this process's rank
+  // halo overlap: the halo runs on `side` while the interior stages run
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_owned = nullptr, ev_halo = nullptr;
   // IPC transport
   std::string board_name;
   IpcBoard* board = nullptr;
@@ -265,8 +268,12 @@ int setup_rank(enprop_dist* D, DistRank& d, int r) {
   EP_CUDA(cudaMalloc(&d.up_start, (d.store_rows + 1) * sizeof(int)));
   EP_CUDA(build_sym(d.store_rows, d.row_map, d.col_entry, d.vpos, &d.nnz_stored, st, d.up_start, d.lo_rows));
   EP_CUDA(cudaMalloc(&d.values, (size_t)d.nnz_stored * s * sizeof(double)));
+  // interior stages: rows at least one plane away from every ghost plane
+  // (ranks with a neighbour; ENPROP_DIST_OVERLAP=0 keeps one launch, A/B)
+  const bool split = (d.lo_rows || d.hi_rows) && env_int("ENPROP_DIST_OVERLAP", 1) != 0;
+  const int ilo = split ? (d.lo_rows ? plane : 0) : 0, ihi = split ? (d.hi_rows ? d.rows - plane : d.rows) : 0;
   EP_CUDA(build_stage_map(s, d.tm, N, d.row_map + d.lo_rows, d.col_entry, d.vpos, d.up_start + d.lo_rows,
-                          d.stage, st, -d.lo_rows, d.rows + d.hi_rows));
+                          d.stage, st, -d.lo_rows, d.rows + d.hi_rows, ilo, ihi));
   D->ctx->launches += 4;
   return ENPROP_OK;
 }
@@ -333,11 +340,11 @@ int ipc_publish(enprop_dist* D, int kind) {
   return ENPROP_OK;
 }
 
-// make the stream wait for rank q's record of `kind` matching ours
-int ipc_wait(enprop_dist* D, int q, int kind) {
+// make stream `st` (default: the context's) wait for rank q's record of `kind` matching ours
+int ipc_wait(enprop_dist* D, int q, int kind, cudaStream_t st = nullptr) {
   int rc = ipc_wait_seq(D, q, kind, D->seq[kind]);
   if (rc) return rc;
-  EP_CUDA(cudaStreamWaitEvent(D->ctx->stream, D->peer_ev[kind][q], 0));
+  EP_CUDA(cudaStreamWaitEvent(st ? st : D->ctx->stream, D->peer_ev[kind][q], 0));
   return ENPROP_OK;
 }
 
@@ -444,11 +451,13 @@ void ipc_teardown(enprop_dist* D) {
 }
 
 // halo of the p buffer `which` (first owned plane -> rank-1's hi ghost, last
-// owned plane -> rank+1's lo ghost)
-int halo(enprop_dist* D, int which) {
+// owned plane -> rank+1's lo ghost), its copies on stream `st` (default: the
+// context's); the owned planes must be complete on the context's stream
+// (IPC: publish = false when the caller already published the owned planes)
+int halo(enprop_dist* D, int which, cudaStream_t st = nullptr, bool publish = true) {
   const int s = D->desc.ensemble_size;
   const size_t pe = (size_t)D->plane * s;
-  cudaStream_t st = D->ctx->stream;
+  if (!st) st = D->ctx->stream;
   if (D->emulated) {
     for (size_t i = 0; i < D->ranks.size(); ++i) {
       DistRank& d = D->ranks[i];
@@ -467,19 +476,19 @@ int halo(enprop_dist* D, int which) {
   }
   DistRank& d = D->ranks[0];
   if (D->transport == kIpc) {  // publish p[which], pull the neighbours' boundary planes
-    int rc = ipc_publish(D, kEvP);
+    int rc = publish ? ipc_publish(D, kEvP) : ENPROP_OK;
     if (rc) return rc;
     if (d.rank > 0) {
       int lo, lr, rws;
       rank_layout(D, d.rank - 1, lo, lr, rws);
-      if ((rc = ipc_wait(D, d.rank - 1, kEvP))) return rc;
+      if ((rc = ipc_wait(D, d.rank - 1, kEvP, st))) return rc;
       EP_CUDA(cudaMemcpyAsync(d.p[which], D->peer_p[which][d.rank - 1] + (size_t)(lr + rws - D->plane) * s,
                               pe * sizeof(double), cudaMemcpyDefault, st));
     }
     if (d.rank + 1 < D->nranks) {
       int lo, lr, rws;
       rank_layout(D, d.rank + 1, lo, lr, rws);
-      if ((rc = ipc_wait(D, d.rank + 1, kEvP))) return rc;
+      if ((rc = ipc_wait(D, d.rank + 1, kEvP, st))) return rc;
       EP_CUDA(cudaMemcpyAsync(d.p[which] + (size_t)(d.lo_rows + d.rows) * s, D->peer_p[which][d.rank + 1] + (size_t)lr * s,
                               pe * sizeof(double), cudaMemcpyDefault, st));
     }
@@ -553,6 +562,9 @@ int enprop_dist_destroy(enprop_dist* D) {
   if (!D) return ENPROP_OK;
   ipc_teardown(D);
   for (auto& d : D->ranks) free_rank(d);
+  if (D->side) cudaStreamDestroy(D->side);
+  if (D->ev_owned) cudaEventDestroy(D->ev_owned);
+  if (D->ev_halo) cudaEventDestroy(D->ev_halo);
   free_asm_setup(D->setup);
   if (D->comm) nccl().CommDestroy(D->comm);
   delete D;
@@ -585,6 +597,10 @@ static int dist_create(enprop_ctx* c, const enprop_problem_desc* desc, int nrank
   };
   int rc = make_asm_setup(c, n, &desc->kl, &desc->coeffs, D->setup);
   if (rc) return bail(rc);
+  if (cudaStreamCreateWithFlags(&D->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&D->ev_owned, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&D->ev_halo, cudaEventDisableTiming) != cudaSuccess)
+    return bail(fail(ENPROP_ERR_CUDA, "enprop_dist_create: stream / event creation failed"));
   if (D->transport == kNccl) {
     if (!nccl().load()) return bail(fail(ENPROP_ERR_CUDA, "libnccl.so.2 could not be loaded"));
     ncclUniqueId id;
@@ -796,6 +812,14 @@ int enprop_predicted_speedup(double a, double b, double s, double* speedup) {
   return ENPROP_OK;
 }
 
+int enprop_dist_stages(enprop_dist* D, int index, int* interior, int* total) {
+  if (!D || index < 0 || index >= (int)D->ranks.size()) return fail(ENPROP_ERR_INVALID, "enprop_dist_stages: bad index");
+  const DistRank& d = D->ranks[index];
+  if (interior) *interior = d.staged ? d.stage.n_interior : 0;
+  if (total) *total = d.staged ? d.stage.nstages : 0;
+  return ENPROP_OK;
+}
+
 int enprop_dist_local_count(enprop_dist* D) { return D ? (int)D->ranks.size() : 0; }
 
 int enprop_dist_local(enprop_dist* D, int index, int* rank, int* row_begin, int* rows, double** x) {
@@ -903,11 +927,30 @@ int enprop_dist_solve(enprop_dist* D, const enprop_cg_options* opt, int* iterati
                                     d.p[pn] + (size_t)d.lo_rows * s, d.x, d.state, st));
         ctx->launches += 1;
       }
-      if ((rc = halo(D, pn))) return rc;
+      // halo on the side stream, overlapped with the interior stages (DESIGN.md
+      // §7). IPC: the owned planes are published before the interior launch
+      // (peers pull them meanwhile), and the pulls are enqueued after it,
+      // since waiting for the peers' publishes blocks this host thread.
+      EP_CUDA(cudaEventRecord(D->ev_owned, st));
+      EP_CUDA(cudaStreamWaitEvent(D->side, D->ev_owned, 0));
+      const bool ipc = D->transport == kIpc;
+      if ((rc = ipc ? ipc_publish(D, kEvP) : halo(D, pn, D->side))) return rc;
+      for (auto& d : D->ranks) {
+        if (d.staged && d.stage.n_interior > 0) {  // owned rows only: x runs clipped to [0, rows)
+          EP_CUDA(launch_cg_spmv_staged(s, true, false, stage_range(d.stage, 0, d.stage.n_interior, 0, d.rows),
+                                        d.values, d.p[pn] + (size_t)d.lo_rows * s, d.q, rank_fin(d, kPhasePQ), st));
+          ctx->launches += 1;
+        }
+      }
+      if (ipc && (rc = halo(D, pn, D->side, false))) return rc;
+      EP_CUDA(cudaEventRecord(D->ev_halo, D->side));
+      EP_CUDA(cudaStreamWaitEvent(st, D->ev_halo, 0));
       for (auto& d : D->ranks) {
         if (d.staged)
-          EP_CUDA(launch_cg_spmv_staged(s, true, false, d.stage, d.values, d.p[pn] + (size_t)d.lo_rows * s, d.q,
-                                        rank_fin(d, kPhasePQ), st));
+          EP_CUDA(launch_cg_spmv_staged(s, true, false,
+                                        stage_range(d.stage, d.stage.n_interior, d.stage.nstages - d.stage.n_interior,
+                                                    d.stage.xlo, d.stage.xhi),
+                                        d.values, d.p[pn] + (size_t)d.lo_rows * s, d.q, rank_fin(d, kPhasePQ), st));
         else
           EP_CUDA(launch_cg_spmv(s, true, false, false, d.tm, d.row_map, d.col_entry, d.values, d.r,
                                  d.p[po] + (size_t)d.lo_rows * s, d.p[pn] + (size_t)d.lo_rows * s, d.q,

@@ -185,6 +185,8 @@ struct StageMap {
   StageDesc* desc = nullptr;
   unsigned char* blk = nullptr;
   int64_t blk_bytes = 0;
+  int idx_bytes = 0;   // one stage's index block
+  int n_interior = 0;  // slabs: the first n_interior sweep positions read no ghost plane
 };
 
 bool staged_supported(int s, int N);
@@ -195,8 +197,15 @@ bool staged_supported(int s, int N);
 // may reach [xlo, xhi) (defaults: [0, tm.rows)).
 cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
                             const int* col_entry, const int* vpos, const int* up_start,
-                            StageMap& sm, cudaStream_t st, int xlo = 0, int xhi = -1);
+                            StageMap& sm, cudaStream_t st, int xlo = 0, int xhi = -1,
+                            int interior_lo = 0, int interior_hi = -1);
 void free_stage_map(StageMap& sm);
+// Halo overlap (slabs): with interior_lo < interior_hi, the stages whose rows
+// all lie in [interior_lo, interior_hi) go first in the sweep (n_interior of
+// them). Their x runs then stay inside the owned rows, so they can run while
+// the ghost planes are in flight. stage_range views sweep positions
+// [pos0, pos0 + count) as a map of its own, with x runs clipped to [xlo, xhi).
+StageMap stage_range(const StageMap& sm, int pos0, int count, int xlo, int xhi);
 // q = A p and (tiles) the canonical p.q tile partials; bitwise equal to the
 // warp-per-tile kernel
 // fuse_fin (tiles only): the kernel also runs the canonical finalize of p.q

@@ -532,7 +532,8 @@ bool staged_supported(int s, int N) { return (s == 4 || s == 16 || s == 32) && N
 
 cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
                             const int* col_entry, const int* vpos, const int* up_start,
-                            StageMap& sm, cudaStream_t st, int xlo, int xhi) {
+                            StageMap& sm, cudaStream_t st, int xlo, int xhi, int interior_lo,
+                            int interior_hi) {
   free_stage_map(sm);
   if (!staged_supported(s, N) || tm.rows <= 0 || tm.rows % (N * N) != 0) return cudaErrorInvalidValue;
   int T = 0, L = 0, RS = 0, max_upper = 0, idx_bytes = 0, zc = 0;
@@ -591,6 +592,12 @@ cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
     if (env_int("ENPROP_STAGED_ORDER", 1) != 0)  // 0: plain row order (A/B)
       std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return key[a] < key[b]; });
   }
+  sm.n_interior = 0;
+  if (interior_lo < interior_hi) {  // interior stages first, each part in sweep order
+    auto interior = [&](int g) { return hd[g].R0 >= interior_lo && hd[g].R1 <= interior_hi; };
+    const auto mid = std::stable_partition(ord.begin(), ord.end(), interior);
+    sm.n_interior = (int)(mid - ord.begin());
+  }
   {  // store descriptors and index blocks in sweep order
     std::vector<StageDesc> sorted(hd.size());
     for (size_t q = 0; q < hd.size(); ++q) {
@@ -606,6 +613,7 @@ cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
   sm.xlo = xlo;
   sm.xhi = xhi < 0 ? tm.rows : xhi;
   sm.blk_bytes = off;
+  sm.idx_bytes = idx_bytes;
   int* bad = nullptr;
   err = cudaMalloc(&sm.desc, hd.size() * sizeof(StageDesc) + 16);
 
@@ -628,6 +636,18 @@ cudaError_t build_stage_map(int s, const TileMap& tm, int N, const int* row_map,
   if (err == cudaSuccess && hbad) err = cudaErrorInvalidValue;  // not the structured 27-point graph
   if (err != cudaSuccess) free_stage_map(sm);
   return err;
+}
+
+StageMap stage_range(const StageMap& sm, int pos0, int count, int xlo, int xhi) {
+  StageMap r = sm;  // a view: desc / blk are not owned (never free_stage_map it)
+  r.desc = sm.desc + pos0;
+  r.blk = sm.blk + (int64_t)pos0 * sm.idx_bytes;
+  r.nstages = count;
+  r.blk_bytes = (int64_t)count * sm.idx_bytes;
+  r.n_interior = 0;
+  r.xlo = xlo;
+  r.xhi = xhi;
+  return r;
 }
 
 void free_stage_map(StageMap& sm) {

@@ -84,6 +84,26 @@ def test_dist_newton_rejects_serial_order(ctx):
     d.close()
 
 
+def test_halo_overlap_splits_interior_stages(ctx):
+    """Staged slabs order their interior stages (no ghost plane read) first; the
+    iteration runs them while the halo is in flight. Ranks with >= 3 planes have
+    some, a lone rank (no ghosts) runs every stage in one launch (0 interior),
+    and unstaged widths report none."""
+    n = 10  # 11 planes
+    kl = ep.KlField(3, 1.0, 0.1, 1.0)
+    d = ep.Dist(ctx, n, 32, 3, kl=kl)  # 4 + 4 + 3 planes
+    for (interior, total), (_, rb, rows, _) in zip(d.stages(), d.local()):
+        assert 0 < interior < total
+    d.close()
+    d = ep.Dist(ctx, n, 32, 1, kl=kl)
+    (interior, total), = d.stages()
+    assert interior == 0 and total > 0
+    d.close()
+    d = ep.Dist(ctx, n, 8, 3, kl=kl)
+    assert all(st == (0, 0) for st in d.stages())
+    d.close()
+
+
 def test_partition_matches_reference_rule(ctx):
     R = RefLib()
     n = 10
