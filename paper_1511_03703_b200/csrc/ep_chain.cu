@@ -11,8 +11,8 @@
 //  * one CTA per dot; warp 0 consumes: lane e < S runs sample e's chain, so a
 //    row's S values are one contiguous 8S-byte read from shared memory and the
 //    chain never hands off between lanes;
-//  * warp 1 lane 0 produces: rows arrive as 16 KB stages (per operand) via
-//    cp.async.bulk into an 8-stage ring (6 for two operands), completing on
+//  * warp 1 lane 0 produces: rows arrive as 32 KB stages (per operand) via
+//    cp.async.bulk into a 4-stage ring (3 for two operands), completing on
 //    mbarriers; the producer alone waits on `empty` barriers, so copy issue
 //    stays off the chain;
 //  * the consumer walks a stage in fully unrolled 64-row blocks (the compiler
@@ -24,8 +24,12 @@
 // shared-memory rings (<= 16 KB) at 20-80 (too few bytes in flight for the
 // ~900-cycle TMA latency, and every consumer-side barrier probe stalls issue);
 // register-batched consumption of a big ring at 16-19 (moves + batch waits);
-// ring depth (A/B, profiles/round2/README.md §3, 24-32 groups): 4 / 6 stages
-// 494-503 samples/s, 8 stages 548-555, 10 / 12 stages 539-555.
+// ring shape (A/B, profiles/round2/README.md §3, 24 groups): 16 KB stages x 4
+// / 6 gave 494-503 samples/s, x 8 548-569; 32 KB x 4 (the same 128 KB, half the
+// per-stage waits) 574-577, with the p.q / r.r chains at 1.41 / 1.63 ms
+// vs 1.57 / 1.84 ms for 16 KB x 8. A software-pipelined consumer (the next
+// 32-row block's terms formed ahead) ran at ~18 cycles per row: ptxas issued
+// the next block as one run before the DADDs, plus the register copies.
 // The CG scalar phase (ep_fin.cuh cg_phase) runs in the consumer warp.
 //
 // In the CG loop the SpMV writes the products p*q (f.prod) and the r.r chain
@@ -43,13 +47,13 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-constexpr int kChainChunkBytes = 16384;  // per operand vector per stage
+constexpr int kChainChunkBytes = 32768;  // per operand vector per stage
 constexpr int kChainBlock = 64;          // rows per unrolled consumer block
 
 template <int NV, int CB = kChainChunkBytes>
 struct ChainRing {
   static constexpr int STAGE = CB * NV;
-  static constexpr int D = NV == 1 ? 8 : 6;  // stages in the ring (128 / 192 KB)
+  static constexpr int D = (NV == 1 ? 131072 : 196608) / STAGE;  // stages in the ring (128 / 192 KB)
   static constexpr int SMEM = D * STAGE + 2 * D * 8;
 };
 
@@ -148,10 +152,10 @@ bool chain_aligned(const void* u, const void* v) {
   return ((reinterpret_cast<uintptr_t>(u) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
 }
 
-template <int S, int KIND>
+template <int S, int KIND, int CB = kChainChunkBytes>
 static cudaError_t chain_sk(int rows, const double* u, const double* v, const FinArgs& f, cudaStream_t st) {
   constexpr int NV = KIND == kChainProduct ? 2 : 1;
-  constexpr int SMEM = ChainRing<NV>::SMEM;
+  constexpr int SMEM = ChainRing<NV, CB>::SMEM;
   // shared-memory opt-in once per device (solves on several host threads)
   static std::atomic<int> ready[64];
   static std::mutex mu;
@@ -162,12 +166,12 @@ static cudaError_t chain_sk(int rows, const double* u, const double* v, const Fi
   if (!ready[dev].load(std::memory_order_acquire)) {
     std::lock_guard<std::mutex> lock(mu);
     if (!ready[dev].load(std::memory_order_relaxed)) {
-      err = cudaFuncSetAttribute(k_chain<S, KIND, kChainChunkBytes>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+      err = cudaFuncSetAttribute(k_chain<S, KIND, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
       if (err != cudaSuccess) return err;
       ready[dev].store(1, std::memory_order_release);
     }
   }
-  launch_kk(4, k_chain<S, KIND, kChainChunkBytes>, dim3(1), dim3(64), SMEM, st, rows, u, v, f);
+  launch_kk(4, k_chain<S, KIND, CB>, dim3(1), dim3(64), SMEM, st, rows, u, v, f);
   return cudaGetLastError();
 }
 
