@@ -318,7 +318,11 @@ def run_ours(args):
         extra["cfg5"] = bench_cfg5(ep, torch, local)
         extra["cfg4_one_gpu"] = bench_cfg4_one_gpu(ep, torch, local)
     if not args.skip_dd:  # every rank takes part (strong scaling of one 256^3 ensemble)
-        dd = bench_cfg4_dd(ep, torch, dist, local, rank, world, args.dd_mesh)
+        try:
+            dd = bench_cfg4_dd(ep, torch, dist, local, rank, world, args.dd_mesh)
+        except Exception as e:  # never lose the headline line to this extra (peers time out too)
+            dd = {"mesh": args.dd_mesh, "ranks": world, "error": repr(e)[:300]}
+            torch.cuda.empty_cache()
         if rank == 0:
             extra["cfg4_dd"] = dd
     cpu = None
