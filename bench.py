@@ -383,7 +383,8 @@ def bench_roofline(ep, w, y, cfg, dot, hbm, peak_kind):
     it_bytes = byt + direction_bytes(rows, S) + 3 * 8 * S * rows  # + update (r, q -> r)
     out = {"bound": "hbm", "kernel": kname,
            "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-           "frac": round(achieved / hbm, 4), "traffic": measured_traffic(kname),
+           "frac": round(achieved / hbm, 4), "frac_of_8000_spec": round(achieved / 8000.0, 4),
+           "traffic": measured_traffic(kname),
            "bytes_per_launch": byt, "avg_launch_ms": round(avg_spmv_ms, 4), "launches_timed": spmv_n,
            "share_of_iteration_hbm_work": round(avg_spmv_ms / (avg_spmv_ms + det["direction"] / nit + det["update"] / nit), 3),
            "per_iteration_ms": {k: round(det[k] / nit, 4) for k in
