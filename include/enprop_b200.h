@@ -81,7 +81,8 @@ int64_t enprop_ctx_launch_count(enprop_ctx* ctx);
  *   (entries per gather batch / CTAs per SM): 0: 4/4, 1: 4/4 + index prefetch,
  *   2: 8/2, 3: 8/2 + index prefetch, 4: 4/4 zero-padded, 5: 8/3, 6: 16/1;
  *   auto = 2 with symmetric storage, 0 otherwise.
- *   ENPROP_OPT_GRAPHS (default 1): CG iterations are replayed from a CUDA graph
+ *   ENPROP_OPT_GRAPHS (default 1; the environment variable ENPROP_GRAPHS=0
+ *   makes it 0 for new contexts): CG iterations are replayed from a CUDA graph
  *   of one convergence-check chunk (check_every iterations) instead of being
  *   launched kernel by kernel (not while profiling).
  * Options are per context: calls through a context (and through problems and

@@ -417,6 +417,12 @@ int enprop_ctx_create(int device, enprop_ctx** out) {
   auto* c = new (std::nothrow) enprop_ctx();
   if (!c) return fail(ENPROP_ERR_OOM, "enprop_ctx_create: out of host memory");
   c->device = device;
+  // ENPROP_GRAPHS=0 (env) makes "off" the default of ENPROP_OPT_GRAPHS: Nsight
+  // Compute 2025.2.1 aborts with host heap corruption when many threads capture and
+  // replay CUDA graphs concurrently (24-group bench, graphs on; clean with them
+  // off, and clean without the profiler under MALLOC_CHECK_=3), so profiling
+  // runs launch kernel by kernel
+  c->graphs = env_int("ENPROP_GRAPHS", 1) != 0 ? 1 : 0;
   EP_CUDA(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   c->stream = c->own;
   EP_CUDA(cudaMallocHost(&c->pinned_flags, 2 * sizeof(int)));

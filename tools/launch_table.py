@@ -1,14 +1,15 @@
 """Summarise an ncu launch list (``ncu --metrics gpu__time_duration.sum --csv
 --log-file X``) into the markdown table kept under profiles/.
-    python tools/launch_table.py launches.csv"""
+    python tools/launch_table.py launches.csv[.xz]"""
 import collections
 import csv
+import lzma
 import statistics
 import sys
 
 
 def main(path):
-    rows = list(csv.reader(open(path)))
+    rows = list(csv.reader(lzma.open(path, "rt") if path.endswith(".xz") else open(path)))
     i = 0
     while not rows[i] or rows[i][0] != "ID":
         i += 1
