@@ -47,7 +47,7 @@ SPMV_MESH = 128
 # order reproduces them bitwise (tests/test_gpu_cfg.py).
 CFG2_FIXTURE = os.path.join(ROOT, "tests", "golden", "cfg2_64_s32.npz")
 # scalar CG iterations per sample in the reference arm's bounded sample
-# (extrapolation checked against a full solve: tools/ref_extrapolation.py)
+# (extrapolation checked against a full solve: tests/ref_extrapolation.py)
 REF_SAMPLE_ITERS = 6
 
 
@@ -317,6 +317,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.skip_configs:
         extra["cfg5"] = bench_cfg5(ep, torch, local)
         extra["cfg4_one_gpu"] = bench_cfg4_one_gpu(ep, torch, local)
+        extra["multigrid_newton"] = bench_multigrid(ep, torch, local)
     if not args.skip_dd:  # every rank takes part (strong scaling of one 256^3 ensemble)
         try:
             dd = bench_cfg4_dd(ep, torch, dist, local, rank, world, args.dd_mesh)
@@ -546,6 +547,57 @@ def bench_cfg5(ep, torch, device):
         out[name] = {"iterations": it if fl == ep.CG_UNCOUPLED else it[0],  # per lane / coupled
                      "samples_per_s": round(S / (ms / 1e3), 3), "ms": round(ms, 1)}
     w.close()
+    return out
+
+
+def bench_multigrid(ep, torch, device, n=32):
+    """f4 and f3 measured where the reference's multigrid is practical (its
+    dense-LU coarse level): cfg 1's mesh, s = 32, KL m = 3,
+    sigma = 0.1, the reference's serial dot order (bitwise its MG-PCG and
+    newton_solve: tests/test_gpu_mg.py). Host-driven solves, so wall times
+    with the device synchronised on both sides."""
+    s = S
+    ctx = ep.Context(device)
+    kl = ep.KlField(M_TERMS, 1.0, SIGMA, 1.0)
+    y = ep.pack_sample_group(ep.draw_samples(0, s, M_TERMS), s, 0).cuda()
+
+    def wall(fn):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = fn()
+        torch.cuda.synchronize()
+        return (time.perf_counter() - t0) * 1e3, r
+
+    out = {"mesh": n, "s": s, "dot_order": "serial (bitwise the reference)"}
+    p = ep.Problem(ctx, n, s, kl)
+    p.assemble(y)
+    vals, b = p.values, (-p.residual).contiguous()
+    cfg = ep.SolverConfig(tol=TOL, max_iterations=10000, flavour=ep.CG_COUPLED, dot_mode=ep.DOT_SERIAL)
+    h = ep.MgHierarchy(ctx, s, p.row_map, p.col_entry, vals)  # warm-up build
+    h.close()
+    ms_build, h = wall(lambda: ep.MgHierarchy(ctx, s, p.row_map, p.col_entry, vals))
+    rows, _ = h.describe()
+    h.pcg(b, cfg)  # warm-up
+    ms_mg, res = wall(lambda: h.pcg(b, cfg))
+    p.solve(cfg)
+    ms_id, (it_id, _, _) = wall(lambda: p.solve(cfg))
+    out["mg_pcg_coupled"] = {"levels_rows": rows, "build_ms": round(ms_build, 1), "solve_ms": round(ms_mg, 1),
+                             "iterations": res.iterations}
+    out["identity_cg_coupled"] = {"solve_ms": round(ms_id, 1), "iterations": it_id}
+    h.close()
+    del vals
+    p.close()
+    q = ep.Problem(ctx, n, s, kl, coeffs=ep.PdeCoefficients(0.0, 1.0))
+    nopt = ep.NewtonOptions(tol=1e-8, max_iterations=20,
+                            linear=ep.SolverConfig(tol=1e-8, max_iterations=1000, dot_mode=ep.DOT_SERIAL))
+    q.newton(y, nopt, multigrid=ep.MgOptions())
+    ms_nmg, r_mg = wall(lambda: q.newton(y, nopt, multigrid=ep.MgOptions()))
+    ms_nid, r_id = wall(lambda: q.newton(y, nopt))
+    out["newton_beta1"] = {
+        "multigrid": {"ms": round(ms_nmg, 1), "steps": r_mg.iterations, "cg_iterations": r_mg.total_cg_iterations},
+        "identity": {"ms": round(ms_nid, 1), "steps": r_id.iterations, "cg_iterations": r_id.total_cg_iterations}}
+    q.close()
+    ctx.close()
     return out
 
 

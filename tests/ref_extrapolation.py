@@ -1,4 +1,6 @@
-"""Check bench.py's reference-arm extrapolation once: the reference's uncoupled
+"""Check bench.py's reference-arm extrapolation once (a measurement script kept
+under tests/ because it runs the reference, oracle/_ref; not collected by
+pytest): the reference's uncoupled
 cfg-2 solve of group 0 (assemble<Ensemble<32>> + apply_dirichlet + 32 x
 pcg_solve<double> on extract_component, tol 1e-6) timed in full on one host
 core, against the bounded sample bench.py uses (full assembly + 2 scalar

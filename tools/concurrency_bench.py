@@ -11,11 +11,9 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tests"))
 import torch  # noqa: E402
 
 import paper_1511_03703_b200 as ep  # noqa: E402
-from oracles import Oracle, pack_group  # noqa: E402
 
 
 def main():
@@ -28,11 +26,10 @@ def main():
     ap.add_argument("--pdl", type=int, default=0)
     args = ap.parse_args()
     n, s = args.n, 32
-    O = Oracle()
     Gmax = max(int(g) for g in args.groups.split(","))
-    pool = O.draw_samples(0, s * Gmax * (args.rounds + 1), 3)
+    pool = ep.draw_samples(0, s * Gmax * (args.rounds + 1), 3)
     workers = []
-    shared = [torch.as_tensor(pack_group(pool, s, g)).cuda() for g in range(3)]
+    shared = [ep.pack_sample_group(pool, s, s * g).cuda() for g in range(3)]
     for g in range(Gmax):
         ctx = ep.Context(0, use_torch_stream=False)
         if args.torch_streams:
@@ -44,7 +41,7 @@ def main():
         if args.torch_streams:
             ys = [shared[g % 3] for r in range(args.rounds + 1)]
         else:
-            ys = [torch.as_tensor(pack_group(pool, s, r * Gmax + g)).cuda() for r in range(args.rounds + 1)]
+            ys = [ep.pack_sample_group(pool, s, s * (r * Gmax + g)).cuda() for r in range(args.rounds + 1)]
         workers.append((ctx, p, ys))
     torch.cuda.synchronize()
     mode = ep.DOT_CANONICAL if args.dot == "canonical" else ep.DOT_SERIAL

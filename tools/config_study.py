@@ -19,15 +19,13 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tests"))
 import torch  # noqa: E402
 
 import paper_1511_03703_b200 as ep  # noqa: E402
-from oracles import Oracle, pack_group  # noqa: E402
 
 
 def solve_line(ctx, O, n, s, m, sigma, flavour, dot, reps=2, tag=""):
-    y = torch.as_tensor(pack_group(O.draw_samples(0, s, m), s)).cuda()
+    y = ep.pack_sample_group(ep.draw_samples(0, s, m), s, 0).cuda()
     p = ep.Problem(ctx, n, s, ep.KlField(m, 1.0, sigma, 1.0))
     cfg = ep.SolverConfig(tol=1e-6, max_iterations=20000, flavour=flavour,
                           dot_mode=ep.DOT_CANONICAL if dot == "canonical" else ep.DOT_SERIAL)
@@ -59,7 +57,6 @@ def main():
     args = ap.parse_args()
     which = set(args.which.split(","))
     ctx = ep.Context(0)
-    O = Oracle()
     if "1" in which:
         for fl in (ep.CG_COUPLED, ep.CG_UNCOUPLED):
             print(json.dumps(solve_line(ctx, O, 32, 16, 3, 0.1, fl, args.dot, tag="cfg1")), flush=True)

@@ -11,12 +11,10 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import torch  # noqa: E402
 
 import paper_1511_03703_b200 as ep  # noqa: E402
-from oracles import Oracle, pack_group  # noqa: E402
 
 
 def main():
@@ -37,8 +35,7 @@ def main():
     ctx = ep.Context(0)
     ctx.set_option(ep.OPT_SPMV_VARIANT, args.variant)
     ctx.set_option(ep.OPT_PDL, args.pdl)
-    O = Oracle()
-    y = torch.as_tensor(pack_group(O.draw_samples(0, s, 3), s)).cuda()
+    y = ep.pack_sample_group(ep.draw_samples(0, s, 3), s, 0).cuda()
     ctx.set_option(ep.OPT_SYMMETRIC_STORAGE, 0)
     pfull = ep.Problem(ctx, n, s, ep.KlField(3, 1.0, 0.1, 1.0))
     ctx.set_option(ep.OPT_SYMMETRIC_STORAGE, args.sym)

@@ -8,11 +8,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tests"))
 import torch  # noqa: E402
 
 import paper_1511_03703_b200 as ep  # noqa: E402
-from oracles import Oracle, pack_group  # noqa: E402
 
 
 def main():
@@ -22,7 +20,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=4)
     args = ap.parse_args()
     ctx = ep.Context(0)
-    y = torch.as_tensor(pack_group(Oracle().draw_samples(0, args.s, 3), args.s)).cuda()
+    y = ep.pack_sample_group(ep.draw_samples(0, args.s, 3), args.s, 0).cuda()
     p = ep.Problem(ctx, args.n, args.s, ep.KlField(3, 1.0, 0.1, 1.0))
     p.assemble(y)
     cfg = ep.SolverConfig(tol=1e-6, max_iterations=10000, flavour=ep.CG_UNCOUPLED, dot_mode=ep.DOT_CANONICAL)

@@ -43,12 +43,9 @@ def phase_times(s=32, n=64, dot="serial"):
     """Per-iteration phase times (CUDA events) of one single-stream solve."""
     import torch
     import paper_1511_03703_b200 as ep
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracles import Oracle, pack_group
-    O = Oracle()
     ctx = ep.Context(0)
     p = ep.Problem(ctx, n, s, ep.KlField(3, 1.0, 0.1, 1.0))
-    y = torch.as_tensor(pack_group(O.draw_samples(0, s, 3), s)).cuda()
+    y = ep.pack_sample_group(ep.draw_samples(0, s, 3), s, 0).cuda()
     cfg = ep.SolverConfig(tol=1e-6, max_iterations=10000, flavour=ep.CG_UNCOUPLED,
                           dot_mode=ep.DOT_SERIAL if dot == "serial" else ep.DOT_CANONICAL)
     p.assemble(y)

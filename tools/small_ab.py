@@ -12,12 +12,10 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import torch  # noqa: E402
 
 import paper_1511_03703_b200 as ep  # noqa: E402
-from oracles import Oracle, pack_group  # noqa: E402
 from bench import time_queued  # noqa: E402
 
 
@@ -27,11 +25,10 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     args = ap.parse_args()
     ctx = ep.Context(0)
-    O = Oracle()
     out = {"nt": os.environ.get("ENPROP_SMALL_NT", "default"), "n": args.n}
     st = torch.cuda.current_stream()
     for s in (1, 2, 4, 8, 16, 32):
-        y = torch.as_tensor(pack_group(O.draw_samples(0, s, 3), s)).cuda()
+        y = ep.pack_sample_group(ep.draw_samples(0, s, 3), s, 0).cuda()
         p = ep.Problem(ctx, args.n, s, ep.KlField(3, 1.0, 0.1, 1.0))
         p.assemble(y)
         vals = p.values

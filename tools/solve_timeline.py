@@ -10,16 +10,13 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tests"))
 import torch  # noqa: E402
 
 import paper_1511_03703_b200 as ep  # noqa: E402
-from oracles import Oracle, pack_group  # noqa: E402
 
 n, s = 64, 32
 ctx = ep.Context(0)
-O = Oracle()
-y = torch.as_tensor(pack_group(O.draw_samples(0, s, 3), s)).cuda()
+y = ep.pack_sample_group(ep.draw_samples(0, s, 3), s, 0).cuda()
 p = ep.Problem(ctx, n, s, ep.KlField(3, 1.0, 0.1, 1.0))
 p.assemble(y)
 st = torch.cuda.current_stream()

@@ -7,11 +7,9 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-sys.path.insert(0, os.path.join(ROOT, "tests"))
 import torch  # noqa: E402
 
 import paper_1511_03703_b200 as ep  # noqa: E402
-from oracles import Oracle, pack_group  # noqa: E402
 
 
 def main():
@@ -22,7 +20,7 @@ def main():
     ap.add_argument("--sigma", type=float, default=0.1)
     args = ap.parse_args()
     ctx = ep.Context(0)
-    y = torch.as_tensor(pack_group(Oracle().draw_samples(0, args.s, args.m), args.s)).cuda()
+    y = ep.pack_sample_group(ep.draw_samples(0, args.s, args.m), args.s, 0).cuda()
     p = ep.Problem(ctx, args.n, args.s, ep.KlField(args.m, 1.0, args.sigma, 1.0))
     p.assemble(y)
     for flavour in (ep.CG_COUPLED, ep.CG_UNCOUPLED):
