@@ -11,8 +11,8 @@
 //    on the device from the uploaded level (device_power_lambda_max: the
 //    same operations, 1.8 s -> milliseconds at 32^3, s = 32).
 //  * The coarsest operator is factored by dense LU with partial pivoting per
-//    component ON THE DEVICE (DenseLuSolver::factor, :297-317): one CTA per
-//    component, the reference's right-looking order (pivot = first maximum,
+//    component ON THE DEVICE (DenseLuSolver::factor, :297-317): one 4-CTA
+//    cluster per component, the reference's right-looking order (pivot = first maximum,
 //    full-row swaps, multiplier then trailing update), so the factors are the
 //    reference's bits. The reference's own host LU makes >= 64^3 infeasible
 //    (the Dirichlet rows stay singleton aggregates: >= 2(n+1)^2 coarse rows).
@@ -28,6 +28,7 @@
 //    reference's serial dot order through the chain kernel (ep_chain.cu);
 //    coupled (one decision) or uncoupled (per-lane scalars, converged lanes
 //    frozen), matching s x pcg_solve<double> on extracted components.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -116,25 +117,42 @@ __global__ void k_direction_masked(int64_t n, const double* __restrict__ beta, c
   if (act[e]) p[g] = EP_DADD(EP_DMUL(1.0, z[g]), EP_DMUL(beta[e], p[g]));
 }
 
-// Dense LU with partial pivoting of one component per CTA (DenseLuSolver::factor,
+// Dense LU with partial pivoting per component (DenseLuSolver::factor,
 // multigrid.hpp:297-317): lu is [s][n][n] row-major, piv [s][n]. Pivot row = the
 // first row with the largest |lu[row][k]| (strict '>' in row order).
 constexpr int kLuThreads = 1024;
 
-__global__ void __launch_bounds__(kLuThreads) k_lu_factor(int n, double* __restrict__ lu_all,
-                                                           int* __restrict__ piv_all, int* __restrict__ singular) {
-  double* lu = lu_all + (size_t)blockIdx.x * n * n;
-  int* piv = piv_all + (size_t)blockIdx.x * n;
+// A cluster of kLuCluster CTAs factors one component, so each step's pivot
+// search, row swap and trailing update are spread over kLuCluster SMs (a
+// single CTA per component was bound by one SM's memory pipe: 2.2 s for
+// 32 x 2179^2). The cluster combines the CTAs' pivot candidates through
+// distributed shared memory; barriers separate the phases of a step, and
+// every element sees the reference's operations in the reference's order.
+constexpr int kLuCluster = 4;
+
+__global__ void __cluster_dims__(kLuCluster, 1, 1) __launch_bounds__(kLuThreads)
+    k_lu_factor(int n, double* __restrict__ lu_all, int* __restrict__ piv_all, int* __restrict__ singular) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int q = (int)cluster.block_rank();
+  const int comp = blockIdx.x / kLuCluster;
+  double* lu = lu_all + (size_t)comp * n * n;
+  int* piv = piv_all + (size_t)comp * n;
   __shared__ double s_best[kLuThreads / 32];
   __shared__ int s_row[kLuThreads / 32];
+  __shared__ double c_best;  // this CTA's pivot candidate, read by the whole cluster
+  __shared__ int c_row;
   __shared__ int s_pivot;
-  __shared__ double s_inv;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int T = kLuCluster * kLuThreads;          // threads of the cluster
+  constexpr int W = kLuCluster * (kLuThreads / 32);   // warps of the cluster
+  const int gt = q * kLuThreads + tid, gw = q * (kLuThreads / 32) + warp;
   for (int k = 0; k < n; ++k) {
-    // argmax over rows >= k, first index on ties
+    // pivot: the first row with the largest |lu[row][k]|, row >= k (each
+    // thread scans its rows in order with '>', combines keep the smaller row)
     double best = -1.0;
     int brow = n;
-    for (int row = k + tid; row < n; row += kLuThreads) {
+    for (int row = k + gt; row < n; row += T) {
       const double c = fabs(lu[(size_t)row * n + k]);
       if (c > best) {
         best = c;
@@ -156,45 +174,58 @@ __global__ void __launch_bounds__(kLuThreads) k_lu_factor(int n, double* __restr
     }
     __syncthreads();
     if (tid == 0) {
-      double b = s_best[0];
+      double bb = s_best[0];
       int r = s_row[0];
       for (int w = 1; w < kLuThreads / 32; ++w)
-        if (s_best[w] > b || (s_best[w] == b && s_row[w] < r)) {
-          b = s_best[w];
+        if (s_best[w] > bb || (s_best[w] == bb && s_row[w] < r)) {
+          bb = s_best[w];
           r = s_row[w];
         }
-      if (b == 0.0) atomicExch(singular, 1);
+      c_best = bb;
+      c_row = r;
+    }
+    cluster.sync();  // candidates visible to the cluster
+    if (tid == 0) {
+      double bb = -1.0;
+      int r = n;
+      for (int j = 0; j < kLuCluster; ++j) {
+        const double bj = *cluster.map_shared_rank(&c_best, j);
+        const int rj = *cluster.map_shared_rank(&c_row, j);
+        if (bj > bb || (bj == bb && rj < r)) {
+          bb = bj;
+          r = rj;
+        }
+      }
+      if (q == 0) {
+        if (bb == 0.0) atomicExch(singular, 1);
+        piv[k] = r < n ? r : k;
+      }
       s_pivot = r < n ? r : k;
-      piv[k] = s_pivot;
     }
     __syncthreads();
     const int pr = s_pivot;
-    if (pr != k)
-      for (int col = tid; col < n; col += kLuThreads) {
+    if (pr != k)  // full-row swap, columns split over the cluster
+      for (int col = gt; col < n; col += T) {
         const double t = lu[(size_t)k * n + col];
         lu[(size_t)k * n + col] = lu[(size_t)pr * n + col];
         lu[(size_t)pr * n + col] = t;
       }
-    __syncthreads();
-    if (tid == 0) s_inv = __ddiv_rn(1.0, lu[(size_t)k * n + k]);
-    __syncthreads();
-    const double inv = s_inv;
-    // multipliers, then the trailing update row by row (each element's
-    // operations are the reference's: lu[row][col] -= mult * lu[k][col])
-    const int rows = n - k - 1;
-    for (int i = tid; i < rows; i += kLuThreads) {
-      const int row = k + 1 + i;
-      lu[(size_t)row * n + k] = EP_DMUL(lu[(size_t)row * n + k], inv);
+    cluster.sync();  // row k final for this step; the candidates were read
+    // multipliers, then each row's trailing update (a warp per row):
+    // mult = lu[row][k] * inv_pivot; lu[row][col] -= mult * lu[k][col]
+    const double inv = __ddiv_rn(1.0, lu[(size_t)k * n + k]);
+    for (int row = k + 1 + gw; row < n; row += W) {
+      double mult = 0.0;
+      if (lane == 0) {
+        mult = EP_DMUL(lu[(size_t)row * n + k], inv);
+        lu[(size_t)row * n + k] = mult;
+      }
+      mult = __shfl_sync(0xffffffffu, mult, 0);
+      double* lrow = lu + (size_t)row * n;
+      const double* krow = lu + (size_t)k * n;
+      for (int col = k + 1 + lane; col < n; col += 32) lrow[col] = EP_DSUB(lrow[col], EP_DMUL(mult, krow[col]));
     }
-    __syncthreads();
-    const int cols = n - k - 1;
-    const int64_t work = (int64_t)rows * cols;
-    for (int64_t t = tid; t < work; t += kLuThreads) {
-      const int row = k + 1 + (int)(t / cols), col = k + 1 + (int)(t % cols);
-      const double mult = lu[(size_t)row * n + k];
-      lu[(size_t)row * n + col] = EP_DSUB(lu[(size_t)row * n + col], EP_DMUL(mult, lu[(size_t)k * n + col]));
-    }
-    __syncthreads();
+    cluster.sync();  // step complete: the next pivot search reads column k + 1
   }
 }
 
@@ -232,34 +263,39 @@ __global__ void __launch_bounds__(kLuThreads) k_lu_solve(int n, const double* __
   }
   // backward (:283-287): acc = y[row]; acc -= lu[row][col]*y[col] for col =
   // row+1..n-1; y[row] = acc / lu[row][row]. Row r's first term needs y[r+1],
-  // so the rows run one after another: warp 0 forms 32 products at a time
-  // into shared memory and lane 0 subtracts them in column order.
-  __shared__ double pbuf[32];
-  if (tid < 32) {
-    const int lane = tid;
-    for (int row = n - 1; row >= 0; --row) {
-      const double* lr = lu + (size_t)row * n;
-      double acc = y[row];
-      for (int col = row + 1; col < n; col += 32) {
-        const int c = col + lane;
-        pbuf[lane] = c < n ? EP_DMUL(lr[c], y[c]) : 0.0;
-        __syncwarp();
-        if (lane == 0) {
-          if (n - col >= 32) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) acc = EP_DSUB(acc, pbuf[j]);
-          } else {
-            for (int j = 0; j < n - col; ++j) acc = EP_DSUB(acc, pbuf[j]);
-          }
-        }
-        __syncwarp();
-      }
-      if (lane == 0) y[row] = __ddiv_rn(acc, lr[row]);
-      __syncwarp();
+  // so the rows run one after another on thread 0, whose chain reads its
+  // products from shared memory: the other threads form row r-1's products
+  // lu[r-1][c]*y[c] for c >= r+1 (all final) while row r's chain runs, and
+  // thread 0 forms each row's first, dependent product itself. Products,
+  // subtractions and their column order are the reference's.
+  double* pb[2] = {y + n, y + 2 * n};  // products of rows of even / odd index
+  for (int r = n - 1; r >= 0; --r) {
+    if (tid == 0) {
+      const double* lr = lu + (size_t)r * n;
+      const double* cur = pb[r & 1];  // lu[r][c]*y[c] for c >= r+2
+      double acc = y[r];
+      if (r + 1 < n) acc = EP_DSUB(acc, EP_DMUL(lr[r + 1], y[r + 1]));
+      for (int c = r + 2; c < n; ++c) acc = EP_DSUB(acc, cur[c]);
+      y[r] = __ddiv_rn(acc, lr[r]);
+    } else if (r >= 1) {
+      const double* lq = lu + (size_t)(r - 1) * n;
+      double* nxt = pb[(r - 1) & 1];
+      for (int c = r + 1 + (tid - 1); c < n; c += kLuThreads - 1) nxt[c] = EP_DMUL(lq[c], y[c]);
     }
+    __syncthreads();
   }
   __syncthreads();
   for (int row = tid; row < n; row += kLuThreads) x[(size_t)row * S + e] = y[row];
+}
+
+// dense[e][row][col] = values[k][e] for the entries k of row (thread = (row, e))
+__global__ void k_dense_scatter(int n, int s, const int* __restrict__ rm, const int* __restrict__ ce,
+                                const double* __restrict__ vals, double* __restrict__ dense) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= (int64_t)n * s) return;
+  const int row = (int)(g / s), e = (int)(g % s);
+  double* d = dense + (size_t)e * n * n + (size_t)row * n;
+  for (int k = rm[row]; k < rm[row + 1]; ++k) d[ce[k]] = vals[(size_t)k * s + e];
 }
 
 __global__ void k_transpose_sq(int n, const double* __restrict__ a, double* __restrict__ t) {
@@ -272,6 +308,21 @@ __global__ void k_transpose_sq(int n, const double* __restrict__ a, double* __re
 }
 
 inline int blocks_for(int64_t work) { return (int)((work + 255) / 256); }
+
+// k_lu_solve's shared memory: y and the two product buffers of the back substitution
+inline size_t lu_solve_smem(int n) { return (size_t)3 * n * sizeof(double); }
+
+cudaError_t lu_solve_smem_optin(int s, size_t bytes) {
+  switch (s) {
+    case 1: return cudaFuncSetAttribute(k_lu_solve<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    case 2: return cudaFuncSetAttribute(k_lu_solve<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    case 4: return cudaFuncSetAttribute(k_lu_solve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    case 8: return cudaFuncSetAttribute(k_lu_solve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    case 16: return cudaFuncSetAttribute(k_lu_solve<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    case 32: return cudaFuncSetAttribute(k_lu_solve<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 #define EP_MG_DISPATCH(s, KER, grid, block, smem, st, ...) \
   switch (s) {                                               \
@@ -597,7 +648,7 @@ int chebyshev(enprop_mg* h, LevelDev& l, const double* b, double* x) {
 
 int coarse_solve(enprop_mg* h, const double* b, double* x) {
   const int n = h->coarse_n, s = h->s;
-  const size_t smem = (size_t)n * sizeof(double);
+  const size_t smem = lu_solve_smem(n);
   EP_MG_DISPATCH(s, k_lu_solve, s, kLuThreads, smem, h->ctx->stream, n, h->lu, h->luT, h->piv, b, x);
   h->ctx->launches += 1;
   EP_CUDA(cudaGetLastError());
@@ -732,20 +783,26 @@ int enprop_mg_build(enprop_ctx* c, int s, int rows, const int* row_map, const in
     h->lv.push_back(l);
     const int n = a.rows;
     h->coarse_n = n;
-    if ((size_t)n * sizeof(double) > 200 * 1024)
+    if (lu_solve_smem(n) > 220 * 1024)
       return bail(fail(ENPROP_ERR_INVALID, "build_hierarchy: coarse level too large for the device LU solve"));
-    std::vector<double> dense((size_t)s * n * n, 0.0);
-    for (int row = 0; row < n; ++row)
-      for (int k = a.rm[row]; k < a.rm[row + 1]; ++k)
-        for (int e = 0; e < s; ++e) dense[(size_t)e * n * n + (size_t)row * n + a.ce[k]] = a.v[(size_t)k * s + e];
+    if (lu_solve_smem_optin(s, lu_solve_smem(n)) != cudaSuccess)
+      return bail(cuda_fail(cudaGetLastError(), "build_hierarchy: coarse solve shared memory"));
+    // the dense operator per component, scattered on the device from the
+    // coarsest CSR just uploaded (zeros elsewhere, DenseLuSolver's ctor :262-275)
+    const size_t dense = (size_t)s * n * n;
     int* singular = nullptr;
-    if ((rc = upload(&h->lu, dense))) return bail(rc);
-    if (cudaMalloc(&h->luT, dense.size() * sizeof(double)) != cudaSuccess ||
+    if (cudaMalloc(&h->lu, dense * sizeof(double)) != cudaSuccess)
+      return bail(cuda_fail(cudaErrorMemoryAllocation, "build_hierarchy"));
+    EP_CUDA(cudaMemsetAsync(h->lu, 0, dense * sizeof(double), st));
+    k_dense_scatter<<<blocks_for((int64_t)n * s), 256, 0, st>>>(n, s, h->lv.back().rm, h->lv.back().ce,
+                                                                  h->lv.back().vals, h->lu);
+    c->launches += 1;
+    if (cudaMalloc(&h->luT, dense * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&h->piv, (size_t)s * n * sizeof(int)) != cudaSuccess ||
         cudaMalloc(&singular, sizeof(int)) != cudaSuccess)
       return bail(cuda_fail(cudaErrorMemoryAllocation, "build_hierarchy"));
     cudaMemsetAsync(singular, 0, sizeof(int), st);
-    k_lu_factor<<<s, kLuThreads, 0, st>>>(n, h->lu, h->piv, singular);
+    k_lu_factor<<<s * kLuCluster, kLuThreads, 0, st>>>(n, h->lu, h->piv, singular);
     k_transpose_sq<<<dim3(blocks_for((int64_t)n * n), s), 256, 0, st>>>(n, h->lu, h->luT);
     c->launches += 2;
     int hs = 0;
