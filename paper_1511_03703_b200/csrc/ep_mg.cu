@@ -11,8 +11,9 @@
 //    on the device from the uploaded level (device_power_lambda_max: the
 //    same operations, 1.8 s -> milliseconds at 32^3, s = 32).
 //  * The coarsest operator is factored by dense LU with partial pivoting per
-//    component ON THE DEVICE (DenseLuSolver::factor, :297-317): one 4-CTA
-//    cluster per component, the reference's right-looking order (pivot = first maximum,
+//    component ON THE DEVICE (DenseLuSolver::factor, :297-317): blocked in
+//    32-column panels (a 4-CTA cluster per component factors a panel) with
+//    the unblocked right-looking algorithm's per-element operation order (pivot = first maximum,
 //    full-row swaps, multiplier then trailing update), so the factors are the
 //    reference's bits. The reference's own host LU makes >= 64^3 infeasible
 //    (the Dirichlet rows stay singleton aggregates: >= 2(n+1)^2 coarse rows).
@@ -131,7 +132,8 @@ constexpr int kLuThreads = 1024;
 constexpr int kLuCluster = 4;
 
 __global__ void __cluster_dims__(kLuCluster, 1, 1) __launch_bounds__(kLuThreads)
-    k_lu_factor(int n, double* __restrict__ lu_all, int* __restrict__ piv_all, int* __restrict__ singular) {
+    k_lu_factor(int n, int k0, int k1, double* __restrict__ lu_all, int* __restrict__ piv_all,
+                int* __restrict__ singular) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const int q = (int)cluster.block_rank();
@@ -147,7 +149,7 @@ __global__ void __cluster_dims__(kLuCluster, 1, 1) __launch_bounds__(kLuThreads)
   constexpr int T = kLuCluster * kLuThreads;          // threads of the cluster
   constexpr int W = kLuCluster * (kLuThreads / 32);   // warps of the cluster
   const int gt = q * kLuThreads + tid, gw = q * (kLuThreads / 32) + warp;
-  for (int k = 0; k < n; ++k) {
+  for (int k = k0; k < k1; ++k) {  // the panel's columns [k0, k1)
     // pivot: the first row with the largest |lu[row][k]|, row >= k (each
     // thread scans its rows in order with '>', combines keep the smaller row)
     double best = -1.0;
@@ -204,8 +206,8 @@ __global__ void __cluster_dims__(kLuCluster, 1, 1) __launch_bounds__(kLuThreads)
     }
     __syncthreads();
     const int pr = s_pivot;
-    if (pr != k)  // full-row swap, columns split over the cluster
-      for (int col = gt; col < n; col += T) {
+    if (pr != k)  // the swap within the panel's columns (k_lu_swaps does the rest)
+      for (int col = k0 + gt; col < k1; col += T) {
         const double t = lu[(size_t)k * n + col];
         lu[(size_t)k * n + col] = lu[(size_t)pr * n + col];
         lu[(size_t)pr * n + col] = t;
@@ -223,10 +225,105 @@ __global__ void __cluster_dims__(kLuCluster, 1, 1) __launch_bounds__(kLuThreads)
       mult = __shfl_sync(0xffffffffu, mult, 0);
       double* lrow = lu + (size_t)row * n;
       const double* krow = lu + (size_t)k * n;
-      for (int col = k + 1 + lane; col < n; col += 32) lrow[col] = EP_DSUB(lrow[col], EP_DMUL(mult, krow[col]));
+      for (int col = k + 1 + lane; col < k1; col += 32) lrow[col] = EP_DSUB(lrow[col], EP_DMUL(mult, krow[col]));
     }
     cluster.sync();  // step complete: the next pivot search reads column k + 1
   }
+}
+
+// Blocked LU with the unblocked algorithm's bits. After the panel [k0, k1) is
+// factored (k_lu_factor on its columns), the other columns receive the
+// panel's row swaps in order (k_lu_swaps), the panel rows of the trailing
+// columns their updates from the panel steps (k_lu_u12), and the trailing
+// rows theirs (k_lu_trailing). Every element still sees each step's update
+// lu[i][j] -= lu[i][t] * lu[t][j] one at a time in increasing t, with the
+// multiplier and pivot row the unblocked algorithm uses (swaps move whole
+// rows, multipliers included), so the factors are the reference's.
+constexpr int kLuPanel = 32;
+
+__global__ void k_lu_swaps(int n, int k0, int k1, double* __restrict__ lu_all, const int* __restrict__ piv_all) {
+  const int comp = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n || (j >= k0 && j < k1)) return;
+  double* lu = lu_all + (size_t)comp * n * n;
+  const int* piv = piv_all + (size_t)comp * n;
+  for (int k = k0; k < k1; ++k) {
+    const int p = piv[k];
+    if (p != k) {
+      const double t = lu[(size_t)k * n + j];
+      lu[(size_t)k * n + j] = lu[(size_t)p * n + j];
+      lu[(size_t)p * n + j] = t;
+    }
+  }
+}
+
+// rows k0..k1-1 of column j >= k1: u[r] -= lu[r][t] * u[t] for t = k0..r-1
+__global__ void __launch_bounds__(128) k_lu_u12(int n, int k0, int k1, double* __restrict__ lu_all) {
+  __shared__ double L[kLuPanel][kLuPanel];
+  const int comp = blockIdx.y;
+  double* lu = lu_all + (size_t)comp * n * n;
+  const int bw = k1 - k0;
+  for (int i = threadIdx.x; i < bw * bw; i += blockDim.x) L[i / bw][i % bw] = lu[(size_t)(k0 + i / bw) * n + k0 + i % bw];
+  __syncthreads();
+  const int j = k1 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double u[kLuPanel];
+#pragma unroll
+  for (int r = 0; r < kLuPanel; ++r) u[r] = r < bw ? lu[(size_t)(k0 + r) * n + j] : 0.0;
+#pragma unroll
+  for (int r = 1; r < kLuPanel; ++r) {
+    if (r < bw) {
+      double acc = u[r];
+#pragma unroll
+      for (int t = 0; t < r; ++t) acc = EP_DSUB(acc, EP_DMUL(L[r][t], u[t]));
+      u[r] = acc;
+    }
+  }
+#pragma unroll
+  for (int r = 1; r < kLuPanel; ++r)
+    if (r < bw) lu[(size_t)(k0 + r) * n + j] = u[r];
+}
+
+// trailing rows and columns >= k1: lu[i][j] -= lu[i][t] * lu[t][j], t = k0..k1-1
+// in order; 64 x 64 output tiles, 256 threads, 4 x 4 outputs each
+constexpr int kLuTile = 64;
+__global__ void __launch_bounds__(256) k_lu_trailing(int n, int k0, int k1, double* __restrict__ lu_all) {
+  __shared__ double Ls[kLuTile][kLuPanel + 1];
+  __shared__ double Us[kLuPanel][kLuTile];
+  const int comp = blockIdx.z;
+  double* lu = lu_all + (size_t)comp * n * n;
+  const int bw = k1 - k0;
+  const int i0 = k1 + blockIdx.y * kLuTile, j0 = k1 + blockIdx.x * kLuTile;
+  for (int idx = threadIdx.x; idx < kLuTile * kLuPanel; idx += blockDim.x) {
+    const int r = idx / kLuPanel, t = idx % kLuPanel;
+    Ls[r][t] = (i0 + r < n && t < bw) ? lu[(size_t)(i0 + r) * n + k0 + t] : 0.0;
+    const int tt = idx / kLuTile, c = idx % kLuTile;
+    Us[tt][c] = (j0 + c < n && tt < bw) ? lu[(size_t)(k0 + tt) * n + j0 + c] : 0.0;
+  }
+  __syncthreads();
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
+      acc[a][b] = (i < n && j < n) ? lu[(size_t)i * n + j] : 0.0;
+    }
+  for (int t = 0; t < bw; ++t)
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const double l = Ls[ty + 16 * a][t];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = EP_DSUB(acc[a][b], EP_DMUL(l, Us[t][tx + 16 * b]));
+    }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
+      if (i < n && j < n) lu[(size_t)i * n + j] = acc[a][b];
+    }
 }
 
 // DenseLuSolver::solve (multigrid.hpp:269-290) of one component per CTA:
@@ -802,7 +899,17 @@ int enprop_mg_build(enprop_ctx* c, int s, int rows, const int* row_map, const in
         cudaMalloc(&singular, sizeof(int)) != cudaSuccess)
       return bail(cuda_fail(cudaErrorMemoryAllocation, "build_hierarchy"));
     cudaMemsetAsync(singular, 0, sizeof(int), st);
-    k_lu_factor<<<s * kLuCluster, kLuThreads, 0, st>>>(n, h->lu, h->piv, singular);
+    for (int k0 = 0; k0 < n; k0 += kLuPanel) {  // blocked, with the unblocked algorithm's bits
+      const int k1 = std::min(n, k0 + kLuPanel);
+      k_lu_factor<<<s * kLuCluster, kLuThreads, 0, st>>>(n, k0, k1, h->lu, h->piv, singular);
+      k_lu_swaps<<<dim3((n + 255) / 256, s), 256, 0, st>>>(n, k0, k1, h->lu, h->piv);
+      if (k1 < n) {
+        k_lu_u12<<<dim3((n - k1 + 127) / 128, s), 128, 0, st>>>(n, k0, k1, h->lu);
+        const int tiles = (n - k1 + kLuTile - 1) / kLuTile;
+        k_lu_trailing<<<dim3(tiles, tiles, s), 256, 0, st>>>(n, k0, k1, h->lu);
+      }
+      c->launches += k1 < n ? 4 : 2;
+    }
     k_transpose_sq<<<dim3(blocks_for((int64_t)n * n), s), 256, 0, st>>>(n, h->lu, h->luT);
     c->launches += 2;
     int hs = 0;
