@@ -9,6 +9,13 @@ each neighbour per SpMV (send/recv), and all-gathers its per-plane canonical
 dot sums; totals are summed in global plane order.  The result must equal the
 one-process canonical CG of the C oracle bit for bit (solution and iteration
 counts), for coupled and uncoupled CG.
+
+The distributed Newton (enprop_dist_newton, f3 with Alg. 2's u halo) is
+restated the same way: each step imports the neighbours' boundary planes of u,
+assembles the owned rows from u known only on [lo ghost | owned | hi ghost],
+forms the coupled canonical residual norm from all-gathered plane sums, and
+solves by the protocol's CG. Norms, steps and u equal the one-process Newton
+composed from the oracle's pieces (canonical order) bit for bit.
 """
 import os
 import socket
@@ -169,6 +176,151 @@ def worker(rank, world, port, n, s, flavour, out):
         out.put((xg, iters.tolist()))
     dist.barrier()
     dist.destroy_process_group()
+
+
+def newton_worker(rank, world, port, n, s, beta, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from oracles import Oracle, pack_group
+    O = Oracle()
+    N, plane = n + 1, (n + 1) ** 2
+    f = O.kl(3, 1.0, 0.2, 1.0)
+    y = pack_group(O.draw_samples(5, s, 3), s)
+    rm_g, ce_g = O.graph(n)
+    k0, k1 = plane_range(N, world, rank)
+    rb, re_ = k0 * plane, k1 * plane
+    lo = plane if k0 > 0 else 0
+    hi = plane if k1 < N else 0
+    ext_begin = rb - lo
+    rm = (rm_g[rb:re_ + 1] - rm_g[rb]).astype(np.int64)
+    ce = (ce_g[rm_g[rb]:rm_g[re_]] - ext_begin).astype(np.int64)
+    rows = re_ - rb
+    maxplanes = (N + world - 1) // world
+
+    def total(u, v):
+        ps = np.zeros((maxplanes, s))
+        ps[:k1 - k0] = plane_sums(u, v, plane, s)
+        bufs = [torch.zeros((maxplanes, s), dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(bufs, torch.from_numpy(ps))
+        acc = np.zeros(s)
+        for q in range(world):
+            a, c = plane_range(N, world, q)
+            for k in range(c - a):
+                acc = acc + bufs[q].numpy()[k]
+        return acc
+
+    def coupled(d):
+        acc = 0.0
+        for e in range(s):
+            acc = acc + d[e]
+        return acc
+
+    def halo(own):
+        pe = np.zeros((lo + rows + hi, s))
+        pe[lo:lo + rows] = own
+        reqs = []
+        lo_buf = torch.zeros((plane, s), dtype=torch.float64)
+        hi_buf = torch.zeros((plane, s), dtype=torch.float64)
+        if rank > 0:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(own[:plane])), rank - 1))
+            reqs.append(dist.irecv(lo_buf, rank - 1))
+        if rank + 1 < world:
+            reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(own[rows - plane:])), rank + 1))
+            reqs.append(dist.irecv(hi_buf, rank + 1))
+        for r_ in reqs:
+            r_.wait()
+        if lo:
+            pe[:plane] = lo_buf.numpy()
+        if hi:
+            pe[lo + rows:] = hi_buf.numpy()
+        return pe
+
+    def cg(vals, b, tol=1e-10, maxit=1000):  # coupled, canonical totals (pcg.hpp:52-103)
+        x = np.zeros((rows, s))
+        r = b.copy()
+        dd = coupled(total(b, b))
+        bnorm = np.sqrt(dd)
+        if bnorm == 0.0:
+            return x
+        rz = dd
+        p = r.copy()
+        for it in range(maxit):
+            q = spmv(rm, ce, vals, halo(p), s)
+            alpha = rz / coupled(total(p, q))
+            x = alpha * p + x
+            r = (-alpha) * q + r
+            rr = coupled(total(r, r))
+            beta_ = rr / rz
+            rz = rr
+            if np.sqrt(rr) / bnorm < tol:
+                break
+            p = r + beta_ * p
+        return x
+
+    u = np.zeros((rows, s))
+    norms, steps, tol = [], 0, 1e-9
+    for step in range(21):
+        ue = halo(u)  # Alg. 2: import the neighbours' boundary planes of u
+        uf = np.zeros(((n + 1) ** 3, s))
+        uf[ext_begin:ext_begin + lo + rows + hi] = ue
+        vals_g, res_g = O.assemble(s, n, f, y, u=uf, beta=beta, dirichlet=True)
+        vals, res = vals_g[rm_g[rb]:rm_g[re_]], res_g[rb:re_]
+        norm = np.sqrt(coupled(total(res, res)))
+        norms.append(norm)
+        if step == 0 and norm == 0.0:
+            break
+        if step > 0 and norm < tol * norms[0]:
+            steps = step
+            break
+        du = cg(vals, -res)
+        u = 1.0 * du + 1.0 * u  # axpby(1.0, du, 1.0, u) (fem.hpp:300)
+    us = [None] * world
+    dist.all_gather_object(us, (rb, u))
+    if rank == 0:
+        ug = np.concatenate([v for _, v in sorted(us, key=lambda t: t[0])])
+        out.put((ug, norms, steps))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_newton_protocol_equals_single_process_newton(world):
+    from oracles import CG_COUPLED, DOT_CANONICAL, Oracle, bits, pack_group
+    n, s, beta = 4, 2, 1.0
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=newton_worker, args=(r, world, port, n, s, beta, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    ug, norms, steps = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    # the one-process Newton from the oracle's pieces, canonical order (segments = planes)
+    O = Oracle()
+    f = O.kl(3, 1.0, 0.2, 1.0)
+    y = pack_group(O.draw_samples(5, s, 3), s)
+    rm, ce = O.graph(n)
+    seg = (n + 1) ** 2
+    u = np.zeros(((n + 1) ** 3, s))
+    rn, rsteps = [], 0
+    for step in range(21):
+        vals, res = O.assemble(s, n, f, y, u=u, beta=beta, dirichlet=True)
+        norm = np.sqrt(O.dot(s, res, res, DOT_CANONICAL, TILE, seg))
+        rn.append(norm)
+        if step > 0 and norm < 1e-9 * rn[0]:
+            rsteps = step
+            break
+        du = O.pcg(s, rm, ce, vals, -res, 1e-10, 1000, flavour=CG_COUPLED, mode=DOT_CANONICAL, tile=TILE,
+                   seg=seg)["x"]
+        u = 1.0 * du + 1.0 * u
+    assert rsteps >= 2 and steps == rsteps
+    assert (bits(np.array(norms)) == bits(np.array(rn))).all()
+    assert (bits(ug) == bits(u)).all()
 
 
 def free_port():
