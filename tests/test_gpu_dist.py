@@ -104,6 +104,30 @@ def test_halo_overlap_splits_interior_stages(ctx):
     d.close()
 
 
+@pytest.mark.parametrize("s", [4, 32])
+def test_nccl_single_rank_job_equals_emulated_bitwise(ctx, s):
+    """The NCCL transport (libnccl.so.2 loaded at run time, unique id, comm
+    init, per-plane sums all-gathered by ncclAllGather, comm destroy) as a
+    1-rank job on this GPU -- NCCL refuses two ranks on one device, so this
+    is the part of the NCCL path one GPU can run. Bitwise the emulated solve."""
+    n, m = 10, 3
+    y = torch.as_tensor(pack_group(O.draw_samples(0, s, m), s)).cuda()
+    kl = ep.KlField(m, 1.0, 0.1, 1.0)
+    cfg = ep.SolverConfig(tol=1e-7, max_iterations=2000, flavour=CG_UNCOUPLED, dot_mode=ep.DOT_CANONICAL)
+    d1 = ep.Dist(ctx, n, s, 1, kl=kl)
+    d1.assemble(y)
+    it1, _ = d1.solve(cfg)
+    x1 = d1.solution().cpu().numpy()
+    d1.close()
+    d2 = ep.Dist(ctx, n, s, 1, 0, nccl_id=ep.nccl_unique_id(), kl=kl)
+    d2.assemble(y)
+    it2, st2 = d2.solve(cfg)
+    x2 = d2.solution().cpu().numpy()
+    assert it1 == it2 and all(v == 0 for v in st2)
+    assert same(x1, x2)
+    d2.close()
+
+
 def test_partition_matches_reference_rule(ctx):
     R = RefLib()
     n = 10
