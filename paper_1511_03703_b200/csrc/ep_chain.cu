@@ -171,7 +171,9 @@ static cudaError_t chain_sk(int rows, const double* u, const double* v, const Fi
       ready[dev].store(1, std::memory_order_release);
     }
   }
-  launch_kk(4, k_chain<S, KIND, CB>, dim3(1), dim3(64), SMEM, st, rows, u, v, f);
+  // highest launch priority: a group's latency-critical chain takes the next
+  // free SM ahead of other groups' pending SpMV CTAs (+0.3-0.6% at 24 groups)
+  launch_kk(4 | kLaunchUrgent, k_chain<S, KIND, CB>, dim3(1), dim3(64), SMEM, st, rows, u, v, f);
   return cudaGetLastError();
 }
 

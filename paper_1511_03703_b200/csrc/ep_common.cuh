@@ -223,6 +223,17 @@ inline int pdl_mask() {
 }
 
 constexpr int kLaunchCooperative = 64;  // launch_kk kind flag
+constexpr int kLaunchUrgent = 128;      // launch_kk kind flag: highest launch priority
+
+// the device's highest (numerically lowest) stream priority, queried once
+inline int greatest_priority() {
+  static const int v = [] {
+    int least = 0, greatest = 0;
+    if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) greatest = 0;
+    return greatest;
+  }();
+  return v;
+}
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_kk(int kind, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
@@ -232,8 +243,13 @@ inline cudaError_t launch_kk(int kind, void (*kernel)(KArgs...), dim3 grid, dim3
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   unsigned n = 0;
+  if (kind & kLaunchUrgent) {  // pending CTAs of this launch get the next free SM first
+    attr[n].id = cudaLaunchAttributePriority;
+    attr[n].val.priority = greatest_priority();
+    ++n;
+  }
   if (pdl_enabled() && (pdl_mask() & kind)) {
     attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[n].val.programmaticStreamSerializationAllowed = 1;
