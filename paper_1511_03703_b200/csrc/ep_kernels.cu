@@ -412,7 +412,8 @@ cudaError_t launch_fin_gathered(int s, int planes, const double* gathered, const
 // Serial finalize: the reference's own order (kernels.hpp:66-67), one chain
 // per sample: acc = 0; acc += u[row]*v[row] for row = 0, 1, ...  The chain is
 // latency-bound (one dependent DADD per row, ~8 cycles on B200), so the design
-// keeps the chain's operands in registers: one warp per sample; in a chunk of
+// keeps the chain's operands in registers (enprop_dot's path for operands that
+// are not 16-byte aligned; the CG loop uses k_chain): one warp per sample; in a chunk of
 // 32*K rows lane j holds the products of rows [jK, jK+K) and the running sum
 // walks lane 0 -> lane 31 by shuffles, while the next chunk's loads are in
 // flight.  A block holds the warps of LG = min(s, 4) samples (one 32-byte
@@ -518,8 +519,8 @@ cudaError_t launch_fin_serial(int s, int rows, const double* u, const double* v,
 // CG vector kernels.  Flat row mapping: TPR threads per row, one row per slot,
 // P slots per thread, so every row of the grid is in flight at once.  With
 // kTiles the slots are the block's canonical tiles and the fused finalize
-// closes the dot; without (serial order) rows are contiguous and a separate
-// k_fin_serial forms the dot.  All kernels early-exit once the solve is done,
+// closes the dot; without (serial order) rows are contiguous and the chain
+// kernel (ep_chain.cu) forms the dot.  All kernels early-exit once the solve is done,
 // so the host may enqueue ahead of its convergence check.
 // =============================================================================
 template <int S, int P, bool kTiles, int NT = 256>
