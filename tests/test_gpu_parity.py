@@ -243,6 +243,13 @@ def test_dot_serial_equals_reference(ctx, R, s):
         lanes, coupled = ep.dot_lanes(ctx, s, dev(u), dev(v), ep.DOT_SERIAL)
         assert coupled == R.dot(s, u, v)
         assert lanes == list(O.dot_lanes(s, u, v, DOT_SERIAL))
+        # operands 8 bytes off a 16-byte boundary take the register-chain
+        # fallback (k_fin_serial) instead of the TMA-fed k_chain: same bits
+        ub = torch.zeros(n * s + 1, dtype=torch.float64, device="cuda")
+        ub[1:] = dev(u).reshape(-1)
+        lanes2, coupled2 = ep.dot_lanes(ctx, s, ub[1:].view(n, s), dev(v), ep.DOT_SERIAL)
+        assert ub[1:].data_ptr() % 16 == 8
+        assert coupled2 == coupled and lanes2 == lanes
 
 
 @pytest.mark.parametrize("s", WIDTHS)
