@@ -218,7 +218,6 @@ cudaError_t launch_cg_spmv_staged(int s, bool tiles, bool fuse_fin, const StageM
                                   cudaStream_t st);
 bool staged_fuse_fin();  // ENPROP_STAGED_FUSE (env, default 1)
 bool staged_serial();    // ENPROP_STAGED_SERIAL (env, default 1)
-bool chain_forms_pq();   // ENPROP_CHAIN_PQ (env, A/B, default 0): the p.q chain reads p and q (no SpMV products)
 bool plain_cg_spmv();    // ENPROP_PLAIN_CG_SPMV (env, default 1): public SpMV kernels in unstaged full-storage CG
 int spmv_variant();  // ENPROP_OPT_SPMV_VARIANT of the calling context (-1 = auto)
 

@@ -509,11 +509,6 @@ int staged_pf() {
   return v;
 }
 
-bool chain_forms_pq() {
-  static const int on = env_int("ENPROP_CHAIN_PQ", 0);
-  return on != 0;
-}
-
 bool plain_cg_spmv() {
   static const int on = env_int("ENPROP_PLAIN_CG_SPMV", 1);
   return on != 0;
