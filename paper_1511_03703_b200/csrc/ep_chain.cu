@@ -11,11 +11,11 @@
 //  * one CTA per dot; warp 0 consumes: lane e < S runs sample e's chain, so a
 //    row's S values are one contiguous 8S-byte read from shared memory and the
 //    chain never hands off between lanes;
-//  * warp 1 lane 0 produces: rows arrive as 32 KB stages (per operand) via
-//    cp.async.bulk into a 4-stage ring (3 for two operands), completing on
+//  * warp 1 lane 0 produces: rows arrive as 48 KB stages (per operand) via
+//    cp.async.bulk into a 3-stage ring (2 for two operands), completing on
 //    mbarriers; the producer alone waits on `empty` barriers, so copy issue
 //    stays off the chain;
-//  * the consumer walks a stage in fully unrolled 64-row blocks (the compiler
+//  * the consumer walks a stage in fully unrolled 96-row blocks (the compiler
 //    hoists the block's shared-memory loads ahead of its DADDs), which runs at
 //    the DADD latency; what remains per stage is one `full` wait.
 // Measured alternatives (chain_bench.cu): register-prefetched global loads
@@ -27,7 +27,8 @@
 // ring shape (A/B, profiles/round2/README.md §3, 24 groups): 16 KB stages x 4
 // / 6 gave 494-503 samples/s, x 8 548-569; 32 KB x 4 (the same 128 KB, half the
 // per-stage waits) 574-577, with the p.q / r.r chains at 1.41 / 1.63 ms
-// vs 1.57 / 1.84 ms for 16 KB x 8. A software-pipelined consumer (the next
+// vs 1.57 / 1.84 ms for 16 KB x 8; 48 KB x 3 with 96-row blocks: chains
+// 1.32 / 1.60 ms, +0.2-0.4% at 24 groups (same box). A software-pipelined consumer (the next
 // 32-row block's terms formed ahead) ran at ~18 cycles per row: ptxas issued
 // the next block as one run before the DADDs, plus the register copies.
 // The CG scalar phase (ep_fin.cuh cg_phase) runs in the consumer warp.
@@ -47,13 +48,13 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-constexpr int kChainChunkBytes = 32768;  // per operand vector per stage
-constexpr int kChainBlock = 64;          // rows per unrolled consumer block
+constexpr int kChainChunkBytes = 49152;  // per operand vector per stage
+constexpr int kChainBlock = 96;          // rows per unrolled consumer block
 
 template <int NV, int CB = kChainChunkBytes>
 struct ChainRing {
   static constexpr int STAGE = CB * NV;
-  static constexpr int D = (NV == 1 ? 131072 : 196608) / STAGE;  // stages in the ring (128 / 192 KB)
+  static constexpr int D = (NV == 1 ? 147456 : 196608) / STAGE;  // stages in the ring (3 x 48 KB / 2 x 96 KB)
   static constexpr int SMEM = D * STAGE + 2 * D * 8;
 };
 
